@@ -1,0 +1,205 @@
+"""Seeded synthetic QP generators shared by the oracle tests, the CUDA parity
+tests and bench.py.
+
+This module holds NONE of the method's arithmetic (no residuals, no
+retraction, no KKT algebra): it only draws problem data.  Both the oracle
+(`oracle/`) and the CUDA path (`paper_2605_17913_b200`) receive the arrays it
+returns.  Every problem i of config c is drawn from its own stream
+``np.random.SeedSequence([c, i])`` (PCG64), so any subset of a batch can be
+regenerated bit-identically on its own (SURVEY.md §8(d) "Synthetic inputs").
+
+All data is drawn in float64 and then rounded ONCE to float32; the float32
+values are the problem.  The f64 oracle runs on those same (exactly
+representable) values, so GPU-vs-oracle differences are solver differences,
+never input differences.
+
+Workload recipes (DESIGN.md §3 restates them with citations):
+
+* ``g_rand(n, m, p)`` — "random feasible dense QP" (BASELINE.json configs 1,
+  2, 5; shared data of config 4): M~N(0,1)^{n×n}, Q = M Mᵀ/n + 0.1·I
+  (strictly convex), q~N(0,1); A~N(0,1)/√n, x0~N(0,1), b = A x0;
+  G~N(0,1)/√n, s0~U(0,1), h = G x0 + s0 (x0 strictly feasible);
+  ∇ₓℓ~N(0,1).
+* ``g_proj(n, p, m_act, d)`` — polytope projection of PAPER.md App. D
+  (P:887-921): unit-norm rows of G, boundary point y0, m_act
+  active rows h_A = G_A y0, inactive rows h = G y0 + margin with margin
+  log-uniform in [1e-3, 1] ("near-active", BASELINE config 3), query
+  x = y0 + G_Aᵀ(d·ξ), ξ~U(0.5,1.5); Q = I, q = −x;
+  ∇ₓℓ = probe v~N(0,I).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+F32 = np.float32
+
+
+def _rng(cfg: int, i: int) -> np.random.Generator:
+    return np.random.Generator(np.random.PCG64(np.random.SeedSequence([int(cfg), int(i)])))
+
+
+@dataclass
+class QPBatch:
+    """A batch of dense QPs in the C-ABI layout: batch-major, row-major f32.
+
+    A field whose batch dimension is 1 and whose ``shared_*`` flag is set is
+    shared across the batch (C-ABI batch stride 0)."""
+
+    n: int
+    m: int
+    p: int
+    Q: np.ndarray  # [B|1, n, n]
+    q: np.ndarray  # [B|1, n]
+    A: np.ndarray  # [B|1, m, n]
+    b: np.ndarray  # [B|1, m]
+    G: np.ndarray  # [B|1, p, n]
+    h: np.ndarray  # [B|1, p]
+    dl_dx: np.ndarray  # [B, n]
+    batch: int
+    shared: dict = field(default_factory=dict)  # name -> True if stride 0
+    meta: dict = field(default_factory=dict)
+
+    def problem(self, i: int) -> dict:
+        """Dense f32 arrays of problem i (shared fields broadcast)."""
+        def pick(name):
+            arr = getattr(self, name)
+            return arr[0] if self.shared.get(name, False) else arr[i]
+        return {k: pick(k) for k in ("Q", "q", "A", "b", "G", "h")} | {"dl_dx": self.dl_dx[i]}
+
+    def subset(self, idx) -> "QPBatch":
+        idx = np.asarray(idx, dtype=np.int64)
+        def sel(name):
+            arr = getattr(self, name)
+            return arr if self.shared.get(name, False) else np.ascontiguousarray(arr[idx])
+        return QPBatch(self.n, self.m, self.p, sel("Q"), sel("q"), sel("A"), sel("b"),
+                       sel("G"), sel("h"), np.ascontiguousarray(self.dl_dx[idx]), len(idx),
+                       dict(self.shared), dict(self.meta))
+
+
+def _sym(Q: np.ndarray) -> np.ndarray:
+    return 0.5 * (Q + Q.T)
+
+
+def g_rand_one(rng: np.random.Generator, n: int, m: int, p: int):
+    M = rng.standard_normal((n, n))
+    Q = _sym(M @ M.T / n + 0.1 * np.eye(n))
+    q = rng.standard_normal(n)
+    A = rng.standard_normal((m, n)) / np.sqrt(n)
+    x0 = rng.standard_normal(n)
+    G = rng.standard_normal((p, n)) / np.sqrt(n)
+    s0 = rng.uniform(0.0, 1.0, p)
+    # Round the matrices first so that b and h are computed from the f32 data
+    # the solver actually sees (x0 stays strictly feasible up to f32 rounding
+    # of b, h themselves).
+    A32, G32 = A.astype(F32), G.astype(F32)
+    b = A32.astype(np.float64) @ x0
+    h = G32.astype(np.float64) @ x0 + s0
+    dl = rng.standard_normal(n)
+    return Q.astype(F32), q.astype(F32), A32, b.astype(F32), G32, h.astype(F32), dl.astype(F32)
+
+
+def g_rand(cfg: int, batch: int, n: int, m: int, p: int, start: int = 0) -> QPBatch:
+    """Config-`cfg` batch of random feasible strictly convex QPs."""
+    Qs = np.empty((batch, n, n), F32); qs = np.empty((batch, n), F32)
+    As = np.empty((batch, m, n), F32); bs = np.empty((batch, m), F32)
+    Gs = np.empty((batch, p, n), F32); hs = np.empty((batch, p), F32)
+    dls = np.empty((batch, n), F32)
+    for j in range(batch):
+        Q, q, A, b, G, h, dl = g_rand_one(_rng(cfg, start + j), n, m, p)
+        Qs[j], qs[j], As[j], bs[j], Gs[j], hs[j], dls[j] = Q, q, A, b, G, h, dl
+    return QPBatch(n, m, p, Qs, qs, As, bs, Gs, hs, dls, batch,
+                   meta={"recipe": "g_rand", "cfg": cfg, "start": start})
+
+
+def g_rand_shared(cfg: int, batch: int, n: int, m: int, p: int, start: int = 0) -> QPBatch:
+    """Config 4 ("end-to-end/bilevel"): Q, A, b, G, h shared across the batch
+    (drawn once from stream [cfg, 0]); per-instance q_b~N(0,1) and ∇ₓℓ_b~N(0,1)
+    from streams [cfg, 1+i]."""
+    Q, _, A, b, G, h, _ = g_rand_one(_rng(cfg, 0), n, m, p)
+    qs = np.empty((batch, n), F32); dls = np.empty((batch, n), F32)
+    for j in range(batch):
+        r = _rng(cfg, 1 + start + j)
+        qs[j] = r.standard_normal(n).astype(F32)
+        dls[j] = r.standard_normal(n).astype(F32)
+    return QPBatch(n, m, p, Q[None], qs, A[None], b[None], G[None], h[None], dls, batch,
+                   shared={"Q": True, "A": True, "b": True, "G": True, "h": True},
+                   meta={"recipe": "g_rand_shared", "cfg": cfg, "start": start})
+
+
+def g_proj_one(rng: np.random.Generator, n: int, p: int, m_act: int, d: float,
+               margin_lo: float = 1e-3, margin_hi: float = 1.0):
+    """One polytope-projection instance (App. D.1-D.3).
+
+    Returns f32 (Q, q, A, b, G, h, probe) plus f64 (y0, active_idx) for the
+    hard-Jacobian reference.  Active rows are redrawn until G_A has full row
+    rank ("rank(G_A) = m")."""
+    for _ in range(100):
+        G = rng.standard_normal((p, n))
+        G /= np.linalg.norm(G, axis=1, keepdims=True)
+        active = np.sort(rng.choice(p, size=m_act, replace=False))
+        if m_act == 0 or np.linalg.matrix_rank(G[active]) == m_act:
+            break
+    else:  # pragma: no cover
+        raise RuntimeError("rank-deficient active set after 100 redraws")
+    G32 = G.astype(F32)
+    Gd = G32.astype(np.float64)
+    y0 = rng.standard_normal(n)
+    margin = np.exp(rng.uniform(np.log(margin_lo), np.log(margin_hi), p))
+    h = Gd @ y0
+    inactive = np.ones(p, bool); inactive[active] = False
+    h[inactive] += margin[inactive]
+    xi = rng.uniform(0.5, 1.5, m_act)
+    xq = y0 + Gd[active].T @ (d * xi)
+    probe = rng.standard_normal(n)
+    Q = np.eye(n, dtype=F32)
+    return (Q, (-xq).astype(F32), np.zeros((0, n), F32), np.zeros(0, F32), G32,
+            h.astype(F32), probe.astype(F32), y0, active)
+
+
+D_GRID = np.logspace(-2, 2, 21)
+MR_GRID = (0.2, 0.6, 0.8)
+
+
+def g_proj(cfg: int, batch: int, n: int, p: int, start: int = 0) -> QPBatch:
+    """Config 3 batch: instance i cycles (m_r, d) over MR_GRID × D_GRID
+     with its own seed stream [cfg, i]."""
+    Qs = np.empty((batch, n, n), F32); qs = np.empty((batch, n), F32)
+    Gs = np.empty((batch, p, n), F32); hs = np.empty((batch, p), F32)
+    dls = np.empty((batch, n), F32)
+    y0s = np.empty((batch, n)); actives = []
+    mrs = np.empty(batch); ds = np.empty(batch)
+    for j in range(batch):
+        i = start + j
+        mr = MR_GRID[i % 3]; d = D_GRID[(i // 3) % len(D_GRID)]
+        m_act = int(round(mr * n))
+        Q, q, _, _, G, h, pr, y0, act = g_proj_one(_rng(cfg, i), n, p, m_act, d)
+        Qs[j], qs[j], Gs[j], hs[j], dls[j] = Q, q, G, h, pr
+        y0s[j] = y0; actives.append(act); mrs[j] = mr; ds[j] = d
+    return QPBatch(n, 0, p, Qs, qs, np.zeros((batch, 0, n), F32), np.zeros((batch, 0), F32),
+                   Gs, hs, dls, batch,
+                   meta={"recipe": "g_proj", "cfg": cfg, "start": start, "y0": y0s,
+                         "active": actives, "m_r": mrs, "d": ds})
+
+
+# BASELINE.json configs (m_eq/p readings for 4 and 5 are
+# SURVEY's proposal, restated in DESIGN.md).
+CONFIGS = {
+    1: dict(name="cfg1_rand_n10_m2_p20_B16", n=10, m=2, p=20, batch=16, recipe="g_rand"),
+    2: dict(name="cfg2_optnet_n50_m10_p100_B1024", n=50, m=10, p=100, batch=1024, recipe="g_rand"),
+    3: dict(name="cfg3_proj_n100_p125_B4096", n=100, m=0, p=125, batch=4096, recipe="g_proj"),
+    4: dict(name="cfg4_bilevel_shared_n200_p400_B8192", n=200, m=0, p=400, batch=8192,
+            recipe="g_rand_shared"),
+    5: dict(name="cfg5_large_n1024_p2048_B256", n=1024, m=0, p=2048, batch=256, recipe="g_rand"),
+}
+
+
+def make_config(cfg: int, batch: int | None = None, start: int = 0) -> QPBatch:
+    c = CONFIGS[cfg]
+    B = c["batch"] if batch is None else batch
+    if c["recipe"] == "g_rand":
+        return g_rand(cfg, B, c["n"], c["m"], c["p"], start)
+    if c["recipe"] == "g_rand_shared":
+        return g_rand_shared(cfg, B, c["n"], c["m"], c["p"], start)
+    return g_proj(cfg, B, c["n"], c["p"], start)

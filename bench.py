@@ -1,0 +1,324 @@
+#!/usr/bin/env python
+"""Benchmark: batched f32 QP solve + backward (Alg. 1 + Alg. 2 + Alg. 3 of
+arxiv 2605.17913) through the C ABI on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+One step = qp_solve_batched + qp_backward_batched over one batch per GPU
+(weak scaling: every rank owns its own batch of distinct problems), plus the
+NCCL all-reduce of shared-parameter gradients when the config shares them.
+Metric (BASELINE.json): QP solve+backward/sec, f32, device-timed, whole job.
+Rank 0 prints ONE JSON line.  See DESIGN.md §7 for every field."""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from paper_2605_17913_b200 import flops as FL  # noqa: E402
+from paper_2605_17913_b200 import generators as gen  # noqa: E402
+
+METRIC = "QP solve+backward/sec (f32, device-timed)"
+UNIT = "QP/s"
+FIELDS = ("Q", "q", "A", "b", "G", "h")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2, help="BASELINE.json config index (1-based)")
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled DURING the timed region (B200_PROFILING.md "clocks" line)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("uuid,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, uuid: str | None):
+        self.uuid = uuid
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                         text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        rows = [r for r in self.rows if self.uuid is None or self.uuid in r[0]] or self.rows
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(r[1]) for r in rows if num(r[1]) is not None]
+        mx = [num(r[2]) for r in rows if num(r[2]) is not None]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({nm for r in rows for nm, v in zip(names, r[5:9]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# the oracle (CPU) legs
+# ---------------------------------------------------------------------------
+def oracle_rate(cfg_idx: int, target_s: float, batch_cap: int, start: int = 0):
+    """Time the f64 oracle (K14 + GEPP, the parity reference) on a bounded
+    sample of the workload, all host cores.  Returns (QP/s, cores, sample, n_problems)."""
+    import oracle
+    nt = oracle.hardware_threads()
+    pilot = gen.make_config(cfg_idx, batch=min(nt, batch_cap), start=start)
+    t0 = time.perf_counter()
+    r = oracle.solve(pilot, oracle.Cfg.f64(), "f64", nthreads=nt)
+    oracle.backward(pilot, r, oracle.Cfg.f64(), "f64", nthreads=nt)
+    dt = time.perf_counter() - t0
+    rate = pilot.batch / max(dt, 1e-6)
+    ns = int(min(batch_cap, max(pilot.batch, round(rate * target_s))))
+    ns = max(nt, (ns // nt) * nt) if ns >= nt else ns
+    samp = gen.make_config(cfg_idx, batch=ns, start=start)
+    t0 = time.perf_counter()
+    r = oracle.solve(samp, oracle.Cfg.f64(), "f64", nthreads=nt)
+    oracle.backward(samp, r, oracle.Cfg.f64(), "f64", nthreads=nt)
+    dt = time.perf_counter() - t0
+    return ns / dt, nt, ns, dt
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return 0
+    c = gen.CONFIGS[a.config]
+    import oracle
+    nt = oracle.hardware_threads()
+    # calibrate one step to ~4 s of CPU work so K+W steps finish in minutes
+    _, _, ns, _ = oracle_rate(a.config, 4.0, c["batch"])
+    samp = gen.make_config(a.config, batch=ns)
+    times = []
+    for i in range(a.warmup + a.steps):
+        t0 = time.perf_counter()
+        r = oracle.solve(samp, oracle.Cfg.f64(), "f64", nthreads=nt)
+        oracle.backward(samp, r, oracle.Cfg.f64(), "f64", nthreads=nt)
+        if i >= a.warmup:
+            times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    val = ns * a.steps / tot
+    sample = (f"first {ns} problems of {c['name']} per step (seed streams [{a.config}, i]); f64 oracle "
+              f"(Eq. 14 + GEPP), init + Alg. 1 + Alg. 2 + Alg. 3, std::thread over problems")
+    out = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+           "ms_per_step": 1e3 * tot / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "f64", "data": "synthetic", "impl": "reference",
+           "config": {"workload": c["name"], "batch_per_step": ns, "n": c["n"], "m_eq": c["m"], "p": c["p"]},
+           "cpu_baseline": {"value": val, "unit": UNIT, "cores": nt, "kind": "oracle", "sample": sample},
+           "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "gpu_launches": 0}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+    import torch
+    from paper_2605_17913_b200 import dist as D
+    from paper_2605_17913_b200.solver import QPSolver
+
+    rank, world, local = D.init()
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    c = gen.CONFIGS[a.config]
+    B, n, m, p = c["batch"], c["n"], c["m"], c["p"]
+    batch = gen.make_config(a.config, batch=B, start=rank * B)  # distinct problems per rank
+    shared = [k for k, v in batch.shared.items() if v]
+    S = QPSolver(B, n, m, p, shared=shared, device=local)
+    info = S.info()
+
+    def T(f):
+        arr = getattr(batch, f)
+        arr = arr[0] if f in shared else arr
+        return torch.from_numpy(np.ascontiguousarray(arr)).to(dev)
+
+    data = [T(f) for f in FIELDS]
+    dl = torch.from_numpy(batch.dl_dx).to(dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        out = S.solve(*data)
+        g = S.backward(dl)
+        D.allreduce_shared_grads(g, shared)
+        return out, g
+
+    for _ in range(a.warmup):
+        out, g = step()
+    torch.cuda.synchronize(dev)
+    D.barrier()
+    torch.cuda.synchronize(dev)
+    props = torch.cuda.get_device_properties(dev)
+    uuid = str(getattr(props, "uuid", "")) or None
+    clk = ClockSampler(uuid)
+    clk.start()
+    time.sleep(0.3)
+    t_solve = t_bwd = 0.0
+    for _ in range(a.steps):
+        flush.fill_(1.0)  # L2 flush between timed steps (outside the events)
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record(stream)
+        out = S.solve(*data)
+        e1.record(stream)
+        g = S.backward(dl)
+        D.allreduce_shared_grads(g, shared)
+        e2.record(stream)
+        e2.synchronize()
+        t_solve += e0.elapsed_time(e1)
+        t_bwd += e1.elapsed_time(e2)
+    torch.cuda.synchronize(dev)
+    clk.stop()
+    D.barrier()
+    total_ms = D.max_over_ranks(t_solve + t_bwd, dev)
+    value = B * world * a.steps / (total_ms / 1e3)
+
+    iters = out["iters"].cpu().numpy()
+    riters = g["relax_iters"].cpu().numpy()
+    status = out["status"].cpu().numpy()
+    gstatus = g["status"].cpu().numpy()
+    f_solve = float(sum(FL.solve_flops(n, m, p, int(k)) for k in iters))
+    f_bwd = float(sum(FL.backward_flops(n, m, p, int(k)) for k in riters))
+    ms_solve, ms_bwd = t_solve / a.steps, t_bwd / a.steps
+    peak = FL.fp32_peak_tflops(props.multi_processor_count)
+    dom_solve = ms_solve >= ms_bwd
+    f_dom, ms_dom = (f_solve, ms_solve) if dom_solve else (f_bwd, ms_bwd)
+    achieved = f_dom / (ms_dom / 1e3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_cfg{a.config}.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("ipm_solve_kernel" if dom_solve else "ipm_backward_kernel")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "alu", "kernel": "ipm_solve_kernel" if dom_solve else "ipm_backward_kernel",
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": traffic,
+                "peak_note": "FP32 FMA: SMs x 128 lanes x 2 flop x 1965 MHz (derived, DESIGN.md §6)",
+                "flops_per_launch": f_dom, "ms_per_launch": ms_dom,
+                "solve_ms": ms_solve, "backward_ms": ms_bwd,
+                "solve_tflops": f_solve / (ms_solve / 1e3) / 1e12,
+                "backward_tflops": f_bwd / (ms_bwd / 1e3) / 1e12}
+
+    # ---- e2e: host buffers through the C ABI, H2D/D2H inside the timed region
+    e2e = None
+    if not a.no_e2e:
+        Sh = QPSolver(B, n, m, p, shared=shared, device=local, mem="host")
+        hdata = [torch.from_numpy(np.ascontiguousarray(getattr(batch, f)[0] if f in shared else getattr(batch, f)))
+                 .pin_memory() for f in FIELDS]
+        hdl = torch.from_numpy(batch.dl_dx).pin_memory()
+
+        def hstep():
+            o = Sh.solve(*hdata)
+            gg = Sh.backward(hdl)
+            if shared:
+                dd = {k: v.to(dev) for k, v in gg.items() if k in ("dQ", "dq", "dA", "db", "dG", "dh")}
+                D.allreduce_shared_grads(dd, shared)
+            return o, gg
+
+        for _ in range(max(1, a.warmup)):
+            hstep()
+        torch.cuda.synchronize(dev)
+        D.barrier()
+        h_ms = 0.0
+        for _ in range(a.steps):
+            flush.fill_(1.0)
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(torch.cuda.default_stream(dev))
+            o, gg = hstep()
+            e1.record(torch.cuda.default_stream(dev))
+            e1.synchronize()
+            h_ms += e0.elapsed_time(e1)
+        h_ms = D.max_over_ranks(h_ms, dev)
+        per, sh = FL.data_bytes(n, m, p, shared)
+        h2d = B * per + sh + B * n * 4
+        d2h = sum(int(v.numel() * v.element_size()) for v in o.values()) + \
+            sum(int(v.numel() * v.element_size()) for v in gg.values())
+        e2e = {"value": B * world * a.steps / (h_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": h_ms / a.steps}
+        Sh.close()
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        rate, cores, ns, dt = oracle_rate(a.config, a.cpu_seconds, B)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"first {ns} problems of {c['name']} ({dt:.1f} s): f64 oracle (Eq. 14 + GEPP), "
+                         f"init + Alg. 1 + Alg. 2 + Alg. 3, std::thread over problems"}
+
+    clocks = clk.summary()
+    if rank == 0:
+        res = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+               "warmup": a.warmup, "ms_per_step": total_ms / a.steps, "higher_is_better": True, "scaling": "weak",
+               "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+               "config": {"workload": c["name"], "batch_per_gpu": B, "global_batch": B * world, "n": n, "m_eq": m,
+                          "p": p, "shared": shared, "parallelism": f"dp{world} (batch sharded, no collective"
+                          + (", shared-grad all-reduce" if shared else "") + ")",
+                          "l2": "flushed between timed steps (256 MiB write outside the events)",
+                          "tol": S.cfg.tol, "kappa_relax": S.cfg.kappa_relax, "sigma": S.cfg.sigma},
+               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+               "gpu_launches": a.steps * (info["launches_solve"] + info["launches_backward"]),
+               "clocks": clocks,
+               "solver": {"converged": int((status == 0).sum()), "grad_ok": int((gstatus == 0).sum()),
+                          "iters_mean": float(iters.mean()), "iters_max": int(iters.max()),
+                          "relax_iters_mean": float(riters.mean()), "kernel_info": info}}
+        print(json.dumps(res), flush=True)
+    S.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,146 @@
+/*
+ * qpb200.h — C ABI of the B200 (sm_100a) batched f32 interior-point QP solver
+ * with implicit (spectrally bounded) complementarity, arxiv 2605.17913.
+ *
+ * Citations: "P:L" = PAPER.md line L (section / equation / algorithm given),
+ * "S:L" = SPEC.md line L, "Qn" = a reading of the paper listed in DESIGN.md §2.
+ *
+ * The library solves, for every problem b of a batch, the QP of Eq. 1-2
+ *
+ *      minimize ½ xᵀQx + qᵀx   s.t.  A x = b,  G x ≤ h   (x ∈ ℝⁿ, A: m×n, G: p×n)
+ * with Algorithm 1, and differentiates the solution with
+ * Algorithm 2 (relaxation to κ_relax) followed by Algorithm 3
+ * (implicit-function-theorem gradients; sign reading Q7).
+ *
+ * Memory and layout (all entry points):
+ *   - f32, batch-major, row-major, contiguous: Q[B][n][n], q[B][n], A[B][m][n],
+ *     b[B][m], G[B][p][n], h[B][p].  The batch stride of each data tensor is
+ *     given in qp_dims (in elements); a stride of 0 marks a tensor SHARED by
+ *     all problems of the batch (end-to-end learning, BASELINE config 4).
+ *   - Q must be symmetric (Q ∈ 𝕊ⁿ₊).  It is not symmetrised.
+ *   - Pointers must be 4-byte aligned (QP_ERR_ALIGN otherwise).
+ *   - qp_config.mem_kind == QP_MEM_DEVICE: every pointer is device memory of
+ *     the ctx's device; calls are asynchronous and stream-ordered on the ctx
+ *     stream; the caller synchronises.  QP_MEM_HOST: every pointer is host
+ *     memory (ideally pinned); the library copies in and out through its own
+ *     device staging buffers and the call returns after the results are back
+ *     in host memory.
+ *   - All buffers are caller-owned.  The ctx owns its workspaces only.
+ *   - qp_backward_batched reuses the problem data and the solution of the
+ *     LAST qp_solve_batched call on the same ctx: with QP_MEM_DEVICE the
+ *     caller must keep Q…h and x, s, z, y alive and unmodified in between
+ *     (autograd saved-tensor semantics); with QP_MEM_HOST the ctx keeps device
+ *     copies itself.
+ *
+ * Errors: an API-level qp_err return covers argument, shape and CUDA errors.
+ * The numerical outcome is per problem in status[] and never aborts a call
+ * (S:262): a failed problem keeps its last finite iterate, its gradients are
+ * zero-filled and its status says why.
+ */
+#ifndef QPB200_H
+#define QPB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  QP_OK = 0,
+  QP_ERR_INVALID_ARG = -1,  /* null pointer where required, bad config value   */
+  QP_ERR_SHAPE = -2,        /* n < 1, negative m/p, or n+p+m beyond the kernels */
+  QP_ERR_ALIGN = -3,        /* pointer not 4-byte aligned                        */
+  QP_ERR_CUDA = -4,         /* a CUDA runtime call failed                        */
+  QP_ERR_OOM = -5,          /* workspace allocation failed                       */
+  QP_ERR_NOT_SOLVED = -6,   /* backward before any solve on this ctx             */
+  QP_ERR_UNSUPPORTED = -7   /* option not available for this size / formulation */
+} qp_err;
+
+/* Per-problem status (low byte; numbers mirror S:484) and failure stage
+ * (bits 8..15; the Table 1 categories of P:1009-1013). */
+enum { QP_CONVERGED = 0, QP_MAX_ITER = 2, QP_NUMERICAL_FAILURE = 3 };
+enum {
+  QP_STAGE_NONE = 0, QP_STAGE_SCALING = 1, QP_STAGE_PREDICTOR = 2, QP_STAGE_CENTERING = 3,
+  QP_STAGE_CORRECTOR = 4, QP_STAGE_LINESEARCH = 5, QP_STAGE_RELAX = 6, QP_STAGE_BACKWARD = 7,
+  QP_STAGE_INIT = 8
+};
+
+enum { QP_IMPLICIT = 0, QP_EXPLICIT = 1 };   /* formulation: Eq. 14 or Eq. 8 */
+enum { QP_MEM_DEVICE = 0, QP_MEM_HOST = 1 };
+
+typedef struct {
+  int32_t batch;   /* B ≥ 1                                                     */
+  int32_t n;       /* variables, ≥ 1                                            */
+  int32_t m_eq;    /* equality constraints, ≥ 0                         */
+  int32_t p;       /* inequality constraints, ≥ 0                               */
+  int64_t bstride_Q, bstride_q, bstride_A, bstride_b, bstride_G, bstride_h; /* elements; 0 = shared */
+} qp_dims;
+
+typedef struct {
+  float tol;              /* relative residual + gap tolerance (Q4); default 1e-5          */
+  int32_t max_iter;       /* Alg. 1 iterations; default 100                        */
+  float sigma;            /* κ_target = σκ (Q2); default 0.1                        */
+  float tau;              /* α = min(1, τ·α_max) (Eq. 6 + Q3); default 0.99                */
+  float kappa_relax;      /* Alg. 2 target; default 1e-4                           */
+  float relax_ktol;       /* |κ/κ_relax − 1| tolerance (Q5); default 1e-4                  */
+  int32_t relax_max_iter; /* Alg. 2 iterations (Q22); default 50                           */
+  int32_t formulation;    /* QP_IMPLICIT (default) | QP_EXPLICIT (config-3 standard arm)   */
+  float pivot_floor_rel;  /* LDLᵀ pivot floor θ = rel·max|diag| (Q12); default √ε_f32     */
+  int32_t mem_kind;       /* QP_MEM_DEVICE (default) | QP_MEM_HOST                         */
+} qp_config;
+
+typedef struct qp_ctx qp_ctx;
+
+typedef struct {
+  int32_t path;            /* 1 = CTA-per-QP smem-resident kernel                          */
+  int32_t threads;         /* threads per CTA                                              */
+  int32_t smem_bytes;      /* dynamic shared memory per CTA                                */
+  int32_t ctas_per_sm;     /* occupancy of the chosen kernel                               */
+  int32_t kkt_dim;         /* N = n4 + p + m (n4 = n rounded up to 4)                      */
+  int32_t launches_solve;  /* kernel launches per qp_solve_batched                         */
+  int32_t launches_backward;
+  int64_t workspace_bytes;
+} qp_info;
+
+/* Fill *cfg with the defaults listed above. */
+qp_err qp_config_default(qp_config* cfg);
+
+/* Create a solver context for fixed dims/config on CUDA device `device`,
+ * issuing work on `stream` (a cudaStream_t; NULL = legacy default stream).
+ * Fails with QP_ERR_SHAPE if n+p+m exceeds what the kernels support
+ * (qp_max_kkt_dim). */
+qp_err qp_create(qp_ctx** ctx, const qp_dims* dims, const qp_config* cfg, int device, void* stream);
+qp_err qp_set_stream(qp_ctx* ctx, void* stream);
+qp_err qp_get_info(const qp_ctx* ctx, qp_info* info);
+int32_t qp_max_kkt_dim(int32_t formulation);
+
+/* Algorithm 1 on every problem: CVXOPT initialisation (Q11)
+ * then Newton steps on the implicit partially condensed system Eq. 14
+ * until the relative test of Q4 holds or max_iter.
+ * Outputs (caller-owned, [B][·]): x[n], s[p], z[p], y[m]; iters = Newton
+ * steps taken; status per problem (see enum).  x is Alg. 1's x* (κ → 0), not
+ * the relaxed point (Q14). */
+qp_err qp_solve_batched(qp_ctx* ctx, const float* Q, const float* q, const float* A, const float* b,
+                        const float* G, const float* h, float* x, float* s, float* z, float* y,
+                        int32_t* iters, int32_t* status);
+
+/* Algorithm 2 (relax to κ_relax, exact Newton, factor-then-check: Q5, Q6)
+ * followed by Algorithm 3: solve the bounded KKT system with
+ * right-hand side (−∇ₓℓ, 0, 0) using the relaxed factorisation (Q7), dz =
+ * d₊⊙dv (Q8), then ∇Q = ½(dx xᵀ + x dxᵀ), ∇q = dx, ∇A = dy xᵀ + y dxᵀ,
+ * ∇b = −dy, ∇G = dz xᵀ + z dxᵀ, ∇h = −dz at the relaxed (x, y, z).
+ * dl_dx: [B][n].  Gradient outputs have the batch layout of the matching
+ * input: for a shared input (stride 0) the gradient is the BATCH SUM, a single
+ * [n][n] / [n] / [m][n] / [m] / [p][n] / [p] array.  Any gradient pointer may be
+ * NULL to skip it.  relax_iters/status: per problem (may be NULL). */
+qp_err qp_backward_batched(qp_ctx* ctx, const float* dl_dx, float* dQ, float* dq, float* dA, float* db,
+                           float* dG, float* dh, int32_t* relax_iters, int32_t* status);
+
+qp_err qp_destroy(qp_ctx* ctx);
+const char* qp_error_string(qp_err err);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QPB200_H */

@@ -1,0 +1,397 @@
+// qpb200.cu — host side of the C ABI declared in include/qpb200.h: context,
+// validation, workspace management, dispatch and stream-ordered launches.
+// Every step of the hot path runs in the kernels of ipm_kernels.cuh; this file
+// only marshals.  There is no CPU fallback: without a CUDA device every entry
+// point returns QP_ERR_CUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <new>
+
+#include "../../include/qpb200.h"
+#include "ipm_kernels.cuh"
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr size_t kMaxSmem = 232448;  // 227 KB opt-in dynamic shared memory per CTA (sm_100a)
+
+struct Layout {
+  int n4, nw, N, N4, ld;
+  size_t smem;
+};
+
+Layout make_layout(int n, int m, int p, int formulation) {
+  Layout L;
+  L.n4 = (n + 3) & ~3;
+  L.nw = formulation == QP_IMPLICIT ? p : 0;
+  L.N = L.n4 + L.nw + m;
+  L.N4 = (L.N + 3) & ~3;
+  L.ld = L.N4;
+  if (((L.ld >> 2) & 1) == 0) L.ld += 4;  // ld/4 odd: conflict-free 16-byte row accesses
+  L.smem = qpb::ipm_smem_bytes(L.n4, m, p, L.N4, L.ld);
+  return L;
+}
+
+bool aligned4(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 3u) == 0; }
+
+}  // namespace
+
+struct qp_ctx {
+  qp_dims d;
+  qp_config c;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  Layout L{};
+  int ctas_per_sm = 0;
+  bool solved = false;
+  // pointers of the last solve (device memory)
+  const float *Q = nullptr, *q = nullptr, *A = nullptr, *b = nullptr, *G = nullptr, *h = nullptr;
+  float *x = nullptr, *s = nullptr, *z = nullptr, *y = nullptr;
+  int32_t* status = nullptr;
+  // owned device buffers
+  int32_t* own_status = nullptr;  // forward status (kept for backward)
+  float *wx = nullptr, *wy = nullptr, *wz = nullptr, *wdx = nullptr, *wdy = nullptr, *wdz = nullptr;
+  // host-memory mode staging
+  float *dQ_ = nullptr, *dq_ = nullptr, *dA_ = nullptr, *db_ = nullptr, *dG_ = nullptr, *dh_ = nullptr;
+  float *dx_ = nullptr, *ds_ = nullptr, *dz_ = nullptr, *dy_ = nullptr, *ddl_ = nullptr;
+  int32_t *dit_ = nullptr, *dst_ = nullptr;
+  float *gQ_ = nullptr, *gq_ = nullptr, *gA_ = nullptr, *gb_ = nullptr, *gG_ = nullptr, *gh_ = nullptr;
+  int64_t workspace = 0;
+};
+
+namespace {
+
+qp_err cuda_ok(cudaError_t e) { return e == cudaSuccess ? QP_OK : QP_ERR_CUDA; }
+
+template <typename T>
+qp_err dalloc(qp_ctx* c, T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) return QP_OK;
+  if (cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T)) != cudaSuccess) return QP_ERR_OOM;
+  c->workspace += (int64_t)(count * sizeof(T));
+  return QP_OK;
+}
+
+size_t field_elems(int64_t stride, int32_t B, size_t per) { return stride == 0 ? per : (size_t)B * per; }
+
+void free_all(qp_ctx* c) {
+  void* ptrs[] = {c->own_status, c->wx, c->wy, c->wz, c->wdx, c->wdy, c->wdz, c->dQ_, c->dq_, c->dA_, c->db_,
+                  c->dG_, c->dh_, c->dx_, c->ds_, c->dz_, c->dy_, c->ddl_, c->dit_, c->dst_, c->gQ_, c->gq_,
+                  c->gA_, c->gb_, c->gG_, c->gh_};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+}
+
+bool any_shared(const qp_dims& d) {
+  return d.bstride_Q == 0 || d.bstride_q == 0 || d.bstride_A == 0 || d.bstride_b == 0 || d.bstride_G == 0 ||
+         d.bstride_h == 0;
+}
+
+qpb::Args base_args(const qp_ctx* c) {
+  qpb::Args a;
+  std::memset(&a, 0, sizeof(a));
+  a.B = c->d.batch; a.n = c->d.n; a.m = c->d.m_eq; a.p = c->d.p;
+  a.n4 = c->L.n4; a.nw = c->L.nw; a.N = c->L.N; a.N4 = c->L.N4; a.ld = c->L.ld;
+  a.sQ = c->d.bstride_Q; a.sq = c->d.bstride_q; a.sA = c->d.bstride_A;
+  a.sb = c->d.bstride_b; a.sG = c->d.bstride_G; a.sh = c->d.bstride_h;
+  a.tol = c->c.tol; a.sigma = c->c.sigma; a.tau = c->c.tau; a.kappa_relax = c->c.kappa_relax;
+  a.relax_ktol = c->c.relax_ktol; a.floor_rel = c->c.pivot_floor_rel;
+  a.max_iter = c->c.max_iter; a.relax_max_iter = c->c.relax_max_iter;
+  return a;
+}
+
+// m = 0 / p = 0 tensors may legitimately be NULL: point them at a dummy.
+__device__ float g_dummy[4];
+
+const float* nz(const float* p) {
+  if (p) return p;
+  void* d = nullptr;
+  cudaGetSymbolAddress(&d, g_dummy);
+  return static_cast<const float*>(d);
+}
+
+static qp_err h2d(qp_ctx* c, float* dst, const float* src, size_t count) {
+  if (count == 0 || !src) return QP_OK;
+  return cuda_ok(cudaMemcpyAsync(dst, src, count * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+}
+template <typename T>
+static qp_err d2h(qp_ctx* c, T* dst, const T* src, size_t count) {
+  if (count == 0 || !dst) return QP_OK;
+  return cuda_ok(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+}
+
+}  // namespace
+
+extern "C" {
+
+qp_err qp_config_default(qp_config* cfg) {
+  if (!cfg) return QP_ERR_INVALID_ARG;
+  cfg->tol = 1e-5f;
+  cfg->max_iter = 100;
+  cfg->sigma = 0.1f;
+  cfg->tau = 0.99f;
+  cfg->kappa_relax = 1e-4f;
+  cfg->relax_ktol = 1e-4f;
+  cfg->relax_max_iter = 50;
+  cfg->formulation = QP_IMPLICIT;
+  cfg->pivot_floor_rel = 3.4526698e-4f;  // sqrt(FLT_EPSILON)
+  cfg->mem_kind = QP_MEM_DEVICE;
+  return QP_OK;
+}
+
+int32_t qp_max_kkt_dim(int32_t formulation) {
+  (void)formulation;
+  // largest N4 whose CTA footprint fits in 227 KB with the vector segments of
+  // a balanced problem; qp_create does the exact check.
+  return 232;
+}
+
+const char* qp_error_string(qp_err e) {
+  switch (e) {
+    case QP_OK: return "ok";
+    case QP_ERR_INVALID_ARG: return "invalid argument";
+    case QP_ERR_SHAPE: return "unsupported shape";
+    case QP_ERR_ALIGN: return "pointer not 4-byte aligned";
+    case QP_ERR_CUDA: return "CUDA error";
+    case QP_ERR_OOM: return "out of device memory";
+    case QP_ERR_NOT_SOLVED: return "backward called before solve";
+    case QP_ERR_UNSUPPORTED: return "unsupported option";
+  }
+  return "unknown error";
+}
+
+qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int device, void* stream) {
+  if (!out || !d) return QP_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (d->batch < 1 || d->n < 1 || d->m_eq < 0 || d->p < 0) return QP_ERR_SHAPE;
+  qp_config c;
+  if (cfg) c = *cfg; else qp_config_default(&c);
+  if (!(c.tol > 0.f) || c.max_iter < 0 || !(c.sigma > 0.f && c.sigma < 1.f) || !(c.tau > 0.f && c.tau <= 1.f) ||
+      !(c.kappa_relax > 0.f) || !(c.relax_ktol > 0.f) || c.relax_max_iter < 0 || !(c.pivot_floor_rel >= 0.f) ||
+      (c.formulation != QP_IMPLICIT && c.formulation != QP_EXPLICIT) ||
+      (c.mem_kind != QP_MEM_DEVICE && c.mem_kind != QP_MEM_HOST))
+    return QP_ERR_INVALID_ARG;
+  if (c.formulation == QP_EXPLICIT) return QP_ERR_UNSUPPORTED;  // standard arm: see qp_explicit.cu (next)
+  const int64_t strides[6] = {d->bstride_Q, d->bstride_q, d->bstride_A, d->bstride_b, d->bstride_G, d->bstride_h};
+  const int64_t need[6] = {(int64_t)d->n * d->n, d->n, (int64_t)d->m_eq * d->n, d->m_eq, (int64_t)d->p * d->n,
+                           d->p};
+  for (int i = 0; i < 6; ++i)
+    if (strides[i] != 0 && strides[i] < need[i]) return QP_ERR_SHAPE;
+  Layout L = make_layout(d->n, d->m_eq, d->p, c.formulation);
+  if (L.smem > kMaxSmem) return QP_ERR_SHAPE;  // large-N path not in this build
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) return QP_ERR_CUDA;
+  if (cudaSetDevice(device) != cudaSuccess) return QP_ERR_CUDA;
+  qp_ctx* ctx = new (std::nothrow) qp_ctx();
+  if (!ctx) return QP_ERR_OOM;
+  ctx->d = *d; ctx->c = c; ctx->device = device; ctx->stream = static_cast<cudaStream_t>(stream); ctx->L = L;
+  qp_err e = QP_OK;
+  if (cudaFuncSetAttribute(qpb::ipm_solve_kernel<kThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)L.smem) != cudaSuccess ||
+      cudaFuncSetAttribute(qpb::ipm_backward_kernel<kThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)L.smem) != cudaSuccess) {
+    delete ctx;
+    return QP_ERR_CUDA;
+  }
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->ctas_per_sm, qpb::ipm_solve_kernel<kThreads>, kThreads,
+                                                L.smem);
+  const int B = d->batch, n = d->n, m = d->m_eq, p = d->p;
+  if ((e = dalloc(ctx, &ctx->own_status, B)) != QP_OK) { free_all(ctx); delete ctx; return e; }
+  if (any_shared(*d)) {
+    if ((e = dalloc(ctx, &ctx->wx, (size_t)B * n)) || (e = dalloc(ctx, &ctx->wdx, (size_t)B * n)) ||
+        (e = dalloc(ctx, &ctx->wy, (size_t)B * m)) || (e = dalloc(ctx, &ctx->wdy, (size_t)B * m)) ||
+        (e = dalloc(ctx, &ctx->wz, (size_t)B * p)) || (e = dalloc(ctx, &ctx->wdz, (size_t)B * p))) {
+      free_all(ctx); delete ctx; return e;
+    }
+  }
+  if (c.mem_kind == QP_MEM_HOST) {
+    if ((e = dalloc(ctx, &ctx->dQ_, field_elems(d->bstride_Q, B, (size_t)n * n))) ||
+        (e = dalloc(ctx, &ctx->dq_, field_elems(d->bstride_q, B, n))) ||
+        (e = dalloc(ctx, &ctx->dA_, field_elems(d->bstride_A, B, (size_t)m * n))) ||
+        (e = dalloc(ctx, &ctx->db_, field_elems(d->bstride_b, B, m))) ||
+        (e = dalloc(ctx, &ctx->dG_, field_elems(d->bstride_G, B, (size_t)p * n))) ||
+        (e = dalloc(ctx, &ctx->dh_, field_elems(d->bstride_h, B, p))) ||
+        (e = dalloc(ctx, &ctx->dx_, (size_t)B * n)) || (e = dalloc(ctx, &ctx->ds_, (size_t)B * p)) ||
+        (e = dalloc(ctx, &ctx->dz_, (size_t)B * p)) || (e = dalloc(ctx, &ctx->dy_, (size_t)B * m)) ||
+        (e = dalloc(ctx, &ctx->ddl_, (size_t)B * n)) || (e = dalloc(ctx, &ctx->dit_, B)) ||
+        (e = dalloc(ctx, &ctx->dst_, B)) ||
+        (e = dalloc(ctx, &ctx->gQ_, field_elems(d->bstride_Q, B, (size_t)n * n))) ||
+        (e = dalloc(ctx, &ctx->gq_, field_elems(d->bstride_q, B, n))) ||
+        (e = dalloc(ctx, &ctx->gA_, field_elems(d->bstride_A, B, (size_t)m * n))) ||
+        (e = dalloc(ctx, &ctx->gb_, field_elems(d->bstride_b, B, m))) ||
+        (e = dalloc(ctx, &ctx->gG_, field_elems(d->bstride_G, B, (size_t)p * n))) ||
+        (e = dalloc(ctx, &ctx->gh_, field_elems(d->bstride_h, B, p)))) {
+      free_all(ctx); delete ctx; return e;
+    }
+  }
+  *out = ctx;
+  return QP_OK;
+}
+
+qp_err qp_set_stream(qp_ctx* c, void* stream) {
+  if (!c) return QP_ERR_INVALID_ARG;
+  c->stream = static_cast<cudaStream_t>(stream);
+  return QP_OK;
+}
+
+qp_err qp_get_info(const qp_ctx* c, qp_info* info) {
+  if (!c || !info) return QP_ERR_INVALID_ARG;
+  info->path = 1;
+  info->threads = kThreads;
+  info->smem_bytes = (int32_t)c->L.smem;
+  info->ctas_per_sm = c->ctas_per_sm;
+  info->kkt_dim = c->L.N;
+  info->launches_solve = 1;
+  const qp_dims& d = c->d;
+  int extra = 0;
+  if (d.bstride_Q == 0) ++extra;
+  if (d.bstride_q == 0) ++extra;
+  if (d.bstride_A == 0 && d.m_eq > 0) ++extra;
+  if (d.bstride_b == 0 && d.m_eq > 0) ++extra;
+  if (d.bstride_G == 0 && d.p > 0) ++extra;
+  if (d.bstride_h == 0 && d.p > 0) ++extra;
+  info->launches_backward = 1 + extra;
+  info->workspace_bytes = c->workspace;
+  return QP_OK;
+}
+
+qp_err qp_solve_batched(qp_ctx* c, const float* Q, const float* q, const float* A, const float* b, const float* G,
+                        const float* h, float* x, float* s, float* z, float* y, int32_t* iters, int32_t* status) {
+  if (!c) return QP_ERR_INVALID_ARG;
+  const qp_dims& d = c->d;
+  const int B = d.batch, n = d.n, m = d.m_eq, p = d.p;
+  if (!Q || !q || !x || !iters || !status || (m > 0 && (!A || !b || !y)) || (p > 0 && (!G || !h || !s || !z)))
+    return QP_ERR_INVALID_ARG;
+  const void* ptrs[] = {Q, q, A, b, G, h, x, s, z, y, iters, status};
+  for (const void* pp : ptrs)
+    if (pp && !aligned4(pp)) return QP_ERR_ALIGN;
+  if (cudaSetDevice(c->device) != cudaSuccess) return QP_ERR_CUDA;
+  qp_err e;
+  const bool host = c->c.mem_kind == QP_MEM_HOST;
+  if (host) {
+    if ((e = h2d(c, c->dQ_, Q, field_elems(d.bstride_Q, B, (size_t)n * n))) ||
+        (e = h2d(c, c->dq_, q, field_elems(d.bstride_q, B, n))) ||
+        (e = h2d(c, c->dA_, A, field_elems(d.bstride_A, B, (size_t)m * n))) ||
+        (e = h2d(c, c->db_, b, field_elems(d.bstride_b, B, m))) ||
+        (e = h2d(c, c->dG_, G, field_elems(d.bstride_G, B, (size_t)p * n))) ||
+        (e = h2d(c, c->dh_, h, field_elems(d.bstride_h, B, p))))
+      return e;
+    c->Q = c->dQ_; c->q = c->dq_; c->A = c->dA_; c->b = c->db_; c->G = c->dG_; c->h = c->dh_;
+    c->x = c->dx_; c->s = c->ds_; c->z = c->dz_; c->y = c->dy_;
+  } else {
+    c->Q = Q; c->q = q; c->A = A; c->b = b; c->G = G; c->h = h;
+    c->x = x; c->s = s; c->z = z; c->y = y;
+  }
+  qpb::Args a = base_args(c);
+  a.Q = nz(c->Q); a.q = nz(c->q); a.A = nz(c->A); a.b = nz(c->b); a.G = nz(c->G); a.h = nz(c->h);
+  float* dummy = const_cast<float*>(nz(nullptr));
+  a.x = c->x; a.y = c->y ? c->y : dummy; a.z = c->z ? c->z : dummy; a.s = c->s ? c->s : dummy;
+  a.iters = host ? c->dit_ : iters;
+  a.status = c->own_status;
+  qpb::ipm_solve_kernel<kThreads><<<B, kThreads, c->L.smem, c->stream>>>(a);
+  if ((e = cuda_ok(cudaGetLastError())) != QP_OK) return e;
+  if (host) {
+    if ((e = d2h(c, x, c->dx_, (size_t)B * n)) || (e = d2h(c, s, c->ds_, (size_t)B * p)) ||
+        (e = d2h(c, z, c->dz_, (size_t)B * p)) || (e = d2h(c, y, c->dy_, (size_t)B * m)) ||
+        (e = d2h(c, iters, c->dit_, (size_t)B)) || (e = d2h(c, status, c->own_status, (size_t)B)))
+      return e;
+    if ((e = cuda_ok(cudaStreamSynchronize(c->stream))) != QP_OK) return e;
+  } else {
+    if ((e = cuda_ok(cudaMemcpyAsync(status, c->own_status, sizeof(int32_t) * B, cudaMemcpyDeviceToDevice,
+                                     c->stream))) != QP_OK)
+      return e;
+  }
+  c->solved = true;
+  return QP_OK;
+}
+
+qp_err qp_backward_batched(qp_ctx* c, const float* dl_dx, float* dQ, float* dq, float* dA, float* db, float* dG,
+                           float* dh, int32_t* relax_iters, int32_t* status) {
+  if (!c || !dl_dx) return QP_ERR_INVALID_ARG;
+  if (!c->solved) return QP_ERR_NOT_SOLVED;
+  const void* ptrs[] = {dl_dx, dQ, dq, dA, db, dG, dh, relax_iters, status};
+  for (const void* pp : ptrs)
+    if (pp && !aligned4(pp)) return QP_ERR_ALIGN;
+  if (cudaSetDevice(c->device) != cudaSuccess) return QP_ERR_CUDA;
+  const qp_dims& d = c->d;
+  const int B = d.batch, n = d.n, m = d.m_eq, p = d.p;
+  const bool host = c->c.mem_kind == QP_MEM_HOST;
+  qp_err e;
+  const float* dl = dl_dx;
+  float *oQ = dQ, *oq = dq, *oA = dA, *ob = db, *oG = dG, *oh = dh;
+  int32_t *oit = relax_iters, *ost = status;
+  if (host) {
+    if ((e = h2d(c, c->ddl_, dl_dx, (size_t)B * n)) != QP_OK) return e;
+    dl = c->ddl_;
+    oQ = dQ ? c->gQ_ : nullptr; oq = dq ? c->gq_ : nullptr; oA = dA ? c->gA_ : nullptr;
+    ob = db ? c->gb_ : nullptr; oG = dG ? c->gG_ : nullptr; oh = dh ? c->gh_ : nullptr;
+    oit = c->dit_; ost = c->dst_;
+  }
+  qpb::Args a = base_args(c);
+  a.Q = nz(c->Q); a.q = nz(c->q); a.A = nz(c->A); a.b = nz(c->b); a.G = nz(c->G); a.h = nz(c->h);
+  float* dummy = const_cast<float*>(nz(nullptr));
+  a.x = c->x; a.y = c->y ? c->y : dummy; a.z = c->z ? c->z : dummy; a.s = c->s ? c->s : dummy;
+  a.status = c->own_status;
+  a.dl = dl;
+  // per-problem gradients for non-shared fields; shared fields via batch sums
+  a.gQ = d.bstride_Q ? oQ : nullptr;
+  a.gq = d.bstride_q ? oq : nullptr;
+  a.gA = (d.bstride_A && m > 0) ? oA : nullptr;
+  a.gb = (d.bstride_b && m > 0) ? ob : nullptr;
+  a.gG = (d.bstride_G && p > 0) ? oG : nullptr;
+  a.gh = (d.bstride_h && p > 0) ? oh : nullptr;
+  const bool shared = any_shared(d);
+  if (shared) {
+    a.wx = c->wx; a.wdx = c->wdx;
+    a.wy = m ? c->wy : dummy; a.wdy = m ? c->wdy : dummy;
+    a.wz = p ? c->wz : dummy; a.wdz = p ? c->wdz : dummy;
+  }
+  a.riters = oit;
+  a.rstatus = ost;
+  qpb::ipm_backward_kernel<kThreads><<<B, kThreads, c->L.smem, c->stream>>>(a);
+  if ((e = cuda_ok(cudaGetLastError())) != QP_OK) return e;
+  if (shared) {
+    auto osum = [&](float* out, const float* U, const float* V, const float* U2, const float* V2, int R, int Cc,
+                    float scale) {
+      dim3 grid((Cc + 63) / 64, (R + 63) / 64);
+      qpb::outer_sum_kernel<<<grid, 256, 0, c->stream>>>(U, V, U2, V2, B, R, Cc, scale, out);
+    };
+    auto csum = [&](float* out, const float* U, int Cc, float scale) {
+      qpb::col_sum_kernel<<<(Cc + 255) / 256, 256, 0, c->stream>>>(U, B, Cc, scale, out);
+    };
+    if (d.bstride_Q == 0 && oQ) osum(oQ, c->wdx, c->wx, c->wx, c->wdx, n, n, 0.5f);
+    if (d.bstride_q == 0 && oq) csum(oq, c->wdx, n, 1.f);
+    if (d.bstride_A == 0 && oA && m > 0) osum(oA, c->wdy, c->wx, c->wy, c->wdx, m, n, 1.f);
+    if (d.bstride_b == 0 && ob && m > 0) csum(ob, c->wdy, m, -1.f);
+    if (d.bstride_G == 0 && oG && p > 0) osum(oG, c->wdz, c->wx, c->wz, c->wdx, p, n, 1.f);
+    if (d.bstride_h == 0 && oh && p > 0) csum(oh, c->wdz, p, -1.f);
+    if ((e = cuda_ok(cudaGetLastError())) != QP_OK) return e;
+  }
+  if (host) {
+    if ((dQ && (e = d2h(c, dQ, c->gQ_, field_elems(d.bstride_Q, B, (size_t)n * n)))) ||
+        (dq && (e = d2h(c, dq, c->gq_, field_elems(d.bstride_q, B, n)))) ||
+        (dA && (e = d2h(c, dA, c->gA_, field_elems(d.bstride_A, B, (size_t)m * n)))) ||
+        (db && (e = d2h(c, db, c->gb_, field_elems(d.bstride_b, B, m)))) ||
+        (dG && (e = d2h(c, dG, c->gG_, field_elems(d.bstride_G, B, (size_t)p * n)))) ||
+        (dh && (e = d2h(c, dh, c->gh_, field_elems(d.bstride_h, B, p)))) ||
+        (relax_iters && (e = d2h(c, relax_iters, c->dit_, (size_t)B))) ||
+        (status && (e = d2h(c, status, c->dst_, (size_t)B))))
+      return e;
+    if ((e = cuda_ok(cudaStreamSynchronize(c->stream))) != QP_OK) return e;
+  }
+  return QP_OK;
+}
+
+qp_err qp_destroy(qp_ctx* c) {
+  if (!c) return QP_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  free_all(c);
+  delete c;
+  return QP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,75 @@
+"""CPU-side checks of the boundary: the C-ABI library builds for sm_100a,
+loads, and exports every symbol include/qpb200.h declares; argument
+validation runs without a GPU; the oracle stays out of the product path."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HDR = os.path.join(ROOT, "include", "qpb200.h")
+
+
+def declared_symbols():
+    src = open(HDR).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[\w]+\*?\s+\*?(qp_\w+)\s*\(", src, flags=re.M)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2605_17913_b200 import _build
+    _build.build()
+    from paper_2605_17913_b200 import capi
+    return capi.load()
+
+
+def test_header_declares_the_boundary():
+    syms = declared_symbols()
+    for s in ("qp_create", "qp_solve_batched", "qp_backward_batched", "qp_destroy", "qp_error_string",
+              "qp_config_default", "qp_get_info", "qp_set_stream", "qp_max_kkt_dim"):
+        assert s in syms, s
+
+
+def test_library_exports_every_declared_symbol(lib):
+    from paper_2605_17913_b200 import _build
+    out = subprocess.run(["nm", "-D", "--defined-only", _build.LIB], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (qp_\w+)", out))
+    for s in declared_symbols():
+        assert s in exported, s
+        assert hasattr(lib, s)
+
+
+def test_sass_is_sm100a(lib):
+    from paper_2605_17913_b200 import _build
+    out = subprocess.run(["cuobjdump", "--list-elf", _build.LIB], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_validation_without_gpu(lib):
+    from paper_2605_17913_b200 import capi
+    cfg = capi.default_config()
+    assert abs(cfg.tol - 1e-5) < 1e-9 and cfg.max_iter == 100 and abs(cfg.sigma - 0.1) < 1e-7
+    h = C.c_void_p()
+    bad = capi.QpDims(0, 5, 0, 3, 25, 5, 0, 0, 15, 3)
+    assert lib.qp_create(C.byref(h), C.byref(bad), C.byref(cfg), 0, None) == -2  # QP_ERR_SHAPE
+    good = capi.QpDims(4, 5, 0, 3, 25, 5, 0, 0, 15, 3)
+    cfg.sigma = 1.5
+    assert lib.qp_create(C.byref(h), C.byref(good), C.byref(cfg), 0, None) == -1  # invalid config
+    cfg = capi.default_config()
+    big = capi.QpDims(4, 1024, 0, 2048, 1024 * 1024, 1024, 0, 0, 2048 * 1024, 2048)
+    assert lib.qp_create(C.byref(h), C.byref(big), C.byref(cfg), 0, None) == -2
+    assert lib.qp_error_string(-4) == b"CUDA error"
+    assert lib.qp_solve_batched(*([None] * 13)) == -1
+    assert lib.qp_backward_batched(*([None] * 10)) == -1
+
+
+def test_product_path_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_2605_17913_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt and "qp_oracle" not in txt, f

@@ -1,0 +1,127 @@
+"""CUDA path (through the C ABI) vs the oracle on seeded workloads shaped like
+BASELINE.json's configs, plus edge cases.  Tolerances: tests/helpers.py."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2605_17913_b200 import generators as gen
+from paper_2605_17913_b200.generators import QPBatch
+
+from .helpers import (GRADS, TOL_GRAD, TOL_RES, TOL_X, rel_err_rows, rel_residuals, run_gpu, shared_sum,
+                      x_rel)
+
+pytestmark = pytest.mark.gpu
+
+
+def check_against_oracle(batch, g, iters_slack=1, grad_tol=TOL_GRAD):
+    r64 = O.solve(batch, O.Cfg.f64(), "f64")
+    r32 = O.solve(batch, O.Cfg.f32(), "f32")
+    assert np.all(r64["status"] == 0)
+    ok32 = r32["status"] == 0
+    # every instance the f32 oracle solves must be solved, without NaN/Inf
+    assert np.all(g["status"][ok32] == 0), (g["status"], r32["status"])
+    for k in ("x", "s", "z", "y"):
+        assert np.all(np.isfinite(g[k][ok32]))
+    res = rel_residuals(batch, g["x"], g["y"], g["z"], g["s"])
+    assert res[ok32].max() <= 2 * TOL_RES, res.max(axis=0)
+    assert x_rel(g["x"], r64["x"])[ok32].max() <= TOL_X
+    d_it = np.abs(g["iters"].astype(int) - r32["iters"].astype(int))
+    assert d_it[ok32].max() <= iters_slack, (g["iters"], r32["iters"])
+    b64 = O.backward(batch, r64, O.Cfg.f64(), "f64")
+    ref = shared_sum(batch, b64)
+    assert np.all(g["grad_status"][ok32] == 0)
+    for k in GRADS:
+        if ref[k].size == 0:
+            continue
+        if ref[k].ndim == g[k].ndim and g[k].shape[0] == batch.batch and not batch.shared.get(k[1:], False):
+            err = rel_err_rows(g[k][ok32], ref[k][ok32])
+            assert err.max() <= grad_tol, (k, err.max())
+        else:
+            err = np.linalg.norm(g[k] - ref[k]) / max(np.linalg.norm(ref[k]), 1e-30)
+            assert err <= grad_tol, (k, err)
+    return dict(r64=r64, r32=r32, iters_equal=float(np.mean(d_it == 0)))
+
+
+def test_cfg1_full_batch():
+    b = gen.make_config(1)
+    g = run_gpu(b)
+    st = check_against_oracle(b, g)
+    assert st["iters_equal"] >= 0.5
+
+
+def test_cfg2_subset_many_tiles():
+    b = gen.make_config(2, batch=96)
+    g = run_gpu(b)
+    check_against_oracle(b, g)
+
+
+def test_cfg3_projection_subset():
+    b = gen.make_config(3, batch=48)
+    g = run_gpu(b)
+    check_against_oracle(b, g)
+
+
+def test_cfg2_full_size_sampled():
+    """Full config-2 batch in the bench launch configuration; the oracle checks
+    a deterministic sample of 24 problems one by one."""
+    b = gen.make_config(2)
+    g = run_gpu(b)
+    assert np.all(g["status"] == 0)
+    idx = np.linspace(0, b.batch - 1, 24).astype(int)
+    sub = b.subset(idx)
+    gs = {k: (v[idx] if isinstance(v, np.ndarray) and v.shape[:1] == (b.batch,) else v) for k, v in g.items()}
+    check_against_oracle(sub, gs)
+
+
+@pytest.mark.parametrize("n,m,p", [(1, 0, 1), (3, 1, 5), (7, 2, 0), (5, 0, 0), (13, 3, 17), (33, 5, 40),
+                                   (62, 1, 70)])
+def test_ragged_shapes(n, m, p):
+    b = gen.g_rand(11, 12, n, m, p)
+    g = run_gpu(b)
+    check_against_oracle(b, g)
+
+
+def test_shared_parameters_batch_sum():
+    """Config-4 structure at a small size: Q, A, b, G, h shared (stride 0);
+    their gradients are batch sums (Alg. 3 summed over the batch)."""
+    b = gen.g_rand_shared(4, 40, 20, 0, 40)
+    g = run_gpu(b)
+    check_against_oracle(b, g)
+
+
+def test_printed_examples_on_gpu():
+    """S:264 projection of (2,0) onto x1 <= 1 and S:283 gradient example."""
+    Q = np.eye(2, dtype=np.float32)[None]
+    b = QPBatch(2, 0, 1, Q, np.array([[-2, 0]], np.float32), np.zeros((1, 0, 2), np.float32),
+                np.zeros((1, 0), np.float32), np.array([[[1, 0]]], np.float32), np.array([[1]], np.float32),
+                np.array([[0, 1]], np.float32), 1)
+    g = run_gpu(b)
+    assert g["status"][0] == 0
+    assert np.allclose(g["x"][0], [1, 0], atol=1e-4)
+    b2 = QPBatch(2, 0, 0, 2 * Q, np.array([[0.3, -0.7]], np.float32), np.zeros((1, 0, 2), np.float32),
+                 np.zeros((1, 0), np.float32), np.zeros((1, 0, 2), np.float32), np.zeros((1, 0), np.float32),
+                 np.array([[2, 0]], np.float32), 1)
+    g2 = run_gpu(b2)
+    assert np.allclose(g2["dq"][0], [-1, 0], atol=1e-6)
+
+
+def test_host_memory_mode_matches_device():
+    b = gen.make_config(1)
+    gd = run_gpu(b)
+    gh = run_gpu(b, mem="host")
+    for k in ("x", "z", "s", "y", "iters", "dQ", "dG", "dh"):
+        assert np.array_equal(gd[k], gh[k]), k
+
+
+def test_deterministic():
+    b = gen.make_config(2, batch=32)
+    g1, g2 = run_gpu(b), run_gpu(b)
+    for k in ("x", "iters", "dG"):
+        assert np.array_equal(g1[k], g2[k]), k
+
+
+def test_zero_cotangent():
+    b = gen.make_config(1)
+    g = run_gpu(b, dl=np.zeros_like(b.dl_dx))
+    for k in GRADS:
+        assert np.abs(g[k]).max(initial=0) == 0

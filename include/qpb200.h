@@ -88,6 +88,8 @@ typedef struct {
   int32_t formulation;    /* QP_IMPLICIT (default) | QP_EXPLICIT (config-3 standard arm)   */
   float pivot_floor_rel;  /* LDLᵀ pivot floor θ = rel·max|diag| (Q12); default √ε_f32     */
   int32_t mem_kind;       /* QP_MEM_DEVICE (default) | QP_MEM_HOST                         */
+  float relax_tol;        /* Alg. 2 residual tolerance (Q5b); default 1e-6; the relax loop */
+                          /* also stops at the f32 floor (φ ≤ tol and no 10% progress)     */
 } qp_config;
 
 typedef struct qp_ctx qp_ctx;

@@ -44,7 +44,7 @@ class OracleCfg(C.Structure):
     _fields_ = [("tol", C.c_double), ("max_iter", C.c_int32), ("sigma", C.c_double),
                 ("tau", C.c_double), ("kappa_relax", C.c_double), ("relax_ktol", C.c_double),
                 ("relax_max_iter", C.c_int32), ("kkt_solver", C.c_int32),
-                ("formulation", C.c_int32), ("pivot_floor_rel", C.c_double)]
+                ("formulation", C.c_int32), ("pivot_floor_rel", C.c_double), ("relax_tol", C.c_double)]
 
 
 @dataclass
@@ -60,10 +60,11 @@ class Cfg:
     kkt_solver: int = SOLVER_M_LDL
     formulation: int = FORM_IMPLICIT
     pivot_floor_rel: float = float(np.sqrt(np.finfo(np.float32).eps))
+    relax_tol: float = 1e-6
 
     @staticmethod
     def f64(**kw) -> "Cfg":
-        base = dict(tol=1e-10, relax_ktol=1e-10, kkt_solver=SOLVER_K14_GEPP,
+        base = dict(tol=1e-10, relax_ktol=1e-10, relax_tol=1e-12, kkt_solver=SOLVER_K14_GEPP,
                     pivot_floor_rel=float(np.sqrt(np.finfo(np.float64).eps)))
         base.update(kw)
         return Cfg(**base)
@@ -75,7 +76,7 @@ class Cfg:
     def c(self) -> OracleCfg:
         return OracleCfg(self.tol, self.max_iter, self.sigma, self.tau, self.kappa_relax,
                          self.relax_ktol, self.relax_max_iter, self.kkt_solver, self.formulation,
-                         self.pivot_floor_rel)
+                         self.pivot_floor_rel, self.relax_tol)
 
 
 def lib():

@@ -54,6 +54,7 @@ typedef struct {
   int32_t kkt_solver;     // orc::SOLVER_*
   int32_t formulation;    // orc::FORM_*
   double pivot_floor_rel; // LDL pivot floor theta = rel*max|diag| (Q12)
+  double relax_tol;       // Alg. 2 residual tolerance (reading Q5b)
 } oracle_cfg;
 }
 
@@ -231,11 +232,27 @@ static void residuals(const Prob<T>& P, const T* x, const T* y, const T* z, cons
   R.obj = T(0.5) * dotp(x, Qx.data(), n) + dotp(P.q, x, n);
 }
 
-// Reading Q4: relative form of Alg. 1's "||r||_inf < tol".
+// Reading Q4: relative form of Alg. 1's "||r||_inf < tol".  phi is the
+// largest of the four relative residuals; feasible <=> phi <= tol.
+template <typename T> static T rel_phi(const Res<T>& R) {
+  auto mx = [](std::initializer_list<T> l) { T r = T(1); for (T v : l) r = std::max(r, v); return r; };
+  T a = R.nrt / mx({R.sQx, R.sq_, R.sGz, R.sAy});
+  T b = R.nre / mx({R.sAx, R.sb});
+  T c = R.nri / mx({R.sGx, R.ss, R.sh});
+  T d = std::max(R.nrz, R.nrs) / mx({R.sz, R.ss});
+  return std::max(std::max(a, b), std::max(c, d));
+}
 template <typename T> static bool feasible_rel(const Res<T>& R, T tol) {
   auto mx = [](std::initializer_list<T> l) { T r = T(1); for (T v : l) r = std::max(r, v); return r; };
   return R.nrt <= tol * mx({R.sQx, R.sq_, R.sGz, R.sAy}) && R.nre <= tol * mx({R.sAx, R.sb}) &&
          R.nri <= tol * mx({R.sGx, R.ss, R.sh}) && std::max(R.nrz, R.nrs) <= tol * mx({R.sz, R.ss});
+}
+// Reading Q5b: Alg. 2 stops when kappa is at kappa_relax and either phi <=
+// relax_tol, or phi <= tol and the last Newton step no longer reduced phi by
+// 10% (the working-precision floor).
+template <typename T> static bool relax_done(const Res<T>& R, T tol, T relax_tol, T phi_prev) {
+  const T phi = rel_phi(R);
+  return phi <= relax_tol || (phi <= tol && phi > T(0.9) * phi_prev);
 }
 template <typename T> static bool converged_solve(const Res<T>& R, T tol) {
   return feasible_rel(R, tol) && R.gap <= tol * std::max(T(1), std::fabs(R.obj));
@@ -468,9 +485,10 @@ static int relax_qp_implicit(const Prob<T>& P, const oracle_cfg& cfg, T* x, T* y
                              Factor<T>& F) {
   const int n = P.n, m = P.m, p = P.p;
   const T tol = T(cfg.tol), tau = T(cfg.tau), kr = T(cfg.kappa_relax), ktol = T(cfg.relax_ktol),
-          fr = T(cfg.pivot_floor_rel);
+          fr = T(cfg.pivot_floor_rel), rtol = T(cfg.relax_tol);
   std::vector<T> v(p), dx(n), dy(m), dz(p), ds(p), dv(p);
   Res<T> R;
+  T phi_prev = std::numeric_limits<T>::infinity();
   for (int k = 0;; ++k) {
     for (int i = 0; i < p; ++i) v[i] = z[i] - s[i];
     T kappa = mean_sz(s, z, p);
@@ -479,7 +497,8 @@ static int relax_qp_implicit(const Prob<T>& P, const oracle_cfg& cfg, T* x, T* y
     *iters = k;
     if (!finite_all(F.dp) || !finite_all(F.dm) || !F.ok) return ST_NUMERICAL_FAILURE | (STG_RELAX << 8);
     bool kok = p == 0 || std::fabs(kappa / kr - T(1)) <= ktol;
-    if (feasible_rel(R, tol) && kok) return ST_CONVERGED;
+    if (kok && relax_done(R, tol, rtol, phi_prev)) return ST_CONVERGED;
+    phi_prev = kok ? rel_phi(R) : std::numeric_limits<T>::infinity();
     if (k == cfg.relax_max_iter) return ST_MAX_ITER | (STG_RELAX << 8);
     T rk = kappa - kr;  // kappa_target = kappa_relax
     T dk;
@@ -667,9 +686,10 @@ static int relax_qp_explicit(const Prob<T>& P, const oracle_cfg& cfg, T* x, T* y
                              XFactor<T>& F) {
   const int n = P.n, m = P.m, p = P.p;
   const T tol = T(cfg.tol), tau = T(cfg.tau), kr = T(cfg.kappa_relax), ktol = T(cfg.relax_ktol),
-          fr = T(cfg.pivot_floor_rel);
+          fr = T(cfg.pivot_floor_rel), rtol = T(cfg.relax_tol);
   std::vector<T> dx(n), dy(m), dz(p), ds(p), rc(p);
   Res<T> R;
+  T phi_prev = std::numeric_limits<T>::infinity();
   for (int k = 0;; ++k) {
     residuals(P, x, y, z, s, T(0), false, R);
     F = factor_explicit(P, z, s, cfg.kkt_solver, fr);
@@ -677,7 +697,8 @@ static int relax_qp_explicit(const Prob<T>& P, const oracle_cfg& cfg, T* x, T* y
     if (!finite_all(F.w) || !F.ok) return ST_NUMERICAL_FAILURE | (STG_RELAX << 8);
     T dev = 0;
     for (int i = 0; i < p; ++i) dev = std::max(dev, std::fabs(z[i] * s[i] / kr - T(1)));
-    if (feasible_rel(R, tol) && dev <= ktol) return ST_CONVERGED;
+    if (dev <= ktol && relax_done(R, tol, rtol, phi_prev)) return ST_CONVERGED;
+    phi_prev = dev <= ktol ? rel_phi(R) : std::numeric_limits<T>::infinity();
     if (k == cfg.relax_max_iter) return ST_MAX_ITER | (STG_RELAX << 8);
     for (int i = 0; i < p; ++i) rc[i] = z[i] * s[i] - kr;
     explicit_direction(P, F, z, s, R.rt.data(), R.re.data(), R.ri.data(), rc.data(), dx.data(), dy.data(),

@@ -28,7 +28,8 @@ class QpDims(C.Structure):
 class QpConfig(C.Structure):
     _fields_ = [("tol", C.c_float), ("max_iter", C.c_int32), ("sigma", C.c_float), ("tau", C.c_float),
                 ("kappa_relax", C.c_float), ("relax_ktol", C.c_float), ("relax_max_iter", C.c_int32),
-                ("formulation", C.c_int32), ("pivot_floor_rel", C.c_float), ("mem_kind", C.c_int32)]
+                ("formulation", C.c_int32), ("pivot_floor_rel", C.c_float), ("mem_kind", C.c_int32),
+                ("relax_tol", C.c_float)]
 
 
 class QpInfo(C.Structure):

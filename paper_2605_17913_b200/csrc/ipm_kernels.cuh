@@ -24,7 +24,7 @@ struct Args {
   float *gQ, *gq, *gA, *gb, *gG, *gh;        // per-problem gradients (nullptr = skip)
   float *wx, *wy, *wz, *wdx, *wdy, *wdz;     // per-problem vectors for shared sums (nullptr = skip)
   int *riters, *rstatus;
-  float tol, sigma, tau, kappa_relax, relax_ktol, floor_rel;
+  float tol, sigma, tau, kappa_relax, relax_ktol, floor_rel, relax_tol;
   int max_iter, relax_max_iter;
 };
 
@@ -279,6 +279,20 @@ __device__ __forceinline__ bool feasible_rel(const Norms& R, float tol) {
   const float sz = fmaxf(1.f, fmaxf(R.sz, R.ss));
   return R.nrt <= tol * st && R.nre <= tol * se && R.nri <= tol * si && R.nrzs <= tol * sz;
 }
+// phi = largest of the four relative residuals (feasible_rel <=> phi <= tol).
+__device__ __forceinline__ float rel_phi(const Norms& R) {
+  const float st = fmaxf(1.f, fmaxf(fmaxf(R.sQx, R.sq), fmaxf(R.sGz, R.sAy)));
+  const float se = fmaxf(1.f, fmaxf(R.sAx, R.sb));
+  const float si = fmaxf(1.f, fmaxf(R.sGx, fmaxf(R.ss, R.sh)));
+  const float sz = fmaxf(1.f, fmaxf(R.sz, R.ss));
+  return fmaxf(fmaxf(R.nrt / st, R.nre / se), fmaxf(R.nri / si, R.nrzs / sz));
+}
+// Reading Q5b: Alg. 2 stops (with κ at κ_relax) when phi <= relax_tol, or
+// phi <= tol and the last Newton step did not reduce phi by 10% (f32 floor).
+__device__ __forceinline__ bool relax_done(const Norms& R, float tol, float relax_tol, float phi_prev) {
+  const float phi = rel_phi(R);
+  return phi <= relax_tol || (phi <= tol && phi > 0.9f * phi_prev);
+}
 __device__ __forceinline__ bool converged_solve(const Norms& R, float tol) {
   return feasible_rel(R, tol) && R.gap <= tol * fmaxf(1.f, fabsf(R.obj));
 }
@@ -447,6 +461,7 @@ __global__ void __launch_bounds__(NT) ipm_backward_kernel(const Args a) {
   int status = (a.status[bid] & 0xff) == ST_CONVERGED ? ST_CONVERGED : (ST_FAIL | (STG_RELAX << 8));
   int it = 0;
   if (status == ST_CONVERGED) {
+    float phi_prev = INFINITY;
     for (int k = 0;; ++k) {
       float kappa = manifold_coords<NT>(S, a);
       const Norms R = residuals<NT>(S, a, P, kappa, kappa - a.kappa_relax);
@@ -455,7 +470,8 @@ __global__ void __launch_bounds__(NT) ipm_backward_kernel(const Args a) {
       it = k;
       if (R.nonfin > 0.f) { status = ST_FAIL | (STG_RELAX << 8); break; }
       const bool kok = p == 0 || fabsf(kappa / a.kappa_relax - 1.f) <= a.relax_ktol;
-      if (feasible_rel(R, a.tol) && kok) break;
+      if (kok && relax_done(R, a.tol, a.relax_tol, phi_prev)) break;
+      phi_prev = kok ? rel_phi(R) : INFINITY;
       if (k == a.relax_max_iter) { status = ST_MAX_ITER | (STG_RELAX << 8); break; }
       solve_qd<NT>(S.K, a.ld, a.N, n4, S.rinv, S.rhs);
       int stage = 0;

@@ -99,7 +99,7 @@ qpb::Args base_args(const qp_ctx* c) {
   a.sQ = c->d.bstride_Q; a.sq = c->d.bstride_q; a.sA = c->d.bstride_A;
   a.sb = c->d.bstride_b; a.sG = c->d.bstride_G; a.sh = c->d.bstride_h;
   a.tol = c->c.tol; a.sigma = c->c.sigma; a.tau = c->c.tau; a.kappa_relax = c->c.kappa_relax;
-  a.relax_ktol = c->c.relax_ktol; a.floor_rel = c->c.pivot_floor_rel;
+  a.relax_ktol = c->c.relax_ktol; a.floor_rel = c->c.pivot_floor_rel; a.relax_tol = c->c.relax_tol;
   a.max_iter = c->c.max_iter; a.relax_max_iter = c->c.relax_max_iter;
   return a;
 }
@@ -140,6 +140,7 @@ qp_err qp_config_default(qp_config* cfg) {
   cfg->formulation = QP_IMPLICIT;
   cfg->pivot_floor_rel = 3.4526698e-4f;  // sqrt(FLT_EPSILON)
   cfg->mem_kind = QP_MEM_DEVICE;
+  cfg->relax_tol = 1e-6f;
   return QP_OK;
 }
 
@@ -171,7 +172,7 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
   qp_config c;
   if (cfg) c = *cfg; else qp_config_default(&c);
   if (!(c.tol > 0.f) || c.max_iter < 0 || !(c.sigma > 0.f && c.sigma < 1.f) || !(c.tau > 0.f && c.tau <= 1.f) ||
-      !(c.kappa_relax > 0.f) || !(c.relax_ktol > 0.f) || c.relax_max_iter < 0 || !(c.pivot_floor_rel >= 0.f) ||
+      !(c.kappa_relax > 0.f) || !(c.relax_ktol > 0.f) || !(c.relax_tol > 0.f) || c.relax_max_iter < 0 || !(c.pivot_floor_rel >= 0.f) ||
       (c.formulation != QP_IMPLICIT && c.formulation != QP_EXPLICIT) ||
       (c.mem_kind != QP_MEM_DEVICE && c.mem_kind != QP_MEM_HOST))
     return QP_ERR_INVALID_ARG;

@@ -2,19 +2,23 @@
 // kernel (one CTA owns one QP; its KKT matrix stays resident in shared memory
 // for the whole of Alg. 1, or of Alg. 2 + Alg. 3).
 //
-// KKT layout: the bounded system of Eq. 14 is
+// KKT matrix: the bounded system of Eq. 14 is
 // factored in its congruent quasi-definite form (reading Q12)
 //       M = [[Q + Gᵀ D₊ G,  Gᵀ D₊,  Aᵀ],
 //            [D₊ G,         −D₋,    0 ],
 //            [A,            0,      0 ]]      unknowns (Δx, w, Δy), Δv = GΔx + w
 // with D₊ = diag(∂b_κ(v)), D₋ = diag(∂b_κ(−v)) ∈ (0,1] (Eq. 11).  Rows/cols:
-//   x-block [0, n4)   (n4 = n rounded up to 4; padded rows are identity)
-//   w-block [n4, n4+nw)
-//   y-block [n4+nw, N)
-// stored row-major, lower triangle, leading dimension ld (ld/4 odd so that
-// 16-byte accesses of 8 consecutive rows hit 8 distinct bank groups).
-// Factorisation: M = L S Lᵀ, S = diag(+1 on the x-block, −1 elsewhere), a
-// "signed Cholesky" that needs no pivoting because M is quasi-definite.
+//   x-block [0, n4)   (n4 = n rounded up to 4; padded rows are +identity)
+//   w-block [n4, n4+nw), y-block [n4+nw, N), padding [N, N4) (−identity).
+// Factorisation M = L S Lᵀ, S = diag(+1 on the x-block, −1 elsewhere): a
+// "signed Cholesky" with no pivoting, valid because M is quasi-definite.
+//
+// Storage: packed lower triangle in 16-row blocks.  Row i of block b = i/16
+// holds columns [0, 16(b+1)) (the whole diagonal block) plus 4 floats of
+// padding, so that every row starts 16-byte aligned and consecutive rows are
+// an ODD number of 16-byte units apart (8 consecutive rows read as float4 hit
+// 8 distinct bank groups).  The last block may be partial (N4 not a multiple
+// of 16).
 #pragma once
 #include <cuda_runtime.h>
 #include <math.h>
@@ -22,7 +26,7 @@
 
 namespace qpb {
 
-constexpr int KB = 16;  // panel width of the blocked factorisation / solves
+constexpr int KB = 16;  // block / panel width
 
 // ------------------------------------------------------------------------
 // Retraction map, App. C, written for f32 on the device.
@@ -44,26 +48,36 @@ __device__ __forceinline__ float ret_db(float v, float k) {
 }
 __device__ __forceinline__ float ret_dk(float v, float k) { return 1.f / sqrtf(v * v + 4.f * k); }
 
-__device__ __forceinline__ int r4(int x) { return (x + 3) & ~3; }
+__host__ __device__ __forceinline__ int r4(int x) { return (x + 3) & ~3; }
 
-// Panel boundaries: width KB, never straddling npos (so the sign is uniform
-// inside a panel).
-__device__ __forceinline__ int panel_end(int k0, int N, int npos) {
-  int k1 = min(k0 + KB, N);
-  if (k0 < npos) k1 = min(k1, npos);
-  return k1;
-}
-__device__ __forceinline__ int last_panel_start(int N, int npos) {
-  if (N > npos) return npos + ((N - 1 - npos) / KB) * KB;
-  return ((N - 1) / KB) * KB;
-}
-__device__ __forceinline__ int prev_panel_start(int k0, int npos) {
-  // panel preceding the one starting at k0 (k0 > 0)
-  if (k0 > npos) return k0 - KB;
-  // k0 == npos (or k0 inside the x-block, which is KB-aligned)
-  if (k0 == npos) return ((npos - 1) / KB) * KB;
-  return k0 - KB;
-}
+// ------------------------------------------------------------------------
+// Packed block layout of the lower triangle.
+// ------------------------------------------------------------------------
+struct KLayout {
+  int N, N4, NB, npos;  // real dim, padded dim (×4), #16-blocks, #positive pivots
+  int wl, Ll, baseL;    // last block: width, row length, offset
+  __host__ __device__ static KLayout make(int N, int npos) {
+    KLayout L;
+    L.N = N;
+    L.N4 = r4(N);
+    L.NB = (L.N4 + KB - 1) / KB;
+    L.npos = npos;
+    L.wl = L.N4 - KB * (L.NB - 1);
+    L.Ll = ((L.N4 >> 2) & 1) ? L.N4 : L.N4 + 4;
+    const int b = L.NB - 1;
+    L.baseL = 128 * b * (b + 1) + 64 * b;
+    return L;
+  }
+  __host__ __device__ int size() const { return baseL + wl * Ll; }
+  __host__ __device__ __forceinline__ int len(int b) const { return b < NB - 1 ? 16 * b + 20 : Ll; }
+  __host__ __device__ __forceinline__ int off(int i) const {
+    const int b = i >> 4, t = i & 15;
+    return b < NB - 1 ? 128 * b * (b + 1) + 64 * b + t * (16 * b + 20) : baseL + t * Ll;
+  }
+  __host__ __device__ __forceinline__ int bw(int b) const { return b < NB - 1 ? KB : wl; }
+};
+
+__device__ __forceinline__ float sgn_of(int k, int npos) { return k < npos ? 1.f : -1.f; }
 
 // ------------------------------------------------------------------------
 // Block reductions: NS sums followed by NM maxima, fixed order (deterministic).
@@ -115,139 +129,211 @@ __device__ __forceinline__ float block_min(float a, float* red) {
 }
 
 // ------------------------------------------------------------------------
-// Signed Cholesky (quasi-definite LDLᵀ) of the N×N lower triangle held in
-// K (leading dimension ld, N4 = r4(N) rows allocated, rows ≥ N zero).
-// Pivots k < npos must be positive, k ≥ npos negative; a pivot on the wrong
-// side of ±θ is replaced by ±θ (reading Q12) and counted.  On exit the lower
-// triangle holds L with M = L S Lᵀ and rinv[k] = 1/L[k][k].
-// Right-looking, panel width KB:
-//   (a) warp 0 factors the kb×kb diagonal block in registers (shuffles);
-//   (b) every thread solves one row of the panel below (TRSM);
-//   (c) the trailing lower triangle takes the rank-kb update (SYRK) in 32×32
-//       super-tiles, 64 threads per super-tile, 4×4 strided register tiles.
-// Returns the number of floored pivots (block-uniform).
+// Diagonal block factorisation by ONE warp: block b (width kb ≤ 16) of the
+// packed matrix.  Lane r holds row r of the block in registers.  Step k: the
+// pivot comes from lane k (its diagonal is already final), column k is
+// scaled, and every lane updates its row; the next pivot only needs lane k+1's
+// own l_{k+1,k}, so the critical chain per step is shfl → rsqrt → mul → fma.
+// Returns the number of floored pivots (valid on every lane).
 // ------------------------------------------------------------------------
-template <int NT>
-__device__ int factor_qd(float* __restrict__ K, const int ld, const int N, const int N4, const int npos,
-                         const float theta, float* __restrict__ rinv, int* __restrict__ flag) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+__device__ __forceinline__ int factor_diag_block(float* __restrict__ K, const KLayout& L, int b, float theta,
+                                                 float* __restrict__ rinv) {
+  const int lane = threadIdx.x & 31;
+  const int k0 = KB * b, kb = L.bw(b);
+  float* row = K + L.off(k0 + (lane < kb ? lane : 0));
+  float a[KB];
+#pragma unroll
+  for (int j4 = 0; j4 < KB / 4; ++j4) {
+    float4 t = (lane < kb && 4 * j4 < kb) ? *reinterpret_cast<const float4*>(row + k0 + 4 * j4)
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+    a[4 * j4] = t.x; a[4 * j4 + 1] = t.y; a[4 * j4 + 2] = t.z; a[4 * j4 + 3] = t.w;
+  }
   int nfloor = 0;
-  for (int k0 = 0; k0 < N;) {
-    const int k1 = panel_end(k0, N, npos);
-    const int kb = k1 - k0;
-    const float sgn = k0 < npos ? 1.f : -1.f;
-    // ---- (a) diagonal block -------------------------------------------------
-    if (warp == 0) {
-      float a[KB];
 #pragma unroll
-      for (int j = 0; j < KB; ++j) a[j] = (lane < kb && j < kb) ? K[(k0 + lane) * ld + k0 + j] : 0.f;
+  for (int k = 0; k < KB; ++k) {
+    if (k < kb) {
+      const float s = sgn_of(k0 + k, L.npos);
+      float d = s * __shfl_sync(0xffffffffu, a[k], k);
+      if (!(d >= theta)) { d = theta; ++nfloor; }
+      const float ri = rsqrtf(d);        // 1/l_kk
+      const float l = d * ri;            // l_kk
+      if (lane == k) a[k] = l;
+      else if (lane > k) a[k] *= s * ri;  // l_rk = a_rk / (s_k l_kk)
+      if (lane == 0) rinv[k0 + k] = ri;
+      const float nl = -s * a[k];
 #pragma unroll
-      for (int k = 0; k < KB; ++k) {
-        if (k < kb) {
-          float d = sgn * __shfl_sync(0xffffffffu, a[k], k);
-          if (!(d >= theta)) { d = theta; ++nfloor; }
-          const float l = sqrtf(d);
-          const float ri = 1.f / l;
-          if (lane == k) a[k] = l;
-          else if (lane > k) a[k] *= sgn * ri;  // l_rk = a_rk / (s_k l_kk)
-          if (lane == 0) rinv[k0 + k] = ri;
-#pragma unroll
-          for (int j = k + 1; j < KB; ++j) {
-            const float ljk = __shfl_sync(0xffffffffu, a[k], j);
-            if (j < kb && lane >= j) a[j] = fmaf(-sgn * a[k], ljk, a[j]);
-          }
-        }
-      }
-      if (lane < kb) {
-#pragma unroll
-        for (int j = 0; j < KB; ++j)
-          if (j <= lane) K[(k0 + lane) * ld + k0 + j] = a[j];
+      for (int j = k + 1; j < KB; ++j) {
+        const float ljk = __shfl_sync(0xffffffffu, a[k], j);
+        if (lane >= j) a[j] = fmaf(nl, ljk, a[j]);
       }
     }
-    __syncthreads();
-    // ---- (b) panel rows below the diagonal block: x L11ᵀ = a, l = s·x -------
-    for (int i = k1 + tid; i < N; i += NT) {
-      float a[KB];
-      const float4* row = reinterpret_cast<const float4*>(K + i * ld + k0);
+  }
+  if (lane < kb) {
 #pragma unroll
-      for (int j4 = 0; j4 < KB / 4; ++j4) {
-        float4 t = (4 * j4 < kb) ? row[j4] : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j4 = 0; j4 < KB / 4; ++j4)
+      if (4 * j4 < kb)
+        *reinterpret_cast<float4*>(row + k0 + 4 * j4) = make_float4(a[4 * j4], a[4 * j4 + 1], a[4 * j4 + 2],
+                                                                   a[4 * j4 + 3]);
+  }
+  return nfloor;
+}
+
+// ------------------------------------------------------------------------
+// Signed Cholesky of the packed matrix K (layout L), right-looking with a
+// depth-1 look-ahead, full 16-wide panels:
+//   prologue: warp 0 factors diagonal block 0
+//   for each block b with rows below it:
+//     (1) TRSM   rows i ≥ 16(b+1):  x L_bbᵀ = a, l = S_b x         (thread per row)
+//     (2) update block column b+1:  A[:, b+1] −= L[:, b] S_b L[b+1, b]ᵀ  (thread per row)
+//     (3) warp 0 factors diagonal block b+1 WHILE warps 1.. apply the rank-16
+//         update to the trailing lower triangle beyond block b+1 (32×32
+//         super-tiles, one warp each, 8×4 strided register tiles).
+// A pivot on the wrong side of ±θ is replaced by ±θ (reading Q12) and
+// counted.  On exit K holds L (M = L S Lᵀ) and rinv[k] = 1/L[k][k].
+// ------------------------------------------------------------------------
+template <int NT>
+__device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float theta, float* __restrict__ rinv,
+                         int* __restrict__ flag) {
+  constexpr int NW = NT / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int N4 = L.N4, npos = L.npos;
+  int nfloor = 0;
+  if (warp == 0) nfloor += factor_diag_block(K, L, 0, theta, rinv);
+  __syncthreads();
+  for (int b = 0; b + 1 < L.NB; ++b) {
+    const int k0 = KB * b, r0 = k0 + KB;
+    // ---- (1) TRSM of the panel rows below block b (full 16-wide panel) -------------
+    for (int i = r0 + tid; i < N4; i += NT) {
+      float* row = K + L.off(i) + k0;
+      float a[KB];
+#pragma unroll
+      for (int j4 = 0; j4 < 4; ++j4) {
+        const float4 t = reinterpret_cast<const float4*>(row)[j4];
         a[4 * j4] = t.x; a[4 * j4 + 1] = t.y; a[4 * j4 + 2] = t.z; a[4 * j4 + 3] = t.w;
       }
 #pragma unroll
       for (int k = 0; k < KB; ++k) {
-        if (k < kb) {
-          const float xk = a[k] * rinv[k0 + k];
-          a[k] = xk;
+        const float xk = a[k] * rinv[k0 + k];
+        a[k] = xk;
 #pragma unroll
-          for (int j = k + 1; j < KB; ++j)
-            if (j < kb) a[j] = fmaf(-xk, K[(k0 + j) * ld + k0 + k], a[j]);
-        }
+        for (int j = k + 1; j < KB; ++j) a[j] = fmaf(-xk, K[L.off(k0 + j) + k0 + k], a[j]);
       }
-      float4* wrow = reinterpret_cast<float4*>(K + i * ld + k0);
 #pragma unroll
-      for (int j4 = 0; j4 < KB / 4; ++j4)
-        if (4 * j4 < kb)
-          wrow[j4] = make_float4(sgn * a[4 * j4], sgn * a[4 * j4 + 1], sgn * a[4 * j4 + 2], sgn * a[4 * j4 + 3]);
+      for (int j4 = 0; j4 < 4; ++j4) {
+        const float s0 = sgn_of(k0 + 4 * j4, npos);  // npos is a multiple of 4
+        reinterpret_cast<float4*>(row)[j4] =
+            make_float4(s0 * a[4 * j4], s0 * a[4 * j4 + 1], s0 * a[4 * j4 + 2], s0 * a[4 * j4 + 3]);
+      }
     }
     __syncthreads();
-    // ---- (c) trailing update A22 -= s · L21 L21ᵀ (lower super-tiles) -------
-    if (k1 < N) {
-      const int T = (N4 - k1 + 31) >> 5;
-      const int nst = T * (T + 1) / 2;
-      const int grp = tid >> 6, gt = tid & 63, ty = gt >> 3, tx = gt & 7;
-      const int kq = (kb + 3) >> 2;  // kb is a multiple of 4 except on a final panel (no trailing then)
-      for (int st = grp; st < nst; st += NT / 64) {
-        int I = (int)((sqrtf(8.f * st + 1.f) - 1.f) * 0.5f);
-        while ((I + 1) * (I + 2) / 2 <= st) ++I;
-        while (I * (I + 1) / 2 > st) --I;
-        const int J = st - I * (I + 1) / 2;
-        const int rb = k1 + 32 * I + ty, cb = k1 + 32 * J + tx;
-        float acc[4][4];
+    // ---- (2) look-ahead: block column b+1, rows i ≥ r0 -------------------------------
+    const int w1 = L.bw(b + 1);
+    for (int i = r0 + tid; i < N4; i += NT) {
+      const float* li = K + L.off(i) + k0;
+      float* ai = K + L.off(i) + r0;
+      float lv[KB];
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+      for (int j4 = 0; j4 < 4; ++j4) {
+        float4 t = reinterpret_cast<const float4*>(li)[j4];
+        const float s0 = sgn_of(k0 + 4 * j4, npos);
+        lv[4 * j4] = s0 * t.x; lv[4 * j4 + 1] = s0 * t.y; lv[4 * j4 + 2] = s0 * t.z; lv[4 * j4 + 3] = s0 * t.w;
+      }
 #pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            const int r = rb + 8 * a, c = cb + 8 * b;
-            acc[a][b] = (r < N4 && c < N4) ? K[r * ld + c] : 0.f;
+      for (int c4 = 0; c4 < KB / 4; ++c4) {
+        if (4 * c4 < w1) {
+          float4 acc = reinterpret_cast<const float4*>(ai)[c4];
+          float accv[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            const float* lj = K + L.off(r0 + 4 * c4 + cc) + k0;
+            float t = accv[cc];
+#pragma unroll
+            for (int k4 = 0; k4 < 4; ++k4) {
+              const float4 u = reinterpret_cast<const float4*>(lj)[k4];
+              t = fmaf(-lv[4 * k4], u.x, t);
+              t = fmaf(-lv[4 * k4 + 1], u.y, t);
+              t = fmaf(-lv[4 * k4 + 2], u.z, t);
+              t = fmaf(-lv[4 * k4 + 3], u.w, t);
+            }
+            accv[cc] = t;
           }
-        for (int q = 0; q < kq; ++q) {
-          float4 lr[4], lc[4];
+          reinterpret_cast<float4*>(ai)[c4] = make_float4(accv[0], accv[1], accv[2], accv[3]);
+        }
+      }
+    }
+    __syncthreads();
+    // ---- (3) warp 0: diagonal block b+1 ‖ warps 1..: trailing SYRK beyond block b+1 ----
+    if (warp == 0) {
+      nfloor += factor_diag_block(K, L, b + 1, theta, rinv);
+    } else {
+      const int r2 = r0 + KB;
+      if (r2 < N4) {
+        const int T = (N4 - r2 + 31) >> 5;
+        const int nst = T * (T + 1) / 2;
+        const int ty = lane >> 3, tx = lane & 7;
+        for (int st = warp - 1; st < nst; st += NW - 1) {
+          int I = (int)((sqrtf(8.f * st + 1.f) - 1.f) * 0.5f);
+          while ((I + 1) * (I + 2) / 2 <= st) ++I;
+          while (I * (I + 1) / 2 > st) --I;
+          const int J = st - I * (I + 1) / 2;
+          const int rb = r2 + 32 * I + ty, cb = r2 + 32 * J + tx;
+          int roff[8], coff[4];
+          bool rok[8], cok[4];
 #pragma unroll
-          for (int a = 0; a < 4; ++a) {
-            const int r = rb + 8 * a;
-            lr[a] = r < N4 ? *reinterpret_cast<const float4*>(K + r * ld + k0 + 4 * q) : make_float4(0, 0, 0, 0);
+          for (int a = 0; a < 8; ++a) {
+            const int r = rb + 4 * a;
+            rok[a] = r < N4;
+            roff[a] = rok[a] ? L.off(r) : 0;
           }
 #pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            const int c = cb + 8 * b;
-            float4 t = c < N4 ? *reinterpret_cast<const float4*>(K + c * ld + k0 + 4 * q) : make_float4(0, 0, 0, 0);
-            t.x *= sgn; t.y *= sgn; t.z *= sgn; t.w *= sgn;
-            lc[b] = t;
+          for (int c = 0; c < 4; ++c) {
+            const int cc = cb + 8 * c;
+            cok[c] = cc < N4;
+            coff[c] = cok[c] ? L.off(cc) : 0;
+          }
+          float acc[8][4];
+#pragma unroll
+          for (int a = 0; a < 8; ++a)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[a][c] = (rok[a] && cok[c]) ? K[roff[a] + cb + 8 * c] : 0.f;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            // S_b applied to the column operand (npos is a multiple of 4)
+            const float sq = k0 + 4 * q < npos ? -1.f : 1.f;
+            float4 lc[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              float4 t = cok[c] ? *reinterpret_cast<const float4*>(K + coff[c] + k0 + 4 * q) : make_float4(0, 0, 0, 0);
+              t.x *= sq; t.y *= sq; t.z *= sq; t.w *= sq;
+              lc[c] = t;
+            }
+#pragma unroll
+            for (int a = 0; a < 8; ++a) {
+              const float4 lr = rok[a] ? *reinterpret_cast<const float4*>(K + roff[a] + k0 + 4 * q)
+                                       : make_float4(0, 0, 0, 0);
+#pragma unroll
+              for (int c = 0; c < 4; ++c) {
+                float t = acc[a][c];
+                t = fmaf(lr.x, lc[c].x, t);
+                t = fmaf(lr.y, lc[c].y, t);
+                t = fmaf(lr.z, lc[c].z, t);
+                t = fmaf(lr.w, lc[c].w, t);
+                acc[a][c] = t;
+              }
+            }
           }
 #pragma unroll
-          for (int a = 0; a < 4; ++a)
+          for (int a = 0; a < 8; ++a)
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
-              float t = acc[a][b];
-              t = fmaf(-lr[a].x, lc[b].x, t);
-              t = fmaf(-lr[a].y, lc[b].y, t);
-              t = fmaf(-lr[a].z, lc[b].z, t);
-              t = fmaf(-lr[a].w, lc[b].w, t);
-              acc[a][b] = t;
+            for (int c = 0; c < 4; ++c) {
+              const int cc = cb + 8 * c;
+              // lower triangle only (the diagonal block's upper part is never touched)
+              if (rok[a] && cok[c] && cc <= rb + 4 * a) K[roff[a] + cc] = acc[a][c];
             }
         }
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            const int r = rb + 8 * a, c = cb + 8 * b;
-            if (r < N4 && c < N4) K[r * ld + c] = acc[a][b];
-          }
       }
     }
     __syncthreads();
-    k0 = k1;
   }
   if (tid == 0) *flag = nfloor;
   __syncthreads();
@@ -258,19 +344,21 @@ __device__ int factor_qd(float* __restrict__ K, const int ld, const int N, const
 
 // ------------------------------------------------------------------------
 // Solve M u = rhs in place with the factor of factor_qd (M = L S Lᵀ).
+// rhs has N4 entries (padding entries must be 0 on entry).
 // ------------------------------------------------------------------------
 template <int NT>
-__device__ void solve_qd(const float* __restrict__ K, const int ld, const int N, const int npos,
-                         const float* __restrict__ rinv, float* __restrict__ rhs) {
+__device__ void solve_qd(const float* __restrict__ K, const KLayout& L, const float* __restrict__ rinv,
+                         float* __restrict__ rhs) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int N4 = L.N4;
   // forward: L u = b
-  for (int k0 = 0; k0 < N;) {
-    const int k1 = panel_end(k0, N, npos);
-    const int kb = k1 - k0;
+  for (int b = 0; b < L.NB; ++b) {
+    const int k0 = KB * b, kb = L.bw(b);
     if (warp == 0) {
+      const float* row = K + L.off(k0 + (lane < kb ? lane : 0)) + k0;
       float Lr[KB];
 #pragma unroll
-      for (int j = 0; j < KB; ++j) Lr[j] = (lane < kb && j < lane) ? K[(k0 + lane) * ld + k0 + j] : 0.f;
+      for (int j = 0; j < KB; ++j) Lr[j] = (lane < kb && j < lane) ? row[j] : 0.f;
       float bv = lane < kb ? rhs[k0 + lane] : 0.f;
 #pragma unroll
       for (int k = 0; k < KB; ++k) {
@@ -283,33 +371,35 @@ __device__ void solve_qd(const float* __restrict__ K, const int ld, const int N,
       if (lane < kb) rhs[k0 + lane] = bv;
     }
     __syncthreads();
-    for (int i = k1 + tid; i < N; i += NT) {
-      const float4* row = reinterpret_cast<const float4*>(K + i * ld + k0);
-      float acc = rhs[i];
-      for (int j4 = 0; 4 * j4 < kb; ++j4) {
-        const float4 l = row[j4];
-        const int j = k0 + 4 * j4;
-        acc = fmaf(-l.x, rhs[j], acc);
-        if (4 * j4 + 1 < kb) acc = fmaf(-l.y, rhs[j + 1], acc);
-        if (4 * j4 + 2 < kb) acc = fmaf(-l.z, rhs[j + 2], acc);
-        if (4 * j4 + 3 < kb) acc = fmaf(-l.w, rhs[j + 3], acc);
+    if (b + 1 < L.NB) {
+      for (int i = k0 + KB + tid; i < N4; i += NT) {
+        const float4* row = reinterpret_cast<const float4*>(K + L.off(i) + k0);
+        const float4* u = reinterpret_cast<const float4*>(rhs + k0);
+        float acc = rhs[i];
+#pragma unroll
+        for (int j4 = 0; j4 < 4; ++j4) {
+          const float4 l = row[j4], uu = u[j4];
+          acc = fmaf(-l.x, uu.x, acc);
+          acc = fmaf(-l.y, uu.y, acc);
+          acc = fmaf(-l.z, uu.z, acc);
+          acc = fmaf(-l.w, uu.w, acc);
+        }
+        rhs[i] = acc;
       }
-      rhs[i] = acc;
+      __syncthreads();
     }
-    __syncthreads();
-    k0 = k1;
   }
   // u <- S u
-  for (int i = npos + tid; i < N; i += NT) rhs[i] = -rhs[i];
+  for (int i = L.npos + tid; i < N4; i += NT) rhs[i] = -rhs[i];
   __syncthreads();
-  // backward: Lᵀ x = u, panels in reverse order
-  for (int k0 = last_panel_start(N, npos);; k0 = prev_panel_start(k0, npos)) {
-    const int k1 = panel_end(k0, N, npos);
-    const int kb = k1 - k0;
+  // backward: Lᵀ x = u, blocks in reverse order
+  for (int b = L.NB - 1; b >= 0; --b) {
+    const int k0 = KB * b, kb = L.bw(b);
     if (warp == 0) {
       float Lc[KB];  // lane j holds column j of the diagonal block
 #pragma unroll
-      for (int i = 0; i < KB; ++i) Lc[i] = (lane < kb && i < kb && i > lane) ? K[(k0 + i) * ld + k0 + lane] : 0.f;
+      for (int i = 0; i < KB; ++i)
+        Lc[i] = (lane < kb && i < kb && i > lane) ? K[L.off(k0 + i) + k0 + lane] : 0.f;
       float bv = lane < kb ? rhs[k0 + lane] : 0.f;
 #pragma unroll
       for (int k = KB - 1; k >= 0; --k) {
@@ -322,13 +412,14 @@ __device__ void solve_qd(const float* __restrict__ K, const int ld, const int N,
       if (lane < kb) rhs[k0 + lane] = bv;
     }
     __syncthreads();
-    for (int j = tid; j < k0; j += NT) {
-      float acc = rhs[j];
-      for (int i = 0; i < kb; ++i) acc = fmaf(-K[(k0 + i) * ld + j], rhs[k0 + i], acc);
-      rhs[j] = acc;
+    if (b > 0) {
+      for (int j = tid; j < k0; j += NT) {
+        float acc = rhs[j];
+        for (int i = 0; i < kb; ++i) acc = fmaf(-K[L.off(k0 + i) + j], rhs[k0 + i], acc);
+        rhs[j] = acc;
+      }
+      __syncthreads();
     }
-    __syncthreads();
-    if (k0 == 0) break;
   }
 }
 

@@ -15,7 +15,8 @@ enum { STG_SCALING = 1, STG_PREDICTOR = 2, STG_CENTERING = 3, STG_CORRECTOR = 4,
 
 struct Args {
   int B, n, m, p;
-  int n4, nw, N, N4, ld;  // KKT layout (nw = p for the implicit form)
+  int n4, nw, N, N4;      // KKT layout (nw = p for the implicit form)
+  KLayout kl;             // packed block layout of the KKT lower triangle
   const float *Q, *q, *A, *b, *G, *h;
   long long sQ, sq, sA, sb, sG, sh;
   float *x, *y, *z, *s;  // solution (solve: out; backward: in)
@@ -41,11 +42,11 @@ struct Smem {
   float* end;
 };
 
-__host__ __device__ inline Smem layout(float* base, int n4, int m, int p, int N4, int ld) {
+__host__ __device__ inline Smem layout(float* base, int n4, int m, int p, int N4, int ksize) {
   const int m4 = (m + 3) & ~3, p4 = (p + 3) & ~3;
   Smem S;
   float* q = base;
-  S.K = q; q += N4 * ld;
+  S.K = q; q += ksize;
   S.rinv = q; q += N4;
   S.rhs = q; q += N4;
   S.x = q; q += n4;
@@ -68,18 +69,18 @@ __host__ __device__ inline Smem layout(float* base, int n4, int m, int p, int N4
   S.dv = q; q += p4;
   S.t = q; q += p4;
   S.mx = q; q += p4 + m4;
-  S.red = q; q += 512;
+  S.red = q; q += 160;
   S.flag = reinterpret_cast<int*>(q); q += 4;
   S.end = q;
   return S;
 }
 
-__host__ inline size_t ipm_smem_bytes(int n4, int m, int p, int N4, int ld) {
-  const Smem S = layout(nullptr, n4, m, p, N4, ld);
-  return (size_t)(S.end - (float*)nullptr) * sizeof(float);
+__host__ inline size_t ipm_smem_bytes(int n4, int m, int p, int N4, int ksize) {
+  const Smem S = layout(nullptr, n4, m, p, N4, ksize);
+  return (size_t)(reinterpret_cast<uintptr_t>(S.end)) ;
 }
 
-__device__ inline Smem carve(float* base, const Args& a) { return layout(base, a.n4, a.m, a.p, a.N4, a.ld); }
+__device__ inline Smem carve(float* base, const Args& a) { return layout(base, a.n4, a.m, a.p, a.N4, a.kl.size()); }
 
 struct Prob {
   const float *Q, *q, *A, *b, *G, *h;
@@ -103,26 +104,31 @@ template <int NT>
 __device__ float assemble(const Smem& S, const Args& a, const Prob& P, const float* wH, const float* wC,
                           const float* e, bool unit_wH, bool zero_wC) {
   const int tid = threadIdx.x;
-  const int n = a.n, n4 = a.n4, p = a.nw, m = a.m, N = a.N, N4 = a.N4, ld = a.ld;
+  const int n = a.n, n4 = a.n4, p = a.nw, m = a.m, N = a.N, N4 = a.N4;
+  const KLayout& L = a.kl;
   float* K = S.K;
   // 1. stage raw G into the C block rows [n4, n4+p), cols [0, n4) (zero pad)
   for (int idx = tid; idx < p * n4; idx += NT) {
     const int k = idx / n4, j = idx - k * n4;
-    K[(n4 + k) * ld + j] = j < n ? __ldg(P.G + k * n + j) : 0.f;
+    K[L.off(n4 + k) + j] = j < n ? __ldg(P.G + k * n + j) : 0.f;
   }
-  // A rows and the zero / diagonal parts of the w,y blocks; padding rows
+  // rows ≥ n4: A rows, zeros / −e on the w,y blocks, −1 on padding rows;
+  // every row's tail beyond the diagonal (rest of its diagonal block + pad) is zeroed
   for (int r = n4 + tid; r < N4; r += NT) {
-    float* row = K + r * ld;
+    float* row = K + L.off(r);
+    const int len = L.len(r >> 4);
     if (r >= n4 + p && r < N) {
       const int l = r - n4 - p;
       for (int j = 0; j < n4; ++j) row[j] = j < n ? __ldg(P.A + l * n + j) : 0.f;
     }
-    if (r >= N) for (int j = 0; j < N4; ++j) row[j] = 0.f;
-    else for (int j = n4; j <= r; ++j) row[j] = 0.f;
+    if (r >= N) for (int j = 0; j < n4; ++j) row[j] = 0.f;
+    for (int j = n4; j < len; ++j) row[j] = 0.f;
     if (r < n4 + p) row[r] = -e[r - n4];
+    else if (r >= N) row[r] = -1.f;
   }
   __syncthreads();
-  // 2. H = Q + Gᵀ diag(wH) G, aligned 4×4 tiles of the lower triangle
+  // 2. H = Q + Gᵀ diag(wH) G, aligned 4×4 tiles of the lower triangle (x-block rows
+  //    also get their tails beyond the diagonal zeroed)
   const int T = n4 >> 2;
   const int nt = T * (T + 1) / 2;
   float dmax = 0.f;
@@ -141,8 +147,9 @@ __device__ float assemble(const Smem& S, const Args& a, const Prob& P, const flo
         acc[u][w] = (i < n && j < n) ? __ldg(P.Q + i * n + j) : (i == j ? 1.f : 0.f);
       }
     for (int k = 0; k < p; ++k) {
-      const float4 gi = *reinterpret_cast<const float4*>(K + (n4 + k) * ld + i0);
-      float4 gj = *reinterpret_cast<const float4*>(K + (n4 + k) * ld + j0);
+      const float* gk = K + L.off(n4 + k);
+      const float4 gi = *reinterpret_cast<const float4*>(gk + i0);
+      float4 gj = *reinterpret_cast<const float4*>(gk + j0);
       if (!unit_wH) {
         const float w = wH[k];
         gj.x *= w; gj.y *= w; gj.z *= w; gj.w *= w;
@@ -155,19 +162,25 @@ __device__ float assemble(const Smem& S, const Args& a, const Prob& P, const flo
         for (int w = 0; w < 4; ++w) acc[u][w] = fmaf(gia[u], gja[w], acc[u][w]);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < 4; ++u) {
+      float* row = K + L.off(i0 + u);
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
         const int i = i0 + u, j = j0 + w;
-        if (j <= i) K[i * ld + j] = acc[u][w];
+        if (j <= i) row[j] = acc[u][w];
         if (i == j && i < n) dmax = fmaxf(dmax, fabsf(acc[u][w]));
       }
+      if (I == J) {  // zero the tail of row i0+u beyond the diagonal
+        const int len = L.len((i0 + u) >> 4);
+        for (int j = i0 + u + 1; j < len; ++j) row[j] = 0.f;
+      }
+    }
   }
   __syncthreads();
   // 3. C block scaled in place: diag(wC) G
   for (int idx = tid; idx < p * n4; idx += NT) {
     const int k = idx / n4, j = idx - k * n4;
-    float* el = K + (n4 + k) * ld + j;
+    float* el = K + L.off(n4 + k) + j;
     *el = zero_wC ? 0.f : *el * wC[k];
   }
   for (int k = tid; k < p; k += NT) dmax = fmaxf(dmax, fabsf(e[k]));
@@ -240,6 +253,7 @@ __device__ Norms residuals(const Smem& S, const Args& a, const Prob& P, float ka
     if (!isfinite(rt)) nonfin += 1.f;
   }
   for (int j = n + tid; j < n4; j += NT) S.rhs[j] = 0.f;
+  for (int j = a.N + tid; j < a.N4; j += NT) S.rhs[j] = 0.f;
   // rows: r_i = Gx + s − h, r_e = Ax − b  (warp per row)
   float* mx = S.mx;  // per-row |Gx| / |Ax| stash
   rowdots<NT>(P.G, p, n, S.x, [&](int k, float gx) {
@@ -358,7 +372,7 @@ __device__ bool newton_update(const Smem& S, const Args& a, const Prob& P, float
 // Kernel: initialisation (Q11) + Algorithm 1.
 // ------------------------------------------------------------------------
 template <int NT>
-__global__ void __launch_bounds__(NT) ipm_solve_kernel(const Args a) {
+__global__ void __launch_bounds__(NT, 3) ipm_solve_kernel(const Args a) {
   extern __shared__ __align__(16) float smem[];
   const int bid = blockIdx.x;
   const int tid = threadIdx.x;
@@ -383,8 +397,9 @@ __global__ void __launch_bounds__(NT) ipm_solve_kernel(const Args a) {
     }
     for (int k = tid; k < p; k += NT) S.rhs[n4 + k] = __ldg(P.h + k);
     for (int l = tid; l < m; l += NT) S.rhs[n4 + p + l] = __ldg(P.b + l);
-    factor_qd<NT>(S.K, a.ld, a.N, a.N4, n4, a.floor_rel * dmax, S.rinv, S.flag);
-    solve_qd<NT>(S.K, a.ld, a.N, n4, S.rinv, S.rhs);
+    for (int j = a.N + tid; j < a.N4; j += NT) S.rhs[j] = 0.f;
+    factor_qd<NT>(S.K, a.kl, a.floor_rel * dmax, S.rinv, S.flag);
+    solve_qd<NT>(S.K, a.kl, S.rinv, S.rhs);
     for (int j = tid; j < n; j += NT) S.x[j] = S.rhs[j];
     for (int l = tid; l < m; l += NT) S.y[l] = S.rhs[n4 + p + l];
     __syncthreads();
@@ -420,8 +435,8 @@ __global__ void __launch_bounds__(NT) ipm_solve_kernel(const Args a) {
       if (converged_solve(R, a.tol)) { status = ST_CONVERGED; break; }
       if (k == a.max_iter) { status = ST_MAX_ITER; break; }
       const float dmax = assemble<NT>(S, a, P, S.dp, S.dp, S.dm, false, false);
-      factor_qd<NT>(S.K, a.ld, a.N, a.N4, n4, a.floor_rel * dmax, S.rinv, S.flag);
-      solve_qd<NT>(S.K, a.ld, a.N, n4, S.rinv, S.rhs);
+      factor_qd<NT>(S.K, a.kl, a.floor_rel * dmax, S.rinv, S.flag);
+      solve_qd<NT>(S.K, a.kl, S.rinv, S.rhs);
       int stage = 0;
       if (!newton_update<NT>(S, a, P, kappa, kappa - kt, &stage)) { status = ST_FAIL | (stage << 8); break; }
     }
@@ -444,7 +459,7 @@ __global__ void __launch_bounds__(NT) ipm_solve_kernel(const Args a) {
 // Algorithm 3 (sign reading Q7, dz = d₊⊙dv: Q8).
 // ------------------------------------------------------------------------
 template <int NT>
-__global__ void __launch_bounds__(NT) ipm_backward_kernel(const Args a) {
+__global__ void __launch_bounds__(NT, 3) ipm_backward_kernel(const Args a) {
   extern __shared__ __align__(16) float smem[];
   const int bid = blockIdx.x;
   const int tid = threadIdx.x;
@@ -466,14 +481,14 @@ __global__ void __launch_bounds__(NT) ipm_backward_kernel(const Args a) {
       float kappa = manifold_coords<NT>(S, a);
       const Norms R = residuals<NT>(S, a, P, kappa, kappa - a.kappa_relax);
       const float dmax = assemble<NT>(S, a, P, S.dp, S.dp, S.dm, false, false);
-      factor_qd<NT>(S.K, a.ld, a.N, a.N4, n4, a.floor_rel * dmax, S.rinv, S.flag);
+      factor_qd<NT>(S.K, a.kl, a.floor_rel * dmax, S.rinv, S.flag);
       it = k;
       if (R.nonfin > 0.f) { status = ST_FAIL | (STG_RELAX << 8); break; }
       const bool kok = p == 0 || fabsf(kappa / a.kappa_relax - 1.f) <= a.relax_ktol;
       if (kok && relax_done(R, a.tol, a.relax_tol, phi_prev)) break;
       phi_prev = kok ? rel_phi(R) : INFINITY;
       if (k == a.relax_max_iter) { status = ST_MAX_ITER | (STG_RELAX << 8); break; }
-      solve_qd<NT>(S.K, a.ld, a.N, n4, S.rinv, S.rhs);
+      solve_qd<NT>(S.K, a.kl, S.rinv, S.rhs);
       int stage = 0;
       if (!newton_update<NT>(S, a, P, kappa, kappa - a.kappa_relax, &stage)) {
         status = ST_FAIL | (STG_RELAX << 8);
@@ -486,7 +501,7 @@ __global__ void __launch_bounds__(NT) ipm_backward_kernel(const Args a) {
   if (ok) {
     for (int j = tid; j < a.N4; j += NT) S.rhs[j] = j < n ? -__ldg(a.dl + (long long)bid * n + j) : 0.f;
     __syncthreads();
-    solve_qd<NT>(S.K, a.ld, a.N, n4, S.rinv, S.rhs);
+    solve_qd<NT>(S.K, a.kl, S.rinv, S.rhs);
     rowdots<NT>(P.G, p, n, S.rhs, [&](int k, float gdx) { S.dz[k] = S.dp[k] * (gdx + S.rhs[n4 + k]); });
     for (int j = tid; j < n; j += NT) S.dx[j] = S.rhs[j];
     for (int l = tid; l < m; l += NT) S.dy[l] = S.rhs[n4 + p + l];

@@ -20,7 +20,8 @@ constexpr int kThreads = 256;
 constexpr size_t kMaxSmem = 232448;  // 227 KB opt-in dynamic shared memory per CTA (sm_100a)
 
 struct Layout {
-  int n4, nw, N, N4, ld;
+  int n4, nw, N, N4;
+  qpb::KLayout kl;
   size_t smem;
 };
 
@@ -30,9 +31,8 @@ Layout make_layout(int n, int m, int p, int formulation) {
   L.nw = formulation == QP_IMPLICIT ? p : 0;
   L.N = L.n4 + L.nw + m;
   L.N4 = (L.N + 3) & ~3;
-  L.ld = L.N4;
-  if (((L.ld >> 2) & 1) == 0) L.ld += 4;  // ld/4 odd: conflict-free 16-byte row accesses
-  L.smem = qpb::ipm_smem_bytes(L.n4, m, p, L.N4, L.ld);
+  L.kl = qpb::KLayout::make(L.N, L.n4);
+  L.smem = qpb::ipm_smem_bytes(L.n4, m, p, L.N4, L.kl.size());
   return L;
 }
 
@@ -95,7 +95,7 @@ qpb::Args base_args(const qp_ctx* c) {
   qpb::Args a;
   std::memset(&a, 0, sizeof(a));
   a.B = c->d.batch; a.n = c->d.n; a.m = c->d.m_eq; a.p = c->d.p;
-  a.n4 = c->L.n4; a.nw = c->L.nw; a.N = c->L.N; a.N4 = c->L.N4; a.ld = c->L.ld;
+  a.n4 = c->L.n4; a.nw = c->L.nw; a.N = c->L.N; a.N4 = c->L.N4; a.kl = c->L.kl;
   a.sQ = c->d.bstride_Q; a.sq = c->d.bstride_q; a.sA = c->d.bstride_A;
   a.sb = c->d.bstride_b; a.sG = c->d.bstride_G; a.sh = c->d.bstride_h;
   a.tol = c->c.tol; a.sigma = c->c.sigma; a.tau = c->c.tau; a.kappa_relax = c->c.kappa_relax;

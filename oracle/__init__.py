@@ -27,7 +27,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 _lock = threading.Lock()
 _lib = None
 
-SOLVER_K14_GEPP, SOLVER_M_LDL, SOLVER_NORMAL_CHOL = 0, 1, 2
+SOLVER_K14_GEPP, SOLVER_M_LDL, SOLVER_NORMAL_CHOL, SOLVER_M_PART = 0, 1, 2, 3
 FORM_IMPLICIT, FORM_EXPLICIT = 0, 1
 ST_CONVERGED, ST_MAX_ITER, ST_NUMERICAL_FAILURE = 0, 2, 3
 
@@ -57,7 +57,7 @@ class Cfg:
     kappa_relax: float = 1e-4
     relax_ktol: float = 1e-4
     relax_max_iter: int = 50
-    kkt_solver: int = SOLVER_M_LDL
+    kkt_solver: int = SOLVER_M_PART
     formulation: int = FORM_IMPLICIT
     pivot_floor_rel: float = float(np.sqrt(np.finfo(np.float32).eps))
     relax_tol: float = 1e-6

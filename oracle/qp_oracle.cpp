@@ -37,7 +37,7 @@ enum { ST_CONVERGED = 0, ST_MAX_ITER = 2, ST_NUMERICAL_FAILURE = 3 };
 // failure stage, stored in status bits 8..15 (Table 1 categories).
 enum { STG_NONE = 0, STG_SCALING = 1, STG_PREDICTOR = 2, STG_CENTERING = 3, STG_CORRECTOR = 4,
        STG_LINESEARCH = 5, STG_RELAX = 6, STG_BACKWARD = 7, STG_INIT = 8 };
-enum { SOLVER_K14_GEPP = 0, SOLVER_M_LDL = 1, SOLVER_NORMAL_CHOL = 2 };
+enum { SOLVER_K14_GEPP = 0, SOLVER_M_LDL = 1, SOLVER_NORMAL_CHOL = 2, SOLVER_M_PART = 3 };
 enum { FORM_IMPLICIT = 0, FORM_EXPLICIT = 1 };
 
 }  // namespace orc
@@ -267,6 +267,7 @@ template <typename T> struct Factor {
   std::vector<T> F, D;  // LU (K14) or LDL (M)
   std::vector<int> piv;
   std::vector<T> dp, dm, c;  // d+ = db(v), d- = db(-v), c = db/dkappa
+  std::vector<int> act;      // SOLVER_M_PART: indices i with v_i > 0, in order
   int nfloor = 0;
   bool ok = true;
 };
@@ -321,6 +322,41 @@ static Factor<T> factor_kkt(const Prob<T>& P, const T* v, T kappa, int solver, T
     F.nfloor = ldl_factor(K, N, n, floor_rel, F.D);
     F.ok = true;
   }
+  if (solver == SOLVER_M_PART) {
+    // Reading Q12b: eliminate from M the w_i of every constraint
+    // with v_i <= 0 (pivot -d-_i, d-_i >= 1/2).  Exact block elimination; the
+    // reduced matrix keeps only bounded weights:
+    //   [[Q + G' diag(w) G, G_A' D+_A, A'], [D+_A G_A, -D-_A, 0], [A, 0, 0]],
+    //   w_i = d+_i (v_i > 0),  w_i = d+_i / d-_i = b(v_i)/b(-v_i) <= 1 (v_i <= 0).
+    F.act.clear();
+    for (int i = 0; i < p; ++i)
+      if (v[i] > T(0)) F.act.push_back(i);
+    const int pa = (int)F.act.size(), Nr = n + pa + m;
+    F.N = Nr;
+    K.assign((size_t)Nr * Nr, 0);
+    auto ar = [&](int i, int j) -> T& { return K[(size_t)i * Nr + j]; };
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) {
+        T gg = 0;
+        for (int k = 0; k < p; ++k) {
+          const T w = v[k] > T(0) ? F.dp[k] : F.dp[k] / F.dm[k];
+          gg += P.G[(size_t)k * n + i] * w * P.G[(size_t)k * n + j];
+        }
+        ar(i, j) = P.Q[(size_t)i * n + j] + gg;
+      }
+    for (int a = 0; a < pa; ++a) {
+      const int k = F.act[a];
+      for (int j = 0; j < n; ++j) {
+        T c = F.dp[k] * P.G[(size_t)k * n + j];
+        ar(n + a, j) = c; ar(j, n + a) = c;
+      }
+      ar(n + a, n + a) = -F.dm[k];
+    }
+    for (int k = 0; k < m; ++k)
+      for (int j = 0; j < n; ++j) { ar(n + pa + k, j) = P.A[(size_t)k * n + j]; ar(j, n + pa + k) = P.A[(size_t)k * n + j]; }
+    F.nfloor = ldl_factor(K, Nr, n, floor_rel, F.D);
+    F.ok = true;
+  }
   return F;
 }
 
@@ -338,6 +374,25 @@ static void solve_kkt(const Prob<T>& P, const Factor<T>& F, const T* f1, const T
     for (int i = 0; i < n; ++i) dx[i] = r[i];
     for (int i = 0; i < p; ++i) dv[i] = r[n + i];
     for (int i = 0; i < m; ++i) dy[i] = r[n + p + i];
+  } else if (F.kind == SOLVER_M_PART) {
+    // reduced right-hand side: r1 = f1 + G'f2 + sum_{v_i<=0} g_i (d+_i/d-_i) f2_i
+    const int pa = (int)F.act.size(), Nr = n + pa + m;
+    std::vector<T> rr(Nr), t(p), Gf(n);
+    std::vector<char> isact(p, 0);
+    for (int i : F.act) isact[i] = 1;
+    for (int i = 0; i < p; ++i) t[i] = isact[i] ? f2[i] : f2[i] * (T(1) + F.dp[i] / F.dm[i]);
+    matTvec(P.G, p, n, t.data(), Gf.data());
+    for (int i = 0; i < n; ++i) rr[i] = f1[i] + Gf[i];
+    for (int a = 0; a < pa; ++a) rr[n + a] = f2[F.act[a]];
+    for (int i = 0; i < m; ++i) rr[n + pa + i] = f3[i];
+    ldl_solve(F.F, F.D, Nr, rr.data());
+    for (int i = 0; i < n; ++i) dx[i] = rr[i];
+    std::vector<T> Gdx(p), w(p);
+    matvec(P.G, p, n, dx, Gdx.data());
+    for (int i = 0; i < p; ++i) w[i] = (F.dp[i] * Gdx[i] - f2[i]) / F.dm[i];  // eliminated rows
+    for (int a = 0; a < pa; ++a) w[F.act[a]] = rr[n + a];
+    for (int i = 0; i < p; ++i) dv[i] = Gdx[i] + w[i];
+    for (int i = 0; i < m; ++i) dy[i] = rr[n + pa + i];
   } else {
     // S' (f1, f2, f3) = (f1 + G' f2, f2, f3); solve M; dv = G dx + w.
     std::vector<T> Gf(n);

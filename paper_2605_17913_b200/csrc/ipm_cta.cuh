@@ -211,12 +211,14 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
         const float4 t = reinterpret_cast<const float4*>(row)[j4];
         a[4 * j4] = t.x; a[4 * j4 + 1] = t.y; a[4 * j4 + 2] = t.z; a[4 * j4 + 3] = t.w;
       }
+      const float* D = K + L.off(k0) + k0;  // diagonal block: row j at D + j*Lb
+      const int Lb = L.len(b);
 #pragma unroll
       for (int k = 0; k < KB; ++k) {
         const float xk = a[k] * rinv[k0 + k];
         a[k] = xk;
 #pragma unroll
-        for (int j = k + 1; j < KB; ++j) a[j] = fmaf(-xk, K[L.off(k0 + j) + k0 + k], a[j]);
+        for (int j = k + 1; j < KB; ++j) a[j] = fmaf(-xk, D[j * Lb + k], a[j]);
       }
 #pragma unroll
       for (int j4 = 0; j4 < 4; ++j4) {
@@ -228,6 +230,8 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
     __syncthreads();
     // ---- (2) look-ahead: block column b+1, rows i ≥ r0 -------------------------------
     const int w1 = L.bw(b + 1);
+    const float* B1 = K + L.off(r0) + k0;  // rows of block b+1, panel columns of block b
+    const int L1 = L.len(b + 1);
     for (int i = r0 + tid; i < N4; i += NT) {
       const float* li = K + L.off(i) + k0;
       float* ai = K + L.off(i) + r0;
@@ -245,7 +249,7 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
           float accv[4] = {acc.x, acc.y, acc.z, acc.w};
 #pragma unroll
           for (int cc = 0; cc < 4; ++cc) {
-            const float* lj = K + L.off(r0 + 4 * c4 + cc) + k0;
+            const float* lj = B1 + (4 * c4 + cc) * L1;
             float t = accv[cc];
 #pragma unroll
             for (int k4 = 0; k4 < 4; ++k4) {
@@ -397,9 +401,10 @@ __device__ void solve_qd(const float* __restrict__ K, const KLayout& L, const fl
     const int k0 = KB * b, kb = L.bw(b);
     if (warp == 0) {
       float Lc[KB];  // lane j holds column j of the diagonal block
+      const float* Bk = K + L.off(k0) + k0;
+      const int Lb = L.len(b);
 #pragma unroll
-      for (int i = 0; i < KB; ++i)
-        Lc[i] = (lane < kb && i < kb && i > lane) ? K[L.off(k0 + i) + k0 + lane] : 0.f;
+      for (int i = 0; i < KB; ++i) Lc[i] = (lane < kb && i < kb && i > lane) ? Bk[i * Lb + lane] : 0.f;
       float bv = lane < kb ? rhs[k0 + lane] : 0.f;
 #pragma unroll
       for (int k = KB - 1; k >= 0; --k) {
@@ -413,9 +418,11 @@ __device__ void solve_qd(const float* __restrict__ K, const KLayout& L, const fl
     }
     __syncthreads();
     if (b > 0) {
+      const float* Bk = K + L.off(k0);
+      const int Lb = L.len(b);
       for (int j = tid; j < k0; j += NT) {
         float acc = rhs[j];
-        for (int i = 0; i < kb; ++i) acc = fmaf(-K[L.off(k0 + i) + j], rhs[k0 + i], acc);
+        for (int i = 0; i < kb; ++i) acc = fmaf(-Bk[i * Lb + j], rhs[k0 + i], acc);
         rhs[j] = acc;
       }
       __syncthreads();

@@ -1,9 +1,21 @@
 // ipm_kernels.cuh — the persistent per-problem IPM kernels (solve: init +
-// Alg. 1; backward: Alg. 2 + Alg. 3) and the batch-sum kernel for gradients
+// Alg. 1; backward: Alg. 2 + Alg. 3) and the batch-sum kernels for gradients
 // of shared parameters.  One CTA owns one QP for the whole kernel; the KKT
 // matrix, the iterate and all per-iteration vectors live in shared memory;
-// the problem data (Q, G, A, …) is re-read from global memory (L2) each
-// iteration.  See DESIGN.md §5 for the data layout and §6 for the roofline.
+// the problem data (Q, G, A, …) is re-read from global memory (L1/L2) each
+// iteration.  DESIGN.md §5 (layout) and §6 (roofline).
+//
+// Linear system (readings Q12 + Q12b).  Each Newton step solves
+// the bounded system of Eq. 14.  It is first brought to the
+// congruent quasi-definite form M (Δv = GΔx + w), then every w_i of a
+// constraint with v_i ≤ 0 is eliminated exactly (its pivot is −d₋_i with
+// d₋_i ≥ ½).  The factored matrix is
+//     [[Q + Gᵀ diag(ω) G,  G_Aᵀ D₊_A,  Aᵀ],
+//      [D₊_A G_A,          −D₋_A,      0 ],
+//      [A,                  0,          0 ]]
+// with A = {i : v_i > 0} and ω_i = d₊_i on A, ω_i = d₊_i/d₋_i = b(v_i)/b(−v_i) ≤ 1
+// off A: every entry stays bounded (the property the paper's method rests
+// on), and the size drops from n+p+m to n+|A|+m.
 #pragma once
 #include "ipm_cta.cuh"
 
@@ -15,40 +27,38 @@ enum { STG_SCALING = 1, STG_PREDICTOR = 2, STG_CENTERING = 3, STG_CORRECTOR = 4,
 
 struct Args {
   int B, n, m, p;
-  int n4, nw, N, N4;      // KKT layout (nw = p for the implicit form)
-  KLayout kl;             // packed block layout of the KKT lower triangle
+  int n4, Nmax, N4max, ksize;  // KKT capacity: N ≤ n4 + p + m
   const float *Q, *q, *A, *b, *G, *h;
   long long sQ, sq, sA, sb, sG, sh;
   float *x, *y, *z, *s;  // solution (solve: out; backward: in)
   int *iters, *status;
   const float* dl;
-  float *gQ, *gq, *gA, *gb, *gG, *gh;        // per-problem gradients (nullptr = skip)
-  float *wx, *wy, *wz, *wdx, *wdy, *wdz;     // per-problem vectors for shared sums (nullptr = skip)
+  float *gQ, *gq, *gA, *gb, *gG, *gh;     // per-problem gradients (nullptr = skip)
+  float *wx, *wy, *wz, *wdx, *wdy, *wdz;  // per-problem vectors for shared sums (nullptr = skip)
   int *riters, *rstatus;
   float tol, sigma, tau, kappa_relax, relax_ktol, floor_rel, relax_tol;
   int max_iter, relax_max_iter;
 };
 
 // Shared-memory carve-up (floats).  Every segment is a multiple of 4 floats
-// so that float4 accesses stay 16-byte aligned.  layout() is used by the host
-// (base = nullptr, to size the allocation) and by the kernels.
+// so that float4 accesses stay 16-byte aligned.  layout() sizes the
+// allocation on the host (base = nullptr) and carves it on the device.
 struct Smem {
   float *K, *rinv, *rhs;
-  float *x, *y, *z, *s, *v, *dp, *dm, *c;
-  float *rt, *re, *ri, *rz, *rs;
-  float *dx, *dy, *dz, *ds, *dv, *t, *mx;
+  float *x, *y, *z, *s, *v, *dp, *dm, *c, *om;
+  float *rz, *rs, *f2, *t, *gx, *dx, *dy, *dz;
   float* red;
-  int* flag;
+  int *act, *widx, *flag;
   float* end;
 };
 
-__host__ __device__ inline Smem layout(float* base, int n4, int m, int p, int N4, int ksize) {
+__host__ __device__ inline Smem layout(float* base, int n4, int m, int p, int N4max, int ksize) {
   const int m4 = (m + 3) & ~3, p4 = (p + 3) & ~3;
   Smem S;
   float* q = base;
   S.K = q; q += ksize;
-  S.rinv = q; q += N4;
-  S.rhs = q; q += N4;
+  S.rinv = q; q += N4max;
+  S.rhs = q; q += N4max;
   S.x = q; q += n4;
   S.y = q; q += m4;
   S.z = q; q += p4;
@@ -57,30 +67,31 @@ __host__ __device__ inline Smem layout(float* base, int n4, int m, int p, int N4
   S.dp = q; q += p4;
   S.dm = q; q += p4;
   S.c = q; q += p4;
-  S.rt = q; q += n4;
-  S.re = q; q += m4;
-  S.ri = q; q += p4;
+  S.om = q; q += p4;
   S.rz = q; q += p4;
   S.rs = q; q += p4;
+  S.f2 = q; q += p4;
+  S.t = q; q += p4;
+  S.gx = q; q += p4 + m4;
   S.dx = q; q += n4;
   S.dy = q; q += m4;
   S.dz = q; q += p4;
-  S.ds = q; q += p4;
-  S.dv = q; q += p4;
-  S.t = q; q += p4;
-  S.mx = q; q += p4 + m4;
   S.red = q; q += 160;
-  S.flag = reinterpret_cast<int*>(q); q += 4;
+  S.act = reinterpret_cast<int*>(q); q += p4;
+  S.widx = reinterpret_cast<int*>(q); q += p4;
+  S.flag = reinterpret_cast<int*>(q); q += 16;
   S.end = q;
   return S;
 }
 
-__host__ inline size_t ipm_smem_bytes(int n4, int m, int p, int N4, int ksize) {
-  const Smem S = layout(nullptr, n4, m, p, N4, ksize);
-  return (size_t)(reinterpret_cast<uintptr_t>(S.end)) ;
+__host__ inline size_t ipm_smem_bytes(int n4, int m, int p, int N4max, int ksize) {
+  const Smem S = layout(nullptr, n4, m, p, N4max, ksize);
+  return (size_t)reinterpret_cast<uintptr_t>(S.end);
 }
 
-__device__ inline Smem carve(float* base, const Args& a) { return layout(base, a.n4, a.m, a.p, a.N4, a.kl.size()); }
+__device__ inline Smem carve(float* base, const Args& a) {
+  return layout(base, a.n4, a.m, a.p, a.N4max, a.ksize);
+}
 
 struct Prob {
   const float *Q, *q, *A, *b, *G, *h;
@@ -94,41 +105,68 @@ __device__ __forceinline__ Prob prob_of(const Args& a, int bid) {
 }
 
 // ------------------------------------------------------------------------
-// KKT assembly (bounded scaling): the lower triangle of
-//   [[Q + Gᵀ diag(wH) G, Gᵀ diag(wC), Aᵀ], [diag(wC) G, −diag(e), 0], [A, 0, 0]]
-// Implicit Newton step: wH = wC = d₊, e = d₋ (the M form).  CVXOPT init
-// (congruent form of [[Q,Gᵀ,Aᵀ],[G,−I,0],[A,0,0]]): wH = 1, wC = 0, e = 1.
-// Returns max|diag| over the real rows (for the pivot floor).
+// Active-set compaction: act[0..pa) = {k : v_k > 0} in increasing order,
+// widx[k] = position in act or −1.  Returns pa (block-uniform).
 // ------------------------------------------------------------------------
 template <int NT>
-__device__ float assemble(const Smem& S, const Args& a, const Prob& P, const float* wH, const float* wC,
-                          const float* e, bool unit_wH, bool zero_wC) {
-  const int tid = threadIdx.x;
-  const int n = a.n, n4 = a.n4, p = a.nw, m = a.m, N = a.N, N4 = a.N4;
-  const KLayout& L = a.kl;
-  float* K = S.K;
-  // 1. stage raw G into the C block rows [n4, n4+p), cols [0, n4) (zero pad)
-  for (int idx = tid; idx < p * n4; idx += NT) {
-    const int k = idx / n4, j = idx - k * n4;
-    K[L.off(n4 + k) + j] = j < n ? __ldg(P.G + k * n + j) : 0.f;
+__device__ int compact_active(const Smem& S, int p, bool all_inactive) {
+  constexpr int NW = NT / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int base = 0;
+  for (int c0 = 0; c0 < p; c0 += NT) {
+    const int k = c0 + tid;
+    const bool on = !all_inactive && k < p && S.v[k] > 0.f;
+    const unsigned bal = __ballot_sync(0xffffffffu, on);
+    __syncthreads();
+    if (lane == 0) S.flag[warp] = __popc(bal);  // NW ≤ 16 counters
+    __syncthreads();
+    int before = base;
+    for (int w = 0; w < warp; ++w) before += S.flag[w];
+    int tot = 0;
+    for (int w = 0; w < NW; ++w) tot += S.flag[w];
+    if (k < p) {
+      const int pos = before + __popc(bal & ((1u << lane) - 1u));
+      S.widx[k] = on ? pos : -1;
+      if (on) S.act[pos] = k;
+    }
+    base += tot;
   }
-  // rows ≥ n4: A rows, zeros / −e on the w,y blocks, −1 on padding rows;
-  // every row's tail beyond the diagonal (rest of its diagonal block + pad) is zeroed
+  __syncthreads();
+  return base;
+}
+
+// ------------------------------------------------------------------------
+// KKT assembly of the reduced bounded system (header comment), lower triangle
+// in the packed layout L (N = n4 + pa + m).  cw = weights of the C rows (d₊),
+// e = the −diagonal of the w block (d₋), om = ω.  Returns max|diag|.
+// ------------------------------------------------------------------------
+template <int NT>
+__device__ float assemble(const Smem& S, const Args& a, const Prob& P, const KLayout& L, int pa,
+                          const float* om, const float* cw, const float* e) {
+  const int tid = threadIdx.x;
+  const int n = a.n, n4 = a.n4, p = a.p, N = L.N, N4 = L.N4;
+  float* K = S.K;
+  // 1. rows ≥ n4: C rows of the active constraints, A rows, padding; the tail
+  //    of every row beyond its diagonal (rest of its diagonal block + pad) = 0.
   for (int r = n4 + tid; r < N4; r += NT) {
     float* row = K + L.off(r);
     const int len = L.len(r >> 4);
-    if (r >= n4 + p && r < N) {
-      const int l = r - n4 - p;
-      for (int j = 0; j < n4; ++j) row[j] = j < n ? __ldg(P.A + l * n + j) : 0.f;
+    if (r < n4 + pa) {
+      const int k = S.act[r - n4];
+      const float w = cw[k];
+      const float* g = P.G + k * n;
+      for (int j = 0; j < n4; ++j) row[j] = j < n ? w * __ldg(g + j) : 0.f;
+    } else if (r < N) {
+      const float* arow = P.A + (r - n4 - pa) * n;
+      for (int j = 0; j < n4; ++j) row[j] = j < n ? __ldg(arow + j) : 0.f;
+    } else {
+      for (int j = 0; j < n4; ++j) row[j] = 0.f;
     }
-    if (r >= N) for (int j = 0; j < n4; ++j) row[j] = 0.f;
     for (int j = n4; j < len; ++j) row[j] = 0.f;
-    if (r < n4 + p) row[r] = -e[r - n4];
-    else if (r >= N) row[r] = -1.f;
+    row[r] = r < n4 + pa ? -e[S.act[r - n4]] : (r < N ? 0.f : -1.f);
   }
-  __syncthreads();
-  // 2. H = Q + Gᵀ diag(wH) G, aligned 4×4 tiles of the lower triangle (x-block rows
-  //    also get their tails beyond the diagonal zeroed)
+  // 2. H = Q + Gᵀ diag(ω) G: 4×4 register tiles of the lower triangle; G rows
+  //    are read from global memory (L1-resident across iterations).
   const int T = n4 >> 2;
   const int nt = T * (T + 1) / 2;
   float dmax = 0.f;
@@ -147,19 +185,18 @@ __device__ float assemble(const Smem& S, const Args& a, const Prob& P, const flo
         acc[u][w] = (i < n && j < n) ? __ldg(P.Q + i * n + j) : (i == j ? 1.f : 0.f);
       }
     for (int k = 0; k < p; ++k) {
-      const float* gk = K + L.off(n4 + k);
-      const float4 gi = *reinterpret_cast<const float4*>(gk + i0);
-      float4 gj = *reinterpret_cast<const float4*>(gk + j0);
-      if (!unit_wH) {
-        const float w = wH[k];
-        gj.x *= w; gj.y *= w; gj.z *= w; gj.w *= w;
+      const float* g = P.G + k * n;
+      const float w = om[k];
+      float gi[4], gj[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        gi[u] = i0 + u < n ? __ldg(g + i0 + u) : 0.f;
+        gj[u] = j0 + u < n ? w * __ldg(g + j0 + u) : 0.f;
       }
-      const float gia[4] = {gi.x, gi.y, gi.z, gi.w};
-      const float gja[4] = {gj.x, gj.y, gj.z, gj.w};
 #pragma unroll
       for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int w = 0; w < 4; ++w) acc[u][w] = fmaf(gia[u], gja[w], acc[u][w]);
+        for (int w2 = 0; w2 < 4; ++w2) acc[u][w2] = fmaf(gi[u], gj[w2], acc[u][w2]);
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -176,21 +213,14 @@ __device__ float assemble(const Smem& S, const Args& a, const Prob& P, const flo
       }
     }
   }
-  __syncthreads();
-  // 3. C block scaled in place: diag(wC) G
-  for (int idx = tid; idx < p * n4; idx += NT) {
-    const int k = idx / n4, j = idx - k * n4;
-    float* el = K + L.off(n4 + k) + j;
-    *el = zero_wC ? 0.f : *el * wC[k];
-  }
-  for (int k = tid; k < p; k += NT) dmax = fmaxf(dmax, fabsf(e[k]));
+  for (int r = tid; r < pa; r += NT) dmax = fmaxf(dmax, fabsf(e[S.act[r]]));
   float vals[1] = {dmax};
   block_reduce<NT, 0, 1>(vals, S.red);
   return vals[0];
 }
 
-// Warp-per-row dot products out[r] = Mat[r,:]·vec for r < rows (Mat global,
-// row-major rows×n, vec in smem); fn(r, dot) runs on lane 0.
+// Warp-per-row dot products Mat[r,:]·vec for r < rows (Mat global row-major
+// rows×n, vec in smem); fn(r, dot) runs on lane 0.
 template <int NT, typename F>
 __device__ __forceinline__ void rowdots(const float* __restrict__ Mat, int rows, int n, const float* vec, F fn) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -205,14 +235,18 @@ __device__ __forceinline__ void rowdots(const float* __restrict__ Mat, int rows,
 }
 
 // ------------------------------------------------------------------------
-// Residuals (Eq. 4; Eq. 10), the relative stopping test
-// (reading Q4) and the Newton right-hand side of Eq. 14 in the
-// M coordinates: rhs = (−(r_t − Gᵀ(r_z + c r_κ)), −(r_i − r_s − c r_κ), −r_e).
-// Also fills d₊, d₋, c at (v, κ).  Returns the norms (block-uniform).
+// Residuals (Eq. 4; Eq. 10), the norms of the relative
+// stopping test (reading Q4), d₊, d₋, c, ω and the active set at (v, κ), and
+// the Newton right-hand side of Eq. 14 carried to the reduced
+// system:
+//   f1 = −(r_t − Gᵀ(r_i + r_z − r_s)), f2 = −(r_i − r_s − c r_κ), f3 = −r_e,
+//   rhs_x = f1 + Gᵀ f2 + Σ_{v_i≤0} g_i ω_i f2_i = −(r_t − Gᵀ t),
+//   t_i = r_z,i + c_i r_κ + [v_i ≤ 0] ω_i f2_i;  rhs_w = f2_A;  rhs_y = f3.
 // ------------------------------------------------------------------------
 struct Norms {
   float gap, obj, nonfin;
   float nrt, nre, nri, nrzs, sQx, sq, sGz, sAy, sAx, sb, sGx, ss, sh, sz;
+  int pa;
 };
 
 template <int NT>
@@ -220,17 +254,31 @@ __device__ Norms residuals(const Smem& S, const Args& a, const Prob& P, float ka
   const int tid = threadIdx.x;
   const int n = a.n, n4 = a.n4, p = a.p, m = a.m;
   float mz = 0.f, ms = 0.f, mh = 0.f, mrzs = 0.f, nonfin = 0.f;
-  // elementwise: r_z, r_s, d±, c, t = r_z + c r_κ
   for (int k = tid; k < p; k += NT) {
     const float zk = S.z[k], sk = S.s[k], vk = S.v[k];
     const float rz = zk - ret_b(vk, kappa), rs = sk - ret_b(-vk, kappa);
-    const float c = ret_dk(vk, kappa);
-    S.rz[k] = rz; S.rs[k] = rs; S.c[k] = c;
-    S.dp[k] = ret_db(vk, kappa); S.dm[k] = ret_db(-vk, kappa);
-    S.t[k] = fmaf(c, r_kappa, rz);
+    const float dp = ret_db(vk, kappa), dm = ret_db(-vk, kappa);
+    S.rz[k] = rz; S.rs[k] = rs; S.c[k] = ret_dk(vk, kappa);
+    S.dp[k] = dp; S.dm[k] = dm;
+    S.om[k] = vk > 0.f ? dp : dp / dm;
     mz = fmaxf(mz, fabsf(zk)); ms = fmaxf(ms, fabsf(sk)); mh = fmaxf(mh, fabsf(__ldg(P.h + k)));
     mrzs = fmaxf(mrzs, fmaxf(fabsf(rz), fabsf(rs)));
   }
+  const int pa = compact_active<NT>(S, p, false);
+  // rows: r_i = Gx + s − h, r_e = Ax − b (warp per row); f2, t, rhs_w, rhs_y
+  rowdots<NT>(P.G, p, n, S.x, [&](int k, float gx) {
+    const float ri = gx + S.s[k] - __ldg(P.h + k);
+    const float f2 = -(ri - S.rs[k] - S.c[k] * r_kappa);
+    S.f2[k] = f2;
+    S.gx[k] = gx;
+    S.t[k] = fmaf(S.c[k], r_kappa, S.rz[k]) + (S.v[k] > 0.f ? 0.f : S.om[k] * f2);
+    const int wi = S.widx[k];
+    if (wi >= 0) S.rhs[n4 + wi] = f2;
+  });
+  rowdots<NT>(P.A, m, n, S.x, [&](int l, float ax) {
+    S.rhs[n4 + pa + l] = -(ax - __ldg(P.b + l));
+    S.gx[p + l] = ax;
+  });
   __syncthreads();
   // columns j < n: Qx, Gᵀz, Aᵀy, Gᵀt  (Q symmetric ⇒ (Qx)_j = Σ_i Q_ij x_i)
   float mrt = 0.f, mqx = 0.f, mq = 0.f, mgz = 0.f, may = 0.f, obj = 0.f;
@@ -245,7 +293,6 @@ __device__ Norms residuals(const Smem& S, const Args& a, const Prob& P, float ka
     for (int l = 0; l < m; ++l) ay = fmaf(__ldg(P.A + l * n + j), S.y[l], ay);
     const float qj = __ldg(P.q + j);
     const float rt = qx + qj + gz + ay;
-    S.rt[j] = rt;
     S.rhs[j] = -(rt - gt);
     mrt = fmaxf(mrt, fabsf(rt)); mqx = fmaxf(mqx, fabsf(qx)); mq = fmaxf(mq, fabsf(qj));
     mgz = fmaxf(mgz, fabsf(gz)); may = fmaxf(may, fabsf(ay));
@@ -253,29 +300,19 @@ __device__ Norms residuals(const Smem& S, const Args& a, const Prob& P, float ka
     if (!isfinite(rt)) nonfin += 1.f;
   }
   for (int j = n + tid; j < n4; j += NT) S.rhs[j] = 0.f;
-  for (int j = a.N + tid; j < a.N4; j += NT) S.rhs[j] = 0.f;
-  // rows: r_i = Gx + s − h, r_e = Ax − b  (warp per row)
-  float* mx = S.mx;  // per-row |Gx| / |Ax| stash
-  rowdots<NT>(P.G, p, n, S.x, [&](int k, float gx) {
-    const float ri = gx + S.s[k] - __ldg(P.h + k);
-    S.ri[k] = ri;
-    S.rhs[n4 + k] = -(ri - S.rs[k] - S.c[k] * r_kappa);
-    mx[k] = gx;
-  });
-  rowdots<NT>(P.A, m, n, S.x, [&](int l, float ax) {
-    const float re = ax - __ldg(P.b + l);
-    S.re[l] = re;
-    S.rhs[n4 + p + l] = -re;
-    mx[p + l] = ax;
-  });
-  __syncthreads();
+  const int N = n4 + pa + m;
+  for (int j = N + tid; j < r4(N); j += NT) S.rhs[j] = 0.f;
   float mri = 0.f, mgx = 0.f, mre = 0.f, max_ = 0.f, mb = 0.f, gap = 0.f;
   for (int k = tid; k < p; k += NT) {
-    mri = fmaxf(mri, fabsf(S.ri[k])); mgx = fmaxf(mgx, fabsf(mx[k]));
+    const float gx = S.gx[k];
+    const float ri = gx + S.s[k] - __ldg(P.h + k);
+    if (!isfinite(ri)) nonfin += 1.f;
+    mri = fmaxf(mri, fabsf(ri)); mgx = fmaxf(mgx, fabsf(gx));
     gap = fmaf(S.s[k], S.z[k], gap);
   }
   for (int l = tid; l < m; l += NT) {
-    mre = fmaxf(mre, fabsf(S.re[l])); max_ = fmaxf(max_, fabsf(mx[p + l])); mb = fmaxf(mb, fabsf(__ldg(P.b + l)));
+    const float ax = S.gx[p + l], bl = __ldg(P.b + l);
+    mre = fmaxf(mre, fabsf(ax - bl)); max_ = fmaxf(max_, fabsf(ax)); mb = fmaxf(mb, fabsf(bl));
   }
   float v[17] = {gap, obj, nonfin, mrt, mre, mri, mrzs, mqx, mq, mgz, may, max_, mb, mgx, ms, mh, mz};
   block_reduce<NT, 3, 14>(v, S.red);
@@ -283,6 +320,7 @@ __device__ Norms residuals(const Smem& S, const Args& a, const Prob& P, float ka
   R.gap = v[0]; R.obj = v[1]; R.nonfin = v[2]; R.nrt = v[3]; R.nre = v[4]; R.nri = v[5]; R.nrzs = v[6];
   R.sQx = v[7]; R.sq = v[8]; R.sGz = v[9]; R.sAy = v[10]; R.sAx = v[11]; R.sb = v[12]; R.sGx = v[13];
   R.ss = v[14]; R.sh = v[15]; R.sz = v[16];
+  R.pa = pa;
   return R;
 }
 
@@ -324,31 +362,42 @@ __device__ float manifold_coords(const Smem& S, const Args& a) {
   return a.p > 0 ? v[0] / (float)a.p : 0.f;
 }
 
-// After solve_qd: Δx = rhs[0:n], w = rhs[n4:n4+p], Δy = rhs[n4+p:N];
-// Δv = GΔx + w; Δκ = −r_κ; Δz = −r_z + d₊Δv + cΔκ; Δs = −r_s − d₋Δv + cΔκ
-// (Eq. 13 rows 4-6).  Then α = min(1, τ α_max) (Eq. 6 + Q3), the step on
-// (x, y, v, κ) and the retraction.  Returns false (and leaves the
-// iterate untouched) if the direction is not finite.
+// Recover Δv from the reduced solution: Δv_i = g_iᵀΔx + w_i with w_i solved
+// (i ∈ A) or eliminated: w_i = (d₊_i g_iᵀΔx − f2_i)/d₋_i (v_i ≤ 0).  Writes
+// S.gx[k] = Δv_k.  (f2 = 0 for the adjoint.)
 template <int NT>
-__device__ bool newton_update(const Smem& S, const Args& a, const Prob& P, float& kappa, float r_kappa,
+__device__ void recover_dv(const Smem& S, const Args& a, const Prob& P, bool zero_f2) {
+  const int n4 = a.n4;
+  rowdots<NT>(P.G, a.p, a.n, S.rhs, [&](int k, float gdx) {
+    const int wi = S.widx[k];
+    const float w = wi >= 0 ? S.rhs[n4 + wi] : (S.dp[k] * gdx - (zero_f2 ? 0.f : S.f2[k])) / S.dm[k];
+    S.gx[k] = gdx + w;
+  });
+  __syncthreads();
+}
+
+// Δκ = −r_κ; Δz = −r_z + d₊Δv + cΔκ; Δs = −r_s − d₋Δv + cΔκ (Eq. 13 rows
+// 4-6); α = min(1, τ α_max) (Eq. 6 + Q3); step on (x, y, v, κ) and retract
+// (P:425-429).  Returns false (iterate untouched) if the direction is not
+// finite.
+template <int NT>
+__device__ bool newton_update(const Smem& S, const Args& a, const Prob& P, int pa, float& kappa, float r_kappa,
                               int* stage) {
   const int tid = threadIdx.x;
   const int n = a.n, n4 = a.n4, p = a.p, m = a.m;
   const float dk = -r_kappa;
-  rowdots<NT>(P.G, p, n, S.rhs, [&](int k, float gdx) { S.dv[k] = gdx + S.rhs[n4 + k]; });
-  __syncthreads();
+  recover_dv<NT>(S, a, P, false);
   float amax = INFINITY, bad = 0.f;
   for (int k = tid; k < p; k += NT) {
-    const float dv = S.dv[k];
+    const float dv = S.gx[k];
     const float dz = -S.rz[k] + S.dp[k] * dv + S.c[k] * dk;
     const float ds = -S.rs[k] - S.dm[k] * dv + S.c[k] * dk;
-    S.dz[k] = dz; S.ds[k] = ds;
     if (ds < 0.f) amax = fminf(amax, -S.s[k] / ds);
     if (dz < 0.f) amax = fminf(amax, -S.z[k] / dz);
     if (!isfinite(dz) || !isfinite(ds)) bad = 1.f;
   }
   for (int j = tid; j < n; j += NT) if (!isfinite(S.rhs[j])) bad = 1.f;
-  for (int l = tid; l < m; l += NT) if (!isfinite(S.rhs[n4 + p + l])) bad = 1.f;
+  for (int l = tid; l < m; l += NT) if (!isfinite(S.rhs[n4 + pa + l])) bad = 1.f;
   float vals[1] = {bad};
   block_reduce<NT, 0, 1>(vals, S.red);
   const float am = block_min<NT>(amax, S.red + 64);
@@ -356,10 +405,10 @@ __device__ bool newton_update(const Smem& S, const Args& a, const Prob& P, float
   const float alpha = fminf(1.f, a.tau * am);
   if (!(alpha > 0.f)) { *stage = STG_LINESEARCH; return false; }
   for (int j = tid; j < n; j += NT) S.x[j] = fmaf(alpha, S.rhs[j], S.x[j]);
-  for (int l = tid; l < m; l += NT) S.y[l] = fmaf(alpha, S.rhs[n4 + p + l], S.y[l]);
+  for (int l = tid; l < m; l += NT) S.y[l] = fmaf(alpha, S.rhs[n4 + pa + l], S.y[l]);
   const float kn = fmaf(alpha, dk, kappa);
   for (int k = tid; k < p; k += NT) {
-    const float vn = fmaf(alpha, S.dv[k], S.v[k]);
+    const float vn = fmaf(alpha, S.gx[k], S.v[k]);
     S.z[k] = ret_b(vn, kn);
     S.s[k] = ret_b(-vn, kn);
   }
@@ -371,8 +420,8 @@ __device__ bool newton_update(const Smem& S, const Args& a, const Prob& P, float
 // ------------------------------------------------------------------------
 // Kernel: initialisation (Q11) + Algorithm 1.
 // ------------------------------------------------------------------------
-template <int NT>
-__global__ void __launch_bounds__(NT, 3) ipm_solve_kernel(const Args a) {
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) ipm_solve_kernel(const Args a) {
   extern __shared__ __align__(16) float smem[];
   const int bid = blockIdx.x;
   const int tid = threadIdx.x;
@@ -381,12 +430,15 @@ __global__ void __launch_bounds__(NT, 3) ipm_solve_kernel(const Args a) {
   const int n = a.n, n4 = a.n4, p = a.p, m = a.m;
   int status = ST_CONVERGED, it = 0;
 
-  // ---- initialisation: solve [[Q, Gᵀ, Aᵀ], [G, −I, 0], [A, 0, 0]] (x, ẑ, y) = (−q, h, b)
-  // in the congruent form M(wH=1, wC=0, e=1)(x, w, y) = (−q + Gᵀh, h, b), ẑ = Gx + w = Gx − h.
-  for (int k = tid; k < p; k += NT) S.t[k] = 1.f;
-  __syncthreads();
+  // ---- initialisation: [[Q, Gᵀ, Aᵀ], [G, −I, 0], [A, 0, 0]] (x, ẑ, y) = (−q, h, b).
+  // The congruence ẑ = Gx + w decouples w = −h; the reduced matrix is
+  // [[Q + GᵀG, Aᵀ], [A, 0]] with right-hand side (−q + Gᵀh, b); ẑ = Gx − h.
   {
-    const float dmax = assemble<NT>(S, a, P, S.t, S.t, S.t, true, true);
+    for (int k = tid; k < p; k += NT) { S.om[k] = 1.f; S.v[k] = -1.f; }
+    __syncthreads();
+    compact_active<NT>(S, p, true);
+    const KLayout L = KLayout::make(n4 + m, n4);
+    const float dmax = assemble<NT>(S, a, P, L, 0, S.om, S.om, S.om);
     for (int j = tid; j < n4; j += NT) {
       float acc = 0.f;
       if (j < n) {
@@ -395,13 +447,12 @@ __global__ void __launch_bounds__(NT, 3) ipm_solve_kernel(const Args a) {
       }
       S.rhs[j] = acc;
     }
-    for (int k = tid; k < p; k += NT) S.rhs[n4 + k] = __ldg(P.h + k);
-    for (int l = tid; l < m; l += NT) S.rhs[n4 + p + l] = __ldg(P.b + l);
-    for (int j = a.N + tid; j < a.N4; j += NT) S.rhs[j] = 0.f;
-    factor_qd<NT>(S.K, a.kl, a.floor_rel * dmax, S.rinv, S.flag);
-    solve_qd<NT>(S.K, a.kl, S.rinv, S.rhs);
+    for (int l = tid; l < m; l += NT) S.rhs[n4 + l] = __ldg(P.b + l);
+    for (int j = L.N + tid; j < L.N4; j += NT) S.rhs[j] = 0.f;
+    factor_qd<NT>(S.K, L, a.floor_rel * dmax, S.rinv, S.flag);
+    solve_qd<NT>(S.K, L, S.rinv, S.rhs);
     for (int j = tid; j < n; j += NT) S.x[j] = S.rhs[j];
-    for (int l = tid; l < m; l += NT) S.y[l] = S.rhs[n4 + p + l];
+    for (int l = tid; l < m; l += NT) S.y[l] = S.rhs[n4 + l];
     __syncthreads();
     rowdots<NT>(P.G, p, n, S.x, [&](int k, float gx) { S.dz[k] = gx - __ldg(P.h + k); });  // ẑ
     __syncthreads();
@@ -434,11 +485,12 @@ __global__ void __launch_bounds__(NT, 3) ipm_solve_kernel(const Args a) {
       if (R.nonfin > 0.f) { status = ST_FAIL | (STG_SCALING << 8); break; }
       if (converged_solve(R, a.tol)) { status = ST_CONVERGED; break; }
       if (k == a.max_iter) { status = ST_MAX_ITER; break; }
-      const float dmax = assemble<NT>(S, a, P, S.dp, S.dp, S.dm, false, false);
-      factor_qd<NT>(S.K, a.kl, a.floor_rel * dmax, S.rinv, S.flag);
-      solve_qd<NT>(S.K, a.kl, S.rinv, S.rhs);
+      const KLayout L = KLayout::make(n4 + R.pa + m, n4);
+      const float dmax = assemble<NT>(S, a, P, L, R.pa, S.om, S.dp, S.dm);
+      factor_qd<NT>(S.K, L, a.floor_rel * dmax, S.rinv, S.flag);
+      solve_qd<NT>(S.K, L, S.rinv, S.rhs);
       int stage = 0;
-      if (!newton_update<NT>(S, a, P, kappa, kappa - kt, &stage)) { status = ST_FAIL | (stage << 8); break; }
+      if (!newton_update<NT>(S, a, P, R.pa, kappa, kappa - kt, &stage)) { status = ST_FAIL | (stage << 8); break; }
     }
   }
   // ---- outputs
@@ -455,11 +507,11 @@ __global__ void __launch_bounds__(NT, 3) ipm_solve_kernel(const Args a) {
 }
 
 // ------------------------------------------------------------------------
-// Kernel: Algorithm 2 (relax, exact Newton, factor-then-check: Q5, Q6) and
-// Algorithm 3 (sign reading Q7, dz = d₊⊙dv: Q8).
+// Kernel: Algorithm 2 (relax, exact Newton, factor-then-check: Q5, Q5b, Q6)
+// and Algorithm 3 (sign reading Q7, dz = d₊⊙dv: Q8).
 // ------------------------------------------------------------------------
-template <int NT>
-__global__ void __launch_bounds__(NT, 3) ipm_backward_kernel(const Args a) {
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) ipm_backward_kernel(const Args a) {
   extern __shared__ __align__(16) float smem[];
   const int bid = blockIdx.x;
   const int tid = threadIdx.x;
@@ -475,36 +527,42 @@ __global__ void __launch_bounds__(NT, 3) ipm_backward_kernel(const Args a) {
   __syncthreads();
   int status = (a.status[bid] & 0xff) == ST_CONVERGED ? ST_CONVERGED : (ST_FAIL | (STG_RELAX << 8));
   int it = 0;
+  KLayout L = KLayout::make(n4 + m, n4);
+  int pa = 0;
   if (status == ST_CONVERGED) {
     float phi_prev = INFINITY;
     for (int k = 0;; ++k) {
       float kappa = manifold_coords<NT>(S, a);
       const Norms R = residuals<NT>(S, a, P, kappa, kappa - a.kappa_relax);
-      const float dmax = assemble<NT>(S, a, P, S.dp, S.dp, S.dm, false, false);
-      factor_qd<NT>(S.K, a.kl, a.floor_rel * dmax, S.rinv, S.flag);
+      pa = R.pa;
+      L = KLayout::make(n4 + pa + m, n4);
+      const float dmax = assemble<NT>(S, a, P, L, pa, S.om, S.dp, S.dm);
+      factor_qd<NT>(S.K, L, a.floor_rel * dmax, S.rinv, S.flag);
       it = k;
       if (R.nonfin > 0.f) { status = ST_FAIL | (STG_RELAX << 8); break; }
       const bool kok = p == 0 || fabsf(kappa / a.kappa_relax - 1.f) <= a.relax_ktol;
       if (kok && relax_done(R, a.tol, a.relax_tol, phi_prev)) break;
       phi_prev = kok ? rel_phi(R) : INFINITY;
       if (k == a.relax_max_iter) { status = ST_MAX_ITER | (STG_RELAX << 8); break; }
-      solve_qd<NT>(S.K, a.kl, S.rinv, S.rhs);
+      solve_qd<NT>(S.K, L, S.rinv, S.rhs);
       int stage = 0;
-      if (!newton_update<NT>(S, a, P, kappa, kappa - a.kappa_relax, &stage)) {
+      if (!newton_update<NT>(S, a, P, pa, kappa, kappa - a.kappa_relax, &stage)) {
         status = ST_FAIL | (STG_RELAX << 8);
         break;
       }
     }
   }
-  // ---- Algorithm 3: M (dx, w, dy) = (−∇ₓℓ, 0, 0), dv = G dx + w, dz = d₊ ⊙ dv
+  // ---- Algorithm 3: reduced system with right-hand side (−∇ₓℓ, 0, 0);
+  //      dv = G dx + w, dz = d₊ ⊙ dv
   bool ok = status == ST_CONVERGED;
   if (ok) {
-    for (int j = tid; j < a.N4; j += NT) S.rhs[j] = j < n ? -__ldg(a.dl + (long long)bid * n + j) : 0.f;
+    for (int j = tid; j < L.N4; j += NT) S.rhs[j] = j < n ? -__ldg(a.dl + (long long)bid * n + j) : 0.f;
     __syncthreads();
-    solve_qd<NT>(S.K, a.kl, S.rinv, S.rhs);
-    rowdots<NT>(P.G, p, n, S.rhs, [&](int k, float gdx) { S.dz[k] = S.dp[k] * (gdx + S.rhs[n4 + k]); });
+    solve_qd<NT>(S.K, L, S.rinv, S.rhs);
+    recover_dv<NT>(S, a, P, true);
+    for (int k = tid; k < p; k += NT) S.dz[k] = S.dp[k] * S.gx[k];
     for (int j = tid; j < n; j += NT) S.dx[j] = S.rhs[j];
-    for (int l = tid; l < m; l += NT) S.dy[l] = S.rhs[n4 + p + l];
+    for (int l = tid; l < m; l += NT) S.dy[l] = S.rhs[n4 + pa + l];
     __syncthreads();
     float bad = 0.f;
     for (int j = tid; j < n; j += NT) if (!isfinite(S.dx[j])) bad = 1.f;

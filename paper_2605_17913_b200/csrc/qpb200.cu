@@ -17,22 +17,22 @@
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kMinBlocks = 3;  // register budget for 3 CTAs/SM (config-2 smem fits 3)
 constexpr size_t kMaxSmem = 232448;  // 227 KB opt-in dynamic shared memory per CTA (sm_100a)
 
 struct Layout {
-  int n4, nw, N, N4;
-  qpb::KLayout kl;
+  int n4, Nmax, N4max, ksize;
   size_t smem;
 };
 
 Layout make_layout(int n, int m, int p, int formulation) {
+  (void)formulation;
   Layout L;
   L.n4 = (n + 3) & ~3;
-  L.nw = formulation == QP_IMPLICIT ? p : 0;
-  L.N = L.n4 + L.nw + m;
-  L.N4 = (L.N + 3) & ~3;
-  L.kl = qpb::KLayout::make(L.N, L.n4);
-  L.smem = qpb::ipm_smem_bytes(L.n4, m, p, L.N4, L.kl.size());
+  L.Nmax = L.n4 + p + m;  // reduced system: n4 + |A| + m with |A| <= p
+  L.N4max = (L.Nmax + 3) & ~3;
+  L.ksize = qpb::KLayout::make(L.Nmax, L.n4).size();
+  L.smem = qpb::ipm_smem_bytes(L.n4, m, p, L.N4max, L.ksize);
   return L;
 }
 
@@ -95,7 +95,7 @@ qpb::Args base_args(const qp_ctx* c) {
   qpb::Args a;
   std::memset(&a, 0, sizeof(a));
   a.B = c->d.batch; a.n = c->d.n; a.m = c->d.m_eq; a.p = c->d.p;
-  a.n4 = c->L.n4; a.nw = c->L.nw; a.N = c->L.N; a.N4 = c->L.N4; a.kl = c->L.kl;
+  a.n4 = c->L.n4; a.Nmax = c->L.Nmax; a.N4max = c->L.N4max; a.ksize = c->L.ksize;
   a.sQ = c->d.bstride_Q; a.sq = c->d.bstride_q; a.sA = c->d.bstride_A;
   a.sb = c->d.bstride_b; a.sG = c->d.bstride_G; a.sh = c->d.bstride_h;
   a.tol = c->c.tol; a.sigma = c->c.sigma; a.tau = c->c.tau; a.kappa_relax = c->c.kappa_relax;
@@ -191,14 +191,14 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
   if (!ctx) return QP_ERR_OOM;
   ctx->d = *d; ctx->c = c; ctx->device = device; ctx->stream = static_cast<cudaStream_t>(stream); ctx->L = L;
   qp_err e = QP_OK;
-  if (cudaFuncSetAttribute(qpb::ipm_solve_kernel<kThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (cudaFuncSetAttribute(qpb::ipm_solve_kernel<kThreads, kMinBlocks>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)L.smem) != cudaSuccess ||
-      cudaFuncSetAttribute(qpb::ipm_backward_kernel<kThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(qpb::ipm_backward_kernel<kThreads, kMinBlocks>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)L.smem) != cudaSuccess) {
     delete ctx;
     return QP_ERR_CUDA;
   }
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->ctas_per_sm, qpb::ipm_solve_kernel<kThreads>, kThreads,
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->ctas_per_sm, qpb::ipm_solve_kernel<kThreads, kMinBlocks>, kThreads,
                                                 L.smem);
   const int B = d->batch, n = d->n, m = d->m_eq, p = d->p;
   if ((e = dalloc(ctx, &ctx->own_status, B)) != QP_OK) { free_all(ctx); delete ctx; return e; }
@@ -245,7 +245,7 @@ qp_err qp_get_info(const qp_ctx* c, qp_info* info) {
   info->threads = kThreads;
   info->smem_bytes = (int32_t)c->L.smem;
   info->ctas_per_sm = c->ctas_per_sm;
-  info->kkt_dim = c->L.N;
+  info->kkt_dim = c->L.Nmax;
   info->launches_solve = 1;
   const qp_dims& d = c->d;
   int extra = 0;
@@ -293,7 +293,7 @@ qp_err qp_solve_batched(qp_ctx* c, const float* Q, const float* q, const float* 
   a.x = c->x; a.y = c->y ? c->y : dummy; a.z = c->z ? c->z : dummy; a.s = c->s ? c->s : dummy;
   a.iters = host ? c->dit_ : iters;
   a.status = c->own_status;
-  qpb::ipm_solve_kernel<kThreads><<<B, kThreads, c->L.smem, c->stream>>>(a);
+  qpb::ipm_solve_kernel<kThreads, kMinBlocks><<<B, kThreads, c->L.smem, c->stream>>>(a);
   if ((e = cuda_ok(cudaGetLastError())) != QP_OK) return e;
   if (host) {
     if ((e = d2h(c, x, c->dx_, (size_t)B * n)) || (e = d2h(c, s, c->ds_, (size_t)B * p)) ||
@@ -353,7 +353,7 @@ qp_err qp_backward_batched(qp_ctx* c, const float* dl_dx, float* dQ, float* dq, 
   }
   a.riters = oit;
   a.rstatus = ost;
-  qpb::ipm_backward_kernel<kThreads><<<B, kThreads, c->L.smem, c->stream>>>(a);
+  qpb::ipm_backward_kernel<kThreads, kMinBlocks><<<B, kThreads, c->L.smem, c->stream>>>(a);
   if ((e = cuda_ok(cudaGetLastError())) != QP_OK) return e;
   if (shared) {
     auto osum = [&](float* out, const float* U, const float* V, const float* U2, const float* V2, int R, int Cc,

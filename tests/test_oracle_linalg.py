@@ -64,10 +64,11 @@ def test_condensation_matches_dense_eq13(orc, seed):
     # independent dense solve of Eq. 13 (library primitive) agrees
     ref = np.linalg.solve(K, rhs)
     assert np.allclose(sol, ref, rtol=1e-8, atol=1e-8 * np.abs(ref).max())
-    stm = orc.newton_step(prob, n, m, p, x, y, z, s, kt, solver=orc.SOLVER_M_LDL, floor_rel=1e-14)
-    assert stm["nfloor"] == 0
-    for k in ("dx", "dy", "dz", "ds", "dv"):
-        assert np.allclose(stm[k], st[k], rtol=1e-9, atol=1e-9 * max([1.0, *np.abs(st[k])])), k
+    for solver in (orc.SOLVER_M_LDL, orc.SOLVER_M_PART):
+        stm = orc.newton_step(prob, n, m, p, x, y, z, s, kt, solver=solver, floor_rel=1e-14)
+        assert stm["nfloor"] == 0
+        for k in ("dx", "dy", "dz", "ds", "dv"):
+            assert np.allclose(stm[k], st[k], rtol=1e-9, atol=1e-9 * max([1.0, *np.abs(st[k])])), (solver, k)
 
 
 def test_zero_residual_zero_step(orc):

@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--so", default=os.path.join(os.path.dirname(__file__), "..", "paper_2605_17913_b200",
                                                  "libqpb200.so"))
     ap.add_argument("--top", type=int, default=40)
+    ap.add_argument("--metric", default="Warp Stall Sampling (All Samples)",
+                    help="per-instruction column to aggregate, e.g. 'Instructions Executed'")
     a = ap.parse_args()
     out = subprocess.run(["ncu", "-i", a.report, "--page", "source", "--csv", "--kernel-name", f"regex:{a.kernel}",
                           "--print-source", "sass"], capture_output=True, text=True).stdout
@@ -32,7 +34,7 @@ def main():
     samples = {}
     for r in rows:
         try:
-            samples[int(r["Address"], 16)] = int(r["Warp Stall Sampling (All Samples)"] or 0)
+            samples[int(r["Address"], 16)] = int(r[a.metric] or 0)
         except (ValueError, KeyError):
             pass
     tmp = tempfile.mkdtemp()

@@ -164,7 +164,10 @@ __device__ __forceinline__ int factor_diag_block(float* __restrict__ K, const KL
 #pragma unroll
       for (int j = k + 1; j < KB; ++j) {
         const float ljk = __shfl_sync(0xffffffffu, a[k], j);
-        if (lane >= j) a[j] = fmaf(nl, ljk, a[j]);
+        // lane j already holds l_jk: its own update (which feeds the next
+        // pivot when j = k+1) does not wait for the shuffle
+        if (lane == j) a[j] = fmaf(nl, a[k], a[j]);
+        else if (lane > j) a[j] = fmaf(nl, ljk, a[j]);
       }
     }
   }
@@ -176,6 +179,46 @@ __device__ __forceinline__ int factor_diag_block(float* __restrict__ K, const KL
                                                                    a[4 * j4 + 3]);
   }
   return nfloor;
+}
+
+// ------------------------------------------------------------------------
+// W = L_bb⁻¹ for a factored diagonal block, by ONE warp (lane c computes
+// column c by forward substitution; L entries are broadcast reads).  The
+// strict lower part of W is stored TRANSPOSED in the unused strict upper
+// triangle of the diagonal block: W[r][c] (r > c) at row k0+c, column k0+r;
+// diag(W) = rinv.  Used by solve_qd to turn the serial diagonal-block
+// substitutions into 16×16 matrix-vector products.
+// ------------------------------------------------------------------------
+__device__ __forceinline__ void invert_diag_block(float* __restrict__ K, const KLayout& L, int b,
+                                                  const float* __restrict__ rinv) {
+  const int lane = threadIdx.x & 31;
+  const int k0 = KB * b, kb = L.bw(b);
+  const float* D = K + L.off(k0) + k0;
+  const int Lb = L.len(b);
+  float w[KB];
+#pragma unroll
+  for (int r = 0; r < KB; ++r) w[r] = 0.f;
+  const int c = lane;
+#pragma unroll
+  for (int r = 0; r < KB; ++r) {
+    if (r < kb) {
+      // w_r = (δ_rc − Σ_{j<r} L[r][j] w_j) / L[r][r]; two partial sums shorten the chain
+      float a0 = (r == c) ? 1.f : 0.f, a1 = 0.f;
+#pragma unroll
+      for (int j = 0; j < r; ++j) {
+        const float l = D[r * Lb + j];
+        if (j & 1) a1 = fmaf(-l, w[j], a1); else a0 = fmaf(-l, w[j], a0);
+      }
+      const float wr = (a0 + a1) * rinv[k0 + r];
+      w[r] = (r >= c) ? wr : 0.f;
+    }
+  }
+  if (c < kb) {
+    float* rowc = K + L.off(k0 + c) + k0;
+#pragma unroll
+    for (int r = 0; r < KB; ++r)
+      if (r > c && r < kb) rowc[r] = w[r];
+  }
 }
 
 // ------------------------------------------------------------------------
@@ -200,6 +243,7 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
   int nfloor = 0;
   if (warp == 0) nfloor += factor_diag_block(K, L, 0, theta, rinv);
   __syncthreads();
+  static_assert(NW >= 3, "factor_qd needs >= 3 warps");
   for (int b = 0; b + 1 < L.NB; ++b) {
     const int k0 = KB * b, r0 = k0 + KB;
     // ---- (1) TRSM of the panel rows below block b (full 16-wide panel) -------------
@@ -269,13 +313,15 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
     // ---- (3) warp 0: diagonal block b+1 ‖ warps 1..: trailing SYRK beyond block b+1 ----
     if (warp == 0) {
       nfloor += factor_diag_block(K, L, b + 1, theta, rinv);
+    } else if (warp == 1) {
+      invert_diag_block(K, L, b, rinv);
     } else {
       const int r2 = r0 + KB;
       if (r2 < N4) {
         const int T = (N4 - r2 + 31) >> 5;
         const int nst = T * (T + 1) / 2;
         const int ty = lane >> 3, tx = lane & 7;
-        for (int st = warp - 1; st < nst; st += NW - 1) {
+        for (int st = warp - 2; st < nst; st += NW - 2) {
           int I = (int)((sqrtf(8.f * st + 1.f) - 1.f) * 0.5f);
           while ((I + 1) * (I + 2) / 2 <= st) ++I;
           while (I * (I + 1) / 2 > st) --I;
@@ -339,6 +385,7 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
     }
     __syncthreads();
   }
+  if (warp == 1) invert_diag_block(K, L, L.NB - 1, rinv);
   if (tid == 0) *flag = nfloor;
   __syncthreads();
   const int r = *flag;
@@ -347,38 +394,41 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
 }
 
 // ------------------------------------------------------------------------
-// Solve M u = rhs in place with the factor of factor_qd (M = L S Lᵀ).
+// Solve M u = rhs in place with the factor of factor_qd (M = L S Lᵀ), using
+// the diagonal-block inverses W_b stored by invert_diag_block:
+//   forward  (per block b):  u_b = W_b r_b;  r_i −= L_ib u_b for rows below
+//   backward (per block b, last first):  x_b = W_bᵀ r_b;  r_j −= L_bjᵀ x_b above
 // rhs has N4 entries (padding entries must be 0 on entry).
 // ------------------------------------------------------------------------
 template <int NT>
 __device__ void solve_qd(const float* __restrict__ K, const KLayout& L, const float* __restrict__ rinv,
                          float* __restrict__ rhs) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const int N4 = L.N4;
   // forward: L u = b
   for (int b = 0; b < L.NB; ++b) {
     const int k0 = KB * b, kb = L.bw(b);
-    if (warp == 0) {
-      const float* row = K + L.off(k0 + (lane < kb ? lane : 0)) + k0;
-      float Lr[KB];
+    const float* D = K + L.off(k0) + k0;
+    const int Lb = L.len(b);
+    if (tid < 32) {
+      const int t = tid;
+      float r[KB];
 #pragma unroll
-      for (int j = 0; j < KB; ++j) Lr[j] = (lane < kb && j < lane) ? row[j] : 0.f;
-      float bv = lane < kb ? rhs[k0 + lane] : 0.f;
+      for (int c = 0; c < KB; ++c) r[c] = c < kb ? rhs[k0 + c] : 0.f;
+      __syncwarp();
+      if (t < kb) {
+        float acc = rinv[k0 + t] * r[t];
 #pragma unroll
-      for (int k = 0; k < KB; ++k) {
-        if (k < kb) {
-          const float uk = __shfl_sync(0xffffffffu, bv, k) * rinv[k0 + k];
-          if (lane == k) bv = uk;
-          else if (lane > k) bv = fmaf(-Lr[k], uk, bv);
-        }
+        for (int c = 0; c < KB; ++c)
+          if (c < t) acc = fmaf(D[c * Lb + t], r[c], acc);  // W[t][c] stored at row c, col t
+        rhs[k0 + t] = acc;
       }
-      if (lane < kb) rhs[k0 + lane] = bv;
     }
     __syncthreads();
     if (b + 1 < L.NB) {
+      const float4* u = reinterpret_cast<const float4*>(rhs + k0);
       for (int i = k0 + KB + tid; i < N4; i += NT) {
         const float4* row = reinterpret_cast<const float4*>(K + L.off(i) + k0);
-        const float4* u = reinterpret_cast<const float4*>(rhs + k0);
         float acc = rhs[i];
 #pragma unroll
         for (int j4 = 0; j4 < 4; ++j4) {
@@ -399,27 +449,26 @@ __device__ void solve_qd(const float* __restrict__ K, const KLayout& L, const fl
   // backward: Lᵀ x = u, blocks in reverse order
   for (int b = L.NB - 1; b >= 0; --b) {
     const int k0 = KB * b, kb = L.bw(b);
-    if (warp == 0) {
-      float Lc[KB];  // lane j holds column j of the diagonal block
-      const float* Bk = K + L.off(k0) + k0;
-      const int Lb = L.len(b);
+    const float* D = K + L.off(k0) + k0;
+    const int Lb = L.len(b);
+    if (tid < 32) {
+      const int t = tid;
+      float r[KB];
 #pragma unroll
-      for (int i = 0; i < KB; ++i) Lc[i] = (lane < kb && i < kb && i > lane) ? Bk[i * Lb + lane] : 0.f;
-      float bv = lane < kb ? rhs[k0 + lane] : 0.f;
+      for (int c = 0; c < KB; ++c) r[c] = c < kb ? rhs[k0 + c] : 0.f;
+      __syncwarp();
+      if (t < kb) {
+        float acc = rinv[k0 + t] * r[t];
+        const float* Dt = D + t * Lb;  // W[r][t] for r > t lives in row t, column r
 #pragma unroll
-      for (int k = KB - 1; k >= 0; --k) {
-        if (k < kb) {
-          const float xk = __shfl_sync(0xffffffffu, bv, k) * rinv[k0 + k];
-          if (lane == k) bv = xk;
-          else if (lane < k) bv = fmaf(-Lc[k], xk, bv);
-        }
+        for (int c = 0; c < KB; ++c)
+          if (c > t && c < kb) acc = fmaf(Dt[c], r[c], acc);
+        rhs[k0 + t] = acc;
       }
-      if (lane < kb) rhs[k0 + lane] = bv;
     }
     __syncthreads();
     if (b > 0) {
       const float* Bk = K + L.off(k0);
-      const int Lb = L.len(b);
       for (int j = tid; j < k0; j += NT) {
         float acc = rhs[j];
         for (int i = 0; i < kb; ++i) acc = fmaf(-Bk[i * Lb + j], rhs[k0 + i], acc);

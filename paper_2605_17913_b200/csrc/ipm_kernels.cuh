@@ -220,17 +220,31 @@ __device__ float assemble(const Smem& S, const Args& a, const Prob& P, const KLa
 }
 
 // Warp-per-row dot products Mat[r,:]·vec for r < rows (Mat global row-major
-// rows×n, vec in smem); fn(r, dot) runs on lane 0.
+// rows×n, vec in smem); each warp keeps 4 rows in flight so the loads and the
+// shuffle reductions overlap; fn(r, dot) runs on lane 0.
 template <int NT, typename F>
 __device__ __forceinline__ void rowdots(const float* __restrict__ Mat, int rows, int n, const float* vec, F fn) {
+  constexpr int NW = NT / 32, R = 4;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int r = warp; r < rows; r += NT / 32) {
-    const float* row = Mat + r * n;
-    float acc = 0.f;
-    for (int j = lane; j < n; j += 32) acc = fmaf(__ldg(row + j), vec[j], acc);
+  for (int r0 = warp * R; r0 < rows; r0 += NW * R) {
+    float acc[R];
 #pragma unroll
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) fn(r, acc);
+    for (int u = 0; u < R; ++u) acc[u] = 0.f;
+    for (int j = lane; j < n; j += 32) {
+      const float xv = vec[j];
+#pragma unroll
+      for (int u = 0; u < R; ++u)
+        if (r0 + u < rows) acc[u] = fmaf(__ldg(Mat + (r0 + u) * n + j), xv, acc[u]);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1)
+#pragma unroll
+      for (int u = 0; u < R; ++u) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
+    if (lane == 0) {
+#pragma unroll
+      for (int u = 0; u < R; ++u)
+        if (r0 + u < rows) fn(r0 + u, acc[u]);
+    }
   }
 }
 

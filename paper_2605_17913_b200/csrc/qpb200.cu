@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <cstdlib>
 #include <new>
 
 #include "../../include/qpb200.h"
@@ -16,8 +17,9 @@
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kMinBlocks = 3;  // register budget for 3 CTAs/SM (config-2 smem fits 3)
+// Two kernel shapes: 256 threads (register budget for 3 CTAs/SM) and 128
+// threads (same smem, 3 CTAs/SM, no register spills).  qp_create picks one;
+// QPB200_THREADS=128|256 overrides (experiments).
 constexpr size_t kMaxSmem = 232448;  // 227 KB opt-in dynamic shared memory per CTA (sm_100a)
 
 struct Layout {
@@ -36,6 +38,20 @@ Layout make_layout(int n, int m, int p, int formulation) {
   return L;
 }
 
+struct KernelSet {
+  int threads;
+  void (*solve)(const qpb::Args);
+  void (*backward)(const qpb::Args);
+};
+
+KernelSet pick_kernels(const Layout& L) {
+  int t = 128;
+  if (const char* e = getenv("QPB200_THREADS")) t = atoi(e) == 256 ? 256 : 128;
+  (void)L;
+  if (t == 256) return {256, qpb::ipm_solve_kernel<256, 3>, qpb::ipm_backward_kernel<256, 3>};
+  return {128, qpb::ipm_solve_kernel<128, 3>, qpb::ipm_backward_kernel<128, 3>};
+}
+
 bool aligned4(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 3u) == 0; }
 
 }  // namespace
@@ -46,6 +62,7 @@ struct qp_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   Layout L{};
+  KernelSet ks{};
   int ctas_per_sm = 0;
   bool solved = false;
   // pointers of the last solve (device memory)
@@ -191,15 +208,14 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
   if (!ctx) return QP_ERR_OOM;
   ctx->d = *d; ctx->c = c; ctx->device = device; ctx->stream = static_cast<cudaStream_t>(stream); ctx->L = L;
   qp_err e = QP_OK;
-  if (cudaFuncSetAttribute(qpb::ipm_solve_kernel<kThreads, kMinBlocks>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)L.smem) != cudaSuccess ||
-      cudaFuncSetAttribute(qpb::ipm_backward_kernel<kThreads, kMinBlocks>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)L.smem) != cudaSuccess) {
+  ctx->ks = pick_kernels(L);
+  if (cudaFuncSetAttribute(ctx->ks.solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem) != cudaSuccess ||
+      cudaFuncSetAttribute(ctx->ks.backward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem) !=
+          cudaSuccess) {
     delete ctx;
     return QP_ERR_CUDA;
   }
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->ctas_per_sm, qpb::ipm_solve_kernel<kThreads, kMinBlocks>, kThreads,
-                                                L.smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->ctas_per_sm, ctx->ks.solve, ctx->ks.threads, L.smem);
   const int B = d->batch, n = d->n, m = d->m_eq, p = d->p;
   if ((e = dalloc(ctx, &ctx->own_status, B)) != QP_OK) { free_all(ctx); delete ctx; return e; }
   if (any_shared(*d)) {
@@ -242,7 +258,7 @@ qp_err qp_set_stream(qp_ctx* c, void* stream) {
 qp_err qp_get_info(const qp_ctx* c, qp_info* info) {
   if (!c || !info) return QP_ERR_INVALID_ARG;
   info->path = 1;
-  info->threads = kThreads;
+  info->threads = c->ks.threads;
   info->smem_bytes = (int32_t)c->L.smem;
   info->ctas_per_sm = c->ctas_per_sm;
   info->kkt_dim = c->L.Nmax;
@@ -293,7 +309,7 @@ qp_err qp_solve_batched(qp_ctx* c, const float* Q, const float* q, const float* 
   a.x = c->x; a.y = c->y ? c->y : dummy; a.z = c->z ? c->z : dummy; a.s = c->s ? c->s : dummy;
   a.iters = host ? c->dit_ : iters;
   a.status = c->own_status;
-  qpb::ipm_solve_kernel<kThreads, kMinBlocks><<<B, kThreads, c->L.smem, c->stream>>>(a);
+  c->ks.solve<<<B, c->ks.threads, c->L.smem, c->stream>>>(a);
   if ((e = cuda_ok(cudaGetLastError())) != QP_OK) return e;
   if (host) {
     if ((e = d2h(c, x, c->dx_, (size_t)B * n)) || (e = d2h(c, s, c->ds_, (size_t)B * p)) ||
@@ -353,7 +369,7 @@ qp_err qp_backward_batched(qp_ctx* c, const float* dl_dx, float* dQ, float* dq, 
   }
   a.riters = oit;
   a.rstatus = ost;
-  qpb::ipm_backward_kernel<kThreads, kMinBlocks><<<B, kThreads, c->L.smem, c->stream>>>(a);
+  c->ks.backward<<<B, c->ks.threads, c->L.smem, c->stream>>>(a);
   if ((e = cuda_ok(cudaGetLastError())) != QP_OK) return e;
   if (shared) {
     auto osum = [&](float* out, const float* U, const float* V, const float* U2, const float* V2, int R, int Cc,

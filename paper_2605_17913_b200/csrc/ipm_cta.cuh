@@ -129,59 +129,6 @@ __device__ __forceinline__ float block_min(float a, float* red) {
 }
 
 // ------------------------------------------------------------------------
-// Diagonal block factorisation by ONE warp: block b (width kb ≤ 16) of the
-// packed matrix.  Lane r holds row r of the block in registers.  Step k: the
-// pivot comes from lane k (its diagonal is already final), column k is
-// scaled, and every lane updates its row; the next pivot only needs lane k+1's
-// own l_{k+1,k}, so the critical chain per step is shfl → rsqrt → mul → fma.
-// Returns the number of floored pivots (valid on every lane).
-// ------------------------------------------------------------------------
-__device__ __forceinline__ int factor_diag_block(float* __restrict__ K, const KLayout& L, int b, float theta,
-                                                 float* __restrict__ rinv) {
-  const int lane = threadIdx.x & 31;
-  const int k0 = KB * b, kb = L.bw(b);
-  float* row = K + L.off(k0 + (lane < kb ? lane : 0));
-  float a[KB];
-#pragma unroll
-  for (int j4 = 0; j4 < KB / 4; ++j4) {
-    float4 t = (lane < kb && 4 * j4 < kb) ? *reinterpret_cast<const float4*>(row + k0 + 4 * j4)
-                                          : make_float4(0.f, 0.f, 0.f, 0.f);
-    a[4 * j4] = t.x; a[4 * j4 + 1] = t.y; a[4 * j4 + 2] = t.z; a[4 * j4 + 3] = t.w;
-  }
-  int nfloor = 0;
-#pragma unroll
-  for (int k = 0; k < KB; ++k) {
-    if (k < kb) {
-      const float s = sgn_of(k0 + k, L.npos);
-      float d = s * __shfl_sync(0xffffffffu, a[k], k);
-      if (!(d >= theta)) { d = theta; ++nfloor; }
-      const float ri = rsqrtf(d);        // 1/l_kk
-      const float l = d * ri;            // l_kk
-      if (lane == k) a[k] = l;
-      else if (lane > k) a[k] *= s * ri;  // l_rk = a_rk / (s_k l_kk)
-      if (lane == 0) rinv[k0 + k] = ri;
-      const float nl = -s * a[k];
-#pragma unroll
-      for (int j = k + 1; j < KB; ++j) {
-        const float ljk = __shfl_sync(0xffffffffu, a[k], j);
-        // lane j already holds l_jk: its own update (which feeds the next
-        // pivot when j = k+1) does not wait for the shuffle
-        if (lane == j) a[j] = fmaf(nl, a[k], a[j]);
-        else if (lane > j) a[j] = fmaf(nl, ljk, a[j]);
-      }
-    }
-  }
-  if (lane < kb) {
-#pragma unroll
-    for (int j4 = 0; j4 < KB / 4; ++j4)
-      if (4 * j4 < kb)
-        *reinterpret_cast<float4*>(row + k0 + 4 * j4) = make_float4(a[4 * j4], a[4 * j4 + 1], a[4 * j4 + 2],
-                                                                   a[4 * j4 + 3]);
-  }
-  return nfloor;
-}
-
-// ------------------------------------------------------------------------
 // W = L_bb⁻¹ for a factored diagonal block, by ONE warp (lane c computes
 // column c by forward substitution; L entries are broadcast reads).  The
 // strict lower part of W is stored TRANSPOSED in the unused strict upper
@@ -222,15 +169,18 @@ __device__ __forceinline__ void invert_diag_block(float* __restrict__ K, const K
 }
 
 // ------------------------------------------------------------------------
-// Signed Cholesky of the packed matrix K (layout L), right-looking with a
-// depth-1 look-ahead, full 16-wide panels:
-//   prologue: warp 0 factors diagonal block 0
-//   for each block b with rows below it:
-//     (1) TRSM   rows i ≥ 16(b+1):  x L_bbᵀ = a, l = S_b x         (thread per row)
-//     (2) update block column b+1:  A[:, b+1] −= L[:, b] S_b L[b+1, b]ᵀ  (thread per row)
-//     (3) warp 0 factors diagonal block b+1 WHILE warps 1.. apply the rank-16
-//         update to the trailing lower triangle beyond block b+1 (32×32
-//         super-tiles, one warp each, 8×4 strided register tiles).
+// Signed Cholesky of the packed matrix K (layout L), right-looking, 16-wide
+// panels:
+//   for each block b:
+//     (1) panel factorisation by the whole CTA: every thread owns one (or
+//         RPT) rows of the panel [k0, N4) × [k0, k0+16) in registers; per
+//         column k one barrier, then every thread reads the pivot and the
+//         column-k entries of the diagonal-block rows (broadcast), scales its
+//         own l_ik and updates its row; diagonal-block rows publish their next
+//         column entry for the next step.
+//     (2) rank-16 update of the trailing lower triangle (SYRK): 32×32
+//         super-tiles, one warp each, 8×4 strided register tiles.
+//   finally every warp inverts diagonal blocks (W_b = L_bb⁻¹, for solve_qd).
 // A pivot on the wrong side of ±θ is replaced by ±θ (reading Q12) and
 // counted.  On exit K holds L (M = L S Lᵀ) and rinv[k] = 1/L[k][k].
 // ------------------------------------------------------------------------
@@ -238,154 +188,144 @@ template <int NT>
 __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float theta, float* __restrict__ rinv,
                          int* __restrict__ flag) {
   constexpr int NW = NT / 32;
+  constexpr int RPT = (256 + NT - 1) / NT;  // rows per thread (N4 ≤ 256)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int N4 = L.N4, npos = L.npos;
   int nfloor = 0;
-  if (warp == 0) nfloor += factor_diag_block(K, L, 0, theta, rinv);
-  __syncthreads();
-  static_assert(NW >= 3, "factor_qd needs >= 3 warps");
-  for (int b = 0; b + 1 < L.NB; ++b) {
-    const int k0 = KB * b, r0 = k0 + KB;
-    // ---- (1) TRSM of the panel rows below block b (full 16-wide panel) -------------
-    for (int i = r0 + tid; i < N4; i += NT) {
-      float* row = K + L.off(i) + k0;
-      float a[KB];
+  for (int b = 0; b < L.NB; ++b) {
+    const int k0 = KB * b, kb = L.bw(b), k1 = k0 + kb;
+    const float* D = K + L.off(k0) + k0;  // diagonal block, row j at D + j*Lb
+    const int Lb = L.len(b);
+    // ---- (1) panel factorisation ------------------------------------------------
+    float a[RPT][KB];
+    float* rowp[RPT];
+    bool has[RPT];
 #pragma unroll
-      for (int j4 = 0; j4 < 4; ++j4) {
-        const float4 t = reinterpret_cast<const float4*>(row)[j4];
-        a[4 * j4] = t.x; a[4 * j4 + 1] = t.y; a[4 * j4 + 2] = t.z; a[4 * j4 + 3] = t.w;
-      }
-      const float* D = K + L.off(k0) + k0;  // diagonal block: row j at D + j*Lb
-      const int Lb = L.len(b);
+    for (int u = 0; u < RPT; ++u) {
+      const int i = k0 + tid + u * NT;
+      has[u] = i < N4;
+      rowp[u] = K + L.off(has[u] ? i : k0) + k0;
 #pragma unroll
-      for (int k = 0; k < KB; ++k) {
-        const float xk = a[k] * rinv[k0 + k];
-        a[k] = xk;
-#pragma unroll
-        for (int j = k + 1; j < KB; ++j) a[j] = fmaf(-xk, D[j * Lb + k], a[j]);
-      }
-#pragma unroll
-      for (int j4 = 0; j4 < 4; ++j4) {
-        const float s0 = sgn_of(k0 + 4 * j4, npos);  // npos is a multiple of 4
-        reinterpret_cast<float4*>(row)[j4] =
-            make_float4(s0 * a[4 * j4], s0 * a[4 * j4 + 1], s0 * a[4 * j4 + 2], s0 * a[4 * j4 + 3]);
+      for (int j4 = 0; j4 < KB / 4; ++j4) {
+        const float4 t = (has[u] && 4 * j4 < kb) ? reinterpret_cast<const float4*>(rowp[u])[j4]
+                                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+        a[u][4 * j4] = t.x; a[u][4 * j4 + 1] = t.y; a[u][4 * j4 + 2] = t.z; a[u][4 * j4 + 3] = t.w;
       }
     }
-    __syncthreads();
-    // ---- (2) look-ahead: block column b+1, rows i ≥ r0 -------------------------------
-    const int w1 = L.bw(b + 1);
-    const float* B1 = K + L.off(r0) + k0;  // rows of block b+1, panel columns of block b
-    const int L1 = L.len(b + 1);
-    for (int i = r0 + tid; i < N4; i += NT) {
-      const float* li = K + L.off(i) + k0;
-      float* ai = K + L.off(i) + r0;
-      float lv[KB];
 #pragma unroll
-      for (int j4 = 0; j4 < 4; ++j4) {
-        float4 t = reinterpret_cast<const float4*>(li)[j4];
-        const float s0 = sgn_of(k0 + 4 * j4, npos);
-        lv[4 * j4] = s0 * t.x; lv[4 * j4 + 1] = s0 * t.y; lv[4 * j4 + 2] = s0 * t.z; lv[4 * j4 + 3] = s0 * t.w;
-      }
+    for (int k = 0; k < KB; ++k) {
+      if (k < kb) {
+        __syncthreads();
+        const float s = sgn_of(k0 + k, npos);
+        float d = s * D[k * Lb + k];
+        const bool fl = !(d >= theta);
+        if (fl) d = theta;
+        const float rs = rsqrtf(d);  // 1/l_kk
+        if (tid == 0) { rinv[k0 + k] = rs; nfloor += fl; }
+        const float sr = s * rs;
+        float lc[KB];
 #pragma unroll
-      for (int c4 = 0; c4 < KB / 4; ++c4) {
-        if (4 * c4 < w1) {
-          float4 acc = reinterpret_cast<const float4*>(ai)[c4];
-          float accv[4] = {acc.x, acc.y, acc.z, acc.w};
+        for (int j = k + 1; j < KB; ++j) lc[j] = (j < kb) ? D[j * Lb + k] * sr : 0.f;
 #pragma unroll
-          for (int cc = 0; cc < 4; ++cc) {
-            const float* lj = B1 + (4 * c4 + cc) * L1;
-            float t = accv[cc];
+        for (int u = 0; u < RPT; ++u) {
+          const int il = tid + u * NT;  // row index relative to k0
+          if (has[u]) {
+            if (il == k) {
+              a[u][k] = d * rs;  // l_kk
+            } else if (il > k) {
+              const float l = a[u][k] * sr;  // l_ik = a_ik / (s_k l_kk)
+              a[u][k] = l;
+              const float nl = -s * l;
 #pragma unroll
-            for (int k4 = 0; k4 < 4; ++k4) {
-              const float4 u = reinterpret_cast<const float4*>(lj)[k4];
-              t = fmaf(-lv[4 * k4], u.x, t);
-              t = fmaf(-lv[4 * k4 + 1], u.y, t);
-              t = fmaf(-lv[4 * k4 + 2], u.z, t);
-              t = fmaf(-lv[4 * k4 + 3], u.w, t);
+              for (int j = k + 1; j < KB; ++j)
+                if (j < kb && j <= il) a[u][j] = fmaf(nl, lc[j], a[u][j]);
+              if (k + 1 < kb && il < kb) rowp[u][k + 1] = a[u][k + 1];  // publish column k+1
             }
-            accv[cc] = t;
           }
-          reinterpret_cast<float4*>(ai)[c4] = make_float4(accv[0], accv[1], accv[2], accv[3]);
         }
       }
     }
-    __syncthreads();
-    // ---- (3) warp 0: diagonal block b+1 ‖ warps 1..: trailing SYRK beyond block b+1 ----
-    if (warp == 0) {
-      nfloor += factor_diag_block(K, L, b + 1, theta, rinv);
-    } else if (warp == 1) {
-      invert_diag_block(K, L, b, rinv);
-    } else {
-      const int r2 = r0 + KB;
-      if (r2 < N4) {
-        const int T = (N4 - r2 + 31) >> 5;
-        const int nst = T * (T + 1) / 2;
-        const int ty = lane >> 3, tx = lane & 7;
-        for (int st = warp - 2; st < nst; st += NW - 2) {
-          int I = (int)((sqrtf(8.f * st + 1.f) - 1.f) * 0.5f);
-          while ((I + 1) * (I + 2) / 2 <= st) ++I;
-          while (I * (I + 1) / 2 > st) --I;
-          const int J = st - I * (I + 1) / 2;
-          const int rb = r2 + 32 * I + ty, cb = r2 + 32 * J + tx;
-          int roff[8], coff[4];
-          bool rok[8], cok[4];
 #pragma unroll
-          for (int a = 0; a < 8; ++a) {
-            const int r = rb + 4 * a;
-            rok[a] = r < N4;
-            roff[a] = rok[a] ? L.off(r) : 0;
+    for (int u = 0; u < RPT; ++u)
+      if (has[u]) {
+#pragma unroll
+        for (int j4 = 0; j4 < KB / 4; ++j4)
+          if (4 * j4 < kb)
+            reinterpret_cast<float4*>(rowp[u])[j4] =
+                make_float4(a[u][4 * j4], a[u][4 * j4 + 1], a[u][4 * j4 + 2], a[u][4 * j4 + 3]);
+      }
+    __syncthreads();
+    // ---- (2) trailing update A22 −= L21 S_b L21ᵀ --------------------------------
+    if (k1 < N4) {
+      const int T = (N4 - k1 + 31) >> 5;
+      const int nst = T * (T + 1) / 2;
+      const int ty = lane >> 3, tx = lane & 7;
+      for (int st = warp; st < nst; st += NW) {
+        int I = (int)((sqrtf(8.f * st + 1.f) - 1.f) * 0.5f);
+        while ((I + 1) * (I + 2) / 2 <= st) ++I;
+        while (I * (I + 1) / 2 > st) --I;
+        const int J = st - I * (I + 1) / 2;
+        const int rb = k1 + 32 * I + ty, cb = k1 + 32 * J + tx;
+        int roff[8], coff[4];
+        bool rok[8], cok[4];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int r = rb + 4 * q;
+          rok[q] = r < N4;
+          roff[q] = rok[q] ? L.off(r) : 0;
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int cc = cb + 8 * c;
+          cok[c] = cc < N4;
+          coff[c] = cok[c] ? L.off(cc) : 0;
+        }
+        float acc[8][4];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[q][c] = (rok[q] && cok[c]) ? K[roff[q] + cb + 8 * c] : 0.f;
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          // S_b applied to the column operand (npos is a multiple of 4)
+          const float sq = k0 + 4 * q4 < npos ? -1.f : 1.f;
+          float4 lc[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            float4 t = cok[c] ? *reinterpret_cast<const float4*>(K + coff[c] + k0 + 4 * q4)
+                              : make_float4(0, 0, 0, 0);
+            t.x *= sq; t.y *= sq; t.z *= sq; t.w *= sq;
+            lc[c] = t;
           }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 lr = rok[q] ? *reinterpret_cast<const float4*>(K + roff[q] + k0 + 4 * q4)
+                                     : make_float4(0, 0, 0, 0);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              float t = acc[q][c];
+              t = fmaf(lr.x, lc[c].x, t);
+              t = fmaf(lr.y, lc[c].y, t);
+              t = fmaf(lr.z, lc[c].z, t);
+              t = fmaf(lr.w, lc[c].w, t);
+              acc[q][c] = t;
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             const int cc = cb + 8 * c;
-            cok[c] = cc < N4;
-            coff[c] = cok[c] ? L.off(cc) : 0;
+            // lower triangle only (a diagonal block's upper part is never touched)
+            if (rok[q] && cok[c] && cc <= rb + 4 * q) K[roff[q] + cc] = acc[q][c];
           }
-          float acc[8][4];
-#pragma unroll
-          for (int a = 0; a < 8; ++a)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) acc[a][c] = (rok[a] && cok[c]) ? K[roff[a] + cb + 8 * c] : 0.f;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            // S_b applied to the column operand (npos is a multiple of 4)
-            const float sq = k0 + 4 * q < npos ? -1.f : 1.f;
-            float4 lc[4];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              float4 t = cok[c] ? *reinterpret_cast<const float4*>(K + coff[c] + k0 + 4 * q) : make_float4(0, 0, 0, 0);
-              t.x *= sq; t.y *= sq; t.z *= sq; t.w *= sq;
-              lc[c] = t;
-            }
-#pragma unroll
-            for (int a = 0; a < 8; ++a) {
-              const float4 lr = rok[a] ? *reinterpret_cast<const float4*>(K + roff[a] + k0 + 4 * q)
-                                       : make_float4(0, 0, 0, 0);
-#pragma unroll
-              for (int c = 0; c < 4; ++c) {
-                float t = acc[a][c];
-                t = fmaf(lr.x, lc[c].x, t);
-                t = fmaf(lr.y, lc[c].y, t);
-                t = fmaf(lr.z, lc[c].z, t);
-                t = fmaf(lr.w, lc[c].w, t);
-                acc[a][c] = t;
-              }
-            }
-          }
-#pragma unroll
-          for (int a = 0; a < 8; ++a)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              const int cc = cb + 8 * c;
-              // lower triangle only (the diagonal block's upper part is never touched)
-              if (rok[a] && cok[c] && cc <= rb + 4 * a) K[roff[a] + cc] = acc[a][c];
-            }
-        }
       }
+      __syncthreads();
     }
-    __syncthreads();
   }
-  if (warp == 1) invert_diag_block(K, L, L.NB - 1, rinv);
+  // ---- W_b = L_bb⁻¹ for every diagonal block (solve_qd) -------------------------
+  for (int b = warp; b < L.NB; b += NW) invert_diag_block(K, L, b, rinv);
   if (tid == 0) *flag = nfloor;
   __syncthreads();
   const int r = *flag;

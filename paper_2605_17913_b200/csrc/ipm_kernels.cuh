@@ -38,6 +38,7 @@ struct Args {
   int *riters, *rstatus;
   float tol, sigma, tau, kappa_relax, relax_ktol, floor_rel, relax_tol;
   int max_iter, relax_max_iter;
+  unsigned long long* prof;  // optional per-CTA phase cycle counters (diagnostics; nullptr = off)
 };
 
 // Shared-memory carve-up (floats).  Every segment is a multiple of 4 floats
@@ -490,22 +491,33 @@ __global__ void __launch_bounds__(NT, MINB) ipm_solve_kernel(const Args a) {
   }
 
   // ---- Algorithm 1 -----------------------------------------------------------
+  unsigned long long tph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long t0 = clock64();
   if (status == ST_CONVERGED) {
     for (int k = 0;; ++k) {
       float kappa = manifold_coords<NT>(S, a);
       const float kt = a.sigma * kappa;  // κ_target = σκ
       const Norms R = residuals<NT>(S, a, P, kappa, kappa - kt);
+      long long t1 = clock64(); tph[0] += t1 - t0; t0 = t1;
       it = k;
       if (R.nonfin > 0.f) { status = ST_FAIL | (STG_SCALING << 8); break; }
       if (converged_solve(R, a.tol)) { status = ST_CONVERGED; break; }
       if (k == a.max_iter) { status = ST_MAX_ITER; break; }
       const KLayout L = KLayout::make(n4 + R.pa + m, n4);
+      tph[5] += R.pa; tph[6] += L.N;
       const float dmax = assemble<NT>(S, a, P, L, R.pa, S.om, S.dp, S.dm);
+      t1 = clock64(); tph[1] += t1 - t0; t0 = t1;
       factor_qd<NT>(S.K, L, a.floor_rel * dmax, S.rinv, S.flag);
+      t1 = clock64(); tph[2] += t1 - t0; t0 = t1;
       solve_qd<NT>(S.K, L, S.rinv, S.rhs);
+      t1 = clock64(); tph[3] += t1 - t0; t0 = t1;
       int stage = 0;
       if (!newton_update<NT>(S, a, P, R.pa, kappa, kappa - kt, &stage)) { status = ST_FAIL | (stage << 8); break; }
+      t1 = clock64(); tph[4] += t1 - t0; t0 = t1;
     }
+  }
+  if (a.prof && tid == 0) {
+    for (int i = 0; i < 8; ++i) a.prof[bid * 8 + i] = tph[i];
   }
   // ---- outputs
   for (int j = tid; j < n; j += NT) a.x[(long long)bid * n + j] = S.x[j];

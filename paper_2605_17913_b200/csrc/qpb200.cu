@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <cstdio>
 #include <cstdlib>
 #include <new>
 
@@ -78,6 +79,7 @@ struct qp_ctx {
   int32_t *dit_ = nullptr, *dst_ = nullptr;
   float *gQ_ = nullptr, *gq_ = nullptr, *gA_ = nullptr, *gb_ = nullptr, *gG_ = nullptr, *gh_ = nullptr;
   int64_t workspace = 0;
+  unsigned long long* prof = nullptr;  // QPB200_PHASE_PROFILE diagnostics
 };
 
 namespace {
@@ -309,6 +311,8 @@ qp_err qp_solve_batched(qp_ctx* c, const float* Q, const float* q, const float* 
   a.x = c->x; a.y = c->y ? c->y : dummy; a.z = c->z ? c->z : dummy; a.s = c->s ? c->s : dummy;
   a.iters = host ? c->dit_ : iters;
   a.status = c->own_status;
+  if (getenv("QPB200_PHASE_PROFILE") && !c->prof) cudaMalloc(&c->prof, sizeof(unsigned long long) * 8 * B);
+  a.prof = c->prof;
   c->ks.solve<<<B, c->ks.threads, c->L.smem, c->stream>>>(a);
   if ((e = cuda_ok(cudaGetLastError())) != QP_OK) return e;
   if (host) {
@@ -323,6 +327,18 @@ qp_err qp_solve_batched(qp_ctx* c, const float* Q, const float* q, const float* 
       return e;
   }
   c->solved = true;
+  if (c->prof) {
+    cudaStreamSynchronize(c->stream);
+    unsigned long long* hp = new unsigned long long[8 * (size_t)B];
+    cudaMemcpy(hp, c->prof, sizeof(unsigned long long) * 8 * B, cudaMemcpyDeviceToHost);
+    double tot[8] = {0};
+    for (int i = 0; i < B; ++i)
+      for (int j = 0; j < 8; ++j) tot[j] += (double)hp[i * 8 + j];
+    fprintf(stderr, "[qpb200 phase cycles per CTA] resid %.0f assemble %.0f factor %.0f solve %.0f update %.0f"
+                    " | sum pa %.1f sum N %.1f\n",
+            tot[0] / B, tot[1] / B, tot[2] / B, tot[3] / B, tot[4] / B, tot[5] / B, tot[6] / B);
+    delete[] hp;
+  }
   return QP_OK;
 }
 

@@ -196,7 +196,9 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
     const int k0 = KB * b, kb = L.bw(b), k1 = k0 + kb;
     const float* D = K + L.off(k0) + k0;  // diagonal block, row j at D + j*Lb
     const int Lb = L.len(b);
-    // ---- (1) panel factorisation ------------------------------------------------
+    // ---- (1) panel factorisation (unscaled LDLᵀ updates: a_ij −= a_ik a_jk / a_kk,
+    //      column k is read-only during step k, so one barrier per column suffices;
+    //      the columns are scaled to L at the end: l_ik = a_ik s_k / l_kk) ----------
     float a[RPT][KB];
     float* rowp[RPT];
     bool has[RPT];
@@ -212,42 +214,59 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
         a[u][4 * j4] = t.x; a[u][4 * j4 + 1] = t.y; a[u][4 * j4 + 2] = t.z; a[u][4 * j4 + 3] = t.w;
       }
     }
+    // runtime k loop (compact code: the body stays in the instruction cache);
+    // a[u][k] is selected with an unrolled compare instead of dynamic indexing
+    for (int k = 0; k < kb; ++k) {
+      __syncthreads();
+      const float s = sgn_of(k0 + k, npos);
+      float d = s * D[k * Lb + k];
+      const bool fl = !(d >= theta);
+      if (fl) d = theta;
+      const float rs = rsqrtf(d);  // 1/l_kk
+      if (tid == 0) { rinv[k0 + k] = rs; nfloor += fl; }
+      const float inv = s * rs * rs;  // 1/a_kk (floored)
+      float col[KB];
 #pragma unroll
-    for (int k = 0; k < KB; ++k) {
-      if (k < kb) {
-        __syncthreads();
-        const float s = sgn_of(k0 + k, npos);
-        float d = s * D[k * Lb + k];
-        const bool fl = !(d >= theta);
-        if (fl) d = theta;
-        const float rs = rsqrtf(d);  // 1/l_kk
-        if (tid == 0) { rinv[k0 + k] = rs; nfloor += fl; }
-        const float sr = s * rs;
-        float lc[KB];
+      for (int j = 0; j < KB; ++j) col[j] = (j > k && j < kb) ? D[j * Lb + k] : 0.f;
 #pragma unroll
-        for (int j = k + 1; j < KB; ++j) lc[j] = (j < kb) ? D[j * Lb + k] * sr : 0.f;
+      for (int u = 0; u < RPT; ++u) {
+        const int il = tid + u * NT;  // row index relative to k0
+        if (has[u] && il > k) {
+          float aik = 0.f;
 #pragma unroll
-        for (int u = 0; u < RPT; ++u) {
-          const int il = tid + u * NT;  // row index relative to k0
-          if (has[u]) {
-            if (il == k) {
-              a[u][k] = d * rs;  // l_kk
-            } else if (il > k) {
-              const float l = a[u][k] * sr;  // l_ik = a_ik / (s_k l_kk)
-              a[u][k] = l;
-              const float nl = -s * l;
+          for (int j = 0; j < KB; ++j) aik = (j == k) ? a[u][j] : aik;
+          const float f = -aik * inv;
+          float nxt = 0.f;
 #pragma unroll
-              for (int j = k + 1; j < KB; ++j)
-                if (j < kb && j <= il) a[u][j] = fmaf(nl, lc[j], a[u][j]);
-              if (k + 1 < kb && il < kb) rowp[u][k + 1] = a[u][k + 1];  // publish column k+1
-            }
+          for (int j = 0; j < KB; ++j) {
+            if (j > k && j <= il) a[u][j] = fmaf(f, col[j], a[u][j]);
+            nxt = (j == k + 1) ? a[u][j] : nxt;
           }
+          if (k + 1 < kb && il < kb) rowp[u][k + 1] = nxt;  // publish column k+1
         }
+      }
+    }
+    // scale the panel columns to L: l_ik = a_ik s_k / l_kk, l_kk = √(s_k a_kk)
+    __syncthreads();
+    float srk[KB];
+#pragma unroll
+    for (int j = 0; j < KB; ++j) srk[j] = j < kb ? sgn_of(k0 + j, npos) * rinv[k0 + j] : 0.f;
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      const int il = tid + u * NT;
+      if (has[u] && il < kb) {  // diagonal entry: l_ii = s_i a_ii / l_ii... = √(s_i a_ii)
+#pragma unroll
+        for (int j = 0; j < KB; ++j)
+          if (j == il) a[u][j] = 1.f / rinv[k0 + j];
       }
     }
 #pragma unroll
     for (int u = 0; u < RPT; ++u)
       if (has[u]) {
+        const int il = tid + u * NT;
+#pragma unroll
+        for (int j = 0; j < KB; ++j)
+          if (j < il) a[u][j] *= srk[j];
 #pragma unroll
         for (int j4 = 0; j4 < KB / 4; ++j4)
           if (4 * j4 < kb)

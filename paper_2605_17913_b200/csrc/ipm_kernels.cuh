@@ -220,11 +220,14 @@ __device__ float assemble(const Smem& S, const Args& a, const Prob& P, const KLa
   return vals[0];
 }
 
-// Warp-per-row dot products Mat[r,:]·vec for r < rows (Mat global row-major
-// rows×n, vec in smem); each warp keeps 4 rows in flight so the loads and the
-// shuffle reductions overlap; fn(r, dot) runs on lane 0.
-template <int NT, typename F>
-__device__ __forceinline__ void rowdots(const float* __restrict__ Mat, int rows, int n, const float* vec, F fn) {
+// Warp-per-row dot products out[r] = Mat[r,:]·vec for r < rows (Mat global
+// row-major rows×n, vec and out in shared memory); each warp keeps 4 rows in
+// flight so the loads and the shuffle reductions overlap.  Not inlined: one
+// copy of the code serves every call site (instruction-cache footprint).
+// Ends with a barrier.
+template <int NT>
+__device__ __noinline__ void rowdots(const float* __restrict__ Mat, int rows, int n, const float* vec,
+                                     float* out) {
   constexpr int NW = NT / 32, R = 4;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int r0 = warp * R; r0 < rows; r0 += NW * R) {
@@ -241,12 +244,14 @@ __device__ __forceinline__ void rowdots(const float* __restrict__ Mat, int rows,
     for (int o = 16; o; o >>= 1)
 #pragma unroll
       for (int u = 0; u < R; ++u) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
-    if (lane == 0) {
+    if (lane < R && r0 + lane < rows) {
+      float v = acc[0];
 #pragma unroll
-      for (int u = 0; u < R; ++u)
-        if (r0 + u < rows) fn(r0 + u, acc[u]);
+      for (int u = 1; u < R; ++u) v = lane == u ? acc[u] : v;
+      out[r0 + lane] = v;
     }
   }
+  __syncthreads();
 }
 
 // ------------------------------------------------------------------------
@@ -281,19 +286,17 @@ __device__ Norms residuals(const Smem& S, const Args& a, const Prob& P, float ka
   }
   const int pa = compact_active<NT>(S, p, false);
   // rows: r_i = Gx + s − h, r_e = Ax − b (warp per row); f2, t, rhs_w, rhs_y
-  rowdots<NT>(P.G, p, n, S.x, [&](int k, float gx) {
-    const float ri = gx + S.s[k] - __ldg(P.h + k);
+  rowdots<NT>(P.G, p, n, S.x, S.gx);
+  rowdots<NT>(P.A, m, n, S.x, S.gx + p);
+  for (int k = tid; k < p; k += NT) {
+    const float ri = S.gx[k] + S.s[k] - __ldg(P.h + k);
     const float f2 = -(ri - S.rs[k] - S.c[k] * r_kappa);
     S.f2[k] = f2;
-    S.gx[k] = gx;
     S.t[k] = fmaf(S.c[k], r_kappa, S.rz[k]) + (S.v[k] > 0.f ? 0.f : S.om[k] * f2);
     const int wi = S.widx[k];
     if (wi >= 0) S.rhs[n4 + wi] = f2;
-  });
-  rowdots<NT>(P.A, m, n, S.x, [&](int l, float ax) {
-    S.rhs[n4 + pa + l] = -(ax - __ldg(P.b + l));
-    S.gx[p + l] = ax;
-  });
+  }
+  for (int l = tid; l < m; l += NT) S.rhs[n4 + pa + l] = -(S.gx[p + l] - __ldg(P.b + l));
   __syncthreads();
   // columns j < n: Qx, Gᵀz, Aᵀy, Gᵀt  (Q symmetric ⇒ (Qx)_j = Σ_i Q_ij x_i)
   float mrt = 0.f, mqx = 0.f, mq = 0.f, mgz = 0.f, may = 0.f, obj = 0.f;
@@ -383,11 +386,13 @@ __device__ float manifold_coords(const Smem& S, const Args& a) {
 template <int NT>
 __device__ void recover_dv(const Smem& S, const Args& a, const Prob& P, bool zero_f2) {
   const int n4 = a.n4;
-  rowdots<NT>(P.G, a.p, a.n, S.rhs, [&](int k, float gdx) {
+  rowdots<NT>(P.G, a.p, a.n, S.rhs, S.gx);
+  for (int k = threadIdx.x; k < a.p; k += NT) {
+    const float gdx = S.gx[k];
     const int wi = S.widx[k];
     const float w = wi >= 0 ? S.rhs[n4 + wi] : (S.dp[k] * gdx - (zero_f2 ? 0.f : S.f2[k])) / S.dm[k];
     S.gx[k] = gdx + w;
-  });
+  }
   __syncthreads();
 }
 
@@ -434,6 +439,9 @@ __device__ bool newton_update(const Smem& S, const Args& a, const Prob& P, int p
 
 // ------------------------------------------------------------------------
 // Kernel: initialisation (Q11) + Algorithm 1.
+// The loop is written so that assemble / factor_qd / solve_qd have ONE call
+// site (iteration −1 is the initialisation): the kernel stays small enough for
+// the instruction cache.
 // ------------------------------------------------------------------------
 template <int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) ipm_solve_kernel(const Args a) {
@@ -444,77 +452,78 @@ __global__ void __launch_bounds__(NT, MINB) ipm_solve_kernel(const Args a) {
   const Prob P = prob_of(a, bid);
   const int n = a.n, n4 = a.n4, p = a.p, m = a.m;
   int status = ST_CONVERGED, it = 0;
-
-  // ---- initialisation: [[Q, Gᵀ, Aᵀ], [G, −I, 0], [A, 0, 0]] (x, ẑ, y) = (−q, h, b).
-  // The congruence ẑ = Gx + w decouples w = −h; the reduced matrix is
-  // [[Q + GᵀG, Aᵀ], [A, 0]] with right-hand side (−q + Gᵀh, b); ẑ = Gx − h.
-  {
-    for (int k = tid; k < p; k += NT) { S.om[k] = 1.f; S.v[k] = -1.f; }
-    __syncthreads();
-    compact_active<NT>(S, p, true);
-    const KLayout L = KLayout::make(n4 + m, n4);
-    const float dmax = assemble<NT>(S, a, P, L, 0, S.om, S.om, S.om);
-    for (int j = tid; j < n4; j += NT) {
-      float acc = 0.f;
-      if (j < n) {
-        acc = -__ldg(P.q + j);
-        for (int k = 0; k < p; ++k) acc = fmaf(__ldg(P.G + k * n + j), __ldg(P.h + k), acc);
-      }
-      S.rhs[j] = acc;
-    }
-    for (int l = tid; l < m; l += NT) S.rhs[n4 + l] = __ldg(P.b + l);
-    for (int j = L.N + tid; j < L.N4; j += NT) S.rhs[j] = 0.f;
-    factor_qd<NT>(S.K, L, a.floor_rel * dmax, S.rinv, S.flag);
-    solve_qd<NT>(S.K, L, S.rinv, S.rhs);
-    for (int j = tid; j < n; j += NT) S.x[j] = S.rhs[j];
-    for (int l = tid; l < m; l += NT) S.y[l] = S.rhs[n4 + l];
-    __syncthreads();
-    rowdots<NT>(P.G, p, n, S.x, [&](int k, float gx) { S.dz[k] = gx - __ldg(P.h + k); });  // ẑ
-    __syncthreads();
-    float ap = -INFINITY, ad = -INFINITY, bad = 0.f;
-    for (int k = tid; k < p; k += NT) {
-      const float zh = S.dz[k];
-      ap = fmaxf(ap, zh); ad = fmaxf(ad, -zh);
-      if (!isfinite(zh)) bad = 1.f;
-    }
-    for (int j = tid; j < n; j += NT) if (!isfinite(S.x[j])) bad = 1.f;
-    float v[3] = {ap, ad, bad};
-    block_reduce<NT, 0, 3>(v, S.red);
-    ap = v[0]; ad = v[1];
-    for (int k = tid; k < p; k += NT) {
-      const float zh = S.dz[k];
-      S.s[k] = ap >= 0.f ? -zh + (1.f + ap) : -zh;
-      S.z[k] = ad >= 0.f ? zh + (1.f + ad) : zh;
-    }
-    __syncthreads();
-    if (v[2] > 0.f) status = ST_FAIL | (STG_INIT << 8);
-  }
-
-  // ---- Algorithm 1 -----------------------------------------------------------
   unsigned long long tph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long t0 = clock64();
-  if (status == ST_CONVERGED) {
-    for (int k = 0;; ++k) {
-      float kappa = manifold_coords<NT>(S, a);
-      const float kt = a.sigma * kappa;  // κ_target = σκ
+  for (int k = -1;; ++k) {
+    const bool init = k < 0;
+    float kappa = 0.f, kt = 0.f;
+    int pa = 0;
+    const float *cw = S.om, *ev = S.om;
+    if (init) {
+      // [[Q, Gᵀ, Aᵀ], [G, −I, 0], [A, 0, 0]] (x, ẑ, y) = (−q, h, b); the congruence
+      // ẑ = Gx + w decouples w = −h: reduced matrix [[Q + GᵀG, Aᵀ], [A, 0]],
+      // right-hand side (−q + Gᵀh, b); ẑ = Gx − h.
+      for (int i = tid; i < p; i += NT) { S.om[i] = 1.f; S.v[i] = -1.f; }
+      __syncthreads();
+      compact_active<NT>(S, p, true);
+      for (int j = tid; j < n4; j += NT) {
+        float acc = 0.f;
+        if (j < n) {
+          acc = -__ldg(P.q + j);
+          for (int i = 0; i < p; ++i) acc = fmaf(__ldg(P.G + i * n + j), __ldg(P.h + i), acc);
+        }
+        S.rhs[j] = acc;
+      }
+      for (int l = tid; l < m; l += NT) S.rhs[n4 + l] = __ldg(P.b + l);
+      for (int j = n4 + m + tid; j < r4(n4 + m); j += NT) S.rhs[j] = 0.f;
+    } else {
+      kappa = manifold_coords<NT>(S, a);
+      kt = a.sigma * kappa;  // κ_target = σκ
       const Norms R = residuals<NT>(S, a, P, kappa, kappa - kt);
       long long t1 = clock64(); tph[0] += t1 - t0; t0 = t1;
       it = k;
       if (R.nonfin > 0.f) { status = ST_FAIL | (STG_SCALING << 8); break; }
       if (converged_solve(R, a.tol)) { status = ST_CONVERGED; break; }
       if (k == a.max_iter) { status = ST_MAX_ITER; break; }
-      const KLayout L = KLayout::make(n4 + R.pa + m, n4);
-      tph[5] += R.pa; tph[6] += L.N;
-      const float dmax = assemble<NT>(S, a, P, L, R.pa, S.om, S.dp, S.dm);
-      t1 = clock64(); tph[1] += t1 - t0; t0 = t1;
-      factor_qd<NT>(S.K, L, a.floor_rel * dmax, S.rinv, S.flag);
-      t1 = clock64(); tph[2] += t1 - t0; t0 = t1;
-      solve_qd<NT>(S.K, L, S.rinv, S.rhs);
-      t1 = clock64(); tph[3] += t1 - t0; t0 = t1;
-      int stage = 0;
-      if (!newton_update<NT>(S, a, P, R.pa, kappa, kappa - kt, &stage)) { status = ST_FAIL | (stage << 8); break; }
-      t1 = clock64(); tph[4] += t1 - t0; t0 = t1;
+      pa = R.pa;
+      cw = S.dp; ev = S.dm;
     }
+    const KLayout L = KLayout::make(n4 + pa + m, n4);
+    tph[5] += pa; tph[6] += L.N;
+    const float dmax = assemble<NT>(S, a, P, L, pa, S.om, cw, ev);
+    long long t1 = clock64(); tph[1] += t1 - t0; t0 = t1;
+    factor_qd<NT>(S.K, L, a.floor_rel * dmax, S.rinv, S.flag);
+    t1 = clock64(); tph[2] += t1 - t0; t0 = t1;
+    solve_qd<NT>(S.K, L, S.rinv, S.rhs);
+    t1 = clock64(); tph[3] += t1 - t0; t0 = t1;
+    if (init) {
+      for (int j = tid; j < n; j += NT) S.x[j] = S.rhs[j];
+      for (int l = tid; l < m; l += NT) S.y[l] = S.rhs[n4 + l];
+      __syncthreads();
+      rowdots<NT>(P.G, p, n, S.x, S.dz);
+      for (int i = tid; i < p; i += NT) S.dz[i] -= __ldg(P.h + i);  // ẑ = Gx − h
+      float ap = -INFINITY, ad = -INFINITY, bad = 0.f;
+      for (int i = tid; i < p; i += NT) {
+        const float zh = S.dz[i];
+        ap = fmaxf(ap, zh); ad = fmaxf(ad, -zh);
+        if (!isfinite(zh)) bad = 1.f;
+      }
+      for (int j = tid; j < n; j += NT) if (!isfinite(S.x[j])) bad = 1.f;
+      float v[3] = {ap, ad, bad};
+      block_reduce<NT, 0, 3>(v, S.red);
+      ap = v[0]; ad = v[1];
+      for (int i = tid; i < p; i += NT) {  // s~ = −ẑ, z~ = ẑ, shifted into the interior
+        const float zh = S.dz[i];
+        S.s[i] = ap >= 0.f ? -zh + (1.f + ap) : -zh;
+        S.z[i] = ad >= 0.f ? zh + (1.f + ad) : zh;
+      }
+      __syncthreads();
+      if (v[2] > 0.f) { status = ST_FAIL | (STG_INIT << 8); break; }
+    } else {
+      int stage = 0;
+      if (!newton_update<NT>(S, a, P, pa, kappa, kappa - kt, &stage)) { status = ST_FAIL | (stage << 8); break; }
+    }
+    t1 = clock64(); tph[4] += t1 - t0; t0 = t1;
   }
   if (a.prof && tid == 0) {
     for (int i = 0; i < 8; ++i) a.prof[bid * 8 + i] = tph[i];
@@ -522,9 +531,9 @@ __global__ void __launch_bounds__(NT, MINB) ipm_solve_kernel(const Args a) {
   // ---- outputs
   for (int j = tid; j < n; j += NT) a.x[(long long)bid * n + j] = S.x[j];
   for (int l = tid; l < m; l += NT) a.y[(long long)bid * m + l] = S.y[l];
-  for (int k = tid; k < p; k += NT) {
-    a.z[(long long)bid * p + k] = S.z[k];
-    a.s[(long long)bid * p + k] = S.s[k];
+  for (int i = tid; i < p; i += NT) {
+    a.z[(long long)bid * p + i] = S.z[i];
+    a.s[(long long)bid * p + i] = S.s[i];
   }
   if (tid == 0) {
     a.iters[bid] = it;
@@ -534,7 +543,9 @@ __global__ void __launch_bounds__(NT, MINB) ipm_solve_kernel(const Args a) {
 
 // ------------------------------------------------------------------------
 // Kernel: Algorithm 2 (relax, exact Newton, factor-then-check: Q5, Q5b, Q6)
-// and Algorithm 3 (sign reading Q7, dz = d₊⊙dv: Q8).
+// and Algorithm 3 (sign reading Q7, dz = d₊⊙dv: Q8).  One call
+// site each for assemble / factor_qd / solve_qd (the last solve is the
+// adjoint solve with the relaxed factorisation).
 // ------------------------------------------------------------------------
 template <int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) ipm_backward_kernel(const Args a) {
@@ -546,31 +557,52 @@ __global__ void __launch_bounds__(NT, MINB) ipm_backward_kernel(const Args a) {
   const int n = a.n, n4 = a.n4, p = a.p, m = a.m;
   for (int j = tid; j < n; j += NT) S.x[j] = a.x[(long long)bid * n + j];
   for (int l = tid; l < m; l += NT) S.y[l] = a.y[(long long)bid * m + l];
-  for (int k = tid; k < p; k += NT) {
-    S.z[k] = a.z[(long long)bid * p + k];
-    S.s[k] = a.s[(long long)bid * p + k];
+  for (int i = tid; i < p; i += NT) {
+    S.z[i] = a.z[(long long)bid * p + i];
+    S.s[i] = a.s[(long long)bid * p + i];
   }
   __syncthreads();
   int status = (a.status[bid] & 0xff) == ST_CONVERGED ? ST_CONVERGED : (ST_FAIL | (STG_RELAX << 8));
   int it = 0;
-  KLayout L = KLayout::make(n4 + m, n4);
-  int pa = 0;
+  bool ok = false;
   if (status == ST_CONVERGED) {
     float phi_prev = INFINITY;
     for (int k = 0;; ++k) {
       float kappa = manifold_coords<NT>(S, a);
       const Norms R = residuals<NT>(S, a, P, kappa, kappa - a.kappa_relax);
-      pa = R.pa;
-      L = KLayout::make(n4 + pa + m, n4);
+      const int pa = R.pa;
+      const KLayout L = KLayout::make(n4 + pa + m, n4);
       const float dmax = assemble<NT>(S, a, P, L, pa, S.om, S.dp, S.dm);
       factor_qd<NT>(S.K, L, a.floor_rel * dmax, S.rinv, S.flag);
       it = k;
       if (R.nonfin > 0.f) { status = ST_FAIL | (STG_RELAX << 8); break; }
       const bool kok = p == 0 || fabsf(kappa / a.kappa_relax - 1.f) <= a.relax_ktol;
-      if (kok && relax_done(R, a.tol, a.relax_tol, phi_prev)) break;
+      const bool done = kok && relax_done(R, a.tol, a.relax_tol, phi_prev);
       phi_prev = kok ? rel_phi(R) : INFINITY;
-      if (k == a.relax_max_iter) { status = ST_MAX_ITER | (STG_RELAX << 8); break; }
+      if (!done && k == a.relax_max_iter) { status = ST_MAX_ITER | (STG_RELAX << 8); break; }
+      if (done) {
+        // Algorithm 3: reduced system with right-hand side (−∇ₓℓ, 0, 0)
+        for (int j = tid; j < L.N4; j += NT) S.rhs[j] = j < n ? -__ldg(a.dl + (long long)bid * n + j) : 0.f;
+        __syncthreads();
+      }
       solve_qd<NT>(S.K, L, S.rinv, S.rhs);
+      if (done) {
+        // dv = G dx + w (w eliminated for v_i ≤ 0 with f2 = 0), dz = d₊ ⊙ dv
+        recover_dv<NT>(S, a, P, true);
+        for (int i = tid; i < p; i += NT) S.dz[i] = S.dp[i] * S.gx[i];
+        for (int j = tid; j < n; j += NT) S.dx[j] = S.rhs[j];
+        for (int l = tid; l < m; l += NT) S.dy[l] = S.rhs[n4 + pa + l];
+        __syncthreads();
+        float bad = 0.f;
+        for (int j = tid; j < n; j += NT) if (!isfinite(S.dx[j])) bad = 1.f;
+        for (int i = tid; i < p; i += NT) if (!isfinite(S.dz[i])) bad = 1.f;
+        for (int l = tid; l < m; l += NT) if (!isfinite(S.dy[l])) bad = 1.f;
+        float v[1] = {bad};
+        block_reduce<NT, 0, 1>(v, S.red);
+        ok = !(v[0] > 0.f);
+        if (!ok) status = ST_FAIL | (STG_BACKWARD << 8);
+        break;
+      }
       int stage = 0;
       if (!newton_update<NT>(S, a, P, pa, kappa, kappa - a.kappa_relax, &stage)) {
         status = ST_FAIL | (STG_RELAX << 8);
@@ -578,30 +610,10 @@ __global__ void __launch_bounds__(NT, MINB) ipm_backward_kernel(const Args a) {
       }
     }
   }
-  // ---- Algorithm 3: reduced system with right-hand side (−∇ₓℓ, 0, 0);
-  //      dv = G dx + w, dz = d₊ ⊙ dv
-  bool ok = status == ST_CONVERGED;
-  if (ok) {
-    for (int j = tid; j < L.N4; j += NT) S.rhs[j] = j < n ? -__ldg(a.dl + (long long)bid * n + j) : 0.f;
-    __syncthreads();
-    solve_qd<NT>(S.K, L, S.rinv, S.rhs);
-    recover_dv<NT>(S, a, P, true);
-    for (int k = tid; k < p; k += NT) S.dz[k] = S.dp[k] * S.gx[k];
-    for (int j = tid; j < n; j += NT) S.dx[j] = S.rhs[j];
-    for (int l = tid; l < m; l += NT) S.dy[l] = S.rhs[n4 + pa + l];
-    __syncthreads();
-    float bad = 0.f;
-    for (int j = tid; j < n; j += NT) if (!isfinite(S.dx[j])) bad = 1.f;
-    for (int k = tid; k < p; k += NT) if (!isfinite(S.dz[k])) bad = 1.f;
-    for (int l = tid; l < m; l += NT) if (!isfinite(S.dy[l])) bad = 1.f;
-    float v[1] = {bad};
-    block_reduce<NT, 0, 1>(v, S.red);
-    if (v[0] > 0.f) { ok = false; status = ST_FAIL | (STG_BACKWARD << 8); }
-  }
   if (!ok) {  // zero-filled gradients for failed problems
     for (int j = tid; j < n; j += NT) { S.dx[j] = 0.f; S.x[j] = 0.f; }
     for (int l = tid; l < m; l += NT) { S.dy[l] = 0.f; S.y[l] = 0.f; }
-    for (int k = tid; k < p; k += NT) { S.dz[k] = 0.f; S.z[k] = 0.f; }
+    for (int i = tid; i < p; i += NT) { S.dz[i] = 0.f; S.z[i] = 0.f; }
     __syncthreads();
   }
   // ---- parameter gradients (coalesced stores)
@@ -625,15 +637,15 @@ __global__ void __launch_bounds__(NT, MINB) ipm_backward_kernel(const Args a) {
   if (a.gG) {
     float* o = a.gG + bb * p * n;
     for (int e = tid; e < p * n; e += NT) {
-      const int k = e / n, j = e - k * n;
-      o[e] = S.dz[k] * S.x[j] + S.z[k] * S.dx[j];
+      const int i = e / n, j = e - i * n;
+      o[e] = S.dz[i] * S.x[j] + S.z[i] * S.dx[j];
     }
   }
-  if (a.gh) for (int k = tid; k < p; k += NT) a.gh[bb * p + k] = -S.dz[k];
+  if (a.gh) for (int i = tid; i < p; i += NT) a.gh[bb * p + i] = -S.dz[i];
   if (a.wx) {
     for (int j = tid; j < n; j += NT) { a.wx[bb * n + j] = S.x[j]; a.wdx[bb * n + j] = S.dx[j]; }
     for (int l = tid; l < m; l += NT) { a.wy[bb * m + l] = S.y[l]; a.wdy[bb * m + l] = S.dy[l]; }
-    for (int k = tid; k < p; k += NT) { a.wz[bb * p + k] = S.z[k]; a.wdz[bb * p + k] = S.dz[k]; }
+    for (int i = tid; i < p; i += NT) { a.wz[bb * p + i] = S.z[i]; a.wdz[bb * p + i] = S.dz[i]; }
   }
   if (tid == 0) {
     if (a.riters) a.riters[bid] = it;

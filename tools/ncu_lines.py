@@ -32,9 +32,13 @@ def main():
     kname = lines[0].split(",")[1].strip('"')
     rows = list(csv.DictReader(io.StringIO("\n".join(lines[1:]))))
     samples = {}
+    reasons = {}
+    rcols = [c for c in (rows[0].keys() if rows else []) if c.startswith("stall_") and "Not Issued" not in c]
     for r in rows:
         try:
-            samples[int(r["Address"], 16)] = int(r[a.metric] or 0)
+            ad = int(r["Address"], 16)
+            samples[ad] = int(r[a.metric] or 0)
+            reasons[ad] = {c[6:]: int(r[c] or 0) for c in rcols}
         except (ValueError, KeyError):
             pass
     tmp = tempfile.mkdtemp()
@@ -64,9 +68,16 @@ def main():
     tot = 0
     base = min(samples) if samples else 0
     samples = {ad - base: s for ad, s in samples.items()}
+    reasons = {ad - base: v for ad, v in reasons.items()}
+    ragg = defaultdict(lambda: defaultdict(int))
+    rtot = defaultdict(int)
     for ad, s in samples.items():
-        agg[addr_line.get(ad, ("?", 0))] += s
+        key = addr_line.get(ad, ("?", 0))
+        agg[key] += s
         tot += s
+        for rn, rv in reasons.get(ad, {}).items():
+            ragg[key][rn] += rv
+            rtot[rn] += rv
     src_cache = {}
     print(f"{kname}: {tot} samples")
     for (f, l), s in sorted(agg.items(), key=lambda kv: -kv[1])[: a.top]:
@@ -74,7 +85,12 @@ def main():
             p = os.path.join(os.path.dirname(a.so), "csrc", f)
             src_cache[f] = open(p).read().splitlines() if os.path.exists(p) else []
         txt = src_cache[f][l - 1].strip() if 0 < l <= len(src_cache[f]) else ""
-        print(f"{100.0 * s / max(tot, 1):6.2f}%  {f}:{l:<5d} {txt[:110]}")
+        top = sorted(ragg[(f, l)].items(), key=lambda kv: -kv[1])[:2]
+        rs = " ".join(f"{k}:{v}" for k, v in top if v)
+        print(f"{100.0 * s / max(tot, 1):6.2f}%  {f}:{l:<5d} {txt[:90]:90s} [{rs}]")
+    rt = sum(rtot.values()) or 1
+    print("stall reasons:", ", ".join(f"{k} {100.0 * v / rt:.1f}%" for k, v in
+                                      sorted(rtot.items(), key=lambda kv: -kv[1])[:10]))
 
 
 if __name__ == "__main__":

@@ -196,10 +196,12 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
     const int k0 = KB * b, kb = L.bw(b), k1 = k0 + kb;
     const float* D = K + L.off(k0) + k0;  // diagonal block, row j at D + j*Lb
     const int Lb = L.len(b);
-    // ---- (1) panel factorisation (unscaled LDLᵀ updates: a_ij −= a_ik a_jk / a_kk,
-    //      column k is read-only during step k, so one barrier per column suffices;
-    //      the columns are scaled to L at the end: l_ik = a_ik s_k / l_kk) ----------
-    float a[RPT][KB];
+    // ---- (1) panel factorisation, unscaled LDLᵀ updates a_ij −= a_ik a_jk / a_kk:
+    //      column k is read-only during step k, so one barrier per column
+    //      suffices.  Each thread keeps its row's remaining panel columns in a
+    //      register window that shifts by one per step (w[0] = column k), and
+    //      stores l_ik = a_ik s_k / l_kk as soon as column k is final. ----------
+    float w[RPT][KB];
     float* rowp[RPT];
     bool has[RPT];
 #pragma unroll
@@ -211,13 +213,21 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
       for (int j4 = 0; j4 < KB / 4; ++j4) {
         const float4 t = (has[u] && 4 * j4 < kb) ? reinterpret_cast<const float4*>(rowp[u])[j4]
                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
-        a[u][4 * j4] = t.x; a[u][4 * j4 + 1] = t.y; a[u][4 * j4 + 2] = t.z; a[u][4 * j4 + 3] = t.w;
+        w[u][4 * j4] = t.x; w[u][4 * j4 + 1] = t.y; w[u][4 * j4 + 2] = t.z; w[u][4 * j4 + 3] = t.w;
       }
     }
-    // runtime k loop (compact code: the body stays in the instruction cache);
-    // a[u][k] is selected with an unrolled compare instead of dynamic indexing
+    // l_ik is written one step late (column k is still being read during step k)
+    float pend[RPT];
+    bool pv[RPT];
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) { pend[u] = 0.f; pv[u] = false; }
     for (int k = 0; k < kb; ++k) {
       __syncthreads();
+#pragma unroll
+      for (int u = 0; u < RPT; ++u) {
+        if (pv[u]) rowp[u][k - 1] = pend[u];
+        pv[u] = false;
+      }
       const float s = sgn_of(k0 + k, npos);
       float d = s * D[k * Lb + k];
       const bool fl = !(d >= theta);
@@ -225,54 +235,34 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
       const float rs = rsqrtf(d);  // 1/l_kk
       if (tid == 0) { rinv[k0 + k] = rs; nfloor += fl; }
       const float inv = s * rs * rs;  // 1/a_kk (floored)
-      float col[KB];
+      const float sr = s * rs;
+      float col[KB];  // col[j] = a_{k+j, k}, j ≥ 1 (rows past the block clamped)
 #pragma unroll
-      for (int j = 0; j < KB; ++j) col[j] = (j > k && j < kb) ? D[j * Lb + k] : 0.f;
+      for (int j = 1; j < KB; ++j) col[j] = D[min(k + j, kb - 1) * Lb + k];
 #pragma unroll
       for (int u = 0; u < RPT; ++u) {
         const int il = tid + u * NT;  // row index relative to k0
-        if (has[u] && il > k) {
-          float aik = 0.f;
+        if (has[u] && il >= k) {
+          pv[u] = true;
+          if (il == k) {
+            pend[u] = d * rs;  // l_kk
+          } else {
+            const float f = -w[u][0] * inv;
+            pend[u] = w[u][0] * sr;  // l_ik
 #pragma unroll
-          for (int j = 0; j < KB; ++j) aik = (j == k) ? a[u][j] : aik;
-          const float f = -aik * inv;
-          float nxt = 0.f;
-#pragma unroll
-          for (int j = 0; j < KB; ++j) {
-            if (j > k && j <= il) a[u][j] = fmaf(f, col[j], a[u][j]);
-            nxt = (j == k + 1) ? a[u][j] : nxt;
+            for (int j = 1; j < KB; ++j) w[u][j] = fmaf(f, col[j], w[u][j]);
+            if (il < kb && k + 1 < kb) rowp[u][k + 1] = w[u][1];  // publish column k+1
           }
-          if (k + 1 < kb && il < kb) rowp[u][k + 1] = nxt;  // publish column k+1
         }
+#pragma unroll
+        for (int j = 0; j + 1 < KB; ++j) w[u][j] = w[u][j + 1];
+        w[u][KB - 1] = 0.f;
       }
     }
-    // scale the panel columns to L: l_ik = a_ik s_k / l_kk, l_kk = √(s_k a_kk)
     __syncthreads();
-    float srk[KB];
-#pragma unroll
-    for (int j = 0; j < KB; ++j) srk[j] = j < kb ? sgn_of(k0 + j, npos) * rinv[k0 + j] : 0.f;
-#pragma unroll
-    for (int u = 0; u < RPT; ++u) {
-      const int il = tid + u * NT;
-      if (has[u] && il < kb) {  // diagonal entry: l_ii = s_i a_ii / l_ii... = √(s_i a_ii)
-#pragma unroll
-        for (int j = 0; j < KB; ++j)
-          if (j == il) a[u][j] = 1.f / rinv[k0 + j];
-      }
-    }
 #pragma unroll
     for (int u = 0; u < RPT; ++u)
-      if (has[u]) {
-        const int il = tid + u * NT;
-#pragma unroll
-        for (int j = 0; j < KB; ++j)
-          if (j < il) a[u][j] *= srk[j];
-#pragma unroll
-        for (int j4 = 0; j4 < KB / 4; ++j4)
-          if (4 * j4 < kb)
-            reinterpret_cast<float4*>(rowp[u])[j4] =
-                make_float4(a[u][4 * j4], a[u][4 * j4 + 1], a[u][4 * j4 + 2], a[u][4 * j4 + 3]);
-      }
+      if (pv[u]) rowp[u][kb - 1] = pend[u];
     __syncthreads();
     // ---- (2) trailing update A22 −= L21 S_b L21ᵀ --------------------------------
     if (k1 < N4) {

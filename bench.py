@@ -227,8 +227,8 @@ def main():
     riters = g["relax_iters"].cpu().numpy()
     status = out["status"].cpu().numpy()
     gstatus = g["status"].cpu().numpy()
-    f_solve = float(sum(FL.solve_flops(n, m, p, int(k)) for k in iters))
-    f_bwd = float(sum(FL.backward_flops(n, m, p, int(k)) for k in riters))
+    # algorithmic flops counted inside the kernels (reduced-system sizes)
+    f_solve, f_bwd = S.last_flops()
     ms_solve, ms_bwd = t_solve / a.steps, t_bwd / a.steps
     peak = FL.fp32_peak_tflops(props.multi_processor_count)
     dom_solve = ms_solve >= ms_bwd

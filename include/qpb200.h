@@ -139,6 +139,12 @@ qp_err qp_solve_batched(qp_ctx* ctx, const float* Q, const float* q, const float
 qp_err qp_backward_batched(qp_ctx* ctx, const float* dl_dx, float* dQ, float* dq, float* dA, float* db,
                            float* dG, float* dh, int32_t* relax_iters, int32_t* status);
 
+/* Algorithmic flops executed by the LAST qp_solve_batched / qp_backward_batched
+ * on this ctx, summed over the batch (the work model of DESIGN.md §6, counted
+ * per problem inside the kernels from the actual iteration counts and reduced
+ * system sizes).  Synchronises the ctx stream.  Either pointer may be NULL. */
+qp_err qp_last_flops(qp_ctx* ctx, double* solve_flops, double* backward_flops);
+
 qp_err qp_destroy(qp_ctx* ctx);
 const char* qp_error_string(qp_err err);
 

@@ -39,7 +39,7 @@ class QpInfo(C.Structure):
 
 
 EXPORTS = ("qp_config_default", "qp_create", "qp_set_stream", "qp_get_info", "qp_max_kkt_dim",
-           "qp_solve_batched", "qp_backward_batched", "qp_destroy", "qp_error_string")
+           "qp_solve_batched", "qp_backward_batched", "qp_last_flops", "qp_destroy", "qp_error_string")
 
 _lib = None
 
@@ -67,10 +67,11 @@ def load(path: str | None = None):
     L.qp_solve_batched.argtypes = [V] * 13
     L.qp_backward_batched.argtypes = [V] * 10
     L.qp_destroy.argtypes = [V]
+    L.qp_last_flops.argtypes = [V, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.qp_error_string.argtypes = [C.c_int]
     L.qp_error_string.restype = C.c_char_p
     for f in ("qp_config_default", "qp_create", "qp_set_stream", "qp_get_info", "qp_solve_batched",
-              "qp_backward_batched", "qp_destroy"):
+              "qp_backward_batched", "qp_destroy", "qp_last_flops"):
         getattr(L, f).restype = C.c_int
     if path is None:
         _lib = L
@@ -112,6 +113,12 @@ def qp_solve_batched(h, Q, q, A, b, G, h_, x, s, z, y, iters, status):
 def qp_backward_batched(h, dl_dx, dQ, dq, dA, db, dG, dh, relax_iters, status):
     args = [C.c_void_p(v or 0) for v in (dl_dx, dQ, dq, dA, db, dG, dh, relax_iters, status)]
     check(load().qp_backward_batched(h, *args), "qp_backward_batched")
+
+
+def qp_last_flops(h):
+    a, b = C.c_double(), C.c_double()
+    check(load().qp_last_flops(h, C.byref(a), C.byref(b)), "qp_last_flops")
+    return a.value, b.value
 
 
 def qp_destroy(h):

@@ -39,7 +39,21 @@ struct Args {
   float tol, sigma, tau, kappa_relax, relax_ktol, floor_rel, relax_tol;
   int max_iter, relax_max_iter;
   unsigned long long* prof;  // optional per-CTA phase cycle counters (diagnostics; nullptr = off)
+  float* flops;              // per-problem algorithmic flops of this call, nullptr = off
 };
+
+// Algorithmic flops of one Newton iteration on the reduced system of size
+// Nr = n + |A| + m: assembly p·n(n+1) + |A|·n, factorisation
+// Nr³/3, two triangular solves 2·Nr², residual GEMVs 2n² + 6pn + 4mn,
+// Δv recovery 2pn.
+__device__ __forceinline__ float iter_flops(int n, int m, int p, int pa, bool resid, bool fac, bool solve) {
+  const float Nr = (float)(n + pa + m);
+  float f = 0.f;
+  if (resid) f += 2.f * n * n + 6.f * p * n + 4.f * m * n;
+  if (fac) f += (float)p * n * (n + 1) + (float)pa * n + Nr * Nr * Nr / 3.f;
+  if (solve) f += 2.f * Nr * Nr + 2.f * p * n;
+  return f;
+}
 
 // Shared-memory carve-up (floats).  Every segment is a multiple of 4 floats
 // so that float4 accesses stay 16-byte aligned.  layout() sizes the
@@ -452,6 +466,7 @@ __global__ void __launch_bounds__(NT, MINB) ipm_solve_kernel(const Args a) {
   const Prob P = prob_of(a, bid);
   const int n = a.n, n4 = a.n4, p = a.p, m = a.m;
   int status = ST_CONVERGED, it = 0;
+  float fl = 0.f;  // algorithmic flops of this problem
   unsigned long long tph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long t0 = clock64();
   for (int k = -1;; ++k) {
@@ -483,13 +498,16 @@ __global__ void __launch_bounds__(NT, MINB) ipm_solve_kernel(const Args a) {
       long long t1 = clock64(); tph[0] += t1 - t0; t0 = t1;
       it = k;
       if (R.nonfin > 0.f) { status = ST_FAIL | (STG_SCALING << 8); break; }
+      fl += iter_flops(n, m, p, 0, true, false, false);
       if (converged_solve(R, a.tol)) { status = ST_CONVERGED; break; }
       if (k == a.max_iter) { status = ST_MAX_ITER; break; }
+      fl -= iter_flops(n, m, p, 0, true, false, false);  // counted again below with the step
       pa = R.pa;
       cw = S.dp; ev = S.dm;
     }
     const KLayout L = KLayout::make(n4 + pa + m, n4);
     tph[5] += pa; tph[6] += L.N;
+    fl += iter_flops(n, m, p, pa, !init, true, true);
     const float dmax = assemble<NT>(S, a, P, L, pa, S.om, cw, ev);
     long long t1 = clock64(); tph[1] += t1 - t0; t0 = t1;
     factor_qd<NT>(S.K, L, a.floor_rel * dmax, S.rinv, S.flag);
@@ -538,6 +556,7 @@ __global__ void __launch_bounds__(NT, MINB) ipm_solve_kernel(const Args a) {
   if (tid == 0) {
     a.iters[bid] = it;
     a.status[bid] = status;
+    if (a.flops) a.flops[bid] = fl;
   }
 }
 
@@ -565,6 +584,7 @@ __global__ void __launch_bounds__(NT, MINB) ipm_backward_kernel(const Args a) {
   int status = (a.status[bid] & 0xff) == ST_CONVERGED ? ST_CONVERGED : (ST_FAIL | (STG_RELAX << 8));
   int it = 0;
   bool ok = false;
+  float fl = 0.f;
   if (status == ST_CONVERGED) {
     float phi_prev = INFINITY;
     for (int k = 0;; ++k) {
@@ -574,6 +594,7 @@ __global__ void __launch_bounds__(NT, MINB) ipm_backward_kernel(const Args a) {
       const KLayout L = KLayout::make(n4 + pa + m, n4);
       const float dmax = assemble<NT>(S, a, P, L, pa, S.om, S.dp, S.dm);
       factor_qd<NT>(S.K, L, a.floor_rel * dmax, S.rinv, S.flag);
+      fl += iter_flops(n, m, p, pa, true, true, true);  // the adjoint solve replaces the last step's
       it = k;
       if (R.nonfin > 0.f) { status = ST_FAIL | (STG_RELAX << 8); break; }
       const bool kok = p == 0 || fabsf(kappa / a.kappa_relax - 1.f) <= a.relax_ktol;
@@ -650,6 +671,7 @@ __global__ void __launch_bounds__(NT, MINB) ipm_backward_kernel(const Args a) {
   if (tid == 0) {
     if (a.riters) a.riters[bid] = it;
     if (a.rstatus) a.rstatus[bid] = status;
+    if (a.flops) a.flops[bid] = fl + 2.f * (n * n + m * n + p * n);  // + gradient outer products
   }
 }
 

@@ -80,6 +80,8 @@ struct qp_ctx {
   float *gQ_ = nullptr, *gq_ = nullptr, *gA_ = nullptr, *gb_ = nullptr, *gG_ = nullptr, *gh_ = nullptr;
   int64_t workspace = 0;
   unsigned long long* prof = nullptr;  // QPB200_PHASE_PROFILE diagnostics
+  float* flops_solve = nullptr;        // per-problem algorithmic flops of the last calls
+  float* flops_bwd = nullptr;
 };
 
 namespace {
@@ -98,7 +100,7 @@ qp_err dalloc(qp_ctx* c, T** p, size_t count) {
 size_t field_elems(int64_t stride, int32_t B, size_t per) { return stride == 0 ? per : (size_t)B * per; }
 
 void free_all(qp_ctx* c) {
-  void* ptrs[] = {c->own_status, c->wx, c->wy, c->wz, c->wdx, c->wdy, c->wdz, c->dQ_, c->dq_, c->dA_, c->db_,
+  void* ptrs[] = {c->flops_solve, c->flops_bwd, c->prof, c->own_status, c->wx, c->wy, c->wz, c->wdx, c->wdy, c->wdz, c->dQ_, c->dq_, c->dA_, c->db_,
                   c->dG_, c->dh_, c->dx_, c->ds_, c->dz_, c->dy_, c->ddl_, c->dit_, c->dst_, c->gQ_, c->gq_,
                   c->gA_, c->gb_, c->gG_, c->gh_};
   for (void* p : ptrs)
@@ -219,7 +221,10 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
   }
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->ctas_per_sm, ctx->ks.solve, ctx->ks.threads, L.smem);
   const int B = d->batch, n = d->n, m = d->m_eq, p = d->p;
-  if ((e = dalloc(ctx, &ctx->own_status, B)) != QP_OK) { free_all(ctx); delete ctx; return e; }
+  if ((e = dalloc(ctx, &ctx->own_status, B)) || (e = dalloc(ctx, &ctx->flops_solve, B)) ||
+      (e = dalloc(ctx, &ctx->flops_bwd, B))) {
+    free_all(ctx); delete ctx; return e;
+  }
   if (any_shared(*d)) {
     if ((e = dalloc(ctx, &ctx->wx, (size_t)B * n)) || (e = dalloc(ctx, &ctx->wdx, (size_t)B * n)) ||
         (e = dalloc(ctx, &ctx->wy, (size_t)B * m)) || (e = dalloc(ctx, &ctx->wdy, (size_t)B * m)) ||
@@ -313,6 +318,7 @@ qp_err qp_solve_batched(qp_ctx* c, const float* Q, const float* q, const float* 
   a.status = c->own_status;
   if (getenv("QPB200_PHASE_PROFILE") && !c->prof) cudaMalloc(&c->prof, sizeof(unsigned long long) * 8 * B);
   a.prof = c->prof;
+  a.flops = c->flops_solve;
   c->ks.solve<<<B, c->ks.threads, c->L.smem, c->stream>>>(a);
   if ((e = cuda_ok(cudaGetLastError())) != QP_OK) return e;
   if (host) {
@@ -385,6 +391,7 @@ qp_err qp_backward_batched(qp_ctx* c, const float* dl_dx, float* dQ, float* dq, 
   }
   a.riters = oit;
   a.rstatus = ost;
+  a.flops = c->flops_bwd;
   c->ks.backward<<<B, c->ks.threads, c->L.smem, c->stream>>>(a);
   if ((e = cuda_ok(cudaGetLastError())) != QP_OK) return e;
   if (shared) {
@@ -416,6 +423,24 @@ qp_err qp_backward_batched(qp_ctx* c, const float* dl_dx, float* dQ, float* dq, 
       return e;
     if ((e = cuda_ok(cudaStreamSynchronize(c->stream))) != QP_OK) return e;
   }
+  return QP_OK;
+}
+
+qp_err qp_last_flops(qp_ctx* c, double* solve_flops, double* backward_flops) {
+  if (!c) return QP_ERR_INVALID_ARG;
+  if (cudaSetDevice(c->device) != cudaSuccess || cudaStreamSynchronize(c->stream) != cudaSuccess) return QP_ERR_CUDA;
+  const int B = c->d.batch;
+  float* h = new (std::nothrow) float[B];
+  if (!h) return QP_ERR_OOM;
+  double sums[2] = {0.0, 0.0};
+  float* src[2] = {c->flops_solve, c->flops_bwd};
+  for (int w = 0; w < 2; ++w) {
+    if (cudaMemcpy(h, src[w], sizeof(float) * B, cudaMemcpyDeviceToHost) != cudaSuccess) { delete[] h; return QP_ERR_CUDA; }
+    for (int i = 0; i < B; ++i) sums[w] += (double)h[i];
+  }
+  delete[] h;
+  if (solve_flops) *solve_flops = sums[0];
+  if (backward_flops) *backward_flops = sums[1];
   return QP_OK;
 }
 

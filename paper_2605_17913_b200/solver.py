@@ -48,6 +48,10 @@ class QPSolver:
         i = capi.qp_get_info(self.h)
         return {k: getattr(i, k) for k, _ in i._fields_}
 
+    def last_flops(self):
+        """(solve, backward) algorithmic flops of the last calls."""
+        return capi.qp_last_flops(self.h)
+
     def close(self):
         if getattr(self, "h", None):
             capi.qp_destroy(self.h)

@@ -343,6 +343,172 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
 }
 
 // ------------------------------------------------------------------------
+// Large-N variant (path 2): K lives in a per-CTA GLOBAL workspace (L2
+// resident for config 4), the panel rows are streamed instead of held in
+// registers.  Per 16-wide block:
+//   (a) warp 0 factors the diagonal block (unscaled LDLᵀ updates, register
+//       window per lane, column broadcast through a 16-float smem scratch),
+//       writes L_bb to K and to the smem scratch `l11` (16×16);
+//   (b) every thread solves rows of the panel below (x L_bbᵀ = a, l = S x),
+//       L_bb read from smem (broadcast);
+//   (c) rank-16 update of the trailing lower triangle (32×32 super-tiles per
+//       warp, as in factor_qd).
+// Then the diagonal-block inverses W_b.  scr: ≥ 16·17 + 16 floats of smem.
+// ------------------------------------------------------------------------
+template <int NT>
+__device__ int factor_big(float* __restrict__ K, const KLayout& L, const float theta, float* __restrict__ rinv,
+                          int* __restrict__ flag, float* __restrict__ scr) {
+  constexpr int NW = NT / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int N4 = L.N4, npos = L.npos;
+  float* l11 = scr;            // [16][17]
+  float* colb = scr + 16 * 17;  // [16] column broadcast
+  int nfloor = 0;
+  for (int b = 0; b < L.NB; ++b) {
+    const int k0 = KB * b, kb = L.bw(b), k1 = k0 + kb;
+    const int Lb = L.len(b);
+    // ---- (a) diagonal block ---------------------------------------------------------
+    if (warp == 0) {
+      const int r = lane;
+      float* rowr = K + L.off(k0 + (r < kb ? r : 0)) + k0;
+      float w[KB];
+#pragma unroll
+      for (int j = 0; j < KB; ++j) w[j] = (r < kb && j < kb) ? rowr[j] : 0.f;
+      for (int k = 0; k < kb; ++k) {
+        if (r < kb) colb[r] = w[0];  // current column-k entry of row r
+        __syncwarp();
+        const float s = sgn_of(k0 + k, npos);
+        float d = s * colb[k];
+        const bool fl = !(d >= theta);
+        if (fl) d = theta;
+        const float rs = rsqrtf(d);
+        const float inv = s * rs * rs;
+        float col[KB];
+#pragma unroll
+        for (int j = 1; j < KB; ++j) col[j] = colb[min(k + j, KB - 1)];
+        __syncwarp();
+        if (lane == 0) { rinv[k0 + k] = rs; nfloor += fl; }
+        if (r < kb && r >= k) {
+          float lv;
+          if (r == k) {
+            lv = d * rs;
+          } else {
+            const float f = -w[0] * inv;
+            lv = w[0] * s * rs;
+#pragma unroll
+            for (int j = 1; j < KB; ++j) w[j] = fmaf(f, col[j], w[j]);
+          }
+          rowr[k] = lv;
+          l11[r * 17 + k] = lv;
+        }
+#pragma unroll
+        for (int j = 0; j + 1 < KB; ++j) w[j] = w[j + 1];
+        w[KB - 1] = 0.f;
+      }
+    }
+    __syncthreads();
+    if (k1 >= N4) break;
+    // ---- (b) TRSM of the panel rows below ---------------------------------------------
+    for (int i = k1 + tid; i < N4; i += NT) {
+      float* row = K + L.off(i) + k0;
+      float a[KB];
+#pragma unroll
+      for (int j4 = 0; j4 < 4; ++j4) {
+        const float4 t = reinterpret_cast<const float4*>(row)[j4];
+        a[4 * j4] = t.x; a[4 * j4 + 1] = t.y; a[4 * j4 + 2] = t.z; a[4 * j4 + 3] = t.w;
+      }
+#pragma unroll
+      for (int k = 0; k < KB; ++k) {
+        const float xk = a[k] * rinv[k0 + k];
+        a[k] = xk;
+#pragma unroll
+        for (int j = k + 1; j < KB; ++j) a[j] = fmaf(-xk, l11[j * 17 + k], a[j]);
+      }
+#pragma unroll
+      for (int j4 = 0; j4 < 4; ++j4) {
+        const float s0 = sgn_of(k0 + 4 * j4, npos);
+        reinterpret_cast<float4*>(row)[j4] =
+            make_float4(s0 * a[4 * j4], s0 * a[4 * j4 + 1], s0 * a[4 * j4 + 2], s0 * a[4 * j4 + 3]);
+      }
+    }
+    __syncthreads();
+    // ---- (c) trailing update A22 −= L21 S_b L21ᵀ ---------------------------------------
+    {
+      const int T = (N4 - k1 + 31) >> 5;
+      const int nst = T * (T + 1) / 2;
+      const int ty = lane >> 3, tx = lane & 7;
+      for (int st = warp; st < nst; st += NW) {
+        int I = (int)((sqrtf(8.f * st + 1.f) - 1.f) * 0.5f);
+        while ((I + 1) * (I + 2) / 2 <= st) ++I;
+        while (I * (I + 1) / 2 > st) --I;
+        const int J = st - I * (I + 1) / 2;
+        const int rb = k1 + 32 * I + ty, cb = k1 + 32 * J + tx;
+        int roff[8], coff[4];
+        bool rok[8], cok[4];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int rr = rb + 4 * q;
+          rok[q] = rr < N4;
+          roff[q] = rok[q] ? L.off(rr) : 0;
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int cc = cb + 8 * c;
+          cok[c] = cc < N4;
+          coff[c] = cok[c] ? L.off(cc) : 0;
+        }
+        float acc[8][4];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            acc[q][c] = (rok[q] && cok[c] && cb + 8 * c <= rb + 4 * q) ? K[roff[q] + cb + 8 * c] : 0.f;
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const float sq = k0 + 4 * q4 < npos ? -1.f : 1.f;
+          float4 lc[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            float4 t = cok[c] ? *reinterpret_cast<const float4*>(K + coff[c] + k0 + 4 * q4)
+                              : make_float4(0, 0, 0, 0);
+            t.x *= sq; t.y *= sq; t.z *= sq; t.w *= sq;
+            lc[c] = t;
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 lr = rok[q] ? *reinterpret_cast<const float4*>(K + roff[q] + k0 + 4 * q4)
+                                     : make_float4(0, 0, 0, 0);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              float t = acc[q][c];
+              t = fmaf(lr.x, lc[c].x, t);
+              t = fmaf(lr.y, lc[c].y, t);
+              t = fmaf(lr.z, lc[c].z, t);
+              t = fmaf(lr.w, lc[c].w, t);
+              acc[q][c] = t;
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int cc = cb + 8 * c;
+            if (rok[q] && cok[c] && cc <= rb + 4 * q) K[roff[q] + cc] = acc[q][c];
+          }
+      }
+    }
+    __syncthreads();
+  }
+  for (int b = warp; b < L.NB; b += NW) invert_diag_block(K, L, b, rinv);
+  if (tid == 0) *flag = nfloor;
+  __syncthreads();
+  const int r = *flag;
+  __syncthreads();
+  return r;
+}
+
+// ------------------------------------------------------------------------
 // Solve M u = rhs in place with the factor of factor_qd (M = L S Lᵀ), using
 // the diagonal-block inverses W_b stored by invert_diag_block:
 //   forward  (per block b):  u_b = W_b r_b;  r_i −= L_ib u_b for rows below

@@ -40,6 +40,7 @@ struct Args {
   int max_iter, relax_max_iter;
   unsigned long long* prof;  // optional per-CTA phase cycle counters (diagnostics; nullptr = off)
   float* flops;              // per-problem algorithmic flops of this call, nullptr = off
+  float* kglob;              // path 2 (large N): per-CTA KKT workspaces in global memory, ksize floats each
 };
 
 // Algorithmic flops of one Newton iteration on the reduced system of size
@@ -62,7 +63,7 @@ struct Smem {
   float *K, *rinv, *rhs;
   float *x, *y, *z, *s, *v, *dp, *dm, *c, *om;
   float *rz, *rs, *f2, *t, *gx, *dx, *dy, *dz;
-  float* red;
+  float *red, *scr;
   int *act, *widx, *flag;
   float* end;
 };
@@ -92,6 +93,7 @@ __host__ __device__ inline Smem layout(float* base, int n4, int m, int p, int N4
   S.dy = q; q += m4;
   S.dz = q; q += p4;
   S.red = q; q += 160;
+  S.scr = q; q += 16 * 17 + 16;
   S.act = reinterpret_cast<int*>(q); q += p4;
   S.widx = reinterpret_cast<int*>(q); q += p4;
   S.flag = reinterpret_cast<int*>(q); q += 16;
@@ -104,8 +106,17 @@ __host__ inline size_t ipm_smem_bytes(int n4, int m, int p, int N4max, int ksize
   return (size_t)reinterpret_cast<uintptr_t>(S.end);
 }
 
+template <bool BIG>
 __device__ inline Smem carve(float* base, const Args& a) {
-  return layout(base, a.n4, a.m, a.p, a.N4max, a.ksize);
+  Smem S = layout(base, a.n4, a.m, a.p, a.N4max, BIG ? 0 : a.ksize);
+  if (BIG) S.K = a.kglob + (size_t)blockIdx.x * (size_t)a.ksize;
+  return S;
+}
+
+template <int NT, bool BIG>
+__device__ __forceinline__ int factor_any(const Smem& S, const KLayout& L, float theta) {
+  if (BIG) return factor_big<NT>(S.K, L, theta, S.rinv, S.flag, S.scr);
+  return factor_qd<NT>(S.K, L, theta, S.rinv, S.flag);
 }
 
 struct Prob {
@@ -457,12 +468,9 @@ __device__ bool newton_update(const Smem& S, const Args& a, const Prob& P, int p
 // site (iteration −1 is the initialisation): the kernel stays small enough for
 // the instruction cache.
 // ------------------------------------------------------------------------
-template <int NT, int MINB>
-__global__ void __launch_bounds__(NT, MINB) ipm_solve_kernel(const Args a) {
-  extern __shared__ __align__(16) float smem[];
-  const int bid = blockIdx.x;
+template <int NT, bool BIG>
+__device__ __forceinline__ void solve_problem(const Args& a, const Smem& S, const int bid) {
   const int tid = threadIdx.x;
-  const Smem S = carve(smem, a);
   const Prob P = prob_of(a, bid);
   const int n = a.n, n4 = a.n4, p = a.p, m = a.m;
   int status = ST_CONVERGED, it = 0;
@@ -510,7 +518,7 @@ __global__ void __launch_bounds__(NT, MINB) ipm_solve_kernel(const Args a) {
     fl += iter_flops(n, m, p, pa, !init, true, true);
     const float dmax = assemble<NT>(S, a, P, L, pa, S.om, cw, ev);
     long long t1 = clock64(); tph[1] += t1 - t0; t0 = t1;
-    factor_qd<NT>(S.K, L, a.floor_rel * dmax, S.rinv, S.flag);
+    factor_any<NT, BIG>(S, L, a.floor_rel * dmax);
     t1 = clock64(); tph[2] += t1 - t0; t0 = t1;
     solve_qd<NT>(S.K, L, S.rinv, S.rhs);
     t1 = clock64(); tph[3] += t1 - t0; t0 = t1;
@@ -558,6 +566,14 @@ __global__ void __launch_bounds__(NT, MINB) ipm_solve_kernel(const Args a) {
     a.status[bid] = status;
     if (a.flops) a.flops[bid] = fl;
   }
+  __syncthreads();
+}
+
+template <int NT, int MINB, bool BIG>
+__global__ void __launch_bounds__(NT, MINB) ipm_solve_kernel(const Args a) {
+  extern __shared__ __align__(16) float smem[];
+  const Smem S = carve<BIG>(smem, a);
+  for (int bid = blockIdx.x; bid < a.B; bid += gridDim.x) solve_problem<NT, BIG>(a, S, bid);
 }
 
 // ------------------------------------------------------------------------
@@ -566,12 +582,9 @@ __global__ void __launch_bounds__(NT, MINB) ipm_solve_kernel(const Args a) {
 // site each for assemble / factor_qd / solve_qd (the last solve is the
 // adjoint solve with the relaxed factorisation).
 // ------------------------------------------------------------------------
-template <int NT, int MINB>
-__global__ void __launch_bounds__(NT, MINB) ipm_backward_kernel(const Args a) {
-  extern __shared__ __align__(16) float smem[];
-  const int bid = blockIdx.x;
+template <int NT, bool BIG>
+__device__ __forceinline__ void backward_problem(const Args& a, const Smem& S, const int bid) {
   const int tid = threadIdx.x;
-  const Smem S = carve(smem, a);
   const Prob P = prob_of(a, bid);
   const int n = a.n, n4 = a.n4, p = a.p, m = a.m;
   for (int j = tid; j < n; j += NT) S.x[j] = a.x[(long long)bid * n + j];
@@ -593,7 +606,7 @@ __global__ void __launch_bounds__(NT, MINB) ipm_backward_kernel(const Args a) {
       const int pa = R.pa;
       const KLayout L = KLayout::make(n4 + pa + m, n4);
       const float dmax = assemble<NT>(S, a, P, L, pa, S.om, S.dp, S.dm);
-      factor_qd<NT>(S.K, L, a.floor_rel * dmax, S.rinv, S.flag);
+      factor_any<NT, BIG>(S, L, a.floor_rel * dmax);
       fl += iter_flops(n, m, p, pa, true, true, true);  // the adjoint solve replaces the last step's
       it = k;
       if (R.nonfin > 0.f) { status = ST_FAIL | (STG_RELAX << 8); break; }
@@ -673,6 +686,14 @@ __global__ void __launch_bounds__(NT, MINB) ipm_backward_kernel(const Args a) {
     if (a.rstatus) a.rstatus[bid] = status;
     if (a.flops) a.flops[bid] = fl + 2.f * (n * n + m * n + p * n);  // + gradient outer products
   }
+  __syncthreads();
+}
+
+template <int NT, int MINB, bool BIG>
+__global__ void __launch_bounds__(NT, MINB) ipm_backward_kernel(const Args a) {
+  extern __shared__ __align__(16) float smem[];
+  const Smem S = carve<BIG>(smem, a);
+  for (int bid = blockIdx.x; bid < a.B; bid += gridDim.x) backward_problem<NT, BIG>(a, S, bid);
 }
 
 // ------------------------------------------------------------------------

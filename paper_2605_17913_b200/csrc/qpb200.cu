@@ -25,6 +25,7 @@ constexpr size_t kMaxSmem = 232448;  // 227 KB opt-in dynamic shared memory per 
 
 struct Layout {
   int n4, Nmax, N4max, ksize;
+  bool big;      // path 2: KKT in global memory (does not fit the smem budget)
   size_t smem;
 };
 
@@ -36,11 +37,14 @@ Layout make_layout(int n, int m, int p, int formulation) {
   L.N4max = (L.Nmax + 3) & ~3;
   L.ksize = qpb::KLayout::make(L.Nmax, L.n4).size();
   L.smem = qpb::ipm_smem_bytes(L.n4, m, p, L.N4max, L.ksize);
+  L.big = L.smem > kMaxSmem || getenv("QPB200_FORCE_GLOBAL") != nullptr;  // env: test path 2 on small shapes
+  if (L.big) L.smem = qpb::ipm_smem_bytes(L.n4, m, p, L.N4max, 0);
   return L;
 }
 
 struct KernelSet {
   int threads;
+  bool big;
   void (*solve)(const qpb::Args);
   void (*backward)(const qpb::Args);
 };
@@ -48,9 +52,9 @@ struct KernelSet {
 KernelSet pick_kernels(const Layout& L) {
   int t = 128;
   if (const char* e = getenv("QPB200_THREADS")) t = atoi(e) == 256 ? 256 : 128;
-  (void)L;
-  if (t == 256) return {256, qpb::ipm_solve_kernel<256, 3>, qpb::ipm_backward_kernel<256, 3>};
-  return {128, qpb::ipm_solve_kernel<128, 3>, qpb::ipm_backward_kernel<128, 3>};
+  if (L.big) return {256, true, qpb::ipm_solve_kernel<256, 1, true>, qpb::ipm_backward_kernel<256, 1, true>};
+  if (t == 256) return {256, false, qpb::ipm_solve_kernel<256, 3, false>, qpb::ipm_backward_kernel<256, 3, false>};
+  return {128, false, qpb::ipm_solve_kernel<128, 3, false>, qpb::ipm_backward_kernel<128, 3, false>};
 }
 
 bool aligned4(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 3u) == 0; }
@@ -79,6 +83,8 @@ struct qp_ctx {
   int32_t *dit_ = nullptr, *dst_ = nullptr;
   float *gQ_ = nullptr, *gq_ = nullptr, *gA_ = nullptr, *gb_ = nullptr, *gG_ = nullptr, *gh_ = nullptr;
   int64_t workspace = 0;
+  int grid = 0;               // CTAs per launch (persistent over problems on path 2)
+  float* kglob = nullptr;     // path 2 workspaces
   unsigned long long* prof = nullptr;  // QPB200_PHASE_PROFILE diagnostics
   float* flops_solve = nullptr;        // per-problem algorithmic flops of the last calls
   float* flops_bwd = nullptr;
@@ -100,7 +106,7 @@ qp_err dalloc(qp_ctx* c, T** p, size_t count) {
 size_t field_elems(int64_t stride, int32_t B, size_t per) { return stride == 0 ? per : (size_t)B * per; }
 
 void free_all(qp_ctx* c) {
-  void* ptrs[] = {c->flops_solve, c->flops_bwd, c->prof, c->own_status, c->wx, c->wy, c->wz, c->wdx, c->wdy, c->wdz, c->dQ_, c->dq_, c->dA_, c->db_,
+  void* ptrs[] = {c->kglob, c->flops_solve, c->flops_bwd, c->prof, c->own_status, c->wx, c->wy, c->wz, c->wdx, c->wdy, c->wdz, c->dQ_, c->dq_, c->dA_, c->db_,
                   c->dG_, c->dh_, c->dx_, c->ds_, c->dz_, c->dy_, c->ddl_, c->dit_, c->dst_, c->gQ_, c->gq_,
                   c->gA_, c->gb_, c->gG_, c->gh_};
   for (void* p : ptrs)
@@ -167,9 +173,9 @@ qp_err qp_config_default(qp_config* cfg) {
 
 int32_t qp_max_kkt_dim(int32_t formulation) {
   (void)formulation;
-  // largest N4 whose CTA footprint fits in 227 KB with the vector segments of
-  // a balanced problem; qp_create does the exact check.
-  return 232;
+  // path 1 (KKT in shared memory) up to ≈232; path 2 (KKT in a global
+  // workspace) beyond, limited by the per-problem vectors in shared memory.
+  return 4096;
 }
 
 const char* qp_error_string(qp_err e) {
@@ -204,7 +210,7 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
   for (int i = 0; i < 6; ++i)
     if (strides[i] != 0 && strides[i] < need[i]) return QP_ERR_SHAPE;
   Layout L = make_layout(d->n, d->m_eq, d->p, c.formulation);
-  if (L.smem > kMaxSmem) return QP_ERR_SHAPE;  // large-N path not in this build
+  if (L.smem > kMaxSmem) return QP_ERR_SHAPE;  // vectors alone exceed the smem budget
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) return QP_ERR_CUDA;
   if (cudaSetDevice(device) != cudaSuccess) return QP_ERR_CUDA;
@@ -220,6 +226,15 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
     return QP_ERR_CUDA;
   }
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->ctas_per_sm, ctx->ks.solve, ctx->ks.threads, L.smem);
+  ctx->grid = d->batch;
+  if (L.big) {  // persistent CTAs, one global KKT workspace each
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    ctx->grid = std::min(d->batch, std::max(1, sms * std::max(1, ctx->ctas_per_sm)));
+    if ((e = dalloc(ctx, &ctx->kglob, (size_t)ctx->grid * (size_t)L.ksize)) != QP_OK) {
+      free_all(ctx); delete ctx; return e;
+    }
+  }
   const int B = d->batch, n = d->n, m = d->m_eq, p = d->p;
   if ((e = dalloc(ctx, &ctx->own_status, B)) || (e = dalloc(ctx, &ctx->flops_solve, B)) ||
       (e = dalloc(ctx, &ctx->flops_bwd, B))) {
@@ -264,7 +279,7 @@ qp_err qp_set_stream(qp_ctx* c, void* stream) {
 
 qp_err qp_get_info(const qp_ctx* c, qp_info* info) {
   if (!c || !info) return QP_ERR_INVALID_ARG;
-  info->path = 1;
+  info->path = c->L.big ? 2 : 1;
   info->threads = c->ks.threads;
   info->smem_bytes = (int32_t)c->L.smem;
   info->ctas_per_sm = c->ctas_per_sm;
@@ -319,7 +334,8 @@ qp_err qp_solve_batched(qp_ctx* c, const float* Q, const float* q, const float* 
   if (getenv("QPB200_PHASE_PROFILE") && !c->prof) cudaMalloc(&c->prof, sizeof(unsigned long long) * 8 * B);
   a.prof = c->prof;
   a.flops = c->flops_solve;
-  c->ks.solve<<<B, c->ks.threads, c->L.smem, c->stream>>>(a);
+  a.kglob = c->kglob;
+  c->ks.solve<<<c->grid, c->ks.threads, c->L.smem, c->stream>>>(a);
   if ((e = cuda_ok(cudaGetLastError())) != QP_OK) return e;
   if (host) {
     if ((e = d2h(c, x, c->dx_, (size_t)B * n)) || (e = d2h(c, s, c->ds_, (size_t)B * p)) ||
@@ -392,7 +408,8 @@ qp_err qp_backward_batched(qp_ctx* c, const float* dl_dx, float* dQ, float* dq, 
   a.riters = oit;
   a.rstatus = ost;
   a.flops = c->flops_bwd;
-  c->ks.backward<<<B, c->ks.threads, c->L.smem, c->stream>>>(a);
+  a.kglob = c->kglob;
+  c->ks.backward<<<c->grid, c->ks.threads, c->L.smem, c->stream>>>(a);
   if ((e = cuda_ok(cudaGetLastError())) != QP_OK) return e;
   if (shared) {
     auto osum = [&](float* out, const float* U, const float* V, const float* U2, const float* V2, int R, int Cc,

@@ -126,3 +126,33 @@ def test_zero_cotangent():
     g = run_gpu(b, dl=np.zeros_like(b.dl_dx))
     for k in GRADS:
         assert np.abs(g[k]).max(initial=0) == 0
+
+
+def test_large_n_global_path():
+    """Path 2 (KKT in a global workspace): n=120, m=4, p=200 does not fit the
+    shared-memory budget."""
+    b = gen.g_rand(13, 8, 120, 4, 200)
+    g = run_gpu(b)
+    assert g["info"]["path"] == 2
+    check_against_oracle(b, g)
+
+
+def test_cfg4_shared_subset():
+    """Config 4 shapes (n=200, p=400, shared Q, G, h) on 16 problems: path 2,
+    batch-summed shared gradients."""
+    b = gen.make_config(4, batch=16)
+    g = run_gpu(b)
+    assert g["info"]["path"] == 2
+    check_against_oracle(b, g)
+
+
+def test_global_path_forced_matches_smem_path(monkeypatch):
+    """The same problems through path 1 and (forced) path 2 agree closely."""
+    b = gen.make_config(2, batch=32)
+    g1 = run_gpu(b)
+    monkeypatch.setenv("QPB200_FORCE_GLOBAL", "1")
+    g2 = run_gpu(b)
+    assert g1["info"]["path"] == 1 and g2["info"]["path"] == 2
+    assert np.abs(g1["x"] - g2["x"]).max() <= 1e-4
+    assert np.abs(g1["iters"] - g2["iters"]).max() <= 1
+    check_against_oracle(b, g2)

@@ -95,7 +95,9 @@ typedef struct {
 typedef struct qp_ctx qp_ctx;
 
 typedef struct {
-  int32_t path;            /* 1 = CTA-per-QP smem-resident kernel                          */
+  int32_t path;            /* CTA per QP; KKT matrix in 1 = shared memory, 2 = a global    */
+                           /* workspace (L2), 3 = shared memory when the reduced system    */
+                           /* fits (most iterations), else the global workspace            */
   int32_t threads;         /* threads per CTA                                              */
   int32_t smem_bytes;      /* dynamic shared memory per CTA                                */
   int32_t ctas_per_sm;     /* occupancy of the chosen kernel                               */

@@ -79,6 +79,11 @@ struct KLayout {
 
 __device__ __forceinline__ float sgn_of(int k, int npos) { return k < npos ? 1.f : -1.f; }
 
+// Diagnostics (QPB200_PHASE_PROFILE): cycles spent by thread 0 in the
+// factorisation sub-phases, summed over all CTAs: [panel, SYRK, inverses, count].
+__device__ unsigned long long g_fac_cycles[4];
+__device__ int g_fac_on;
+
 // ------------------------------------------------------------------------
 // Block reductions: NS sums followed by NM maxima, fixed order (deterministic).
 // Every thread returns the reduced values.  `red` is a shared scratch of at
@@ -192,6 +197,7 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int N4 = L.N4, npos = L.npos;
   int nfloor = 0;
+  long long tc0 = clock64(), tpan = 0, tsyrk = 0;
   for (int b = 0; b < L.NB; ++b) {
     const int k0 = KB * b, kb = L.bw(b), k1 = k0 + kb;
     const float* D = K + L.off(k0) + k0;  // diagonal block, row j at D + j*Lb
@@ -264,6 +270,7 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
     for (int u = 0; u < RPT; ++u)
       if (pv[u]) rowp[u][kb - 1] = pend[u];
     __syncthreads();
+    { const long long t = clock64(); tpan += t - tc0; tc0 = t; }
     // ---- (2) trailing update A22 −= L21 S_b L21ᵀ --------------------------------
     if (k1 < N4) {
       const int T = (N4 - k1 + 31) >> 5;
@@ -332,11 +339,18 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
       }
       __syncthreads();
     }
+    { const long long t = clock64(); tsyrk += t - tc0; tc0 = t; }
   }
   // ---- W_b = L_bb⁻¹ for every diagonal block (solve_qd) -------------------------
   for (int b = warp; b < L.NB; b += NW) invert_diag_block(K, L, b, rinv);
   if (tid == 0) *flag = nfloor;
   __syncthreads();
+  if (tid == 0 && g_fac_on) {
+    atomicAdd(&g_fac_cycles[0], (unsigned long long)tpan);
+    atomicAdd(&g_fac_cycles[1], (unsigned long long)tsyrk);
+    atomicAdd(&g_fac_cycles[2], (unsigned long long)(clock64() - tc0));
+    atomicAdd(&g_fac_cycles[3], 1ull);
+  }
   const int r = *flag;
   __syncthreads();
   return r;

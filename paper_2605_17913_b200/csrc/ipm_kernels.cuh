@@ -27,7 +27,9 @@ enum { STG_SCALING = 1, STG_PREDICTOR = 2, STG_CENTERING = 3, STG_CORRECTOR = 4,
 
 struct Args {
   int B, n, m, p;
-  int n4, Nmax, N4max, ksize;  // KKT capacity: N ≤ n4 + p + m
+  int n4, Nmax, N4max;   // KKT capacity: N ≤ n4 + p + m
+  int ksmem, ncap;       // shared-memory KKT buffer (floats) and the largest N it holds
+  long long kglob_size;  // floats per global KKT workspace (worst case N)
   const float *Q, *q, *A, *b, *G, *h;
   long long sQ, sq, sA, sb, sG, sh;
   float *x, *y, *z, *s;  // solution (solve: out; backward: in)
@@ -40,7 +42,7 @@ struct Args {
   int max_iter, relax_max_iter;
   unsigned long long* prof;  // optional per-CTA phase cycle counters (diagnostics; nullptr = off)
   float* flops;              // per-problem algorithmic flops of this call, nullptr = off
-  float* kglob;              // path 2 (large N): per-CTA KKT workspaces in global memory, ksize floats each
+  float* kglob;              // per-CTA KKT workspaces in global memory (iterations with N > ncap)
 };
 
 // Algorithmic flops of one Newton iteration on the reduced system of size
@@ -106,17 +108,22 @@ __host__ inline size_t ipm_smem_bytes(int n4, int m, int p, int N4max, int ksize
   return (size_t)reinterpret_cast<uintptr_t>(S.end);
 }
 
-template <bool BIG>
 __device__ inline Smem carve(float* base, const Args& a) {
-  Smem S = layout(base, a.n4, a.m, a.p, a.N4max, BIG ? 0 : a.ksize);
-  if (BIG) S.K = a.kglob + (size_t)blockIdx.x * (size_t)a.ksize;
-  return S;
+  return layout(base, a.n4, a.m, a.p, a.N4max, a.ksmem);
 }
 
+// Where this iteration's KKT matrix lives: the shared-memory buffer when the
+// reduced system fits (N ≤ ncap), else the CTA's global workspace (L2).
+__device__ __forceinline__ float* kkt_ptr(const Smem& S, const Args& a, const KLayout& L) {
+  return L.N <= a.ncap ? S.K : a.kglob + (size_t)blockIdx.x * (size_t)a.kglob_size;
+}
+
+// factor_qd keeps up to 256/NT panel rows per thread in registers; larger
+// systems stream their panel rows (factor_big).
 template <int NT, bool BIG>
-__device__ __forceinline__ int factor_any(const Smem& S, const KLayout& L, float theta) {
-  if (BIG) return factor_big<NT>(S.K, L, theta, S.rinv, S.flag, S.scr);
-  return factor_qd<NT>(S.K, L, theta, S.rinv, S.flag);
+__device__ __forceinline__ int factor_any(float* K, const Smem& S, const KLayout& L, float theta) {
+  if (BIG && L.N4 > 256) return factor_big<NT>(K, L, theta, S.rinv, S.flag, S.scr);
+  return factor_qd<NT>(K, L, theta, S.rinv, S.flag);
 }
 
 struct Prob {
@@ -167,11 +174,10 @@ __device__ int compact_active(const Smem& S, int p, bool all_inactive) {
 // e = the −diagonal of the w block (d₋), om = ω.  Returns max|diag|.
 // ------------------------------------------------------------------------
 template <int NT>
-__device__ float assemble(const Smem& S, const Args& a, const Prob& P, const KLayout& L, int pa,
+__device__ float assemble(float* K, const Smem& S, const Args& a, const Prob& P, const KLayout& L, int pa,
                           const float* om, const float* cw, const float* e) {
   const int tid = threadIdx.x;
   const int n = a.n, n4 = a.n4, p = a.p, N = L.N, N4 = L.N4;
-  float* K = S.K;
   // 1. rows ≥ n4: C rows of the active constraints, A rows, padding; the tail
   //    of every row beyond its diagonal (rest of its diagonal block + pad) = 0.
   for (int r = n4 + tid; r < N4; r += NT) {
@@ -514,13 +520,14 @@ __device__ __forceinline__ void solve_problem(const Args& a, const Smem& S, cons
       cw = S.dp; ev = S.dm;
     }
     const KLayout L = KLayout::make(n4 + pa + m, n4);
+    float* const K = kkt_ptr(S, a, L);
     tph[5] += pa; tph[6] += L.N;
     fl += iter_flops(n, m, p, pa, !init, true, true);
-    const float dmax = assemble<NT>(S, a, P, L, pa, S.om, cw, ev);
+    const float dmax = assemble<NT>(K, S, a, P, L, pa, S.om, cw, ev);
     long long t1 = clock64(); tph[1] += t1 - t0; t0 = t1;
-    factor_any<NT, BIG>(S, L, a.floor_rel * dmax);
+    factor_any<NT, BIG>(K, S, L, a.floor_rel * dmax);
     t1 = clock64(); tph[2] += t1 - t0; t0 = t1;
-    solve_qd<NT>(S.K, L, S.rinv, S.rhs);
+    solve_qd<NT>(K, L, S.rinv, S.rhs);
     t1 = clock64(); tph[3] += t1 - t0; t0 = t1;
     if (init) {
       for (int j = tid; j < n; j += NT) S.x[j] = S.rhs[j];
@@ -572,7 +579,7 @@ __device__ __forceinline__ void solve_problem(const Args& a, const Smem& S, cons
 template <int NT, int MINB, bool BIG>
 __global__ void __launch_bounds__(NT, MINB) ipm_solve_kernel(const Args a) {
   extern __shared__ __align__(16) float smem[];
-  const Smem S = carve<BIG>(smem, a);
+  const Smem S = carve(smem, a);
   for (int bid = blockIdx.x; bid < a.B; bid += gridDim.x) solve_problem<NT, BIG>(a, S, bid);
 }
 
@@ -605,8 +612,9 @@ __device__ __forceinline__ void backward_problem(const Args& a, const Smem& S, c
       const Norms R = residuals<NT>(S, a, P, kappa, kappa - a.kappa_relax);
       const int pa = R.pa;
       const KLayout L = KLayout::make(n4 + pa + m, n4);
-      const float dmax = assemble<NT>(S, a, P, L, pa, S.om, S.dp, S.dm);
-      factor_any<NT, BIG>(S, L, a.floor_rel * dmax);
+      float* const K = kkt_ptr(S, a, L);
+      const float dmax = assemble<NT>(K, S, a, P, L, pa, S.om, S.dp, S.dm);
+      factor_any<NT, BIG>(K, S, L, a.floor_rel * dmax);
       fl += iter_flops(n, m, p, pa, true, true, true);  // the adjoint solve replaces the last step's
       it = k;
       if (R.nonfin > 0.f) { status = ST_FAIL | (STG_RELAX << 8); break; }
@@ -619,7 +627,7 @@ __device__ __forceinline__ void backward_problem(const Args& a, const Smem& S, c
         for (int j = tid; j < L.N4; j += NT) S.rhs[j] = j < n ? -__ldg(a.dl + (long long)bid * n + j) : 0.f;
         __syncthreads();
       }
-      solve_qd<NT>(S.K, L, S.rinv, S.rhs);
+      solve_qd<NT>(K, L, S.rinv, S.rhs);
       if (done) {
         // dv = G dx + w (w eliminated for v_i ≤ 0 with f2 = 0), dz = d₊ ⊙ dv
         recover_dv<NT>(S, a, P, true);
@@ -692,7 +700,7 @@ __device__ __forceinline__ void backward_problem(const Args& a, const Smem& S, c
 template <int NT, int MINB, bool BIG>
 __global__ void __launch_bounds__(NT, MINB) ipm_backward_kernel(const Args a) {
   extern __shared__ __align__(16) float smem[];
-  const Smem S = carve<BIG>(smem, a);
+  const Smem S = carve(smem, a);
   for (int bid = blockIdx.x; bid < a.B; bid += gridDim.x) backward_problem<NT, BIG>(a, S, bid);
 }
 

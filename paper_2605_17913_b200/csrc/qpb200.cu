@@ -24,10 +24,21 @@ namespace {
 constexpr size_t kMaxSmem = 232448;  // 227 KB opt-in dynamic shared memory per CTA (sm_100a)
 
 struct Layout {
-  int n4, Nmax, N4max, ksize;
-  bool big;      // path 2: KKT in global memory (does not fit the smem budget)
+  int n4, Nmax, N4max;
+  int ksmem, ncap;       // shared-memory KKT buffer and the largest reduced system it holds
+  long long kglob;       // global workspace floats per CTA (worst case)
+  bool big;              // some reduced systems may exceed 256 rows (factor_big compiled in)
+  int threads, minb;     // kernel shape
   size_t smem;
 };
+
+size_t smem_for(const Layout& L, int m, int p, int ncap) {
+  const int ks = ncap > 0 ? qpb::KLayout::make(ncap, L.n4).size() : 0;
+  return qpb::ipm_smem_bytes(L.n4, m, p, L.N4max, ks);
+}
+
+// Shared-memory budget per CTA (dynamic part) for `ctas` CTAs per SM.
+size_t budget(int ctas) { return std::min(kMaxSmem, (size_t)(233472 / ctas) - 1024); }
 
 Layout make_layout(int n, int m, int p, int formulation) {
   (void)formulation;
@@ -35,26 +46,49 @@ Layout make_layout(int n, int m, int p, int formulation) {
   L.n4 = (n + 3) & ~3;
   L.Nmax = L.n4 + p + m;  // reduced system: n4 + |A| + m with |A| <= p
   L.N4max = (L.Nmax + 3) & ~3;
-  L.ksize = qpb::KLayout::make(L.Nmax, L.n4).size();
-  L.smem = qpb::ipm_smem_bytes(L.n4, m, p, L.N4max, L.ksize);
-  L.big = L.smem > kMaxSmem || getenv("QPB200_FORCE_GLOBAL") != nullptr;  // env: test path 2 on small shapes
-  if (L.big) L.smem = qpb::ipm_smem_bytes(L.n4, m, p, L.N4max, 0);
+  L.kglob = qpb::KLayout::make(L.Nmax, L.n4).size();
+  L.big = L.N4max > 256;
+  // Occupancy first: the KKT buffer in smem holds reduced systems up to ncap;
+  // iterations with a larger active set use the CTA's global workspace.
+  // Prefer 5 CTAs/SM (128 threads) if the buffer then still holds at least
+  // 3/4 of the worst-case system or 96 rows, else 4, 3, 2, 1.
+  int env_cap = -1;
+  if (const char* e = getenv("QPB200_NCAP")) env_cap = atoi(e);
+  L.threads = 128; L.minb = 1; L.ncap = 0;
+  const int want[5] = {5, 4, 3, 2, 1};
+  for (int w : want) {
+    const size_t bud = budget(w);
+    if (smem_for(L, m, p, 0) > bud) continue;
+    int lo = 0, hi = L.Nmax;
+    while (lo < hi) {  // largest ncap that fits the budget
+      const int mid = (lo + hi + 1) / 2;
+      if (smem_for(L, m, p, mid) <= bud) lo = mid; else hi = mid - 1;
+    }
+    const int good = std::min(L.Nmax, std::max(96, (3 * L.Nmax) / 4));
+    if (lo >= good || w == 1) { L.ncap = lo; L.minb = w; break; }
+  }
+  if (env_cap >= 0) L.ncap = std::min(env_cap, L.ncap);
+  if (L.big) { L.threads = 256; L.minb = 1; }
+  if (getenv("QPB200_FORCE_GLOBAL")) L.ncap = 0;
+  L.ksmem = L.ncap > 0 ? qpb::KLayout::make(L.ncap, L.n4).size() : 0;
+  L.smem = qpb::ipm_smem_bytes(L.n4, m, p, L.N4max, L.ksmem);
   return L;
 }
 
 struct KernelSet {
   int threads;
-  bool big;
   void (*solve)(const qpb::Args);
   void (*backward)(const qpb::Args);
 };
 
 KernelSet pick_kernels(const Layout& L) {
-  int t = 128;
-  if (const char* e = getenv("QPB200_THREADS")) t = atoi(e) == 256 ? 256 : 128;
-  if (L.big) return {256, true, qpb::ipm_solve_kernel<256, 1, true>, qpb::ipm_backward_kernel<256, 1, true>};
-  if (t == 256) return {256, false, qpb::ipm_solve_kernel<256, 3, false>, qpb::ipm_backward_kernel<256, 3, false>};
-  return {128, false, qpb::ipm_solve_kernel<128, 3, false>, qpb::ipm_backward_kernel<128, 3, false>};
+  if (L.big) return {256, qpb::ipm_solve_kernel<256, 1, true>, qpb::ipm_backward_kernel<256, 1, true>};
+  switch (L.minb) {
+    case 5: return {128, qpb::ipm_solve_kernel<128, 5, false>, qpb::ipm_backward_kernel<128, 5, false>};
+    case 4: return {128, qpb::ipm_solve_kernel<128, 4, false>, qpb::ipm_backward_kernel<128, 4, false>};
+    case 3: return {128, qpb::ipm_solve_kernel<128, 3, false>, qpb::ipm_backward_kernel<128, 3, false>};
+    default: return {128, qpb::ipm_solve_kernel<128, 1, false>, qpb::ipm_backward_kernel<128, 1, false>};
+  }
 }
 
 bool aligned4(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 3u) == 0; }
@@ -122,7 +156,8 @@ qpb::Args base_args(const qp_ctx* c) {
   qpb::Args a;
   std::memset(&a, 0, sizeof(a));
   a.B = c->d.batch; a.n = c->d.n; a.m = c->d.m_eq; a.p = c->d.p;
-  a.n4 = c->L.n4; a.Nmax = c->L.Nmax; a.N4max = c->L.N4max; a.ksize = c->L.ksize;
+  a.n4 = c->L.n4; a.Nmax = c->L.Nmax; a.N4max = c->L.N4max;
+  a.ksmem = c->L.ksmem; a.ncap = c->L.ncap; a.kglob_size = c->L.kglob;
   a.sQ = c->d.bstride_Q; a.sq = c->d.bstride_q; a.sA = c->d.bstride_A;
   a.sb = c->d.bstride_b; a.sG = c->d.bstride_G; a.sh = c->d.bstride_h;
   a.tol = c->c.tol; a.sigma = c->c.sigma; a.tau = c->c.tau; a.kappa_relax = c->c.kappa_relax;
@@ -226,12 +261,13 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
     return QP_ERR_CUDA;
   }
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->ctas_per_sm, ctx->ks.solve, ctx->ks.threads, L.smem);
-  ctx->grid = d->batch;
-  if (L.big) {  // persistent CTAs, one global KKT workspace each
+  // persistent CTAs (one KKT workspace each), looping over the batch
+  {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     ctx->grid = std::min(d->batch, std::max(1, sms * std::max(1, ctx->ctas_per_sm)));
-    if ((e = dalloc(ctx, &ctx->kglob, (size_t)ctx->grid * (size_t)L.ksize)) != QP_OK) {
+    const bool need_glob = L.ncap < L.Nmax;
+    if (need_glob && (e = dalloc(ctx, &ctx->kglob, (size_t)ctx->grid * (size_t)L.kglob)) != QP_OK) {
       free_all(ctx); delete ctx; return e;
     }
   }
@@ -279,7 +315,7 @@ qp_err qp_set_stream(qp_ctx* c, void* stream) {
 
 qp_err qp_get_info(const qp_ctx* c, qp_info* info) {
   if (!c || !info) return QP_ERR_INVALID_ARG;
-  info->path = c->L.big ? 2 : 1;
+  info->path = c->L.ncap >= c->L.Nmax ? 1 : (c->L.ncap > 0 ? 3 : 2);  // 1 smem, 2 global, 3 hybrid
   info->threads = c->ks.threads;
   info->smem_bytes = (int32_t)c->L.smem;
   info->ctas_per_sm = c->ctas_per_sm;
@@ -331,7 +367,15 @@ qp_err qp_solve_batched(qp_ctx* c, const float* Q, const float* q, const float* 
   a.x = c->x; a.y = c->y ? c->y : dummy; a.z = c->z ? c->z : dummy; a.s = c->s ? c->s : dummy;
   a.iters = host ? c->dit_ : iters;
   a.status = c->own_status;
-  if (getenv("QPB200_PHASE_PROFILE") && !c->prof) cudaMalloc(&c->prof, sizeof(unsigned long long) * 8 * B);
+  if (getenv("QPB200_PHASE_PROFILE") && !c->prof) {
+    cudaMalloc(&c->prof, sizeof(unsigned long long) * 8 * B);
+    int on = 1;
+    cudaMemcpyToSymbol(qpb::g_fac_on, &on, sizeof(int));
+  }
+  if (c->prof) {
+    unsigned long long z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbolAsync(qpb::g_fac_cycles, z, sizeof(z), 0, cudaMemcpyHostToDevice, c->stream);
+  }
   a.prof = c->prof;
   a.flops = c->flops_solve;
   a.kglob = c->kglob;
@@ -360,6 +404,10 @@ qp_err qp_solve_batched(qp_ctx* c, const float* Q, const float* q, const float* 
                     " | sum pa %.1f sum N %.1f\n",
             tot[0] / B, tot[1] / B, tot[2] / B, tot[3] / B, tot[4] / B, tot[5] / B, tot[6] / B);
     delete[] hp;
+    unsigned long long fc[4];
+    cudaMemcpyFromSymbol(fc, qpb::g_fac_cycles, sizeof(fc));
+    if (fc[3]) fprintf(stderr, "[qpb200 factor sub-phases per factorisation] panel %.0f syrk %.0f inverses %.0f\n",
+                       (double)fc[0] / fc[3], (double)fc[1] / fc[3], (double)fc[2] / fc[3]);
   }
   return QP_OK;
 }

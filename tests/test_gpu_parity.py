@@ -133,7 +133,7 @@ def test_large_n_global_path():
     shared-memory budget."""
     b = gen.g_rand(13, 8, 120, 4, 200)
     g = run_gpu(b)
-    assert g["info"]["path"] == 2
+    assert g["info"]["path"] in (2, 3)
     check_against_oracle(b, g)
 
 
@@ -142,7 +142,7 @@ def test_cfg4_shared_subset():
     batch-summed shared gradients."""
     b = gen.make_config(4, batch=16)
     g = run_gpu(b)
-    assert g["info"]["path"] == 2
+    assert g["info"]["path"] in (2, 3)
     check_against_oracle(b, g)
 
 
@@ -152,7 +152,7 @@ def test_global_path_forced_matches_smem_path(monkeypatch):
     g1 = run_gpu(b)
     monkeypatch.setenv("QPB200_FORCE_GLOBAL", "1")
     g2 = run_gpu(b)
-    assert g1["info"]["path"] == 1 and g2["info"]["path"] == 2
+    assert g1["info"]["path"] in (1, 3) and g2["info"]["path"] == 2
     assert np.abs(g1["x"] - g2["x"]).max() <= 1e-4
     assert np.abs(g1["iters"] - g2["iters"]).max() <= 1
     check_against_oracle(b, g2)

@@ -48,15 +48,20 @@ Layout make_layout(int n, int m, int p, int formulation) {
   L.N4max = (L.Nmax + 3) & ~3;
   L.kglob = qpb::KLayout::make(L.Nmax, L.n4).size();
   L.big = L.N4max > 256;
-  // Occupancy first: the KKT buffer in smem holds reduced systems up to ncap;
-  // iterations with a larger active set use the CTA's global workspace.
-  // Prefer 5 CTAs/SM (128 threads) if the buffer then still holds at least
-  // 3/4 of the worst-case system or 96 rows, else 4, 3, 2, 1.
+  // The KKT buffer in smem holds reduced systems up to ncap; iterations with
+  // a larger active set use the CTA's global workspace.  Measured on config
+  // 2/3: more CTAs per SM do NOT pay when they shrink L1 (Q, G are re-read
+  // from L1 every iteration), so take the largest CTA count at which the
+  // buffer still holds the worst-case system; only when even one CTA cannot,
+  // run one CTA per SM with the largest buffer (hybrid).
   int env_cap = -1;
   if (const char* e = getenv("QPB200_NCAP")) env_cap = atoi(e);
+  int env_ctas = 0;
+  if (const char* e = getenv("QPB200_CTAS")) env_ctas = atoi(e);
   L.threads = 128; L.minb = 1; L.ncap = 0;
-  const int want[5] = {5, 4, 3, 2, 1};
+  const int want[4] = {4, 3, 2, 1};
   for (int w : want) {
+    if (env_ctas && w != env_ctas) continue;
     const size_t bud = budget(w);
     if (smem_for(L, m, p, 0) > bud) continue;
     int lo = 0, hi = L.Nmax;
@@ -64,8 +69,7 @@ Layout make_layout(int n, int m, int p, int formulation) {
       const int mid = (lo + hi + 1) / 2;
       if (smem_for(L, m, p, mid) <= bud) lo = mid; else hi = mid - 1;
     }
-    const int good = std::min(L.Nmax, std::max(96, (3 * L.Nmax) / 4));
-    if (lo >= good || w == 1) { L.ncap = lo; L.minb = w; break; }
+    if (lo >= L.Nmax || w == 1 || env_ctas) { L.ncap = lo; L.minb = w; break; }
   }
   if (env_cap >= 0) L.ncap = std::min(env_cap, L.ncap);
   if (L.big) { L.threads = 256; L.minb = 1; }

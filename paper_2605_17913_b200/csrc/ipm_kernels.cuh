@@ -115,9 +115,14 @@ __device__ inline Smem carve(float* base, const Args& a) {
   return layout(base, a.n4, a.m, a.p, a.N4max, a.ksmem);
 }
 
-// Where this iteration's KKT matrix lives: the shared-memory buffer when the
-// reduced system fits (N ≤ ncap), else the CTA's global workspace (L2).
+// Where this iteration's KKT matrix lives.  Path 1 kernels (BIG = false)
+// always use the shared-memory buffer (the host guarantees it holds the
+// worst case), so the compiler emits shared-memory instructions; the large-N
+// kernels choose at run time: the smem buffer when the reduced system fits
+// (N ≤ ncap), else the CTA's global workspace (L2).
+template <bool BIG>
 __device__ __forceinline__ float* kkt_ptr(const Smem& S, const Args& a, const KLayout& L) {
+  if (!BIG) return S.K;
   return L.N <= a.ncap ? S.K : a.kglob + (size_t)blockIdx.x * (size_t)a.kglob_size;
 }
 
@@ -552,7 +557,7 @@ __device__ __forceinline__ void solve_problem(const Args& a, const Smem& S, cons
       cw = S.dp; ev = S.dm;
     }
     const KLayout L = KLayout::make(n4 + pa + m, n4);
-    float* const K = kkt_ptr(S, a, L);
+    float* const K = kkt_ptr<BIG>(S, a, L);
     tph[5] += pa; tph[6] += L.N;
     fl += iter_flops(n, m, p, pa, !init, true, true);
     const float dmax = assemble<NT>(K, S, a, P, L, pa, S.om, cw, ev);
@@ -644,7 +649,7 @@ __device__ __forceinline__ void backward_problem(const Args& a, const Smem& S, c
       const Norms R = residuals<NT>(S, a, P, kappa, kappa - a.kappa_relax);
       const int pa = R.pa;
       const KLayout L = KLayout::make(n4 + pa + m, n4);
-      float* const K = kkt_ptr(S, a, L);
+      float* const K = kkt_ptr<BIG>(S, a, L);
       const float dmax = assemble<NT>(K, S, a, P, L, pa, S.om, S.dp, S.dm);
       factor_any<NT, BIG>(K, S, L, a.floor_rel * dmax);
       fl += iter_flops(n, m, p, pa, true, true, true);  // the adjoint solve replaces the last step's

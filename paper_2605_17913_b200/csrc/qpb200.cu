@@ -72,8 +72,11 @@ Layout make_layout(int n, int m, int p, int formulation) {
     if (lo >= L.Nmax || w == 1 || env_ctas) { L.ncap = lo; L.minb = w; break; }
   }
   if (env_cap >= 0) L.ncap = std::min(env_cap, L.ncap);
-  if (L.big) { L.threads = 256; L.minb = 1; }
   if (getenv("QPB200_FORCE_GLOBAL")) L.ncap = 0;
+  // a buffer smaller than the worst case needs the run-time placement of the
+  // large-N kernels (generic pointers); path 1 kernels assume a full fit
+  if (L.ncap < L.Nmax) L.big = true;
+  if (L.big) { L.threads = 256; L.minb = 1; }
   L.ksmem = L.ncap > 0 ? qpb::KLayout::make(L.ncap, L.n4).size() : 0;
   L.smem = qpb::ipm_smem_bytes(L.n4, m, p, L.N4max, L.ksmem);
   return L;

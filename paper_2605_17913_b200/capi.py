@@ -53,7 +53,7 @@ def load(path: str | None = None):
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = path or LIB
+    p = path or os.environ.get("QPB200_LIB") or LIB  # QPB200_LIB: experiment with an alternate build
     if not os.path.exists(p):
         raise QPError(f"CUDA library {p} is missing: run __graft_entry__.build() (no CPU fallback exists)")
     L = C.CDLL(p)

@@ -544,9 +544,10 @@ __device__ void solve_qd(const float* __restrict__ K, const KLayout& L, const fl
       float r[KB];
 #pragma unroll
       for (int c = 0; c < KB; ++c) r[c] = c < kb ? rhs[k0 + c] : 0.f;
+      const float rt = t < kb ? rhs[k0 + t] : 0.f;  // r[t] without dynamic register indexing
       __syncwarp();
       if (t < kb) {
-        float acc = rinv[k0 + t] * r[t];
+        float acc = rinv[k0 + t] * rt;
 #pragma unroll
         for (int c = 0; c < KB; ++c)
           if (c < t) acc = fmaf(D[c * Lb + t], r[c], acc);  // W[t][c] stored at row c, col t
@@ -585,9 +586,10 @@ __device__ void solve_qd(const float* __restrict__ K, const KLayout& L, const fl
       float r[KB];
 #pragma unroll
       for (int c = 0; c < KB; ++c) r[c] = c < kb ? rhs[k0 + c] : 0.f;
+      const float rt = t < kb ? rhs[k0 + t] : 0.f;  // r[t] without dynamic register indexing
       __syncwarp();
       if (t < kb) {
-        float acc = rinv[k0 + t] * r[t];
+        float acc = rinv[k0 + t] * rt;
         const float* Dt = D + t * Lb;  // W[r][t] for r > t lives in row t, column r
 #pragma unroll
         for (int c = 0; c < KB; ++c)

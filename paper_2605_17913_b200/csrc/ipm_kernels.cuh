@@ -58,8 +58,6 @@ __device__ __forceinline__ float iter_flops(int n, int m, int p, int pa, bool re
   return f;
 }
 
-constexpr int GCH = 16;  // G rows staged per chunk in the assembly
-
 // Shared-memory carve-up (floats).  Every segment is a multiple of 4 floats
 // so that float4 accesses stay 16-byte aligned.  layout() sizes the
 // allocation on the host (base = nullptr) and carves it on the device.
@@ -67,7 +65,7 @@ struct Smem {
   float *K, *rinv, *rhs;
   float *x, *y, *z, *s, *v, *dp, *dm, *c, *om;
   float *rz, *rs, *f2, *t, *gx, *dx, *dy, *dz;
-  float *red, *scr, *gst;
+  float *red, *scr;
   int *act, *widx, *flag;
   float* end;
 };
@@ -98,7 +96,6 @@ __host__ __device__ inline Smem layout(float* base, int n4, int m, int p, int N4
   S.dz = q; q += p4;
   S.red = q; q += 160;
   S.scr = q; q += 16 * 17 + 16;
-  S.gst = q; q += GCH * n4 + GCH;  // staged chunk of G rows (+ their weights) for the assembly
   S.act = reinterpret_cast<int*>(q); q += p4;
   S.widx = reinterpret_cast<int*>(q); q += p4;
   S.flag = reinterpret_cast<int*>(q); q += 16;
@@ -130,8 +127,12 @@ __device__ __forceinline__ float* kkt_ptr(const Smem& S, const Args& a, const KL
 // systems stream their panel rows (factor_big).
 template <int NT, bool BIG>
 __device__ __forceinline__ int factor_any(float* K, const Smem& S, const KLayout& L, float theta) {
+#ifdef QPB200_FACTOR_WARP
+  return factor_big<NT>(K, L, theta, S.rinv, S.flag, S.scr);
+#else
   if (BIG && L.N4 > 256) return factor_big<NT>(K, L, theta, S.rinv, S.flag, S.scr);
   return factor_qd<NT>(K, L, theta, S.rinv, S.flag);
+#endif
 }
 
 struct Prob {
@@ -205,82 +206,53 @@ __device__ float assemble(float* K, const Smem& S, const Args& a, const Prob& P,
     for (int j = n4; j < len; ++j) row[j] = 0.f;
     row[r] = r < n4 + pa ? -e[S.act[r - n4]] : (r < N ? 0.f : -1.f);
   }
-  // 2. H = Q + Gᵀ diag(ω) G in 4×4 tiles of the lower triangle: H := Q, then
-  //    chunks of GCH rows of G are staged in smem with coalesced loads and
-  //    every tile accumulates the chunk (read-modify-write of its 16 entries).
+  // 2. H = Q + Gᵀ diag(ω) G: 4×4 register tiles of the lower triangle; G rows
+  //    are read from global memory (L1-resident across iterations).
   const int T = n4 >> 2;
   const int nt = T * (T + 1) / 2;
+  float dmax = 0.f;
   for (int t = tid; t < nt; t += NT) {
     int I = (int)((sqrtf(8.f * t + 1.f) - 1.f) * 0.5f);
     while ((I + 1) * (I + 2) / 2 <= t) ++I;
     while (I * (I + 1) / 2 > t) --I;
     const int J = t - I * (I + 1) / 2;
     const int i0 = 4 * I, j0 = 4 * J;
+    float acc[4][4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      float* row = K + L.off(i0 + u) + j0;
+    for (int u = 0; u < 4; ++u)
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
         const int i = i0 + u, j = j0 + w;
-        row[w] = (i < n && j < n) ? __ldg(P.Q + i * n + j) : (i == j ? 1.f : 0.f);
+        acc[u][w] = (i < n && j < n) ? __ldg(P.Q + i * n + j) : (i == j ? 1.f : 0.f);
       }
-    }
-  }
-  float* gst = S.gst;
-  float* wst = S.gst + GCH * n4;
-  for (int c0 = 0; c0 < p; c0 += GCH) {
-    const int ch = min(GCH, p - c0);
-    __syncthreads();
-    for (int idx = tid; idx < ch * n4; idx += NT) {
-      const int k = idx / n4, j = idx - k * n4;
-      gst[idx] = j < n ? __ldg(P.G + (c0 + k) * n + j) : 0.f;
-    }
-    for (int k = tid; k < ch; k += NT) wst[k] = om[c0 + k];
-    __syncthreads();
-    for (int t = tid; t < nt; t += NT) {
-      int I = (int)((sqrtf(8.f * t + 1.f) - 1.f) * 0.5f);
-      while ((I + 1) * (I + 2) / 2 <= t) ++I;
-      while (I * (I + 1) / 2 > t) --I;
-      const int J = t - I * (I + 1) / 2;
-      const int i0 = 4 * I, j0 = 4 * J;
-      float acc[4][4];
+    for (int k = 0; k < p; ++k) {
+      const float* g = P.G + k * n;
+      const float w = om[k];
+      float gi[4], gj[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const float4 r4v = *reinterpret_cast<const float4*>(K + L.off(i0 + u) + j0);
-        acc[u][0] = r4v.x; acc[u][1] = r4v.y; acc[u][2] = r4v.z; acc[u][3] = r4v.w;
-      }
-      for (int k = 0; k < ch; ++k) {
-        const float4 gi = *reinterpret_cast<const float4*>(gst + k * n4 + i0);
-        float4 gj = *reinterpret_cast<const float4*>(gst + k * n4 + j0);
-        const float w = wst[k];
-        gj.x *= w; gj.y *= w; gj.z *= w; gj.w *= w;
-        const float gia[4] = {gi.x, gi.y, gi.z, gi.w};
-        const float gja[4] = {gj.x, gj.y, gj.z, gj.w};
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int w2 = 0; w2 < 4; ++w2) acc[u][w2] = fmaf(gia[u], gja[w2], acc[u][w2]);
+        gi[u] = i0 + u < n ? __ldg(g + i0 + u) : 0.f;
+        gj[u] = j0 + u < n ? w * __ldg(g + j0 + u) : 0.f;
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        float* row = K + L.off(i0 + u) + j0;
-        if (I != J) {
-          *reinterpret_cast<float4*>(row) = make_float4(acc[u][0], acc[u][1], acc[u][2], acc[u][3]);
-        } else {
+      for (int u = 0; u < 4; ++u)
 #pragma unroll
-          for (int w = 0; w < 4; ++w)
-            if (w <= u) row[w] = acc[u][w];
-        }
+        for (int w2 = 0; w2 < 4; ++w2) acc[u][w2] = fmaf(gi[u], gj[w2], acc[u][w2]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      float* row = K + L.off(i0 + u);
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const int i = i0 + u, j = j0 + w;
+        if (j <= i) row[j] = acc[u][w];
+        if (i == j && i < n) dmax = fmaxf(dmax, fabsf(acc[u][w]));
+      }
+      if (I == J) {  // zero the tail of row i0+u beyond the diagonal
+        const int len = L.len((i0 + u) >> 4);
+        for (int j = i0 + u + 1; j < len; ++j) row[j] = 0.f;
       }
     }
-  }
-  __syncthreads();
-  float dmax = 0.f;
-  for (int i = tid; i < n4; i += NT) {  // diagonal max; zero each x-row's tail beyond its diagonal
-    float* row = K + L.off(i);
-    if (i < n) dmax = fmaxf(dmax, fabsf(row[i]));
-    const int len = L.len(i >> 4);
-    for (int j = i + 1; j < len; ++j) row[j] = 0.f;
   }
   for (int r = tid; r < pa; r += NT) dmax = fmaxf(dmax, fabsf(e[S.act[r]]));
   float vals[1] = {dmax};

@@ -64,7 +64,7 @@ __device__ __forceinline__ float iter_flops(int n, int m, int p, int pa, bool re
 struct Smem {
   float *K, *rinv, *rhs;
   float *x, *y, *z, *s, *v, *dp, *dm, *c, *om;
-  float *rz, *rs, *f2, *t, *gx, *dx, *dy, *dz;
+  float *rz, *rs, *f2, *t, *gx, *dx, *dy, *dz, *ds_x;
   float *red, *scr;
   int *act, *widx, *flag;
   float* end;
@@ -94,6 +94,7 @@ __host__ __device__ inline Smem layout(float* base, int n4, int m, int p, int N4
   S.dx = q; q += n4;
   S.dy = q; q += m4;
   S.dz = q; q += p4;
+  S.ds_x = q; q += n4 + m4;  // standard arm: predictor / centering Δx, Δy
   S.red = q; q += 160;
   S.scr = q; q += 16 * 17 + 16;
   S.act = reinterpret_cast<int*>(q); q += p4;
@@ -598,6 +599,44 @@ __global__ void __launch_bounds__(NT, MINB) ipm_solve_kernel(const Args a) {
 // site each for assemble / factor_qd / solve_qd (the last solve is the
 // adjoint solve with the relaxed factorisation).
 // ------------------------------------------------------------------------
+// Alg. 3 parameter gradients from (x, y, z) and (dx, dy, dz) in
+// shared memory; coalesced stores; per-problem vectors for shared-field sums.
+template <int NT>
+__device__ void write_gradients(const Smem& S, const Args& a, const int bid) {
+  const int tid = threadIdx.x;
+  const int n = a.n, p = a.p, m = a.m;
+  const long long bb = bid;
+  if (a.gQ) {
+    float* o = a.gQ + bb * n * n;
+    for (int e = tid; e < n * n; e += NT) {
+      const int i = e / n, j = e - i * n;
+      o[e] = 0.5f * (S.dx[i] * S.x[j] + S.x[i] * S.dx[j]);
+    }
+  }
+  if (a.gq) for (int j = tid; j < n; j += NT) a.gq[bb * n + j] = S.dx[j];
+  if (a.gA) {
+    float* o = a.gA + bb * m * n;
+    for (int e = tid; e < m * n; e += NT) {
+      const int l = e / n, j = e - l * n;
+      o[e] = S.dy[l] * S.x[j] + S.y[l] * S.dx[j];
+    }
+  }
+  if (a.gb) for (int l = tid; l < m; l += NT) a.gb[bb * m + l] = -S.dy[l];
+  if (a.gG) {
+    float* o = a.gG + bb * p * n;
+    for (int e = tid; e < p * n; e += NT) {
+      const int i = e / n, j = e - i * n;
+      o[e] = S.dz[i] * S.x[j] + S.z[i] * S.dx[j];
+    }
+  }
+  if (a.gh) for (int i = tid; i < p; i += NT) a.gh[bb * p + i] = -S.dz[i];
+  if (a.wx) {
+    for (int j = tid; j < n; j += NT) { a.wx[bb * n + j] = S.x[j]; a.wdx[bb * n + j] = S.dx[j]; }
+    for (int l = tid; l < m; l += NT) { a.wy[bb * m + l] = S.y[l]; a.wdy[bb * m + l] = S.dy[l]; }
+    for (int i = tid; i < p; i += NT) { a.wz[bb * p + i] = S.z[i]; a.wdz[bb * p + i] = S.dz[i]; }
+  }
+}
+
 template <int NT, bool BIG>
 __device__ __forceinline__ void backward_problem(const Args& a, const Smem& S, const int bid) {
   const int tid = threadIdx.x;
@@ -667,37 +706,7 @@ __device__ __forceinline__ void backward_problem(const Args& a, const Smem& S, c
     for (int i = tid; i < p; i += NT) { S.dz[i] = 0.f; S.z[i] = 0.f; }
     __syncthreads();
   }
-  // ---- parameter gradients (coalesced stores)
-  const long long bb = bid;
-  if (a.gQ) {
-    float* o = a.gQ + bb * n * n;
-    for (int e = tid; e < n * n; e += NT) {
-      const int i = e / n, j = e - i * n;
-      o[e] = 0.5f * (S.dx[i] * S.x[j] + S.x[i] * S.dx[j]);
-    }
-  }
-  if (a.gq) for (int j = tid; j < n; j += NT) a.gq[bb * n + j] = S.dx[j];
-  if (a.gA) {
-    float* o = a.gA + bb * m * n;
-    for (int e = tid; e < m * n; e += NT) {
-      const int l = e / n, j = e - l * n;
-      o[e] = S.dy[l] * S.x[j] + S.y[l] * S.dx[j];
-    }
-  }
-  if (a.gb) for (int l = tid; l < m; l += NT) a.gb[bb * m + l] = -S.dy[l];
-  if (a.gG) {
-    float* o = a.gG + bb * p * n;
-    for (int e = tid; e < p * n; e += NT) {
-      const int i = e / n, j = e - i * n;
-      o[e] = S.dz[i] * S.x[j] + S.z[i] * S.dx[j];
-    }
-  }
-  if (a.gh) for (int i = tid; i < p; i += NT) a.gh[bb * p + i] = -S.dz[i];
-  if (a.wx) {
-    for (int j = tid; j < n; j += NT) { a.wx[bb * n + j] = S.x[j]; a.wdx[bb * n + j] = S.dx[j]; }
-    for (int l = tid; l < m; l += NT) { a.wy[bb * m + l] = S.y[l]; a.wdy[bb * m + l] = S.dy[l]; }
-    for (int i = tid; i < p; i += NT) { a.wz[bb * p + i] = S.z[i]; a.wdz[bb * p + i] = S.dz[i]; }
-  }
+  write_gradients<NT>(S, a, bid);
   if (tid == 0) {
     if (a.riters) a.riters[bid] = it;
     if (a.rstatus) a.rstatus[bid] = status;

@@ -14,7 +14,7 @@
 #include <new>
 
 #include "../../include/qpb200.h"
-#include "ipm_kernels.cuh"
+#include "xpm_kernels.cuh"
 
 namespace {
 
@@ -41,10 +41,11 @@ size_t smem_for(const Layout& L, int m, int p, int ncap) {
 size_t budget(int ctas) { return std::min(kMaxSmem, (size_t)(233472 / ctas) - 1024); }
 
 Layout make_layout(int n, int m, int p, int formulation) {
-  (void)formulation;
   Layout L;
   L.n4 = (n + 3) & ~3;
-  L.Nmax = L.n4 + p + m;  // reduced system: n4 + |A| + m with |A| <= p
+  // implicit: reduced system n4 + |A| + m with |A| <= p; standard arm: every
+  // constraint condensed into H = Q + GᵀD(z/s)G, so n4 + m
+  L.Nmax = L.n4 + (formulation == QP_EXPLICIT ? 0 : p) + m;
   L.N4max = (L.Nmax + 3) & ~3;
   L.kglob = qpb::KLayout::make(L.Nmax, L.n4).size();
   L.big = L.N4max > 256;
@@ -88,7 +89,11 @@ struct KernelSet {
   void (*backward)(const qpb::Args);
 };
 
-KernelSet pick_kernels(const Layout& L) {
+KernelSet pick_kernels(const Layout& L, int formulation) {
+  if (formulation == QP_EXPLICIT) {
+    if (L.big) return {0, nullptr, nullptr};
+    return {128, qpb::xpm_solve_kernel<128, 1>, qpb::xpm_backward_kernel<128, 1>};
+  }
   if (L.big) return {256, qpb::ipm_solve_kernel<256, 1, true>, qpb::ipm_backward_kernel<256, 1, true>};
   switch (L.minb) {
     case 5: return {128, qpb::ipm_solve_kernel<128, 5, false>, qpb::ipm_backward_kernel<128, 5, false>};
@@ -245,7 +250,6 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
       (c.formulation != QP_IMPLICIT && c.formulation != QP_EXPLICIT) ||
       (c.mem_kind != QP_MEM_DEVICE && c.mem_kind != QP_MEM_HOST))
     return QP_ERR_INVALID_ARG;
-  if (c.formulation == QP_EXPLICIT) return QP_ERR_UNSUPPORTED;  // standard arm: see qp_explicit.cu (next)
   const int64_t strides[6] = {d->bstride_Q, d->bstride_q, d->bstride_A, d->bstride_b, d->bstride_G, d->bstride_h};
   const int64_t need[6] = {(int64_t)d->n * d->n, d->n, (int64_t)d->m_eq * d->n, d->m_eq, (int64_t)d->p * d->n,
                            d->p};
@@ -260,7 +264,8 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
   if (!ctx) return QP_ERR_OOM;
   ctx->d = *d; ctx->c = c; ctx->device = device; ctx->stream = static_cast<cudaStream_t>(stream); ctx->L = L;
   qp_err e = QP_OK;
-  ctx->ks = pick_kernels(L);
+  ctx->ks = pick_kernels(L, c.formulation);
+  if (!ctx->ks.solve) { delete ctx; return QP_ERR_UNSUPPORTED; }  // standard arm: path 1 sizes only
   if (cudaFuncSetAttribute(ctx->ks.solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem) != cudaSuccess ||
       cudaFuncSetAttribute(ctx->ks.backward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem) !=
           cudaSuccess) {

@@ -23,11 +23,11 @@ TOL_X = 1e-4
 TOL_GRAD = 1e-3
 
 
-def run_gpu(batch, mem="device", need_backward=True, dl=None, **cfg):
+def run_gpu(batch, mem="device", need_backward=True, dl=None, formulation="implicit", **cfg):
     import torch
     from paper_2605_17913_b200.solver import QPSolver
     shared = [k for k, v in batch.shared.items() if v]
-    S = QPSolver(batch.batch, batch.n, batch.m, batch.p, shared=shared, mem=mem, **cfg)
+    S = QPSolver(batch.batch, batch.n, batch.m, batch.p, shared=shared, mem=mem, formulation=formulation, **cfg)
     dev = "cuda:0"
 
     def T(name):

@@ -78,6 +78,7 @@ Layout make_layout(int n, int m, int p, int formulation) {
   // large-N kernels (generic pointers); path 1 kernels assume a full fit
   if (L.ncap < L.Nmax) L.big = true;
   if (L.big) { L.threads = 256; L.minb = 1; }
+  if (const char* e = getenv("QPB200_THREADS")) L.threads = atoi(e);  // experiments: 32|64|128|256
   L.ksmem = L.ncap > 0 ? qpb::KLayout::make(L.ncap, L.n4).size() : 0;
   L.smem = qpb::ipm_smem_bytes(L.n4, m, p, L.N4max, L.ksmem);
   return L;
@@ -93,6 +94,14 @@ KernelSet pick_kernels(const Layout& L, int formulation) {
   if (formulation == QP_EXPLICIT) {
     if (L.big) return {0, nullptr, nullptr};
     return {128, qpb::xpm_solve_kernel<128, 1>, qpb::xpm_backward_kernel<128, 1>};
+  }
+  if (L.threads == 32) {
+    if (L.big) return {32, qpb::ipm_solve_kernel<32, 1, true>, qpb::ipm_backward_kernel<32, 1, true>};
+    return {32, qpb::ipm_solve_kernel<32, 1, false>, qpb::ipm_backward_kernel<32, 1, false>};
+  }
+  if (L.threads == 64) {
+    if (L.big) return {64, qpb::ipm_solve_kernel<64, 1, true>, qpb::ipm_backward_kernel<64, 1, true>};
+    return {64, qpb::ipm_solve_kernel<64, 1, false>, qpb::ipm_backward_kernel<64, 1, false>};
   }
   if (L.big) return {256, qpb::ipm_solve_kernel<256, 1, true>, qpb::ipm_backward_kernel<256, 1, true>};
   switch (L.minb) {

@@ -188,25 +188,29 @@ __device__ float assemble(float* K, const Smem& S, const Args& a, const Prob& P,
                           const float* om, const float* cw, const float* e) {
   const int tid = threadIdx.x;
   const int n = a.n, n4 = a.n4, p = a.p, N = L.N, N4 = L.N4;
-  // 1. rows ≥ n4: C rows of the active constraints, A rows, padding; the tail
-  //    of every row beyond its diagonal (rest of its diagonal block + pad) = 0.
-  for (int r = n4 + tid; r < N4; r += NT) {
-    float* row = K + L.off(r);
-    const int len = L.len(r >> 4);
-    if (r < n4 + pa) {
-      const int k = S.act[r - n4];
-      const float w = cw[k];
-      const float* g = P.G + k * n;
-      for (int j = 0; j < n4; ++j) row[j] = j < n ? w * __ldg(g + j) : 0.f;
-    } else if (r < N) {
-      const float* arow = P.A + (r - n4 - pa) * n;
-      for (int j = 0; j < n4; ++j) row[j] = j < n ? __ldg(arow + j) : 0.f;
-    } else {
-      for (int j = 0; j < n4; ++j) row[j] = 0.f;
-    }
-    for (int j = n4; j < len; ++j) row[j] = 0.f;
-    row[r] = r < n4 + pa ? -e[S.act[r - n4]] : (r < N ? 0.f : -1.f);
+  // 1. zero the whole buffer of this layout (float4 stores), then scatter the
+  //    nonzeros of the rows ≥ n4: C rows d₊_k g_k of the active constraints,
+  //    A rows, −d₋ on the w diagonal, −1 on padding rows.
+  {
+    float4* K4 = reinterpret_cast<float4*>(K);
+    const int nz4 = L.size() >> 2;
+    for (int i = tid; i < nz4; i += NT) K4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
+  __syncthreads();
+  const int nrow = N - n4;  // C rows then A rows
+  for (int idx = tid; idx < nrow * n; idx += NT) {
+    const int rr = idx / n, j = idx - rr * n;
+    const int r = n4 + rr;
+    float val;
+    if (rr < pa) {
+      const int k = S.act[rr];
+      val = cw[k] * __ldg(P.G + k * n + j);
+    } else {
+      val = __ldg(P.A + (rr - pa) * n + j);
+    }
+    K[L.off(r) + j] = val;
+  }
+  for (int r = n4 + tid; r < N4; r += NT) K[L.off(r) + r] = r < n4 + pa ? -e[S.act[r - n4]] : (r < N ? 0.f : -1.f);
   // 2. H = Q + Gᵀ diag(ω) G: 4×4 register tiles of the lower triangle; G rows
   //    are read from global memory (L1-resident across iterations).
   const int T = n4 >> 2;
@@ -242,16 +246,14 @@ __device__ float assemble(float* K, const Smem& S, const Args& a, const Prob& P,
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      float* row = K + L.off(i0 + u);
+      float* row = K + L.off(i0 + u) + j0;
+      if (I != J) {
+        *reinterpret_cast<float4*>(row) = make_float4(acc[u][0], acc[u][1], acc[u][2], acc[u][3]);
+      } else {
 #pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        const int i = i0 + u, j = j0 + w;
-        if (j <= i) row[j] = acc[u][w];
-        if (i == j && i < n) dmax = fmaxf(dmax, fabsf(acc[u][w]));
-      }
-      if (I == J) {  // zero the tail of row i0+u beyond the diagonal
-        const int len = L.len((i0 + u) >> 4);
-        for (int j = i0 + u + 1; j < len; ++j) row[j] = 0.f;
+        for (int w = 0; w < 4; ++w)
+          if (w <= u) row[w] = acc[u][w];
+        if (i0 + u < n) dmax = fmaxf(dmax, fabsf(acc[u][u]));
       }
     }
   }

@@ -65,7 +65,7 @@ struct Smem {
   float *K, *rinv, *rhs;
   float *x, *y, *z, *s, *v, *dp, *dm, *c, *om;
   float *rz, *rs, *f2, *t, *gx, *dx, *dy, *dz, *ds_x;
-  float *red, *scr;
+  float *red, *scr, *colscr;
   int *act, *widx, *flag;
   float* end;
 };
@@ -97,6 +97,7 @@ __host__ __device__ inline Smem layout(float* base, int n4, int m, int p, int N4
   S.ds_x = q; q += n4 + m4;  // standard arm: predictor / centering Δx, Δy
   S.red = q; q += 160;
   S.scr = q; q += 16 * 17 + 16;
+  S.colscr = q; q += 4 * 4 * 64;  // residual column partial sums (≤ 4 groups × 4 sums × 64 columns)
   S.act = reinterpret_cast<int*>(q); q += p4;
   S.widx = reinterpret_cast<int*>(q); q += p4;
   S.flag = reinterpret_cast<int*>(q); q += 16;
@@ -230,7 +231,31 @@ __device__ float assemble(float* K, const Smem& S, const Args& a, const Prob& P,
         const int i = i0 + u, j = j0 + w;
         acc[u][w] = (i < n && j < n) ? __ldg(P.Q + i * n + j) : (i == j ? 1.f : 0.f);
       }
-    for (int k = 0; k < p; ++k) {
+    // 4 rows of G in flight per step (loads issued before the FMAs)
+    int k = 0;
+    for (; k + 4 <= p; k += 4) {
+      float gi[4][4], gj[4][4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float* g = P.G + (k + q) * n;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          gi[q][u] = i0 + u < n ? __ldg(g + i0 + u) : 0.f;
+          gj[q][u] = j0 + u < n ? __ldg(g + j0 + u) : 0.f;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float w = om[k + q];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) gj[q][u] *= w;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int w2 = 0; w2 < 4; ++w2) acc[u][w2] = fmaf(gi[q][u], gj[q][w2], acc[u][w2]);
+      }
+    }
+    for (; k < p; ++k) {
       const float* g = P.G + k * n;
       const float w = om[k];
       float gi[4], gj[4];
@@ -341,17 +366,51 @@ __device__ Norms residuals(const Smem& S, const Args& a, const Prob& P, float ka
   }
   for (int l = tid; l < m; l += NT) S.rhs[n4 + pa + l] = -(S.gx[p + l] - __ldg(P.b + l));
   __syncthreads();
-  // columns j < n: Qx, Gᵀz, Aᵀy, Gᵀt  (Q symmetric ⇒ (Qx)_j = Σ_i Q_ij x_i)
+  // columns j < n: Qx, Gᵀz, Aᵀy, Gᵀt  (Q symmetric ⇒ (Qx)_j = Σ_i Q_ij x_i).
+  // When n < NT the row ranges are split over ng groups of threads (partial
+  // sums in S.colscr) so that every thread has work.
+  const int gw = (n + 31) & ~31;
+  const int ng = gw >= NT ? 1 : min(NT / gw, 4);
+  if (ng > 1) {
+    const int grp = tid / gw, j = tid - grp * gw;
+    if (grp < ng && j < n) {
+      float qx = 0.f, gz = 0.f, gt = 0.f, ay = 0.f;
+      const int i0 = grp * n / ng, i1 = (grp + 1) * n / ng;
+#pragma unroll 4
+      for (int i = i0; i < i1; ++i) qx = fmaf(__ldg(P.Q + i * n + j), S.x[i], qx);
+      const int k0 = grp * p / ng, k1 = (grp + 1) * p / ng;
+#pragma unroll 4
+      for (int k = k0; k < k1; ++k) {
+        const float g = __ldg(P.G + k * n + j);
+        gz = fmaf(g, S.z[k], gz);
+        gt = fmaf(g, S.t[k], gt);
+      }
+      const int l0 = grp * m / ng, l1 = (grp + 1) * m / ng;
+      for (int l = l0; l < l1; ++l) ay = fmaf(__ldg(P.A + l * n + j), S.y[l], ay);
+      float* cs = S.colscr + grp * 4 * gw;
+      cs[j] = qx; cs[gw + j] = gz; cs[2 * gw + j] = gt; cs[3 * gw + j] = ay;
+    }
+    __syncthreads();
+  }
   float mrt = 0.f, mqx = 0.f, mq = 0.f, mgz = 0.f, may = 0.f, obj = 0.f;
   for (int j = tid; j < n; j += NT) {
     float qx = 0.f, gz = 0.f, gt = 0.f, ay = 0.f;
-    for (int i = 0; i < n; ++i) qx = fmaf(__ldg(P.Q + i * n + j), S.x[i], qx);
-    for (int k = 0; k < p; ++k) {
-      const float g = __ldg(P.G + k * n + j);
-      gz = fmaf(g, S.z[k], gz);
-      gt = fmaf(g, S.t[k], gt);
+    if (ng > 1) {
+      for (int g = 0; g < ng; ++g) {
+        const float* cs = S.colscr + g * 4 * gw;
+        qx += cs[j]; gz += cs[gw + j]; gt += cs[2 * gw + j]; ay += cs[3 * gw + j];
+      }
+    } else {
+#pragma unroll 4
+      for (int i = 0; i < n; ++i) qx = fmaf(__ldg(P.Q + i * n + j), S.x[i], qx);
+#pragma unroll 4
+      for (int k = 0; k < p; ++k) {
+        const float g = __ldg(P.G + k * n + j);
+        gz = fmaf(g, S.z[k], gz);
+        gt = fmaf(g, S.t[k], gt);
+      }
+      for (int l = 0; l < m; ++l) ay = fmaf(__ldg(P.A + l * n + j), S.y[l], ay);
     }
-    for (int l = 0; l < m; ++l) ay = fmaf(__ldg(P.A + l * n + j), S.y[l], ay);
     const float qj = __ldg(P.q + j);
     const float rt = qx + qj + gz + ay;
     S.rhs[j] = -(rt - gt);

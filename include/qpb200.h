@@ -148,6 +148,12 @@ qp_err qp_backward_batched(qp_ctx* ctx, const float* dl_dx, float* dQ, float* dq
 qp_err qp_last_flops(qp_ctx* ctx, double* solve_flops, double* backward_flops);
 
 qp_err qp_destroy(qp_ctx* ctx);
+
+/* Diagnostic (tests only): dense H = Q + Gᵀ diag(om) G (n×n, row-major) on
+ * the 3×TF32 tcgen05 tensor-core tile routine used by the large-n assembly.
+ * All pointers device memory; asynchronous on `stream`. */
+qp_err qp_debug_tc_syrk(const float* G, const float* om, const float* Q, int32_t n, int32_t p, float* H,
+                        void* stream);
 const char* qp_error_string(qp_err err);
 
 #ifdef __cplusplus

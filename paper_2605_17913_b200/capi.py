@@ -39,7 +39,8 @@ class QpInfo(C.Structure):
 
 
 EXPORTS = ("qp_config_default", "qp_create", "qp_set_stream", "qp_get_info", "qp_max_kkt_dim",
-           "qp_solve_batched", "qp_backward_batched", "qp_last_flops", "qp_destroy", "qp_error_string")
+           "qp_solve_batched", "qp_backward_batched", "qp_last_flops", "qp_destroy", "qp_error_string",
+           "qp_debug_tc_syrk")
 
 _lib = None
 
@@ -68,6 +69,8 @@ def load(path: str | None = None):
     L.qp_backward_batched.argtypes = [V] * 10
     L.qp_destroy.argtypes = [V]
     L.qp_last_flops.argtypes = [V, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.qp_debug_tc_syrk.argtypes = [V, V, V, C.c_int32, C.c_int32, V, V]
+    L.qp_debug_tc_syrk.restype = C.c_int
     L.qp_error_string.argtypes = [C.c_int]
     L.qp_error_string.restype = C.c_char_p
     for f in ("qp_config_default", "qp_create", "qp_set_stream", "qp_get_info", "qp_solve_batched",
@@ -119,6 +122,11 @@ def qp_last_flops(h):
     a, b = C.c_double(), C.c_double()
     check(load().qp_last_flops(h, C.byref(a), C.byref(b)), "qp_last_flops")
     return a.value, b.value
+
+
+def qp_debug_tc_syrk(G, om, Q, n, p, H, stream=None):
+    check(load().qp_debug_tc_syrk(C.c_void_p(G), C.c_void_p(om), C.c_void_p(Q), n, p, C.c_void_p(H),
+                                  C.c_void_p(stream or 0)), "qp_debug_tc_syrk")
 
 
 def qp_destroy(h):

@@ -191,7 +191,7 @@ __device__ __forceinline__ void invert_diag_block(float* __restrict__ K, const K
 // ------------------------------------------------------------------------
 template <int NT>
 __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float theta, float* __restrict__ rinv,
-                         int* __restrict__ flag) {
+                         int* __restrict__ flag, float* __restrict__ colT) {
   constexpr int NW = NT / 32;
   constexpr int RPT = (256 + NT - 1) / NT;  // rows per thread (N4 ≤ 256)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -207,6 +207,11 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
     //      suffices.  Each thread keeps its row's remaining panel columns in a
     //      register window that shifts by one per step (w[0] = column k), and
     //      stores l_ik = a_ik s_k / l_kk as soon as column k is final. ----------
+    //      The current column k of the diagonal-block rows is published in
+    //      colT[k][·] at positions RELATIVE to k (colT[k][j] = a_{k+j,k}), so
+    //      every thread reads it as four float4 broadcasts at static offsets,
+    //      matching its shifting window.  Warps whose rows all lie past N4 skip
+    //      the step (barriers only).
     float w[RPT][KB];
     float* rowp[RPT];
     bool has[RPT];
@@ -222,6 +227,11 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
         w[u][4 * j4] = t.x; w[u][4 * j4 + 1] = t.y; w[u][4 * j4 + 2] = t.z; w[u][4 * j4 + 3] = t.w;
       }
     }
+    if (tid < KB) colT[tid] = tid < kb ? w[0][0] : 0.f;  // column 0 (NT ≥ 16: rows < 16 have u = 0)
+    // warp-uniform: does any row of (warp, u) lie inside the panel?
+    bool wact[RPT];
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) wact[u] = k0 + 32 * warp + u * NT < N4;
     // l_ik is written one step late (column k is still being read during step k)
     float pend[RPT];
     bool pv[RPT];
@@ -229,24 +239,32 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
     for (int u = 0; u < RPT; ++u) { pend[u] = 0.f; pv[u] = false; }
     for (int k = 0; k < kb; ++k) {
       __syncthreads();
+      if (!wact[0]) continue;  // rows of u ≥ 1 lie further down: inactive too
 #pragma unroll
       for (int u = 0; u < RPT; ++u) {
         if (pv[u]) rowp[u][k - 1] = pend[u];
         pv[u] = false;
       }
+      float col[KB];  // col[j] = a_{k+j, k}
+      {
+        const float4* c4 = reinterpret_cast<const float4*>(colT + KB * k);
+#pragma unroll
+        for (int j4 = 0; j4 < KB / 4; ++j4) {
+          const float4 t = c4[j4];
+          col[4 * j4] = t.x; col[4 * j4 + 1] = t.y; col[4 * j4 + 2] = t.z; col[4 * j4 + 3] = t.w;
+        }
+      }
       const float s = sgn_of(k0 + k, npos);
-      float d = s * D[k * Lb + k];
+      float d = s * col[0];
       const bool fl = !(d >= theta);
       if (fl) d = theta;
       const float rs = rsqrtf(d);  // 1/l_kk
       if (tid == 0) { rinv[k0 + k] = rs; nfloor += fl; }
       const float inv = s * rs * rs;  // 1/a_kk (floored)
       const float sr = s * rs;
-      float col[KB];  // col[j] = a_{k+j, k}, j ≥ 1 (rows past the block clamped)
-#pragma unroll
-      for (int j = 1; j < KB; ++j) col[j] = D[min(k + j, kb - 1) * Lb + k];
 #pragma unroll
       for (int u = 0; u < RPT; ++u) {
+        if (!wact[u]) continue;
         const int il = tid + u * NT;  // row index relative to k0
         if (has[u] && il >= k) {
           pv[u] = true;
@@ -257,7 +275,7 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
             pend[u] = w[u][0] * sr;  // l_ik
 #pragma unroll
             for (int j = 1; j < KB; ++j) w[u][j] = fmaf(f, col[j], w[u][j]);
-            if (il < kb && k + 1 < kb) rowp[u][k + 1] = w[u][1];  // publish column k+1
+            if (u == 0 && il < kb && k + 1 < kb) colT[KB * (k + 1) + il - k - 1] = w[u][1];  // publish
           }
         }
 #pragma unroll

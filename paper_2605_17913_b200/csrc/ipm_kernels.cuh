@@ -18,6 +18,7 @@
 // on), and the size drops from n+p+m to n+|A|+m.
 #pragma once
 #include "ipm_cta.cuh"
+#include "tc_syrk.cuh"
 
 namespace qpb {
 
@@ -43,6 +44,7 @@ struct Args {
   unsigned long long* prof;  // optional per-CTA phase cycle counters (diagnostics; nullptr = off)
   float* flops;              // per-problem algorithmic flops of this call, nullptr = off
   float* kglob;              // per-CTA KKT workspaces in global memory (iterations with N > ncap)
+  int tcf;                   // floats of the tensor-core staging area (large-N kernels; 0 = none)
 };
 
 // Algorithmic flops of one Newton iteration on the reduced system of size
@@ -67,10 +69,11 @@ struct Smem {
   float *rz, *rs, *f2, *t, *gx, *dx, *dy, *dz, *ds_x;
   float *red, *scr, *colscr;
   int *act, *widx, *flag;
+  float* tc;  // tcgen05 operand staging + mbarrier (large-N kernels)
   float* end;
 };
 
-__host__ __device__ inline Smem layout(float* base, int n4, int m, int p, int N4max, int ksize) {
+__host__ __device__ inline Smem layout(float* base, int n4, int m, int p, int N4max, int ksize, int tcf) {
   const int m4 = (m + 3) & ~3, p4 = (p + 3) & ~3;
   Smem S;
   float* q = base;
@@ -101,17 +104,18 @@ __host__ __device__ inline Smem layout(float* base, int n4, int m, int p, int N4
   S.act = reinterpret_cast<int*>(q); q += p4;
   S.widx = reinterpret_cast<int*>(q); q += p4;
   S.flag = reinterpret_cast<int*>(q); q += 16;
+  S.tc = q; q += tcf;
   S.end = q;
   return S;
 }
 
-__host__ inline size_t ipm_smem_bytes(int n4, int m, int p, int N4max, int ksize) {
-  const Smem S = layout(nullptr, n4, m, p, N4max, ksize);
+__host__ inline size_t ipm_smem_bytes(int n4, int m, int p, int N4max, int ksize, int tcf) {
+  const Smem S = layout(nullptr, n4, m, p, N4max, ksize, tcf);
   return (size_t)reinterpret_cast<uintptr_t>(S.end);
 }
 
 __device__ inline Smem carve(float* base, const Args& a) {
-  return layout(base, a.n4, a.m, a.p, a.N4max, a.ksmem);
+  return layout(base, a.n4, a.m, a.p, a.N4max, a.ksmem, a.tcf);
 }
 
 // Where this iteration's KKT matrix lives.  Path 1 kernels (BIG = false)
@@ -133,7 +137,7 @@ __device__ __forceinline__ int factor_any(float* K, const Smem& S, const KLayout
   return factor_big<NT>(K, L, theta, S.rinv, S.flag, S.scr);
 #else
   if (BIG && L.N4 > 256) return factor_big<NT>(K, L, theta, S.rinv, S.flag, S.scr);
-  return factor_qd<NT>(K, L, theta, S.rinv, S.flag);
+  return factor_qd<NT>(K, L, theta, S.rinv, S.flag, S.scr);
 #endif
 }
 
@@ -184,7 +188,7 @@ __device__ int compact_active(const Smem& S, int p, bool all_inactive) {
 // in the packed layout L (N = n4 + pa + m).  cw = weights of the C rows (d₊),
 // e = the −diagonal of the w block (d₋), om = ω.  Returns max|diag|.
 // ------------------------------------------------------------------------
-template <int NT>
+template <int NT, bool TC = false>
 __device__ float assemble(float* K, const Smem& S, const Args& a, const Prob& P, const KLayout& L, int pa,
                           const float* om, const float* cw, const float* e) {
   const int tid = threadIdx.x;
@@ -212,11 +216,33 @@ __device__ float assemble(float* K, const Smem& S, const Args& a, const Prob& P,
     K[L.off(r) + j] = val;
   }
   for (int r = n4 + tid; r < N4; r += NT) K[L.off(r) + r] = r < n4 + pa ? -e[S.act[r - n4]] : (r < N ? 0.f : -1.f);
+  float dmax = 0.f;
+  if constexpr (TC) {
+    // 2'. large n: H = Q + Gᵀ diag(ω) G on the tensor cores (tc_syrk.cuh,
+    //     3×TF32), 128×128 tiles of the lower triangle; the epilogue adds Q
+    //     (identity on the padding rows n..n4) and stores the lower part.
+    const tc::TcState ts = tc::tc_state(S.tc);
+    for (int i0 = 0; i0 < n4; i0 += tc::TM)
+      for (int j0 = 0; j0 <= i0; j0 += tc::TN)
+        tc::syrk_tile<NT>(ts, P.G, om, p, n, i0, j0, [&](int i, int c0, const float* v) {
+          if (i >= n4) return;
+          float* row = K + L.off(i);
+          const float* qrow = P.Q + (size_t)i * n;
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            const int j = c0 + c;
+            if (j <= i) {
+              const float val = (i < n && j < n) ? __ldg(qrow + j) + v[c] : (i == j ? 1.f : 0.f);
+              row[j] = val;
+              if (i == j && i < n) dmax = fmaxf(dmax, fabsf(val));
+            }
+          }
+        });
+  } else {
   // 2. H = Q + Gᵀ diag(ω) G: 4×4 register tiles of the lower triangle; G rows
   //    are read from global memory (L1-resident across iterations).
   const int T = n4 >> 2;
   const int nt = T * (T + 1) / 2;
-  float dmax = 0.f;
   for (int t = tid; t < nt; t += NT) {
     int I = (int)((sqrtf(8.f * t + 1.f) - 1.f) * 0.5f);
     while ((I + 1) * (I + 2) / 2 <= t) ++I;
@@ -281,6 +307,7 @@ __device__ float assemble(float* K, const Smem& S, const Args& a, const Prob& P,
         if (i0 + u < n) dmax = fmaxf(dmax, fabsf(acc[u][u]));
       }
     }
+  }
   }
   for (int r = tid; r < pa; r += NT) dmax = fmaxf(dmax, fabsf(e[S.act[r]]));
   float vals[1] = {dmax};
@@ -594,7 +621,7 @@ __device__ __forceinline__ void solve_problem(const Args& a, const Smem& S, cons
     float* const K = kkt_ptr<BIG>(S, a, L);
     tph[5] += pa; tph[6] += L.N;
     fl += iter_flops(n, m, p, pa, !init, true, true);
-    const float dmax = assemble<NT>(K, S, a, P, L, pa, S.om, cw, ev);
+    const float dmax = assemble<NT, BIG>(K, S, a, P, L, pa, S.om, cw, ev);
     long long t1 = clock64(); tph[1] += t1 - t0; t0 = t1;
     factor_any<NT, BIG>(K, S, L, a.floor_rel * dmax);
     t1 = clock64(); tph[2] += t1 - t0; t0 = t1;
@@ -651,7 +678,9 @@ template <int NT, int MINB, bool BIG>
 __global__ void __launch_bounds__(NT, MINB) ipm_solve_kernel(const Args a) {
   extern __shared__ __align__(16) float smem[];
   const Smem S = carve(smem, a);
+  if constexpr (BIG) tc::tmem_alloc(tc::tc_state(S.tc));
   for (int bid = blockIdx.x; bid < a.B; bid += gridDim.x) solve_problem<NT, BIG>(a, S, bid);
+  if constexpr (BIG) tc::tmem_free(*tc::tc_state(S.tc).tmem_slot);
 }
 
 // ------------------------------------------------------------------------
@@ -722,7 +751,7 @@ __device__ __forceinline__ void backward_problem(const Args& a, const Smem& S, c
       const int pa = R.pa;
       const KLayout L = KLayout::make(n4 + pa + m, n4);
       float* const K = kkt_ptr<BIG>(S, a, L);
-      const float dmax = assemble<NT>(K, S, a, P, L, pa, S.om, S.dp, S.dm);
+      const float dmax = assemble<NT, BIG>(K, S, a, P, L, pa, S.om, S.dp, S.dm);
       factor_any<NT, BIG>(K, S, L, a.floor_rel * dmax);
       fl += iter_flops(n, m, p, pa, true, true, true);  // the adjoint solve replaces the last step's
       it = k;
@@ -780,7 +809,9 @@ template <int NT, int MINB, bool BIG>
 __global__ void __launch_bounds__(NT, MINB) ipm_backward_kernel(const Args a) {
   extern __shared__ __align__(16) float smem[];
   const Smem S = carve(smem, a);
+  if constexpr (BIG) tc::tmem_alloc(tc::tc_state(S.tc));
   for (int bid = blockIdx.x; bid < a.B; bid += gridDim.x) backward_problem<NT, BIG>(a, S, bid);
+  if constexpr (BIG) tc::tmem_free(*tc::tc_state(S.tc).tmem_slot);
 }
 
 // ------------------------------------------------------------------------

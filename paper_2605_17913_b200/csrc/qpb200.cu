@@ -15,12 +15,13 @@
 
 #include "../../include/qpb200.h"
 #include "xpm_kernels.cuh"
+#include "tc_syrk.cuh"
 
 namespace {
 
-// Two kernel shapes: 256 threads (register budget for 3 CTAs/SM) and 128
-// threads (same smem, 3 CTAs/SM, no register spills).  qp_create picks one;
-// QPB200_THREADS=128|256 overrides (experiments).
+// Two kernel shapes: path 1 (the whole KKT system in shared memory, 128
+// threads, 1-4 CTAs/SM) and the large-N kernels (256 threads, 1 CTA/SM,
+// tensor-core assembly, KKT system in smem or in a per-CTA global workspace).
 constexpr size_t kMaxSmem = 232448;  // 227 KB opt-in dynamic shared memory per CTA (sm_100a)
 
 struct Layout {
@@ -32,9 +33,12 @@ struct Layout {
   size_t smem;
 };
 
-size_t smem_for(const Layout& L, int m, int p, int ncap) {
+// floats of the tcgen05 staging area the large-N kernels carry
+int tc_floats(bool big) { return big ? qpb::tc::SMEM_BYTES / 4 : 0; }
+
+size_t smem_for(const Layout& L, int m, int p, int ncap, bool big) {
   const int ks = ncap > 0 ? qpb::KLayout::make(ncap, L.n4).size() : 0;
-  return qpb::ipm_smem_bytes(L.n4, m, p, L.N4max, ks);
+  return qpb::ipm_smem_bytes(L.n4, m, p, L.N4max, ks, tc_floats(big));
 }
 
 // Shared-memory budget per CTA (dynamic part) for `ctas` CTAs per SM.
@@ -48,7 +52,7 @@ Layout make_layout(int n, int m, int p, int formulation) {
   L.Nmax = L.n4 + (formulation == QP_EXPLICIT ? 0 : p) + m;
   L.N4max = (L.Nmax + 3) & ~3;
   L.kglob = qpb::KLayout::make(L.Nmax, L.n4).size();
-  L.big = L.N4max > 256;
+  L.big = false;
   // The KKT buffer in smem holds reduced systems up to ncap; iterations with
   // a larger active set use the CTA's global workspace.  Measured on config
   // 2/3: more CTAs per SM do NOT pay when they shrink L1 (Q, G are re-read
@@ -60,27 +64,40 @@ Layout make_layout(int n, int m, int p, int formulation) {
   int env_ctas = 0;
   if (const char* e = getenv("QPB200_CTAS")) env_ctas = atoi(e);
   L.threads = 128; L.minb = 1; L.ncap = 0;
-  const int want[4] = {4, 3, 2, 1};
-  for (int w : want) {
-    if (env_ctas && w != env_ctas) continue;
-    const size_t bud = budget(w);
-    if (smem_for(L, m, p, 0) > bud) continue;
-    int lo = 0, hi = L.Nmax;
-    while (lo < hi) {  // largest ncap that fits the budget
-      const int mid = (lo + hi + 1) / 2;
-      if (smem_for(L, m, p, mid) <= bud) lo = mid; else hi = mid - 1;
+  // path 1: the worst-case system fits the smem buffer and the register-panel
+  // factorisation (N4max ≤ 256) at some CTA count
+  bool fit = false;
+  if (L.N4max <= 256 && env_cap < 0 && !getenv("QPB200_FORCE_GLOBAL")) {
+    const int want[4] = {4, 3, 2, 1};
+    for (int w : want) {
+      if (env_ctas && w != env_ctas) continue;
+      if (smem_for(L, m, p, L.Nmax, false) <= budget(w)) { L.ncap = L.Nmax; L.minb = w; fit = true; break; }
     }
-    if (lo >= L.Nmax || w == 1 || env_ctas) { L.ncap = lo; L.minb = w; break; }
   }
-  if (env_cap >= 0) L.ncap = std::min(env_cap, L.ncap);
-  if (getenv("QPB200_FORCE_GLOBAL")) L.ncap = 0;
-  // a buffer smaller than the worst case needs the run-time placement of the
-  // large-N kernels (generic pointers); path 1 kernels assume a full fit
-  if (L.ncap < L.Nmax) L.big = true;
-  if (L.big) { L.threads = 256; L.minb = 1; }
-  if (const char* e = getenv("QPB200_THREADS")) L.threads = atoi(e);  // experiments: 32|64|128|256
+  if (!fit) {
+    // large-N kernels: one CTA per SM (256 threads), tensor-core assembly,
+    // the largest smem KKT buffer next to the vectors and the tc staging
+    // area; iterations whose reduced system is larger use the CTA's global
+    // workspace (hybrid)
+    L.big = true;
+    const size_t bud = budget(1);
+    int lo = 0, hi = L.Nmax;
+    if (smem_for(L, m, p, 0, true) > bud) {
+      lo = 0;  // vectors alone do not fit: qp_create reports QP_ERR_SHAPE
+    } else {
+      while (lo < hi) {  // largest ncap that fits the budget
+        const int mid = (lo + hi + 1) / 2;
+        if (smem_for(L, m, p, mid, true) <= bud) lo = mid; else hi = mid - 1;
+      }
+    }
+    L.ncap = lo;
+    if (env_cap >= 0) L.ncap = std::min(env_cap, L.ncap);
+    if (getenv("QPB200_FORCE_GLOBAL")) L.ncap = 0;
+    L.threads = 256; L.minb = 1;
+  }
+  if (const char* e = getenv("QPB200_THREADS"); e && !L.big) L.threads = atoi(e);  // experiments: 128|256
   L.ksmem = L.ncap > 0 ? qpb::KLayout::make(L.ncap, L.n4).size() : 0;
-  L.smem = qpb::ipm_smem_bytes(L.n4, m, p, L.N4max, L.ksmem);
+  L.smem = qpb::ipm_smem_bytes(L.n4, m, p, L.N4max, L.ksmem, tc_floats(L.big));
   return L;
 }
 
@@ -94,14 +111,6 @@ KernelSet pick_kernels(const Layout& L, int formulation) {
   if (formulation == QP_EXPLICIT) {
     if (L.big) return {0, nullptr, nullptr};
     return {128, qpb::xpm_solve_kernel<128, 1>, qpb::xpm_backward_kernel<128, 1>};
-  }
-  if (L.threads == 32) {
-    if (L.big) return {32, qpb::ipm_solve_kernel<32, 1, true>, qpb::ipm_backward_kernel<32, 1, true>};
-    return {32, qpb::ipm_solve_kernel<32, 1, false>, qpb::ipm_backward_kernel<32, 1, false>};
-  }
-  if (L.threads == 64) {
-    if (L.big) return {64, qpb::ipm_solve_kernel<64, 1, true>, qpb::ipm_backward_kernel<64, 1, true>};
-    return {64, qpb::ipm_solve_kernel<64, 1, false>, qpb::ipm_backward_kernel<64, 1, false>};
   }
   if (L.big) return {256, qpb::ipm_solve_kernel<256, 1, true>, qpb::ipm_backward_kernel<256, 1, true>};
   switch (L.minb) {
@@ -179,6 +188,7 @@ qpb::Args base_args(const qp_ctx* c) {
   a.B = c->d.batch; a.n = c->d.n; a.m = c->d.m_eq; a.p = c->d.p;
   a.n4 = c->L.n4; a.Nmax = c->L.Nmax; a.N4max = c->L.N4max;
   a.ksmem = c->L.ksmem; a.ncap = c->L.ncap; a.kglob_size = c->L.kglob;
+  a.tcf = tc_floats(c->L.big);
   a.sQ = c->d.bstride_Q; a.sq = c->d.bstride_q; a.sA = c->d.bstride_A;
   a.sb = c->d.bstride_b; a.sG = c->d.bstride_G; a.sh = c->d.bstride_h;
   a.tol = c->c.tol; a.sigma = c->c.sigma; a.tau = c->c.tau; a.kappa_relax = c->c.kappa_relax;
@@ -528,6 +538,16 @@ qp_err qp_last_flops(qp_ctx* c, double* solve_flops, double* backward_flops) {
   if (solve_flops) *solve_flops = sums[0];
   if (backward_flops) *backward_flops = sums[1];
   return QP_OK;
+}
+
+qp_err qp_debug_tc_syrk(const float* G, const float* om, const float* Q, int32_t n, int32_t p, float* H,
+                        void* stream) {
+  if (!G || !om || !Q || !H || n < 1 || p < 1) return QP_ERR_INVALID_ARG;
+  auto k = qpb::tc::debug_syrk_kernel<128>;
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, qpb::tc::SMEM_BYTES) != cudaSuccess)
+    return QP_ERR_CUDA;
+  k<<<1, 128, qpb::tc::SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(G, om, Q, n, p, H);
+  return cuda_ok(cudaGetLastError());
 }
 
 qp_err qp_destroy(qp_ctx* c) {

@@ -140,7 +140,7 @@ __device__ bool x_init(const Smem& S, const Args& a, const Prob& P) {
   }
   for (int l = tid; l < m; l += NT) S.rhs[n4 + l] = __ldg(P.b + l);
   for (int j = n4 + m + tid; j < r4(n4 + m); j += NT) S.rhs[j] = 0.f;
-  factor_qd<NT>(S.K, L, a.floor_rel * dmax, S.rinv, S.flag);
+  factor_qd<NT>(S.K, L, a.floor_rel * dmax, S.rinv, S.flag, S.scr);
   solve_qd<NT>(S.K, L, S.rinv, S.rhs);
   for (int j = tid; j < n; j += NT) S.x[j] = S.rhs[j];
   for (int l = tid; l < m; l += NT) S.y[l] = S.rhs[n4 + l];
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(NT, MINB) xpm_solve_kernel(const Args a) {
       if (k == a.max_iter) { status = ST_MAX_ITER; break; }
       const float mu = R.gap / (float)p;
       const float dmax = assemble<NT>(S.K, S, a, P, L, 0, S.om, S.om, S.om);
-      factor_qd<NT>(S.K, L, 0.f * dmax, S.rinv, S.flag);  // no pivot floor (Q18)
+      factor_qd<NT>(S.K, L, 0.f * dmax, S.rinv, S.flag, S.scr);  // no pivot floor (Q18)
       fl += iter_flops(n, m, p, 0, false, true, true) + 2.f * L.N * L.N + 4.f * p * n;
       // affine predictor: r_c = z ⊙ s
       for (int i = tid; i < p; i += NT) S.t[i] = S.z[i] * S.s[i];
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(NT, MINB) xpm_backward_kernel(const Args a) {
     for (int k = 0; status == ST_CONVERGED; ++k) {
       const Norms R = x_residuals<NT>(S, a, P);
       const float dmax = assemble<NT>(S.K, S, a, P, L, 0, S.om, S.om, S.om);
-      factor_qd<NT>(S.K, L, 0.f * dmax, S.rinv, S.flag);
+      factor_qd<NT>(S.K, L, 0.f * dmax, S.rinv, S.flag, S.scr);
       fl += iter_flops(n, m, p, 0, true, true, true);
       it = k;
       if (R.nonfin > 0.f) { status = ST_FAIL | (STG_RELAX << 8); break; }

@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--so", default=os.path.join(os.path.dirname(__file__), "..", "paper_2605_17913_b200",
                                                  "libqpb200.so"))
     ap.add_argument("--top", type=int, default=40)
+    ap.add_argument("--fn", default=None, help="regex on the MANGLED name picking the function in the .so "
+                    "(default: the kernel regex); needed when several instantiations match")
     ap.add_argument("--metric", default="Warp Stall Sampling (All Samples)",
                     help="per-instruction column to aggregate, e.g. 'Instructions Executed'")
     a = ap.parse_args()
@@ -48,7 +50,7 @@ def main():
     # locate the function body
     mangled = None
     for m in re.finditer(r"^\.text\.(\S+):", sass, flags=re.M):
-        if re.search(a.kernel, m.group(1)):
+        if re.search(a.fn or a.kernel, m.group(1)):
             mangled = m.group(1)
             break
     body = sass.split(f".text.{mangled}:")[1]

@@ -59,7 +59,9 @@ def test_validation_without_gpu(lib):
     cfg.sigma = 1.5
     assert lib.qp_create(C.byref(h), C.byref(good), C.byref(cfg), 0, None) == -1  # invalid config
     cfg = capi.default_config()
-    big = capi.QpDims(4, 1024, 0, 2048, 1024 * 1024, 1024, 0, 0, 2048 * 1024, 2048)
+    # config 5 (n = 1024, p = 2048) is supported; p = 8192 needs more than the
+    # 227 KB of shared memory for the per-constraint vectors alone
+    big = capi.QpDims(4, 1024, 0, 8192, 1024 * 1024, 1024, 0, 0, 8192 * 1024, 8192)
     assert lib.qp_create(C.byref(h), C.byref(big), C.byref(cfg), 0, None) == -2
     assert lib.qp_error_string(-4) == b"CUDA error"
     assert lib.qp_solve_batched(*([None] * 13)) == -1

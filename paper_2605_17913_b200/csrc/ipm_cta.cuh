@@ -227,66 +227,82 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
         w[u][4 * j4] = t.x; w[u][4 * j4 + 1] = t.y; w[u][4 * j4 + 2] = t.z; w[u][4 * j4 + 3] = t.w;
       }
     }
-    if (tid < KB) colT[tid] = tid < kb ? w[0][0] : 0.f;  // column 0 (NT ≥ 16: rows < 16 have u = 0)
+    // columns 0 and 1 as loaded (NT ≥ 16: the diagonal-block rows have u = 0)
+    if (tid < KB) {
+      colT[tid] = tid < kb ? w[0][0] : 0.f;
+      if (tid >= 1) colT[KB + tid - 1] = tid < kb ? w[0][1] : 0.f;
+    }
     // warp-uniform: does any row of (warp, u) lie inside the panel?
     bool wact[RPT];
 #pragma unroll
     for (int u = 0; u < RPT; ++u) wact[u] = k0 + 32 * warp + u * NT < N4;
-    // l_ik is written one step late (column k is still being read during step k)
-    float pend[RPT];
-    bool pv[RPT];
-#pragma unroll
-    for (int u = 0; u < RPT; ++u) { pend[u] = 0.f; pv[u] = false; }
-    for (int k = 0; k < kb; ++k) {
+    // Two columns per barrier (kb is a multiple of 4).  Published per step:
+    // column k (final) and column k+1 updated through k−1; every thread applies
+    // the column-k update to column k+1 itself (15 redundant FMAs) instead of
+    // waiting for a second barrier.  The panel reads columns only from colT,
+    // so the l values go to K at once.
+    for (int k = 0; k < kb; k += 2) {
       __syncthreads();
       if (!wact[0]) continue;  // rows of u ≥ 1 lie further down: inactive too
-#pragma unroll
-      for (int u = 0; u < RPT; ++u) {
-        if (pv[u]) rowp[u][k - 1] = pend[u];
-        pv[u] = false;
-      }
-      float col[KB];  // col[j] = a_{k+j, k}
+      float c0[KB], c1[KB];  // c0[j] = a_{k+j,k};  c1[j] = a_{k+1+j,k+1}
       {
-        const float4* c4 = reinterpret_cast<const float4*>(colT + KB * k);
+        const float4* p0 = reinterpret_cast<const float4*>(colT + KB * k);
+        const float4* p1 = reinterpret_cast<const float4*>(colT + KB * (k + 1));
 #pragma unroll
         for (int j4 = 0; j4 < KB / 4; ++j4) {
-          const float4 t = c4[j4];
-          col[4 * j4] = t.x; col[4 * j4 + 1] = t.y; col[4 * j4 + 2] = t.z; col[4 * j4 + 3] = t.w;
+          const float4 t = p0[j4], t1 = p1[j4];
+          c0[4 * j4] = t.x; c0[4 * j4 + 1] = t.y; c0[4 * j4 + 2] = t.z; c0[4 * j4 + 3] = t.w;
+          c1[4 * j4] = t1.x; c1[4 * j4 + 1] = t1.y; c1[4 * j4 + 2] = t1.z; c1[4 * j4 + 3] = t1.w;
         }
       }
-      const float s = sgn_of(k0 + k, npos);
-      float d = s * col[0];
-      const bool fl = !(d >= theta);
-      if (fl) d = theta;
-      const float rs = rsqrtf(d);  // 1/l_kk
-      if (tid == 0) { rinv[k0 + k] = rs; nfloor += fl; }
-      const float inv = s * rs * rs;  // 1/a_kk (floored)
-      const float sr = s * rs;
+      const float s0 = sgn_of(k0 + k, npos);
+      float d0 = s0 * c0[0];
+      const bool fl0 = !(d0 >= theta);
+      if (fl0) d0 = theta;
+      const float rs0 = rsqrtf(d0);  // 1/l_kk
+      const float inv0 = s0 * rs0 * rs0, sr0 = s0 * rs0;
+      // same rounding as the owner of row k+1+j applies to its own entry
+#pragma unroll
+      for (int j = 0; j + 1 < KB; ++j) c1[j] = fmaf(-c0[j + 1] * inv0, c0[1], c1[j]);
+      const float s1 = sgn_of(k0 + k + 1, npos);
+      float d1 = s1 * c1[0];
+      const bool fl1 = !(d1 >= theta);
+      if (fl1) d1 = theta;
+      const float rs1 = rsqrtf(d1);
+      const float inv1 = s1 * rs1 * rs1, sr1 = s1 * rs1;
+      if (tid == 0) { rinv[k0 + k] = rs0; rinv[k0 + k + 1] = rs1; nfloor += fl0 + fl1; }
 #pragma unroll
       for (int u = 0; u < RPT; ++u) {
         if (!wact[u]) continue;
         const int il = tid + u * NT;  // row index relative to k0
         if (has[u] && il >= k) {
-          pv[u] = true;
           if (il == k) {
-            pend[u] = d * rs;  // l_kk
+            rowp[u][k] = d0 * rs0;  // l_kk
           } else {
-            const float f = -w[u][0] * inv;
-            pend[u] = w[u][0] * sr;  // l_ik
+            const float f0 = -w[u][0] * inv0;
+            rowp[u][k] = w[u][0] * sr0;
 #pragma unroll
-            for (int j = 1; j < KB; ++j) w[u][j] = fmaf(f, col[j], w[u][j]);
-            if (u == 0 && il < kb && k + 1 < kb) colT[KB * (k + 1) + il - k - 1] = w[u][1];  // publish
+            for (int j = 1; j < KB; ++j) w[u][j] = fmaf(f0, c0[j], w[u][j]);
+            if (il == k + 1) {
+              rowp[u][k + 1] = d1 * rs1;
+            } else {
+              const float f1 = -w[u][1] * inv1;
+              rowp[u][k + 1] = w[u][1] * sr1;
+#pragma unroll
+              for (int j = 2; j < KB; ++j) w[u][j] = fmaf(f1, c1[j - 1], w[u][j]);
+              if (u == 0 && il < kb) {  // publish columns k+2 (final) and k+3 (through k+1)
+                colT[KB * (k + 2) + il - k - 2] = w[u][2];
+                if (il >= k + 3) colT[KB * (k + 3) + il - k - 3] = w[u][3];
+              }
+            }
           }
         }
 #pragma unroll
-        for (int j = 0; j + 1 < KB; ++j) w[u][j] = w[u][j + 1];
+        for (int j = 0; j + 2 < KB; ++j) w[u][j] = w[u][j + 2];
+        w[u][KB - 2] = 0.f;
         w[u][KB - 1] = 0.f;
       }
     }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < RPT; ++u)
-      if (pv[u]) rowp[u][kb - 1] = pend[u];
     __syncthreads();
     { const long long t = clock64(); tpan += t - tc0; tc0 = t; }
     // ---- (2) trailing update A22 −= L21 S_b L21ᵀ --------------------------------

@@ -27,6 +27,10 @@
 namespace qpb {
 
 constexpr int KB = 16;  // block / panel width
+#ifndef QPB200_PANEL_COLS
+#define QPB200_PANEL_COLS 2
+#endif
+constexpr int PC = QPB200_PANEL_COLS;  // panel columns per barrier (2 or 4)
 
 // ------------------------------------------------------------------------
 // Retraction map, App. C, written for f32 on the device.
@@ -227,82 +231,154 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
         w[u][4 * j4] = t.x; w[u][4 * j4 + 1] = t.y; w[u][4 * j4 + 2] = t.z; w[u][4 * j4 + 3] = t.w;
       }
     }
-    // columns 0 and 1 as loaded (NT ≥ 16: the diagonal-block rows have u = 0)
+    // columns 0..PC-1 as loaded (NT ≥ 16: the diagonal-block rows have u = 0)
     if (tid < KB) {
-      colT[tid] = tid < kb ? w[0][0] : 0.f;
-      if (tid >= 1) colT[KB + tid - 1] = tid < kb ? w[0][1] : 0.f;
+#pragma unroll
+      for (int q = 0; q < PC; ++q)
+        if (tid >= q) colT[KB * q + tid - q] = tid < kb ? w[0][q] : 0.f;
     }
     // warp-uniform: does any row of (warp, u) lie inside the panel?
     bool wact[RPT];
 #pragma unroll
     for (int u = 0; u < RPT; ++u) wact[u] = k0 + 32 * warp + u * NT < N4;
-    // Two columns per barrier (kb is a multiple of 4).  Published per step:
-    // column k (final) and column k+1 updated through k−1; every thread applies
-    // the column-k update to column k+1 itself (15 redundant FMAs) instead of
-    // waiting for a second barrier.  The panel reads columns only from colT,
-    // so the l values go to K at once.
-    for (int k = 0; k < kb; k += 2) {
+    // PC columns per barrier (kb is a multiple of 4).  Published per step:
+    // columns k..k+PC-1 updated through column k−1; every thread brings them
+    // up to date itself (a PC×16 triangle of redundant FMAs, with exactly the
+    // rounding the owners of those rows apply to their own entries) instead of
+    // waiting for more barriers.  The panel reads columns only from colT, so
+    // the l values go to K at once.
+#ifdef QPB200_PANEL_UNROLL
+    // static column indices: no window shifts, the updates shrink with k
+#pragma unroll
+    for (int k = 0; k < KB; k += PC) {
+      if (k >= kb) break;
       __syncthreads();
       if (!wact[0]) continue;  // rows of u ≥ 1 lie further down: inactive too
-      float c0[KB], c1[KB];  // c0[j] = a_{k+j,k};  c1[j] = a_{k+1+j,k+1}
-      {
-        const float4* p0 = reinterpret_cast<const float4*>(colT + KB * k);
-        const float4* p1 = reinterpret_cast<const float4*>(colT + KB * (k + 1));
+      float c[PC][KB];  // c[q][j] = a_{k+q+j, k+q}
+#pragma unroll
+      for (int q = 0; q < PC; ++q) {
+        const float4* pq = reinterpret_cast<const float4*>(colT + KB * (k + q));
 #pragma unroll
         for (int j4 = 0; j4 < KB / 4; ++j4) {
-          const float4 t = p0[j4], t1 = p1[j4];
-          c0[4 * j4] = t.x; c0[4 * j4 + 1] = t.y; c0[4 * j4 + 2] = t.z; c0[4 * j4 + 3] = t.w;
-          c1[4 * j4] = t1.x; c1[4 * j4 + 1] = t1.y; c1[4 * j4 + 2] = t1.z; c1[4 * j4 + 3] = t1.w;
+          const float4 t = pq[j4];
+          c[q][4 * j4] = t.x; c[q][4 * j4 + 1] = t.y; c[q][4 * j4 + 2] = t.z; c[q][4 * j4 + 3] = t.w;
         }
       }
-      const float s0 = sgn_of(k0 + k, npos);
-      float d0 = s0 * c0[0];
-      const bool fl0 = !(d0 >= theta);
-      if (fl0) d0 = theta;
-      const float rs0 = rsqrtf(d0);  // 1/l_kk
-      const float inv0 = s0 * rs0 * rs0, sr0 = s0 * rs0;
-      // same rounding as the owner of row k+1+j applies to its own entry
+      float dq[PC], rsq[PC], inv[PC], sr[PC];
+      int nf = 0;
 #pragma unroll
-      for (int j = 0; j + 1 < KB; ++j) c1[j] = fmaf(-c0[j + 1] * inv0, c0[1], c1[j]);
-      const float s1 = sgn_of(k0 + k + 1, npos);
-      float d1 = s1 * c1[0];
-      const bool fl1 = !(d1 >= theta);
-      if (fl1) d1 = theta;
-      const float rs1 = rsqrtf(d1);
-      const float inv1 = s1 * rs1 * rs1, sr1 = s1 * rs1;
-      if (tid == 0) { rinv[k0 + k] = rs0; rinv[k0 + k + 1] = rs1; nfloor += fl0 + fl1; }
+      for (int q = 0; q < PC; ++q) {
+#pragma unroll
+        for (int r = 0; r < q; ++r)
+#pragma unroll
+          for (int j = 0; j + q - r < KB - k; ++j) c[q][j] = fmaf(-c[r][q - r + j] * inv[r], c[r][q - r], c[q][j]);
+        const float sg = sgn_of(k0 + k + q, npos);
+        float d = sg * c[q][0];
+        const bool fl = !(d >= theta);
+        if (fl) d = theta;
+        nf += fl;
+        const float rs = rsqrtf(d);
+        dq[q] = d; rsq[q] = rs; inv[q] = sg * rs * rs; sr[q] = sg * rs;
+      }
+      if (tid == 0) {
+#pragma unroll
+        for (int q = 0; q < PC; ++q) rinv[k0 + k + q] = rsq[q];
+        nfloor += nf;
+      }
 #pragma unroll
       for (int u = 0; u < RPT; ++u) {
         if (!wact[u]) continue;
         const int il = tid + u * NT;  // row index relative to k0
         if (has[u] && il >= k) {
-          if (il == k) {
-            rowp[u][k] = d0 * rs0;  // l_kk
-          } else {
-            const float f0 = -w[u][0] * inv0;
-            rowp[u][k] = w[u][0] * sr0;
+          bool live = true;
 #pragma unroll
-            for (int j = 1; j < KB; ++j) w[u][j] = fmaf(f0, c0[j], w[u][j]);
-            if (il == k + 1) {
-              rowp[u][k + 1] = d1 * rs1;
-            } else {
-              const float f1 = -w[u][1] * inv1;
-              rowp[u][k + 1] = w[u][1] * sr1;
+          for (int q = 0; q < PC; ++q) {
+            if (live) {
+              if (il == k + q) {
+                rowp[u][k + q] = dq[q] * rsq[q];  // l_kk
+                live = false;
+              } else {
+                const float f = -w[u][k + q] * inv[q];
+                rowp[u][k + q] = w[u][k + q] * sr[q];
 #pragma unroll
-              for (int j = 2; j < KB; ++j) w[u][j] = fmaf(f1, c1[j - 1], w[u][j]);
-              if (u == 0 && il < kb) {  // publish columns k+2 (final) and k+3 (through k+1)
-                colT[KB * (k + 2) + il - k - 2] = w[u][2];
-                if (il >= k + 3) colT[KB * (k + 3) + il - k - 3] = w[u][3];
+                for (int j = k + q + 1; j < KB; ++j) w[u][j] = fmaf(f, c[q][j - k - q], w[u][j]);
               }
             }
           }
-        }
+          if (live && u == 0 && il < kb) {  // publish columns k+PC.. (updated through k+PC−1)
 #pragma unroll
-        for (int j = 0; j + 2 < KB; ++j) w[u][j] = w[u][j + 2];
-        w[u][KB - 2] = 0.f;
-        w[u][KB - 1] = 0.f;
+            for (int t = 0; t < PC; ++t)
+              if (k + PC + t < KB && il >= k + PC + t) colT[KB * (k + PC + t) + il - k - PC - t] = w[u][k + PC + t];
+          }
+        }
       }
     }
+#else
+    for (int k = 0; k < kb; k += PC) {
+      __syncthreads();
+      if (!wact[0]) continue;  // rows of u ≥ 1 lie further down: inactive too
+      float c[PC][KB];  // c[q][j] = a_{k+q+j, k+q}
+#pragma unroll
+      for (int q = 0; q < PC; ++q) {
+        const float4* pq = reinterpret_cast<const float4*>(colT + KB * (k + q));
+#pragma unroll
+        for (int j4 = 0; j4 < KB / 4; ++j4) {
+          const float4 t = pq[j4];
+          c[q][4 * j4] = t.x; c[q][4 * j4 + 1] = t.y; c[q][4 * j4 + 2] = t.z; c[q][4 * j4 + 3] = t.w;
+        }
+      }
+      float dq[PC], rsq[PC], inv[PC], sr[PC];
+      int nf = 0;
+#pragma unroll
+      for (int q = 0; q < PC; ++q) {
+#pragma unroll
+        for (int r = 0; r < q; ++r)
+#pragma unroll
+          for (int j = 0; j + q - r < KB; ++j) c[q][j] = fmaf(-c[r][q - r + j] * inv[r], c[r][q - r], c[q][j]);
+        const float sg = sgn_of(k0 + k + q, npos);
+        float d = sg * c[q][0];
+        const bool fl = !(d >= theta);
+        if (fl) d = theta;
+        nf += fl;
+        const float rs = rsqrtf(d);
+        dq[q] = d; rsq[q] = rs; inv[q] = sg * rs * rs; sr[q] = sg * rs;
+      }
+      if (tid == 0) {
+#pragma unroll
+        for (int q = 0; q < PC; ++q) rinv[k0 + k + q] = rsq[q];
+        nfloor += nf;
+      }
+#pragma unroll
+      for (int u = 0; u < RPT; ++u) {
+        if (!wact[u]) continue;
+        const int il = tid + u * NT;  // row index relative to k0
+        if (has[u] && il >= k) {
+          bool live = true;
+#pragma unroll
+          for (int q = 0; q < PC; ++q) {
+            if (live) {
+              if (il == k + q) {
+                rowp[u][k + q] = dq[q] * rsq[q];  // l_kk
+                live = false;
+              } else {
+                const float f = -w[u][q] * inv[q];
+                rowp[u][k + q] = w[u][q] * sr[q];
+#pragma unroll
+                for (int j = q + 1; j < KB; ++j) w[u][j] = fmaf(f, c[q][j - q], w[u][j]);
+              }
+            }
+          }
+          if (live && u == 0 && il < kb) {  // publish columns k+PC.. (updated through k+PC−1)
+#pragma unroll
+            for (int t = 0; t < PC; ++t)
+              if (il >= k + PC + t) colT[KB * (k + PC + t) + il - k - PC - t] = w[u][PC + t];
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < KB; ++j) w[u][j] = j + PC < KB ? w[u][j + PC] : 0.f;
+      }
+    }
+#endif
     __syncthreads();
     { const long long t = clock64(); tpan += t - tc0; tc0 = t; }
     // ---- (2) trailing update A22 −= L21 S_b L21ᵀ --------------------------------

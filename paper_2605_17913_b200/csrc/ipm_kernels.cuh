@@ -619,7 +619,7 @@ __device__ __forceinline__ void solve_problem(const Args& a, const Smem& S, cons
     }
     const KLayout L = KLayout::make(n4 + pa + m, n4);
     float* const K = kkt_ptr<BIG>(S, a, L);
-    tph[5] += pa; tph[6] += L.N;
+    tph[5] += pa; tph[6] += L.N; tph[7] = tph[7] > (unsigned long long)L.N ? tph[7] : (unsigned long long)L.N;
     fl += iter_flops(n, m, p, pa, !init, true, true);
     const float dmax = assemble<NT, BIG>(K, S, a, P, L, pa, S.om, cw, ev);
     long long t1 = clock64(); tph[1] += t1 - t0; t0 = t1;

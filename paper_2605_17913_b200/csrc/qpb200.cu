@@ -13,6 +13,9 @@
 #include <cstdlib>
 #include <new>
 
+#include <algorithm>
+#include <vector>
+
 #include "../../include/qpb200.h"
 #include "xpm_kernels.cuh"
 #include "tc_syrk.cuh"
@@ -434,6 +437,13 @@ qp_err qp_solve_batched(qp_ctx* c, const float* Q, const float* q, const float* 
     fprintf(stderr, "[qpb200 phase cycles per CTA] resid %.0f assemble %.0f factor %.0f solve %.0f update %.0f"
                     " | sum pa %.1f sum N %.1f\n",
             tot[0] / B, tot[1] / B, tot[2] / B, tot[3] / B, tot[4] / B, tot[5] / B, tot[6] / B);
+    {
+      std::vector<unsigned long long> mx(B);
+      for (int i = 0; i < B; ++i) mx[i] = hp[i * 8 + 7];
+      std::sort(mx.begin(), mx.end());
+      fprintf(stderr, "[qpb200 largest reduced system per problem] median %llu p90 %llu p99 %llu max %llu (Nmax %d)\n",
+              mx[B / 2], mx[(size_t)(0.9 * (B - 1))], mx[(size_t)(0.99 * (B - 1))], mx[B - 1], c->L.Nmax);
+    }
     delete[] hp;
     unsigned long long fc[4];
     cudaMemcpyFromSymbol(fc, qpb::g_fac_cycles, sizeof(fc));

@@ -116,6 +116,9 @@ KernelSet pick_kernels(const Layout& L, int formulation) {
     return {128, qpb::xpm_solve_kernel<128, 1>, qpb::xpm_backward_kernel<128, 1>};
   }
   if (L.big) return {256, qpb::ipm_solve_kernel<256, 1, true>, qpb::ipm_backward_kernel<256, 1, true>};
+#ifdef QPB200_EXP_256
+  if (L.threads == 256) return {256, qpb::ipm_solve_kernel<256, 3, false>, qpb::ipm_backward_kernel<256, 3, false>};
+#endif
   switch (L.minb) {
     case 5: return {128, qpb::ipm_solve_kernel<128, 5, false>, qpb::ipm_backward_kernel<128, 5, false>};
     case 4: return {128, qpb::ipm_solve_kernel<128, 4, false>, qpb::ipm_backward_kernel<128, 4, false>};
@@ -155,6 +158,12 @@ struct qp_ctx {
   unsigned long long* prof = nullptr;  // QPB200_PHASE_PROFILE diagnostics
   float* flops_solve = nullptr;        // per-problem algorithmic flops of the last calls
   float* flops_bwd = nullptr;
+  // host-memory mode, path 1: the batch runs in kPipe chunks on their own
+  // streams, so chunk i's kernel overlaps chunk i+1's H2D and chunk i−1's D2H
+  static constexpr int kPipe = 4;
+  bool pipe = false;
+  cudaStream_t pst[kPipe] = {};
+  cudaEvent_t pev[kPipe + 1] = {};
 };
 
 namespace {
@@ -197,6 +206,30 @@ qpb::Args base_args(const qp_ctx* c) {
   a.tol = c->c.tol; a.sigma = c->c.sigma; a.tau = c->c.tau; a.kappa_relax = c->c.kappa_relax;
   a.relax_ktol = c->c.relax_ktol; a.floor_rel = c->c.pivot_floor_rel; a.relax_tol = c->c.relax_tol;
   a.max_iter = c->c.max_iter; a.relax_max_iter = c->c.relax_max_iter;
+  return a;
+}
+
+// The arguments of problems [b0, b0 + nb) (shared fields have stride 0).
+qpb::Args chunk_args(qpb::Args a, int b0, int nb) {
+  const long long o = b0;
+  const long long n = a.n, m = a.m, p = a.p;
+  a.B = nb;
+  a.Q += o * a.sQ; a.q += o * a.sq; a.A += o * a.sA; a.b += o * a.sb; a.G += o * a.sG; a.h += o * a.sh;
+  a.x += o * n; a.y += o * m; a.z += o * p; a.s += o * p;
+  if (a.iters) a.iters += o;
+  if (a.status) a.status += o;
+  if (a.dl) a.dl += o * n;
+  if (a.gQ) a.gQ += o * n * n;
+  if (a.gq) a.gq += o * n;
+  if (a.gA) a.gA += o * m * n;
+  if (a.gb) a.gb += o * m;
+  if (a.gG) a.gG += o * p * n;
+  if (a.gh) a.gh += o * p;
+  if (a.wx) { a.wx += o * n; a.wdx += o * n; a.wy += o * m; a.wdy += o * m; a.wz += o * p; a.wdz += o * p; }
+  if (a.riters) a.riters += o;
+  if (a.rstatus) a.rstatus += o;
+  if (a.flops) a.flops += o;
+  if (a.prof) a.prof += 8 * o;
   return a;
 }
 
@@ -336,6 +369,14 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
         (e = dalloc(ctx, &ctx->gh_, field_elems(d->bstride_h, B, p)))) {
       free_all(ctx); delete ctx; return e;
     }
+    // chunked copy/compute overlap: path 1 only (the chunk kernels run
+    // concurrently; the global KKT workspaces of paths 2/3 are per CTA slot)
+    if (!ctx->kglob && B >= 2 * 64 && !getenv("QPB200_NO_PIPE")) {
+      bool ok = true;
+      for (auto& st : ctx->pst) ok = ok && cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess;
+      for (auto& ev : ctx->pev) ok = ok && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess;
+      ctx->pipe = ok;
+    }
   }
   *out = ctx;
   return QP_OK;
@@ -381,14 +422,16 @@ qp_err qp_solve_batched(qp_ctx* c, const float* Q, const float* q, const float* 
   if (cudaSetDevice(c->device) != cudaSuccess) return QP_ERR_CUDA;
   qp_err e;
   const bool host = c->c.mem_kind == QP_MEM_HOST;
+  // host mode: device copies of the six fields (stride 0 = shared, one copy)
+  float* const stage[6] = {c->dQ_, c->dq_, c->dA_, c->db_, c->dG_, c->dh_};
+  const float* const src[6] = {Q, q, A, b, G, h};
+  const int64_t bstr[6] = {d.bstride_Q, d.bstride_q, d.bstride_A, d.bstride_b, d.bstride_G, d.bstride_h};
+  const size_t per[6] = {(size_t)n * n, (size_t)n, (size_t)m * n, (size_t)m, (size_t)p * n, (size_t)p};
+  const bool pipe = host && c->pipe;
   if (host) {
-    if ((e = h2d(c, c->dQ_, Q, field_elems(d.bstride_Q, B, (size_t)n * n))) ||
-        (e = h2d(c, c->dq_, q, field_elems(d.bstride_q, B, n))) ||
-        (e = h2d(c, c->dA_, A, field_elems(d.bstride_A, B, (size_t)m * n))) ||
-        (e = h2d(c, c->db_, b, field_elems(d.bstride_b, B, m))) ||
-        (e = h2d(c, c->dG_, G, field_elems(d.bstride_G, B, (size_t)p * n))) ||
-        (e = h2d(c, c->dh_, h, field_elems(d.bstride_h, B, p))))
-      return e;
+    for (int f = 0; f < 6; ++f)
+      if (!pipe || bstr[f] == 0)  // pipelined: per-problem fields go chunk by chunk below
+        if ((e = h2d(c, stage[f], src[f], field_elems(bstr[f], B, per[f]))) != QP_OK) return e;
     c->Q = c->dQ_; c->q = c->dq_; c->A = c->dA_; c->b = c->db_; c->G = c->dG_; c->h = c->dh_;
     c->x = c->dx_; c->s = c->ds_; c->z = c->dz_; c->y = c->dy_;
   } else {
@@ -413,9 +456,44 @@ qp_err qp_solve_batched(qp_ctx* c, const float* Q, const float* q, const float* 
   a.prof = c->prof;
   a.flops = c->flops_solve;
   a.kglob = c->kglob;
-  c->ks.solve<<<c->grid, c->ks.threads, c->L.smem, c->stream>>>(a);
-  if ((e = cuda_ok(cudaGetLastError())) != QP_OK) return e;
-  if (host) {
+  if (pipe) {
+    // chunk ch on stream pst[ch]: H2D of its problems, its kernel, D2H of its outputs
+    constexpr int KP = qp_ctx::kPipe;
+    const int cs = (B + KP - 1) / KP;
+    if ((e = cuda_ok(cudaEventRecord(c->pev[KP], c->stream))) != QP_OK) return e;
+    for (int ch = 0; ch < KP; ++ch) {
+      const int b0 = ch * cs, nb = std::min(cs, B - b0);
+      if (nb <= 0) break;
+      cudaStream_t st = c->pst[ch];
+      if ((e = cuda_ok(cudaStreamWaitEvent(st, c->pev[KP], 0))) != QP_OK) return e;
+      for (int f = 0; f < 6; ++f)
+        if (bstr[f] != 0 && per[f] > 0 &&
+            (e = cuda_ok(cudaMemcpyAsync(stage[f] + (size_t)b0 * bstr[f], src[f] + (size_t)b0 * bstr[f],
+                                         sizeof(float) * (size_t)nb * bstr[f], cudaMemcpyHostToDevice, st))) !=
+                QP_OK)
+          return e;
+      const qpb::Args ac = chunk_args(a, b0, nb);
+      c->ks.solve<<<std::min(c->grid, nb), c->ks.threads, c->L.smem, st>>>(ac);
+      if ((e = cuda_ok(cudaGetLastError())) != QP_OK) return e;
+      auto o2h = [&](auto* dst, const auto* dsrc, size_t per_prob) -> qp_err {
+        if (!dst || per_prob == 0) return QP_OK;
+        return cuda_ok(cudaMemcpyAsync(dst + (size_t)b0 * per_prob, dsrc + (size_t)b0 * per_prob,
+                                       sizeof(*dst) * (size_t)nb * per_prob, cudaMemcpyDeviceToHost, st));
+      };
+      if ((e = o2h(x, c->dx_, n)) || (e = o2h(s, c->ds_, p)) || (e = o2h(z, c->dz_, p)) ||
+          (e = o2h(y, c->dy_, m)) || (e = o2h(iters, c->dit_, 1)) || (e = o2h(status, c->own_status, 1)))
+        return e;
+      if ((e = cuda_ok(cudaEventRecord(c->pev[ch], st))) != QP_OK) return e;
+      if ((e = cuda_ok(cudaStreamWaitEvent(c->stream, c->pev[ch], 0))) != QP_OK) return e;
+    }
+    if ((e = cuda_ok(cudaStreamSynchronize(c->stream))) != QP_OK) return e;
+  } else {
+    c->ks.solve<<<c->grid, c->ks.threads, c->L.smem, c->stream>>>(a);
+    if ((e = cuda_ok(cudaGetLastError())) != QP_OK) return e;
+  }
+  if (pipe) {
+    // outputs already copied chunk by chunk
+  } else if (host) {
     if ((e = d2h(c, x, c->dx_, (size_t)B * n)) || (e = d2h(c, s, c->ds_, (size_t)B * p)) ||
         (e = d2h(c, z, c->dz_, (size_t)B * p)) || (e = d2h(c, y, c->dy_, (size_t)B * m)) ||
         (e = d2h(c, iters, c->dit_, (size_t)B)) || (e = d2h(c, status, c->own_status, (size_t)B)))
@@ -468,8 +546,9 @@ qp_err qp_backward_batched(qp_ctx* c, const float* dl_dx, float* dQ, float* dq, 
   const float* dl = dl_dx;
   float *oQ = dQ, *oq = dq, *oA = dA, *ob = db, *oG = dG, *oh = dh;
   int32_t *oit = relax_iters, *ost = status;
+  const bool pipe = host && c->pipe;
   if (host) {
-    if ((e = h2d(c, c->ddl_, dl_dx, (size_t)B * n)) != QP_OK) return e;
+    if (!pipe && (e = h2d(c, c->ddl_, dl_dx, (size_t)B * n)) != QP_OK) return e;
     dl = c->ddl_;
     oQ = dQ ? c->gQ_ : nullptr; oq = dq ? c->gq_ : nullptr; oA = dA ? c->gA_ : nullptr;
     ob = db ? c->gb_ : nullptr; oG = dG ? c->gG_ : nullptr; oh = dh ? c->gh_ : nullptr;
@@ -498,8 +577,45 @@ qp_err qp_backward_batched(qp_ctx* c, const float* dl_dx, float* dQ, float* dq, 
   a.rstatus = ost;
   a.flops = c->flops_bwd;
   a.kglob = c->kglob;
-  c->ks.backward<<<c->grid, c->ks.threads, c->L.smem, c->stream>>>(a);
-  if ((e = cuda_ok(cudaGetLastError())) != QP_OK) return e;
+  if (pipe) {
+    // chunk ch on stream pst[ch]: H2D of its cotangents, its kernel, D2H of its
+    // per-problem gradients; shared-field sums follow on c->stream
+    constexpr int KP = qp_ctx::kPipe;
+    const int cs = (B + KP - 1) / KP;
+    if ((e = cuda_ok(cudaEventRecord(c->pev[KP], c->stream))) != QP_OK) return e;
+    float* const gdev[6] = {a.gQ, a.gq, a.gA, a.gb, a.gG, a.gh};
+    float* const ghost[6] = {dQ, dq, dA, db, dG, dh};
+    const size_t gper[6] = {(size_t)n * n, (size_t)n, (size_t)m * n, (size_t)m, (size_t)p * n, (size_t)p};
+    for (int ch = 0; ch < KP; ++ch) {
+      const int b0 = ch * cs, nb = std::min(cs, B - b0);
+      if (nb <= 0) break;
+      cudaStream_t st = c->pst[ch];
+      if ((e = cuda_ok(cudaStreamWaitEvent(st, c->pev[KP], 0))) != QP_OK) return e;
+      if ((e = cuda_ok(cudaMemcpyAsync(c->ddl_ + (size_t)b0 * n, dl_dx + (size_t)b0 * n, sizeof(float) * (size_t)nb * n,
+                                       cudaMemcpyHostToDevice, st))) != QP_OK)
+        return e;
+      const qpb::Args ac = chunk_args(a, b0, nb);
+      c->ks.backward<<<std::min(c->grid, nb), c->ks.threads, c->L.smem, st>>>(ac);
+      if ((e = cuda_ok(cudaGetLastError())) != QP_OK) return e;
+      for (int f = 0; f < 6; ++f)  // per-problem gradients (a.g* is null for shared / skipped fields)
+        if (gdev[f] && ghost[f] && gper[f] > 0 &&
+            (e = cuda_ok(cudaMemcpyAsync(ghost[f] + (size_t)b0 * gper[f], gdev[f] + (size_t)b0 * gper[f],
+                                         sizeof(float) * (size_t)nb * gper[f], cudaMemcpyDeviceToHost, st))) !=
+                QP_OK)
+          return e;
+      if (relax_iters && (e = cuda_ok(cudaMemcpyAsync(relax_iters + b0, c->dit_ + b0, sizeof(int32_t) * nb,
+                                                      cudaMemcpyDeviceToHost, st))) != QP_OK)
+        return e;
+      if (status && (e = cuda_ok(cudaMemcpyAsync(status + b0, c->dst_ + b0, sizeof(int32_t) * nb,
+                                                 cudaMemcpyDeviceToHost, st))) != QP_OK)
+        return e;
+      if ((e = cuda_ok(cudaEventRecord(c->pev[ch], st))) != QP_OK) return e;
+      if ((e = cuda_ok(cudaStreamWaitEvent(c->stream, c->pev[ch], 0))) != QP_OK) return e;
+    }
+  } else {
+    c->ks.backward<<<c->grid, c->ks.threads, c->L.smem, c->stream>>>(a);
+    if ((e = cuda_ok(cudaGetLastError())) != QP_OK) return e;
+  }
   if (shared) {
     auto osum = [&](float* out, const float* U, const float* V, const float* U2, const float* V2, int R, int Cc,
                     float scale) {
@@ -517,7 +633,16 @@ qp_err qp_backward_batched(qp_ctx* c, const float* dl_dx, float* dQ, float* dq, 
     if (d.bstride_h == 0 && oh && p > 0) csum(oh, c->wdz, p, -1.f);
     if ((e = cuda_ok(cudaGetLastError())) != QP_OK) return e;
   }
-  if (host) {
+  if (pipe) {
+    // shared-field sums (computed on c->stream after every chunk) to the host
+    float* const ghost[6] = {dQ, dq, dA, db, dG, dh};
+    float* const gst[6] = {c->gQ_, c->gq_, c->gA_, c->gb_, c->gG_, c->gh_};
+    const int64_t bstr[6] = {d.bstride_Q, d.bstride_q, d.bstride_A, d.bstride_b, d.bstride_G, d.bstride_h};
+    const size_t gper[6] = {(size_t)n * n, (size_t)n, (size_t)m * n, (size_t)m, (size_t)p * n, (size_t)p};
+    for (int f = 0; f < 6; ++f)
+      if (bstr[f] == 0 && ghost[f] && (e = d2h(c, ghost[f], gst[f], gper[f])) != QP_OK) return e;
+    if ((e = cuda_ok(cudaStreamSynchronize(c->stream))) != QP_OK) return e;
+  } else if (host) {
     if ((dQ && (e = d2h(c, dQ, c->gQ_, field_elems(d.bstride_Q, B, (size_t)n * n)))) ||
         (dq && (e = d2h(c, dq, c->gq_, field_elems(d.bstride_q, B, n)))) ||
         (dA && (e = d2h(c, dA, c->gA_, field_elems(d.bstride_A, B, (size_t)m * n)))) ||
@@ -564,6 +689,10 @@ qp_err qp_destroy(qp_ctx* c) {
   if (!c) return QP_ERR_INVALID_ARG;
   cudaSetDevice(c->device);
   free_all(c);
+  for (auto& st : c->pst)
+    if (st) cudaStreamDestroy(st);
+  for (auto& ev : c->pev)
+    if (ev) cudaEventDestroy(ev);
   delete c;
   return QP_OK;
 }

@@ -53,9 +53,9 @@ class QPSolver:
         return capi.qp_last_flops(self.h)
 
     def close(self):
-        if getattr(self, "h", None):
-            capi.qp_destroy(self.h)
-            self.h = None
+        h, self.h = getattr(self, "h", None), None
+        if h and capi is not None and getattr(capi, "qp_destroy", None) is not None:  # not at interpreter exit
+            capi.qp_destroy(h)
 
     __del__ = close
 
@@ -78,7 +78,7 @@ class QPSolver:
     def _alloc(self, shape, dtype=torch.float32):
         if self.mem == "device":
             return torch.empty(shape, dtype=dtype, device=f"cuda:{self.device}")
-        return torch.empty(shape, dtype=dtype).pin_memory()
+        return torch.empty(shape, dtype=dtype, pin_memory=True)  # no staging copy
 
     @staticmethod
     def _ptr(t):

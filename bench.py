@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=2, help="BASELINE.json config index (1-based)")
+    ap.add_argument("--workload", default=None, choices=sorted(gen.WORKLOADS),
+                    help="an N4 application shape instead of a BASELINE.json config")
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
@@ -104,12 +106,25 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # the oracle (CPU) legs
 # ---------------------------------------------------------------------------
-def oracle_rate(cfg_idx: int, target_s: float, batch_cap: int, start: int = 0):
+def workload_of(a) -> dict:
+    """The workload bench.py runs: BASELINE.json config `--config`, or an N4
+    application shape `--workload` (generators.WORKLOADS)."""
+    if getattr(a, "workload", None):
+        w = gen.WORKLOADS[a.workload]
+        b1 = gen.make_workload(a.workload, batch=1)
+        return dict(name=w["name"], n=b1.n, m=b1.m, p=b1.p, batch=w["batch"], key=a.workload,
+                    make=lambda B, start=0: gen.make_workload(a.workload, batch=B, start=start))
+    c = gen.CONFIGS[a.config]
+    return dict(name=c["name"], n=c["n"], m=c["m"], p=c["p"], batch=c["batch"], key=f"cfg{a.config}",
+                make=lambda B, start=0: gen.make_config(a.config, batch=B, start=start))
+
+
+def oracle_rate(W: dict, target_s: float, batch_cap: int, start: int = 0):
     """Time the f64 oracle (K14 + GEPP, the parity reference) on a bounded
     sample of the workload, all host cores.  Returns (QP/s, cores, sample, n_problems)."""
     import oracle
     nt = oracle.hardware_threads()
-    pilot = gen.make_config(cfg_idx, batch=min(nt, batch_cap), start=start)
+    pilot = W["make"](min(nt, batch_cap), start)
     t0 = time.perf_counter()
     r = oracle.solve(pilot, oracle.Cfg.f64(), "f64", nthreads=nt)
     oracle.backward(pilot, r, oracle.Cfg.f64(), "f64", nthreads=nt)
@@ -117,7 +132,7 @@ def oracle_rate(cfg_idx: int, target_s: float, batch_cap: int, start: int = 0):
     rate = pilot.batch / max(dt, 1e-6)
     ns = int(min(batch_cap, max(pilot.batch, round(rate * target_s))))
     ns = max(nt, (ns // nt) * nt) if ns >= nt else ns
-    samp = gen.make_config(cfg_idx, batch=ns, start=start)
+    samp = W["make"](ns, start)
     t0 = time.perf_counter()
     r = oracle.solve(samp, oracle.Cfg.f64(), "f64", nthreads=nt)
     oracle.backward(samp, r, oracle.Cfg.f64(), "f64", nthreads=nt)
@@ -129,12 +144,12 @@ def run_reference(a):
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
         return 0
-    c = gen.CONFIGS[a.config]
+    c = workload_of(a)
     import oracle
     nt = oracle.hardware_threads()
     # calibrate one step to ~4 s of CPU work so K+W steps finish in minutes
-    _, _, ns, _ = oracle_rate(a.config, 4.0, c["batch"])
-    samp = gen.make_config(a.config, batch=ns)
+    _, _, ns, _ = oracle_rate(c, 4.0, c["batch"])
+    samp = c["make"](ns)
     times = []
     for i in range(a.warmup + a.steps):
         t0 = time.perf_counter()
@@ -144,7 +159,7 @@ def run_reference(a):
             times.append(time.perf_counter() - t0)
     tot = sum(times)
     val = ns * a.steps / tot
-    sample = (f"first {ns} problems of {c['name']} per step (seed streams [{a.config}, i]); f64 oracle "
+    sample = (f"first {ns} problems of {c['name']} per step; f64 oracle "
               f"(Eq. 14 + GEPP), init + Alg. 1 + Alg. 2 + Alg. 3, std::thread over problems")
     out = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
            "ms_per_step": 1e3 * tot / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -171,9 +186,9 @@ def main():
     rank, world, local = D.init()
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
-    c = gen.CONFIGS[a.config]
+    c = workload_of(a)
     B, n, m, p = c["batch"], c["n"], c["m"], c["p"]
-    batch = gen.make_config(a.config, batch=B, start=rank * B)  # distinct problems per rank
+    batch = c["make"](B, rank * B)  # distinct problems per rank
     shared = [k for k, v in batch.shared.items() if v]
     S = QPSolver(B, n, m, p, shared=shared, device=local)
     info = S.info()
@@ -235,7 +250,7 @@ def main():
     f_dom, ms_dom = (f_solve, ms_solve) if dom_solve else (f_bwd, ms_bwd)
     achieved = f_dom / (ms_dom / 1e3) / 1e12
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", f"traffic_cfg{a.config}.json")
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{c['key']}.json")
     if os.path.exists(tpath):
         try:
             traffic = json.load(open(tpath)).get("ipm_solve_kernel" if dom_solve else "ipm_backward_kernel")
@@ -295,7 +310,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
-        rate, cores, ns, dt = oracle_rate(a.config, a.cpu_seconds, B)
+        rate, cores, ns, dt = oracle_rate(c, a.cpu_seconds, B)
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"first {ns} problems of {c['name']} ({dt:.1f} s): f64 oracle (Eq. 14 + GEPP), "
                          f"init + Alg. 1 + Alg. 2 + Alg. 3, std::thread over problems"}

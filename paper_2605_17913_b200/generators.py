@@ -203,3 +203,102 @@ def make_config(cfg: int, batch: int | None = None, start: int = 0) -> QPBatch:
     if c["recipe"] == "g_rand_shared":
         return g_rand_shared(cfg, B, c["n"], c["m"], c["p"], start)
     return g_proj(cfg, B, c["n"], c["p"], start)
+
+
+# ---------------------------------------------------------------------------
+# the paper's application shapes as synthetic batches.
+# ---------------------------------------------------------------------------
+def g_cbf_one(rng: np.random.Generator, agents: int, n_obs: int = 3, r_agent: float = 0.35,
+              u_max: float = 2.0, kp: float = 1.5):
+    """One centralised CBF safety-filter QP (App. F):
+    min_u ½‖u − u_nom‖² s.t. the zeroing-CBF rows for every (agent, obstacle)
+    and every agent pair, and the box |u_k| ≤ u_max; u ∈ R^{2·agents},
+    p = 4n + n·obs + n(n−1)/2 rows (n = agents; 70 for 7 agents).
+
+    Synthetic stand-ins for what the paper learns or rolls out: positions are
+    rejection-sampled safe (every barrier h > 0, so u = 0 is strictly
+    feasible), half of them close to an obstacle boundary and some close to an
+    earlier agent (the paper's data concentrate "near regions where safety
+    constraints become active"); u_nom is the goal-seeking PD proposal
+     clipped to the box plus an N(0, 0.5²) "network" correction that
+    may leave it; the learned gains α are U(0.5, 5)."""
+    L = 2.0 + 1.5 * np.sqrt(agents)
+    c = rng.uniform(0.2 * L, 0.8 * L, (n_obs, 2))
+    r = rng.uniform(0.3, 0.8, n_obs)
+    P = np.empty((agents, 2))
+    for i in range(agents):
+        for _ in range(10000):
+            u = rng.random()
+            if u < 0.5:
+                o = rng.integers(n_obs)
+                ang = rng.uniform(0.0, 2.0 * np.pi)
+                dist = r[o] + 0.02 + rng.exponential(0.2)
+                cand = c[o] + dist * np.array([np.cos(ang), np.sin(ang)])
+            elif u < 0.7 and i > 0:
+                j = rng.integers(i)
+                ang = rng.uniform(0.0, 2.0 * np.pi)
+                dist = 2 * r_agent + 0.02 + rng.exponential(0.1)
+                cand = P[j] + dist * np.array([np.cos(ang), np.sin(ang)])
+            else:
+                cand = rng.uniform(0.0, L, 2)
+            ok = np.all(np.linalg.norm(c - cand, axis=1) > r + 0.01)
+            ok = ok and (i == 0 or np.all(np.linalg.norm(P[:i] - cand, axis=1) > 2 * r_agent + 0.01))
+            if ok:
+                break
+        else:  # pragma: no cover
+            raise RuntimeError("could not place a safe agent")
+        P[i] = cand
+    goals = rng.uniform(0.0, L, (agents, 2))
+    dgo = goals - P
+    u_pd = kp * dgo / np.maximum(np.linalg.norm(dgo, axis=1, keepdims=True), 1e-3)
+    u_nom = np.clip(u_pd, -u_max, u_max) + 0.5 * rng.standard_normal((agents, 2))
+    nv = 2 * agents
+    rows, rhs = [], []
+    for i in range(agents):            # obstacle barriers: −∇h·u_i ≤ α h
+        for o in range(n_obs):
+            g = np.zeros(nv)
+            g[2 * i:2 * i + 2] = -2.0 * (P[i] - c[o])
+            rows.append(g)
+            rhs.append(rng.uniform(0.5, 5.0) * (np.sum((P[i] - c[o]) ** 2) - r[o] ** 2))
+    for i in range(agents):            # pair barriers: −∇h·u ≤ α h
+        for j in range(i + 1, agents):
+            g = np.zeros(nv)
+            dij = P[i] - P[j]
+            g[2 * i:2 * i + 2] = -2.0 * dij
+            g[2 * j:2 * j + 2] = 2.0 * dij
+            rows.append(g)
+            rhs.append(rng.uniform(0.5, 5.0) * (np.sum(dij ** 2) - (2 * r_agent) ** 2))
+    for k in range(nv):                # box
+        g = np.zeros(nv); g[k] = 1.0; rows.append(g); rhs.append(u_max)
+        g = np.zeros(nv); g[k] = -1.0; rows.append(g); rhs.append(u_max)
+    G = np.array(rows)
+    h = np.array(rhs)
+    dl = rng.standard_normal(nv)
+    return (np.eye(nv, dtype=F32), (-u_nom.reshape(-1)).astype(F32), np.zeros((0, nv), F32), np.zeros(0, F32),
+            G.astype(F32), h.astype(F32), dl.astype(F32))
+
+
+def g_cbf(agents: int, batch: int, start: int = 0, stream: int = 100) -> QPBatch:
+    """A batch of safety-filter QPs; problem i uses SeedSequence([stream + agents, i])."""
+    nv = 2 * agents
+    p = 4 * agents + 3 * agents + agents * (agents - 1) // 2
+    Qs = np.empty((batch, nv, nv), F32); qs = np.empty((batch, nv), F32)
+    Gs = np.empty((batch, p, nv), F32); hs = np.empty((batch, p), F32)
+    dls = np.empty((batch, nv), F32)
+    for j in range(batch):
+        Q, q, _, _, G, h, dl = g_cbf_one(_rng(stream + agents, start + j), agents)
+        Qs[j], qs[j], Gs[j], hs[j], dls[j] = Q, q, G, h, dl
+    return QPBatch(nv, 0, p, Qs, qs, np.zeros((batch, 0, nv), F32), np.zeros((batch, 0), F32), Gs, hs, dls,
+                   batch, meta={"recipe": "g_cbf", "agents": agents, "start": start})
+
+
+# N4 workloads (not BASELINE.json configs): name -> (builder, default batch)
+WORKLOADS = {
+    "cbf7": dict(name="cbf7_safety_filter_n14_p70_B4096", build=lambda B, s: g_cbf(7, B, s), batch=4096),
+    "cbf9": dict(name="cbf9_safety_filter_n18_p135_B4096", build=lambda B, s: g_cbf(9, B, s), batch=4096),
+}
+
+
+def make_workload(name: str, batch: int | None = None, start: int = 0) -> QPBatch:
+    w = WORKLOADS[name]
+    return w["build"](w["batch"] if batch is None else batch, start)

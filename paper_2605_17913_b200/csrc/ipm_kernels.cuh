@@ -197,23 +197,41 @@ __device__ float assemble(float* K, const Smem& S, const Args& a, const Prob& P,
   //    nonzeros of the rows ≥ n4: C rows d₊_k g_k of the active constraints,
   //    A rows, −d₋ on the w diagonal, −1 on padding rows.
   {
+    // (the tensor-core epilogue writes every stored entry of rows < n4 itself)
     float4* K4 = reinterpret_cast<float4*>(K);
     const int nz4 = L.size() >> 2;
-    for (int i = tid; i < nz4; i += NT) K4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int z0 = !TC ? 0 : (n4 < L.N4 ? L.off(n4) >> 2 : nz4);
+    for (int i = z0 + tid; i < nz4; i += NT) K4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   __syncthreads();
   const int nrow = N - n4;  // C rows then A rows
-  for (int idx = tid; idx < nrow * n; idx += NT) {
-    const int rr = idx / n, j = idx - rr * n;
-    const int r = n4 + rr;
-    float val;
-    if (rr < pa) {
-      const int k = S.act[rr];
-      val = cw[k] * __ldg(P.G + k * n + j);
-    } else {
-      val = __ldg(P.A + (rr - pa) * n + j);
+  {
+    // 4 elements per thread and step, loads issued before the stores
+    constexpr int UB = 4;
+    const int tot = nrow * n;
+    for (int base = 0; base < tot; base += UB * NT) {
+      float val[UB];
+      int dst[UB];
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        const int idx = base + u * NT + tid;
+        dst[u] = -1;
+        val[u] = 0.f;
+        if (idx < tot) {
+          const int rr = idx / n, j = idx - rr * n;
+          if (rr < pa) {
+            const int k = S.act[rr];
+            val[u] = cw[k] * __ldg(P.G + k * n + j);
+          } else {
+            val[u] = __ldg(P.A + (rr - pa) * n + j);
+          }
+          dst[u] = L.off(n4 + rr) + j;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < UB; ++u)
+        if (dst[u] >= 0) K[dst[u]] = val[u];
     }
-    K[L.off(r) + j] = val;
   }
   for (int r = n4 + tid; r < N4; r += NT) K[L.off(r) + r] = r < n4 + pa ? -e[S.act[r - n4]] : (r < N ? 0.f : -1.f);
   float dmax = 0.f;
@@ -224,16 +242,19 @@ __device__ float assemble(float* K, const Smem& S, const Args& a, const Prob& P,
     const tc::TcState ts = tc::tc_state(S.tc);
     for (int i0 = 0; i0 < n4; i0 += tc::TM)
       for (int j0 = 0; j0 <= i0; j0 += tc::TN)
-        tc::syrk_tile<NT>(ts, P.G, om, p, n, i0, j0, [&](int i, int c0, const float* v) {
-          if (i >= n4) return;
-          float* row = K + L.off(i);
-          const float* qrow = P.Q + (size_t)i * n;
+        tc::syrk_tile<NT>(ts, P.G, om, p, n, i0, j0, [&](int row0, int j, const float* t) {
+          float qv[32];  // all 32 Q loads in flight before the first use
 #pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            const int j = c0 + c;
-            if (j <= i) {
-              const float val = (i < n && j < n) ? __ldg(qrow + j) + v[c] : (i == j ? 1.f : 0.f);
-              row[j] = val;
+          for (int r = 0; r < 32; ++r) {
+            const int i = row0 + r;
+            qv[r] = (i < n && j < n && j <= i) ? __ldg(P.Q + (size_t)i * n + j) : 0.f;
+          }
+#pragma unroll
+          for (int r = 0; r < 32; ++r) {
+            const int i = row0 + r;
+            if (i < n4 && j <= i) {
+              const float val = (i < n && j < n) ? qv[r] + t[33 * r] : (i == j ? 1.f : 0.f);
+              K[L.off(i) + j] = val;
               if (i == j && i < n) dmax = fmaxf(dmax, fabsf(val));
             }
           }

@@ -161,43 +161,62 @@ __device__ __forceinline__ void tmem_free(uint32_t taddr) {
 }
 
 // ------------------------------------------------------------------------
-// Accumulate one 128×128 tile  C[i0+r][j0+c] += Σ_k G[k][i0+r] ω_k G[k][j0+c]
-// (r, c < 128, rows/cols ≥ n treated as zero) and hand the result to
-// `epi(row, col0, v[32])` per thread (row = i0 + lane quarter, 32 columns at a
-// time).  NT threads (multiple of 128).  TMEM address and mbarrier parity
-// are kept in shared memory (tmem_alloc).  Ends with a barrier.
+// Accumulate one 128×128 tile  C[i0+r][j0+c] = Σ_k G[k][i0+r] ω_k G[k][j0+c]
+// (r, c < 128, rows/cols ≥ n treated as zero) and hand it to the epilogue
+// `epi(row0, col, t)` in 32×32 blocks: lane l of a warp gets column col =
+// c0 + l of rows row0 .. row0+31, value of row row0 + r at t[33 r] (so the
+// lanes of a warp cover consecutive columns: coalesced global access).
+// NT threads (multiple of 128).  The G values of K-chunk c+1 are loaded into
+// registers while the tensor core works on chunk c.  TMEM address and
+// mbarrier parity are kept in shared memory (tmem_alloc).  Ends with a
+// barrier.
 // ------------------------------------------------------------------------
 template <int NT, typename Epi>
 __device__ void syrk_tile(const TcState& s, const float* __restrict__ G, const float* om, int p, int n, int i0,
                           int j0, Epi epi) {
+  static_assert(NT % 128 == 0, "syrk_tile: NT must be a multiple of 128");
+  constexpr int U = (TK / 4) * TM / NT;  // 16-byte K-chunk rows staged per thread and operand
   const int tid = threadIdx.x;
   const uint32_t tmem = *s.tmem_slot;
   uint32_t phase = *s.phase_slot;  // read before the first barrier below; written after it
   const uint32_t idesc = make_idesc();
-  for (int k0 = 0; k0 < p; k0 += TK) {
-    // ---- stage A = G[k][i0 + ·] and B = ω_k G[k][j0 + ·] (hi/lo split) ----
-    // one thread: one mn, 4 consecutive k → one 16 B K-chunk row (coalesced
-    // global reads across mn, conflict-free float4 smem stores)
-    for (int u = tid; u < (TK / 4) * TM; u += NT) {
-      const int kc = u / TM, mn = u - kc * TM;
+  float ra[U][4], rb[U][4];
+  // one unit: one mn, 4 consecutive k (coalesced global reads across mn)
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int unit = tid + u * NT, kc = unit / TM, mn = unit - kc * TM;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int k = k0 + 4 * kc + t;
+        const bool kok = k < p;
+        const float* g = G + (size_t)(kok ? k : 0) * n;
+        ra[u][t] = (kok && i0 + mn < n) ? __ldg(g + i0 + mn) : 0.f;
+        rb[u][t] = (kok && j0 + mn < n) ? __ldg(g + j0 + mn) : 0.f;  // ω applied in store()
+      }
+    }
+  };
+  auto store = [&](int k0) {  // ω, hi/lo split, conflict-free float4 stores in the K-major layout
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int unit = tid + u * NT, kc = unit / TM, mn = unit - kc * TM;
       float4 ah, al, bh, bl;
       float* pah = &ah.x; float* pal = &al.x; float* pbh = &bh.x; float* pbl = &bl.x;
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         const int k = k0 + 4 * kc + t;
-        float av = 0.f, bv = 0.f;
-        if (k < p) {
-          const float* g = G + (size_t)k * n;
-          if (i0 + mn < n) av = __ldg(g + i0 + mn);
-          if (j0 + mn < n) bv = om[k] * __ldg(g + j0 + mn);
-        }
-        pah[t] = to_tf32(av); pal[t] = to_tf32(av - pah[t]);
+        const float bv = k < p ? om[k] * rb[u][t] : 0.f;
+        pah[t] = to_tf32(ra[u][t]); pal[t] = to_tf32(ra[u][t] - pah[t]);
         pbh[t] = to_tf32(bv); pbl[t] = to_tf32(bv - pbh[t]);
       }
       const int o = op_offset(mn, 4 * kc);
       *reinterpret_cast<float4*>(s.ahi + o) = ah; *reinterpret_cast<float4*>(s.alo + o) = al;
       *reinterpret_cast<float4*>(s.bhi + o) = bh; *reinterpret_cast<float4*>(s.blo + o) = bl;
     }
+  };
+  load(0);
+  for (int k0 = 0; k0 < p; k0 += TK) {
+    store(k0);
     fence_async_smem();
     __syncthreads();
     if (tid == 0) {
@@ -214,21 +233,29 @@ __device__ void syrk_tile(const TcState& s, const float* __restrict__ G, const f
       }
       commit(s.mbar);
     }
+    if (k0 + TK < p) load(k0 + TK);  // overlaps the MMAs of this chunk
     mbar_wait(s.mbar, phase);
     phase ^= 1u;
     tc_fence_after();
   }
   if (tid == 0) *s.phase_slot = phase;
-  // ---- epilogue: TMEM → registers ----
+  // ---- epilogue: TMEM → registers → per-warp transpose in the (now free)
+  //      operand buffers → coalesced row segments.  Warp w reads TMEM lane
+  //      quarter w % 4; with NT = 256 the two warps of a quarter split the
+  //      columns. ----
   const int warp = tid >> 5, lane = tid & 31;
-  if (warp < 4) {
-    const int row = i0 + 32 * warp + lane;
+  constexpr int NH = NT / 128;
+  const int q = warp & 3, half = warp >> 2;
+  float* T = s.ahi + warp * (32 * 33);
 #pragma unroll 1
-    for (int c0 = 0; c0 < TN; c0 += 32) {
-      float v[32];
-      tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)c0, v);
-      epi(row, j0 + c0, v);
-    }
+  for (int c0 = half * (TN / NH); c0 < (half + 1) * (TN / NH); c0 += 32) {
+    float v[32];
+    tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c0, v);
+#pragma unroll
+    for (int c = 0; c < 32; ++c) T[lane * 33 + c] = v[c];
+    __syncwarp();
+    epi(i0 + 32 * q, j0 + c0 + lane, T + lane);
+    __syncwarp();
   }
   tc_fence_before();
   __syncthreads();
@@ -250,11 +277,10 @@ __global__ void __launch_bounds__(NT, 1) debug_syrk_kernel(const float* G, const
   const uint32_t tmem = tmem_alloc(s);
   for (int i0 = 0; i0 < n; i0 += TM)
     for (int j0 = 0; j0 < n; j0 += TN)
-      syrk_tile<NT>(s, G, om, p, n, i0, j0, [&](int row, int c0, const float* v) {
-        if (row >= n) return;
-        for (int c = 0; c < 32; ++c) {
-          const int j = c0 + c;
-          if (j < n) H[(size_t)row * n + j] = Q[(size_t)row * n + j] + v[c];
+      syrk_tile<NT>(s, G, om, p, n, i0, j0, [&](int row0, int col, const float* t) {
+        for (int r = 0; r < 32; ++r) {
+          const int row = row0 + r;
+          if (row < n && col < n) H[(size_t)row * n + col] = Q[(size_t)row * n + col] + t[33 * r];
         }
       });
   tmem_free(tmem);

@@ -479,16 +479,21 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
 //       warp, as in factor_qd).
 // Then the diagonal-block inverses W_b.  scr: ≥ 16·17 + 16 floats of smem.
 // ------------------------------------------------------------------------
+// Columns [c0, c1) of the factorisation (c0 a multiple of 16, c1 a multiple
+// of 16 or N4): the 16-wide blocks of the range are factored together with
+// every row below them, and the trailing update touches only columns < c1
+// (factor_tc's tensor-core left-looking update brings later columns up to
+// date).  Returns the number of floored pivots (thread 0's count).
 template <int NT>
-__device__ int factor_big(float* __restrict__ K, const KLayout& L, const float theta, float* __restrict__ rinv,
-                          int* __restrict__ flag, float* __restrict__ scr) {
+__device__ int factor_big_range(float* __restrict__ K, const KLayout& L, const float theta, float* __restrict__ rinv,
+                                float* __restrict__ scr, const int c0, const int c1) {
   constexpr int NW = NT / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int N4 = L.N4, npos = L.npos;
   float* l11 = scr;            // [16][17]
   float* colb = scr + 16 * 17;  // [16] column broadcast
   int nfloor = 0;
-  for (int b = 0; b < L.NB; ++b) {
+  for (int b = c0 / KB; b < L.NB && KB * b < c1; ++b) {
     const int k0 = KB * b, kb = L.bw(b), k1 = k0 + kb;
     const int Lb = L.len(b);
     // ---- (a) diagonal block ---------------------------------------------------------
@@ -556,16 +561,17 @@ __device__ int factor_big(float* __restrict__ K, const KLayout& L, const float t
       }
     }
     __syncthreads();
-    // ---- (c) trailing update A22 −= L21 S_b L21ᵀ ---------------------------------------
-    {
-      const int T = (N4 - k1 + 31) >> 5;
-      const int nst = T * (T + 1) / 2;
+    // ---- (c) trailing update A22 −= L21 S_b L21ᵀ, columns < c1 ---------------------------
+    if (k1 < c1) {
+      const int T = (N4 - k1 + 31) >> 5;      // 32-row tiles below
+      const int JT = (c1 - k1 + 31) >> 5;     // 32-column tiles inside the range
+      const int ncol = c1 < N4 ? c1 : N4;     // column bound of this update
+      const int nst = JT * T - JT * (JT - 1) / 2;  // tiles (I, J): J < JT, J ≤ I < T
       const int ty = lane >> 3, tx = lane & 7;
       for (int st = warp; st < nst; st += NW) {
-        int I = (int)((sqrtf(8.f * st + 1.f) - 1.f) * 0.5f);
-        while ((I + 1) * (I + 2) / 2 <= st) ++I;
-        while (I * (I + 1) / 2 > st) --I;
-        const int J = st - I * (I + 1) / 2;
+        int J = 0, rem = st;
+        while (rem >= T - J) { rem -= T - J; ++J; }
+        const int I = J + rem;
         const int rb = k1 + 32 * I + ty, cb = k1 + 32 * J + tx;
         int roff[8], coff[4];
         bool rok[8], cok[4];
@@ -578,7 +584,7 @@ __device__ int factor_big(float* __restrict__ K, const KLayout& L, const float t
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const int cc = cb + 8 * c;
-          cok[c] = cc < N4;
+          cok[c] = cc < ncol;
           coff[c] = cok[c] ? L.off(cc) : 0;
         }
         float acc[8][4];
@@ -624,8 +630,15 @@ __device__ int factor_big(float* __restrict__ K, const KLayout& L, const float t
     }
     __syncthreads();
   }
-  for (int b = warp; b < L.NB; b += NW) invert_diag_block(K, L, b, rinv);
-  if (tid == 0) *flag = nfloor;
+  return nfloor;
+}
+
+template <int NT>
+__device__ int factor_big(float* __restrict__ K, const KLayout& L, const float theta, float* __restrict__ rinv,
+                          int* __restrict__ flag, float* __restrict__ scr) {
+  const int nfloor = factor_big_range<NT>(K, L, theta, rinv, scr, 0, L.N4);
+  for (int b = threadIdx.x >> 5; b < L.NB; b += NT / 32) invert_diag_block(K, L, b, rinv);
+  if (threadIdx.x == 0) *flag = nfloor;
   __syncthreads();
   const int r = *flag;
   __syncthreads();

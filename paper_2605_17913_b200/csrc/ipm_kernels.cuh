@@ -18,6 +18,7 @@
 // on), and the size drops from n+p+m to n+|A|+m.
 #pragma once
 #include "ipm_cta.cuh"
+#include "tc_factor.cuh"
 #include "tc_syrk.cuh"
 
 namespace qpb {
@@ -136,7 +137,14 @@ __device__ __forceinline__ int factor_any(float* K, const Smem& S, const KLayout
 #ifdef QPB200_FACTOR_WARP
   return factor_big<NT>(K, L, theta, S.rinv, S.flag, S.scr);
 #else
-  if (BIG && L.N4 > 256) return factor_big<NT>(K, L, theta, S.rinv, S.flag, S.scr);
+  if constexpr (BIG) {
+    // large N: tensor-core left-looking panels (QPB200_NO_TC_FACTOR: FP32 factor_big, for A/B)
+#ifndef QPB200_NO_TC_FACTOR
+    if (L.N4 > 256) return factor_tc<NT>(K, L, theta, S.rinv, S.flag, S.scr, tc::tc_state(S.tc));
+#else
+    if (L.N4 > 256) return factor_big<NT>(K, L, theta, S.rinv, S.flag, S.scr);
+#endif
+  }
   return factor_qd<NT>(K, L, theta, S.rinv, S.flag, S.scr);
 #endif
 }

@@ -328,6 +328,10 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
     return QP_ERR_CUDA;
   }
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->ctas_per_sm, ctx->ks.solve, ctx->ks.threads, L.smem);
+  if (const char* e = getenv("QPB200_TC_W")) {  // experiments: tensor-core factorisation panel width
+    const int w = atoi(e);
+    cudaMemcpyToSymbol(qpb::g_tc_w, &w, sizeof(int));
+  }
   // persistent CTAs (one KKT workspace each), looping over the batch
   {
     int sms = 0;

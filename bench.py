@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=2, help="BASELINE.json config index (1-based)")
+    ap.add_argument("--batch", type=int, default=None,
+                    help="override the per-GPU batch (plumbing tests only; bench lines use the config's batch)")
     ap.add_argument("--workload", default=None, choices=sorted(gen.WORKLOADS),
                     help="an N4 application shape instead of a BASELINE.json config")
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
@@ -184,10 +186,11 @@ def main():
     from paper_2605_17913_b200.solver import QPSolver
 
     rank, world, local = D.init()
+    local = local % max(1, torch.cuda.device_count())  # = LOCAL_RANK on a node with ≥ world GPUs
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     c = workload_of(a)
-    B, n, m, p = c["batch"], c["n"], c["m"], c["p"]
+    B, n, m, p = a.batch or c["batch"], c["n"], c["m"], c["p"]
     batch = c["make"](B, rank * B)  # distinct problems per rank
     shared = [k for k, v in batch.shared.items() if v]
     S = QPSolver(B, n, m, p, shared=shared, device=local)

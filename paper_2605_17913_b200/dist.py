@@ -21,7 +21,9 @@ def env_rank() -> tuple[int, int, int]:
 def init(backend: str | None = None) -> tuple[int, int, int]:
     rank, world, local = env_rank()
     if world > 1 and not dist.is_initialized():
-        be = backend or ("nccl" if torch.cuda.is_available() else "gloo")
+        # QPB200_DIST_BACKEND=gloo: plumbing checks with several ranks on one GPU
+        # (the ranks' kernels never wait on each other; NCCL refuses shared devices)
+        be = backend or os.environ.get("QPB200_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
         if be == "nccl":
             torch.cuda.set_device(local)
         dist.init_process_group(be, init_method="env://")

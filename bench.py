@@ -115,10 +115,11 @@ def workload_of(a) -> dict:
         w = gen.WORKLOADS[a.workload]
         b1 = gen.make_workload(a.workload, batch=1)
         return dict(name=w["name"], n=b1.n, m=b1.m, p=b1.p, batch=w["batch"], key=a.workload,
-                    make=lambda B, start=0: gen.make_workload(a.workload, batch=B, start=start))
+                    make=lambda B, start=0: gen.make_workload(a.workload, batch=B, start=start),
+                    solver=dict(w.get("solver", {})))
     c = gen.CONFIGS[a.config]
     return dict(name=c["name"], n=c["n"], m=c["m"], p=c["p"], batch=c["batch"], key=f"cfg{a.config}",
-                make=lambda B, start=0: gen.make_config(a.config, batch=B, start=start))
+                make=lambda B, start=0: gen.make_config(a.config, batch=B, start=start), solver={})
 
 
 def oracle_rate(W: dict, target_s: float, batch_cap: int, start: int = 0):
@@ -193,7 +194,7 @@ def main():
     B, n, m, p = a.batch or c["batch"], c["n"], c["m"], c["p"]
     batch = c["make"](B, rank * B)  # distinct problems per rank
     shared = [k for k, v in batch.shared.items() if v]
-    S = QPSolver(B, n, m, p, shared=shared, device=local)
+    S = QPSolver(B, n, m, p, shared=shared, device=local, **c["solver"])
     info = S.info()
 
     def T(f):
@@ -271,7 +272,7 @@ def main():
     # ---- e2e: host buffers through the C ABI, H2D/D2H inside the timed region
     e2e = None
     if not a.no_e2e:
-        Sh = QPSolver(B, n, m, p, shared=shared, device=local, mem="host")
+        Sh = QPSolver(B, n, m, p, shared=shared, device=local, mem="host", **c["solver"])
         hdata = [torch.from_numpy(np.ascontiguousarray(getattr(batch, f)[0] if f in shared else getattr(batch, f)))
                  .pin_memory() for f in FIELDS]
         hdl = torch.from_numpy(batch.dl_dx).pin_memory()

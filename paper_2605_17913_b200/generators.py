@@ -302,3 +302,131 @@ WORKLOADS = {
 def make_workload(name: str, batch: int | None = None, start: int = 0) -> QPBatch:
     w = WORKLOADS[name]
     return w["build"](w["batch"] if batch is None else batch, start)
+
+
+def _bernstein_gram(m: int) -> np.ndarray:
+    """G[i][j] = ∫₀¹ b_i^m(u) b_j^m(u) du = C(m,i) C(m,j) / ((2m+1) C(2m,i+j))."""
+    from math import comb
+    return np.array([[comb(m, i) * comb(m, j) / ((2 * m + 1) * comb(2 * m, i + j)) for j in range(m + 1)]
+                     for i in range(m + 1)])
+
+
+def _bezier_diff(n: int, r: int) -> np.ndarray:
+    """M_r: control points of the r-th u-derivative of a degree-n Bézier curve."""
+    M = np.eye(n + 1)
+    for k in range(r):
+        m = n - k
+        D = np.zeros((m, m + 1))
+        for j in range(m):
+            D[j, j], D[j, j + 1] = -m, m
+        M = D @ M
+    return M
+
+
+def g_bezier_one(rng: np.random.Generator, K: int, deg: int = 4, weights=(0.1, 0.1, 1.0, 0.1),
+                 vel=10.0, acc=2.0):
+    """One inner QP of the bilevel trajectory optimisation (App. E,
+    P:1045-1107): K Bézier segments of degree 4 in the plane, x = stacked
+    control points (K·5·2); Q(T) = Σ_r w_r T_k^{1−2r} M_rᵀ Gram M_r per segment
+    and axis (r = 1..4, w = (0.1, 0.1, 1, 0.1), P:1068-1072), q = 0;
+    equalities: start/goal points, C² continuity across segments
+    (M_r P)/T^r matched for r = 0, 1, 2, rest at both ends (r = 1, 2);
+    inequalities: every control point of segment k inside its safe cell
+    (a rotated box, 4 facets) and |M_r P_k / T_k^r| ≤ (10, 2) for r = 1, 2
+    (P:1090-1094).  Synthetic stand-ins for the maps (pydecomp) and the outer
+    L-BFGS iterate: a corridor of K overlapping cells along a random walk
+    toward the goal, durations T_k ~ U(1.5, 3)."""
+    d, npt = 2, deg + 1
+    nv = K * npt * d
+    # corridor of overlapping rotated boxes
+    centers = np.zeros((K, 2))
+    heading = rng.uniform(0.0, 2.0 * np.pi)
+    for k in range(1, K):
+        heading += rng.uniform(-np.pi / 4, np.pi / 4)
+        centers[k] = centers[k - 1] + 1.5 * np.array([np.cos(heading), np.sin(heading)])
+    half = rng.uniform(0.9, 1.3, (K, 2))
+    theta = rng.uniform(0.0, np.pi / 2, K)
+    T = rng.uniform(1.5, 3.0, K)
+    start, goal = centers[0], centers[-1]
+
+    def idx(k, j, a):  # variable index of control point j of segment k, axis a
+        return (k * npt + j) * d + a
+
+    Q = np.zeros((nv, nv))
+    for k in range(K):
+        Qk = np.zeros((npt, npt))
+        for r, w in enumerate(weights, start=1):
+            Mr = _bezier_diff(deg, r)
+            Qk += w * T[k] ** (1 - 2 * r) * Mr.T @ _bernstein_gram(deg - r) @ Mr
+        for a in range(d):
+            ids = [idx(k, j, a) for j in range(npt)]
+            Q[np.ix_(ids, ids)] += Qk
+    rows, rhs = [], []
+
+    def eq(coeffs, val):
+        g = np.zeros(nv)
+        for (k, j, a), c in coeffs:
+            g[idx(k, j, a)] += c
+        rows.append(g); rhs.append(val)
+    for a in range(d):
+        eq([((0, 0, a), 1.0)], start[a])
+        eq([((K - 1, deg, a), 1.0)], goal[a])
+    for r in (0, 1, 2):
+        Mr = _bezier_diff(deg, r)
+        for a in range(d):
+            for k in range(K - 1):      # (M_r P_k)_end / T_k^r = (M_r P_{k+1})_start / T_{k+1}^r
+                co = [((k, j, a), Mr[-1, j] / T[k] ** r) for j in range(npt)]
+                co += [((k + 1, j, a), -Mr[0, j] / T[k + 1] ** r) for j in range(npt)]
+                eq(co, 0.0)
+            if r > 0:                   # rest at both ends
+                eq([((0, j, a), Mr[0, j] / T[0] ** r) for j in range(npt)], 0.0)
+                eq([((K - 1, j, a), Mr[-1, j] / T[K - 1] ** r) for j in range(npt)], 0.0)
+    A = np.array(rows); b = np.array(rhs)
+    rows, rhs = [], []
+    for k in range(K):                  # cell membership of every control point
+        R = np.array([[np.cos(theta[k]), -np.sin(theta[k])], [np.sin(theta[k]), np.cos(theta[k])]])
+        for j in range(npt):
+            for ax in range(2):
+                for sgn in (1.0, -1.0):
+                    nrm = sgn * R[:, ax]
+                    g = np.zeros(nv)
+                    g[idx(k, j, 0)], g[idx(k, j, 1)] = nrm
+                    rows.append(g); rhs.append(nrm @ centers[k] + half[k, ax])
+    for r, bound in ((1, vel), (2, acc)):  # derivative control polygons
+        Mr = _bezier_diff(deg, r)
+        for k in range(K):
+            for i in range(Mr.shape[0]):
+                for a in range(d):
+                    for sgn in (1.0, -1.0):
+                        g = np.zeros(nv)
+                        for j in range(npt):
+                            g[idx(k, j, a)] = sgn * Mr[i, j] / T[k] ** r
+                        rows.append(g); rhs.append(bound)
+    G = np.array(rows); h = np.array(rhs)
+    dl = rng.standard_normal(nv)
+    return (Q.astype(F32), np.zeros(nv, F32), A.astype(F32), b.astype(F32), G.astype(F32), h.astype(F32),
+            dl.astype(F32))
+
+
+def g_bezier(K: int, batch: int, start: int = 0, stream: int = 200) -> QPBatch:
+    """A batch of Bézier trajectory QPs; problem i uses SeedSequence([stream + K, i])."""
+    Q0, _, A0, _, G0, _, _ = g_bezier_one(_rng(stream + K, start), K)
+    nv, m, p = Q0.shape[0], A0.shape[0], G0.shape[0]
+    Qs = np.empty((batch, nv, nv), F32); qs = np.zeros((batch, nv), F32)
+    As = np.empty((batch, m, nv), F32); bs = np.empty((batch, m), F32)
+    Gs = np.empty((batch, p, nv), F32); hs = np.empty((batch, p), F32)
+    dls = np.empty((batch, nv), F32)
+    for j in range(batch):
+        Q, _, A, b, G, h, dl = g_bezier_one(_rng(stream + K, start + j), K)
+        Qs[j], As[j], bs[j], Gs[j], hs[j], dls[j] = Q, A, b, G, h, dl
+    return QPBatch(nv, m, p, Qs, qs, As, bs, Gs, hs, dls, batch,
+                   meta={"recipe": "g_bezier", "segments": K, "start": start})
+
+
+# solver settings of the paper's bilevel sweep: solver_tol = 1e-4 (P:1111)
+WORKLOADS.update({
+    "bezier4": dict(name="bezier4_trajectory_n40_m30_p192_B2048", build=lambda B, s: g_bezier(4, B, s), batch=2048,
+                    solver=dict(tol=1e-4)),
+    "bezier8": dict(name="bezier8_trajectory_n80_m54_p384_B1024", build=lambda B, s: g_bezier(8, B, s), batch=1024,
+                    solver=dict(tol=1e-4)),
+})

@@ -31,3 +31,27 @@ def test_cbf_deterministic_and_sliced():
     a = gen.make_workload("cbf7", batch=6)
     b = gen.make_workload("cbf7", batch=3, start=3)
     assert np.array_equal(a.G[3:], b.G) and np.array_equal(a.q[3:], b.q)
+
+
+@pytest.mark.parametrize("K", [4, 8])
+def test_bezier_shapes_structure_feasibility(K):
+    """App. E inner QP: x = K·5·2 control points; m = 4 + 6(K−1) + 8
+    equalities (endpoints, C² continuity, rest at both ends); p = K(4·5 + 28)
+    inequalities (4-facet cells × 5 points, velocity/acceleration polygons);
+    Q ⪰ 0 with the translations of each segment in its null space; the
+    constraint set is strictly feasible (LP, scipy)."""
+    from scipy.optimize import linprog
+    b = gen.g_bezier(K, 2)
+    assert (b.n, b.m, b.p) == (10 * K, 6 * K + 6, 48 * K)
+    Q = b.Q[0].astype(np.float64)
+    assert np.allclose(Q, Q.T, atol=1e-6 * np.abs(Q).max())
+    assert np.linalg.eigvalsh(Q).min() > -1e-5 * np.abs(Q).max()
+    t = np.zeros(b.n); t[0::2] = 1.0                    # translate every control point along x
+    assert np.abs(Q @ t).max() < 1e-4 * np.abs(Q).max()
+    assert np.linalg.matrix_rank(b.A[0].astype(np.float64)) == b.m
+    # strict feasibility: max margin eps s.t. A x = b, G x + eps ≤ h
+    A, bb, G, h = (v[0].astype(np.float64) for v in (b.A, b.b, b.G, b.h))
+    c = np.zeros(b.n + 1); c[-1] = -1.0
+    res = linprog(c, A_ub=np.hstack([G, np.ones((b.p, 1))]), b_ub=h, A_eq=np.hstack([A, np.zeros((b.m, 1))]),
+                  b_eq=bb, bounds=[(None, None)] * b.n + [(None, 1.0)], method="highs")
+    assert res.status == 0 and -res.fun > 1e-3, res.message

@@ -81,6 +81,15 @@ struct KLayout {
   __host__ __device__ __forceinline__ int bw(int b) const { return b < NB - 1 ? KB : wl; }
 };
 
+// Row offsets: from a shared-memory table (path 1 kernels fill it once per
+// iteration; one LDS instead of the ~8-instruction formula in the hot loops)
+// or from the formula.
+template <bool TAB>
+__device__ __forceinline__ int row_off(const KLayout& L, const int* __restrict__ tab, int i) {
+  if constexpr (TAB) return tab[i];
+  else return L.off(i);
+}
+
 __device__ __forceinline__ float sgn_of(int k, int npos) { return k < npos ? 1.f : -1.f; }
 
 // Diagnostics (QPB200_PHASE_PROFILE): cycles spent by thread 0 in the
@@ -193,9 +202,9 @@ __device__ __forceinline__ void invert_diag_block(float* __restrict__ K, const K
 // A pivot on the wrong side of ±θ is replaced by ±θ (reading Q12) and
 // counted.  On exit K holds L (M = L S Lᵀ) and rinv[k] = 1/L[k][k].
 // ------------------------------------------------------------------------
-template <int NT>
+template <int NT, bool TAB = false>
 __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float theta, float* __restrict__ rinv,
-                         int* __restrict__ flag, float* __restrict__ colT) {
+                         int* __restrict__ flag, float* __restrict__ colT, const int* __restrict__ tab = nullptr) {
   constexpr int NW = NT / 32;
   constexpr int RPT = (256 + NT - 1) / NT;  // rows per thread (N4 ≤ 256)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -223,7 +232,7 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
     for (int u = 0; u < RPT; ++u) {
       const int i = k0 + tid + u * NT;
       has[u] = i < N4;
-      rowp[u] = K + L.off(has[u] ? i : k0) + k0;
+      rowp[u] = K + row_off<TAB>(L, tab, has[u] ? i : k0) + k0;
 #pragma unroll
       for (int j4 = 0; j4 < KB / 4; ++j4) {
         const float4 t = (has[u] && 4 * j4 < kb) ? reinterpret_cast<const float4*>(rowp[u])[j4]
@@ -398,13 +407,13 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
         for (int q = 0; q < 8; ++q) {
           const int r = rb + 4 * q;
           rok[q] = r < N4;
-          roff[q] = rok[q] ? L.off(r) : 0;
+          roff[q] = rok[q] ? row_off<TAB>(L, tab, r) : 0;
         }
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const int cc = cb + 8 * c;
           cok[c] = cc < N4;
-          coff[c] = cok[c] ? L.off(cc) : 0;
+          coff[c] = cok[c] ? row_off<TAB>(L, tab, cc) : 0;
         }
         float acc[8][4];
 #pragma unroll
@@ -652,15 +661,15 @@ __device__ int factor_big(float* __restrict__ K, const KLayout& L, const float t
 //   backward (per block b, last first):  x_b = W_bᵀ r_b;  r_j −= L_bjᵀ x_b above
 // rhs has N4 entries (padding entries must be 0 on entry).
 // ------------------------------------------------------------------------
-template <int NT>
+template <int NT, bool TAB = false>
 __device__ void solve_qd(const float* __restrict__ K, const KLayout& L, const float* __restrict__ rinv,
-                         float* __restrict__ rhs) {
+                         float* __restrict__ rhs, const int* __restrict__ tab = nullptr) {
   const int tid = threadIdx.x;
   const int N4 = L.N4;
   // forward: L u = b
   for (int b = 0; b < L.NB; ++b) {
     const int k0 = KB * b, kb = L.bw(b);
-    const float* D = K + L.off(k0) + k0;
+    const float* D = K + row_off<TAB>(L, tab, k0) + k0;
     const int Lb = L.len(b);
     if (tid < 32) {
       const int t = tid;
@@ -681,7 +690,7 @@ __device__ void solve_qd(const float* __restrict__ K, const KLayout& L, const fl
     if (b + 1 < L.NB) {
       const float4* u = reinterpret_cast<const float4*>(rhs + k0);
       for (int i = k0 + KB + tid; i < N4; i += NT) {
-        const float4* row = reinterpret_cast<const float4*>(K + L.off(i) + k0);
+        const float4* row = reinterpret_cast<const float4*>(K + row_off<TAB>(L, tab, i) + k0);
         float acc = rhs[i];
 #pragma unroll
         for (int j4 = 0; j4 < 4; ++j4) {
@@ -702,7 +711,7 @@ __device__ void solve_qd(const float* __restrict__ K, const KLayout& L, const fl
   // backward: Lᵀ x = u, blocks in reverse order
   for (int b = L.NB - 1; b >= 0; --b) {
     const int k0 = KB * b, kb = L.bw(b);
-    const float* D = K + L.off(k0) + k0;
+    const float* D = K + row_off<TAB>(L, tab, k0) + k0;
     const int Lb = L.len(b);
     if (tid < 32) {
       const int t = tid;
@@ -722,7 +731,7 @@ __device__ void solve_qd(const float* __restrict__ K, const KLayout& L, const fl
     }
     __syncthreads();
     if (b > 0) {
-      const float* Bk = K + L.off(k0);
+      const float* Bk = K + row_off<TAB>(L, tab, k0);
       for (int j = tid; j < k0; j += NT) {
         float acc = rhs[j];
         for (int i = 0; i < kb; ++i) acc = fmaf(-Bk[i * Lb + j], rhs[k0 + i], acc);

@@ -46,6 +46,7 @@ struct Args {
   float* flops;              // per-problem algorithmic flops of this call, nullptr = off
   float* kglob;              // per-CTA KKT workspaces in global memory (iterations with N > ncap)
   int tcf;                   // floats of the tensor-core staging area (large-N kernels; 0 = none)
+  int rof;                   // entries of the row-offset table (path 1: N4max; 0 = none)
 };
 
 // Algorithmic flops of one Newton iteration on the reduced system of size
@@ -71,10 +72,11 @@ struct Smem {
   float *red, *scr, *colscr;
   int *act, *widx, *flag;
   float* tc;  // tcgen05 operand staging + mbarrier (large-N kernels)
+  int* ro;    // row offsets of this iteration's KKT layout (path 1; N4max entries)
   float* end;
 };
 
-__host__ __device__ inline Smem layout(float* base, int n4, int m, int p, int N4max, int ksize, int tcf) {
+__host__ __device__ inline Smem layout(float* base, int n4, int m, int p, int N4max, int ksize, int tcf, int rof) {
   const int m4 = (m + 3) & ~3, p4 = (p + 3) & ~3;
   Smem S;
   float* q = base;
@@ -106,17 +108,18 @@ __host__ __device__ inline Smem layout(float* base, int n4, int m, int p, int N4
   S.widx = reinterpret_cast<int*>(q); q += p4;
   S.flag = reinterpret_cast<int*>(q); q += 16;
   S.tc = q; q += tcf;
+  S.ro = reinterpret_cast<int*>(q); q += (rof + 3) & ~3;
   S.end = q;
   return S;
 }
 
-__host__ inline size_t ipm_smem_bytes(int n4, int m, int p, int N4max, int ksize, int tcf) {
-  const Smem S = layout(nullptr, n4, m, p, N4max, ksize, tcf);
+__host__ inline size_t ipm_smem_bytes(int n4, int m, int p, int N4max, int ksize, int tcf, int rof) {
+  const Smem S = layout(nullptr, n4, m, p, N4max, ksize, tcf, rof);
   return (size_t)reinterpret_cast<uintptr_t>(S.end);
 }
 
 __device__ inline Smem carve(float* base, const Args& a) {
-  return layout(base, a.n4, a.m, a.p, a.N4max, a.ksmem, a.tcf);
+  return layout(base, a.n4, a.m, a.p, a.N4max, a.ksmem, a.tcf, a.rof);
 }
 
 // Where this iteration's KKT matrix lives.  Path 1 kernels (BIG = false)
@@ -145,7 +148,8 @@ __device__ __forceinline__ int factor_any(float* K, const Smem& S, const KLayout
     if (L.N4 > 256) return factor_big<NT>(K, L, theta, S.rinv, S.flag, S.scr);
 #endif
   }
-  return factor_qd<NT>(K, L, theta, S.rinv, S.flag, S.scr);
+  if constexpr (BIG) return factor_qd<NT>(K, L, theta, S.rinv, S.flag, S.scr);
+  else return factor_qd<NT, true>(K, L, theta, S.rinv, S.flag, S.scr, S.ro);
 #endif
 }
 
@@ -204,6 +208,8 @@ __device__ float assemble(float* K, const Smem& S, const Args& a, const Prob& P,
   // 1. zero the whole buffer of this layout (float4 stores), then scatter the
   //    nonzeros of the rows ≥ n4: C rows d₊_k g_k of the active constraints,
   //    A rows, −d₋ on the w diagonal, −1 on padding rows.
+  if constexpr (!TC)  // row-offset table of this layout (path 1), read after the barrier below
+    for (int i = tid; i < L.N4; i += NT) S.ro[i] = L.off(i);
   {
     // (the tensor-core epilogue writes every stored entry of rows < n4 itself)
     float4* K4 = reinterpret_cast<float4*>(K);
@@ -234,7 +240,7 @@ __device__ float assemble(float* K, const Smem& S, const Args& a, const Prob& P,
           } else {
             val[u] = __ldg(P.A + (rr - pa) * n + j);
           }
-          dst[u] = L.off(n4 + rr) + j;
+          dst[u] = row_off<!TC>(L, S.ro, n4 + rr) + j;
         }
       }
 #pragma unroll
@@ -242,7 +248,8 @@ __device__ float assemble(float* K, const Smem& S, const Args& a, const Prob& P,
         if (dst[u] >= 0) K[dst[u]] = val[u];
     }
   }
-  for (int r = n4 + tid; r < N4; r += NT) K[L.off(r) + r] = r < n4 + pa ? -e[S.act[r - n4]] : (r < N ? 0.f : -1.f);
+  for (int r = n4 + tid; r < N4; r += NT)
+    K[row_off<!TC>(L, S.ro, r) + r] = r < n4 + pa ? -e[S.act[r - n4]] : (r < N ? 0.f : -1.f);
   float dmax = 0.f;
   if constexpr (TC) {
     // 2'. large n: H = Q + Gᵀ diag(ω) G on the tensor cores (tc_syrk.cuh,
@@ -327,7 +334,7 @@ __device__ float assemble(float* K, const Smem& S, const Args& a, const Prob& P,
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      float* row = K + L.off(i0 + u) + j0;
+      float* row = K + row_off<!TC>(L, S.ro, i0 + u) + j0;
       if (I != J) {
         *reinterpret_cast<float4*>(row) = make_float4(acc[u][0], acc[u][1], acc[u][2], acc[u][3]);
       } else {
@@ -655,7 +662,8 @@ __device__ __forceinline__ void solve_problem(const Args& a, const Smem& S, cons
     long long t1 = clock64(); tph[1] += t1 - t0; t0 = t1;
     factor_any<NT, BIG>(K, S, L, a.floor_rel * dmax);
     t1 = clock64(); tph[2] += t1 - t0; t0 = t1;
-    solve_qd<NT>(K, L, S.rinv, S.rhs);
+    if constexpr (BIG) solve_qd<NT>(K, L, S.rinv, S.rhs);
+    else solve_qd<NT, true>(K, L, S.rinv, S.rhs, S.ro);
     t1 = clock64(); tph[3] += t1 - t0; t0 = t1;
     if (init) {
       for (int j = tid; j < n; j += NT) S.x[j] = S.rhs[j];
@@ -795,7 +803,8 @@ __device__ __forceinline__ void backward_problem(const Args& a, const Smem& S, c
         for (int j = tid; j < L.N4; j += NT) S.rhs[j] = j < n ? -__ldg(a.dl + (long long)bid * n + j) : 0.f;
         __syncthreads();
       }
-      solve_qd<NT>(K, L, S.rinv, S.rhs);
+      if constexpr (BIG) solve_qd<NT>(K, L, S.rinv, S.rhs);
+      else solve_qd<NT, true>(K, L, S.rinv, S.rhs, S.ro);
       if (done) {
         // dv = G dx + w (w eliminated for v_i ≤ 0 with f2 = 0), dz = d₊ ⊙ dv
         recover_dv<NT>(S, a, P, true);

@@ -39,9 +39,12 @@ struct Layout {
 // floats of the tcgen05 staging area the large-N kernels carry
 int tc_floats(bool big) { return big ? qpb::tc::SMEM_BYTES / 4 : 0; }
 
+// entries of the shared-memory row-offset table (path 1 kernels only)
+int ro_ints(const Layout& L, bool big) { return big ? 0 : L.N4max; }
+
 size_t smem_for(const Layout& L, int m, int p, int ncap, bool big) {
   const int ks = ncap > 0 ? qpb::KLayout::make(ncap, L.n4).size() : 0;
-  return qpb::ipm_smem_bytes(L.n4, m, p, L.N4max, ks, tc_floats(big));
+  return qpb::ipm_smem_bytes(L.n4, m, p, L.N4max, ks, tc_floats(big), ro_ints(L, big));
 }
 
 // Shared-memory budget per CTA (dynamic part) for `ctas` CTAs per SM.
@@ -100,7 +103,7 @@ Layout make_layout(int n, int m, int p, int formulation) {
   }
   if (const char* e = getenv("QPB200_THREADS"); e && !L.big) L.threads = atoi(e);  // experiments: 128|256
   L.ksmem = L.ncap > 0 ? qpb::KLayout::make(L.ncap, L.n4).size() : 0;
-  L.smem = qpb::ipm_smem_bytes(L.n4, m, p, L.N4max, L.ksmem, tc_floats(L.big));
+  L.smem = qpb::ipm_smem_bytes(L.n4, m, p, L.N4max, L.ksmem, tc_floats(L.big), ro_ints(L, L.big));
   return L;
 }
 
@@ -201,6 +204,7 @@ qpb::Args base_args(const qp_ctx* c) {
   a.n4 = c->L.n4; a.Nmax = c->L.Nmax; a.N4max = c->L.N4max;
   a.ksmem = c->L.ksmem; a.ncap = c->L.ncap; a.kglob_size = c->L.kglob;
   a.tcf = tc_floats(c->L.big);
+  a.rof = ro_ints(c->L, c->L.big);
   a.sQ = c->d.bstride_Q; a.sq = c->d.bstride_q; a.sA = c->d.bstride_A;
   a.sb = c->d.bstride_b; a.sG = c->d.bstride_G; a.sh = c->d.bstride_h;
   a.tol = c->c.tol; a.sigma = c->c.sigma; a.tau = c->c.tau; a.kappa_relax = c->c.kappa_relax;

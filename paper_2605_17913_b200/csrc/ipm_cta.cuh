@@ -256,73 +256,6 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
     // rounding the owners of those rows apply to their own entries) instead of
     // waiting for more barriers.  The panel reads columns only from colT, so
     // the l values go to K at once.
-#ifdef QPB200_PANEL_UNROLL
-    // static column indices: no window shifts, the updates shrink with k
-#pragma unroll
-    for (int k = 0; k < KB; k += PC) {
-      if (k >= kb) break;
-      __syncthreads();
-      if (!wact[0]) continue;  // rows of u ≥ 1 lie further down: inactive too
-      float c[PC][KB];  // c[q][j] = a_{k+q+j, k+q}
-#pragma unroll
-      for (int q = 0; q < PC; ++q) {
-        const float4* pq = reinterpret_cast<const float4*>(colT + KB * (k + q));
-#pragma unroll
-        for (int j4 = 0; j4 < KB / 4; ++j4) {
-          const float4 t = pq[j4];
-          c[q][4 * j4] = t.x; c[q][4 * j4 + 1] = t.y; c[q][4 * j4 + 2] = t.z; c[q][4 * j4 + 3] = t.w;
-        }
-      }
-      float dq[PC], rsq[PC], inv[PC], sr[PC];
-      int nf = 0;
-#pragma unroll
-      for (int q = 0; q < PC; ++q) {
-#pragma unroll
-        for (int r = 0; r < q; ++r)
-#pragma unroll
-          for (int j = 0; j + q - r < KB - k; ++j) c[q][j] = fmaf(-c[r][q - r + j] * inv[r], c[r][q - r], c[q][j]);
-        const float sg = sgn_of(k0 + k + q, npos);
-        float d = sg * c[q][0];
-        const bool fl = !(d >= theta);
-        if (fl) d = theta;
-        nf += fl;
-        const float rs = rsqrtf(d);
-        dq[q] = d; rsq[q] = rs; inv[q] = sg * rs * rs; sr[q] = sg * rs;
-      }
-      if (tid == 0) {
-#pragma unroll
-        for (int q = 0; q < PC; ++q) rinv[k0 + k + q] = rsq[q];
-        nfloor += nf;
-      }
-#pragma unroll
-      for (int u = 0; u < RPT; ++u) {
-        if (!wact[u]) continue;
-        const int il = tid + u * NT;  // row index relative to k0
-        if (has[u] && il >= k) {
-          bool live = true;
-#pragma unroll
-          for (int q = 0; q < PC; ++q) {
-            if (live) {
-              if (il == k + q) {
-                rowp[u][k + q] = dq[q] * rsq[q];  // l_kk
-                live = false;
-              } else {
-                const float f = -w[u][k + q] * inv[q];
-                rowp[u][k + q] = w[u][k + q] * sr[q];
-#pragma unroll
-                for (int j = k + q + 1; j < KB; ++j) w[u][j] = fmaf(f, c[q][j - k - q], w[u][j]);
-              }
-            }
-          }
-          if (live && u == 0 && il < kb) {  // publish columns k+PC.. (updated through k+PC−1)
-#pragma unroll
-            for (int t = 0; t < PC; ++t)
-              if (k + PC + t < KB && il >= k + PC + t) colT[KB * (k + PC + t) + il - k - PC - t] = w[u][k + PC + t];
-          }
-        }
-      }
-    }
-#else
     for (int k = 0; k < kb; k += PC) {
       __syncthreads();
       if (!wact[0]) continue;  // rows of u ≥ 1 lie further down: inactive too
@@ -387,7 +320,6 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
         for (int j = 0; j < KB; ++j) w[u][j] = j + PC < KB ? w[u][j + PC] : 0.f;
       }
     }
-#endif
     __syncthreads();
     { const long long t = clock64(); tpan += t - tc0; tc0 = t; }
     // ---- (2) trailing update A22 −= L21 S_b L21ᵀ --------------------------------

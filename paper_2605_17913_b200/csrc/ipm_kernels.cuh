@@ -137,9 +137,6 @@ __device__ __forceinline__ float* kkt_ptr(const Smem& S, const Args& a, const KL
 // systems stream their panel rows (factor_big).
 template <int NT, bool BIG>
 __device__ __forceinline__ int factor_any(float* K, const Smem& S, const KLayout& L, float theta) {
-#ifdef QPB200_FACTOR_WARP
-  return factor_big<NT>(K, L, theta, S.rinv, S.flag, S.scr);
-#else
   if constexpr (BIG) {
     // large N: tensor-core left-looking panels (QPB200_NO_TC_FACTOR: FP32 factor_big, for A/B)
 #ifndef QPB200_NO_TC_FACTOR
@@ -150,7 +147,6 @@ __device__ __forceinline__ int factor_any(float* K, const Smem& S, const KLayout
   }
   if constexpr (BIG) return factor_qd<NT>(K, L, theta, S.rinv, S.flag, S.scr);
   else return factor_qd<NT, true>(K, L, theta, S.rinv, S.flag, S.scr, S.ro);
-#endif
 }
 
 struct Prob {

@@ -119,9 +119,6 @@ KernelSet pick_kernels(const Layout& L, int formulation) {
     return {128, qpb::xpm_solve_kernel<128, 1>, qpb::xpm_backward_kernel<128, 1>};
   }
   if (L.big) return {256, qpb::ipm_solve_kernel<256, 1, true>, qpb::ipm_backward_kernel<256, 1, true>};
-#ifdef QPB200_EXP_256
-  if (L.threads == 256) return {256, qpb::ipm_solve_kernel<256, 3, false>, qpb::ipm_backward_kernel<256, 3, false>};
-#endif
   switch (L.minb) {
     case 5: return {128, qpb::ipm_solve_kernel<128, 5, false>, qpb::ipm_backward_kernel<128, 5, false>};
     case 4: return {128, qpb::ipm_solve_kernel<128, 4, false>, qpb::ipm_backward_kernel<128, 4, false>};

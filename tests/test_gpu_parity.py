@@ -209,3 +209,28 @@ def test_standard_arm_matches_oracle_where_stable():
     assert x_rel(gx["x"][ok], r64["x"][ok]).max() <= 1e-4
     for k in ("x", "z", "s"):
         assert np.all(np.isfinite(gx[k][ok]))
+
+
+def test_nonfinite_and_infeasible_problems_are_isolated():
+    """A problem with a NaN in its data fails with a numerical-failure status
+    and zero-filled gradients; an infeasible problem (x ≤ -1 and
+    x ≥ 1) ends with a non-converged status within max_iter; neither
+    disturbs the other problems of the batch, which must equal a run without
+    them bitwise."""
+    b = gen.make_config(1)
+    bad = gen.make_config(1)
+    bad.q = bad.q.copy()
+    bad.q[3, 0] = np.nan
+    # problem 5: contradictory bounds on x_0 (rows 0 and 1 of G)
+    bad.G = bad.G.copy(); bad.h = bad.h.copy()
+    bad.G[5, 0, :] = 0.0; bad.G[5, 0, 0] = 1.0; bad.h[5, 0] = -1.0
+    bad.G[5, 1, :] = 0.0; bad.G[5, 1, 0] = -1.0; bad.h[5, 1] = -1.0
+    g_ok = run_gpu(b)
+    g = run_gpu(bad, max_iter=60)
+    assert (g["status"][3] & 0xFF) == 3
+    assert (g["status"][5] & 0xFF) in (2, 3)
+    for k in ("dQ", "dq", "dG", "dh"):
+        assert np.all(g[k][3] == 0) and np.all(g[k][5] == 0), k
+    others = [i for i in range(b.batch) if i not in (3, 5)]
+    for k in ("x", "z", "s", "y", "iters", "dQ", "dG"):
+        assert np.array_equal(g[k][others], g_ok[k][others]), k

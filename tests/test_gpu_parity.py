@@ -234,3 +234,54 @@ def test_nonfinite_and_infeasible_problems_are_isolated():
     others = [i for i in range(b.batch) if i not in (3, 5)]
     for k in ("x", "z", "s", "y", "iters", "dQ", "dG"):
         assert np.array_equal(g[k][others], g_ok[k][others]), k
+
+
+def test_cfg3_full_size_sampled():
+    """Full config-3 batch (4096 projection instances, the bench launch
+    configuration of --config 3); 24 sampled problems against the oracle."""
+    b = gen.make_config(3)
+    g = run_gpu(b)
+    assert np.all(g["status"] == 0)
+    idx = np.linspace(0, b.batch - 1, 24).astype(int)
+    sub = b.subset(idx)
+    gs = {k: (v[idx] if isinstance(v, np.ndarray) and v.shape[:1] == (b.batch,) else v) for k, v in g.items()}
+    check_against_oracle(sub, gs)
+
+
+def test_cfg4_full_size_sampled_and_batch_sums():
+    """Full config-4 batch (8192 problems, shared Q, G, h): (1) 8 sampled
+    problems' solutions and per-problem gradients (q) against the oracle;
+    (2) the batch-summed shared gradients equal the sum of the per-problem
+    gradients of the same batch run with every field replicated (stride ≠ 0),
+    i.e. the outer-sum kernels at full batch size."""
+    import oracle as O
+    import torch
+    from paper_2605_17913_b200.solver import QPSolver
+    b = gen.make_config(4)
+    g = run_gpu(b)
+    assert np.all(g["status"] == 0) and np.all(g["grad_status"] == 0)
+    idx = np.linspace(0, b.batch - 1, 8).astype(int)
+    sub = b.subset(idx)
+    r64 = O.solve(sub, O.Cfg.f64(), "f64")
+    assert x_rel(g["x"][idx], r64["x"]).max() <= TOL_X
+    b64 = O.backward(sub, r64, O.Cfg.f64(), "f64")
+    err = rel_err_rows(g["dq"][idx], b64["dq"], 1e-2 * bundle_norm(b64))
+    assert err.max() <= TOL_GRAD, err.max()
+    # replicated run in chunks of 1024 problems: per-problem dQ, dG, dh summed on the device
+    dev = "cuda:0"
+    sums = {k: torch.zeros_like(torch.from_numpy(g[k]), device=dev, dtype=torch.float64) for k in ("dQ", "dG", "dh")}
+    C = 1024
+    for s0 in range(0, b.batch, C):
+        S = QPSolver(C, b.n, b.m, b.p)
+        rep = lambda a: torch.from_numpy(np.ascontiguousarray(a[0])).to(dev).expand(C, *a.shape[1:]).contiguous()
+        data = [rep(b.Q), torch.from_numpy(b.q[s0:s0 + C]).to(dev), rep(b.A), rep(b.b), rep(b.G), rep(b.h)]
+        S.solve(*data)
+        gg = S.backward(torch.from_numpy(b.dl_dx[s0:s0 + C]).to(dev))
+        for k in sums:
+            sums[k] += gg[k].double().sum(0)
+        S.close()
+    torch.cuda.synchronize()
+    for k in sums:
+        ref = sums[k].cpu().numpy()
+        err = np.linalg.norm(g[k] - ref) / np.linalg.norm(ref)
+        assert err <= 1e-5, (k, err)

@@ -105,6 +105,8 @@ typedef struct {
   int32_t launches_solve;  /* kernel launches per qp_solve_batched                         */
   int32_t launches_backward;
   int64_t workspace_bytes;
+  int32_t partition_cap;   /* largest number of constraints kept in augmented form in one */
+                           /* reduced system (reading Q12c); p = no cap                    */
 } qp_info;
 
 /* Fill *cfg with the defaults listed above. */

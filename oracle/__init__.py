@@ -44,7 +44,8 @@ class OracleCfg(C.Structure):
     _fields_ = [("tol", C.c_double), ("max_iter", C.c_int32), ("sigma", C.c_double),
                 ("tau", C.c_double), ("kappa_relax", C.c_double), ("relax_ktol", C.c_double),
                 ("relax_max_iter", C.c_int32), ("kkt_solver", C.c_int32),
-                ("formulation", C.c_int32), ("pivot_floor_rel", C.c_double), ("relax_tol", C.c_double)]
+                ("formulation", C.c_int32), ("pivot_floor_rel", C.c_double), ("relax_tol", C.c_double),
+                ("partition_cap", C.c_int32)]
 
 
 @dataclass
@@ -61,6 +62,7 @@ class Cfg:
     formulation: int = FORM_IMPLICIT
     pivot_floor_rel: float = float(np.sqrt(np.finfo(np.float32).eps))
     relax_tol: float = 1e-6
+    partition_cap: int = -1  # SOLVER_M_PART: reading Q12c (-1 = keep every v_i > 0)
 
     @staticmethod
     def f64(**kw) -> "Cfg":
@@ -76,7 +78,7 @@ class Cfg:
     def c(self) -> OracleCfg:
         return OracleCfg(self.tol, self.max_iter, self.sigma, self.tau, self.kappa_relax,
                          self.relax_ktol, self.relax_max_iter, self.kkt_solver, self.formulation,
-                         self.pivot_floor_rel, self.relax_tol)
+                         self.pivot_floor_rel, self.relax_tol, self.partition_cap)
 
 
 def lib():
@@ -110,7 +112,7 @@ def _declare(L):
         f.argtypes = [C.c_int] * 3 + [P] * 10
         f.restype = C.c_int
         f = getattr(L, f"oracle_newton_step_{suf}")
-        f.argtypes = [C.c_int] * 3 + [P] * 10 + [ft, C.c_int, ft] + [P] * 7
+        f.argtypes = [C.c_int] * 3 + [P] * 10 + [ft, C.c_int, ft, C.c_int] + [P] * 7
         f.restype = C.c_int
         f = getattr(L, f"oracle_residuals_{suf}")
         f.argtypes = [C.c_int] * 3 + [P] * 10 + [P] * 5
@@ -209,7 +211,8 @@ def initialize(prob, n, m, p, prec="f64"):
     return dict(x=x, y=y, z=z, s=s, ok=(rc == 0))
 
 
-def newton_step(prob, n, m, p, x, y, z, s, kappa_target, solver=SOLVER_K14_GEPP, floor_rel=1e-8, prec="f64"):
+def newton_step(prob, n, m, p, x, y, z, s, kappa_target, solver=SOLVER_K14_GEPP, floor_rel=1e-8, prec="f64",
+                partition_cap=-1):
     L = lib()
     dt, suf = _dt(prec)
     data = _one(prob, dt)
@@ -217,7 +220,7 @@ def newton_step(prob, n, m, p, x, y, z, s, kappa_target, solver=SOLVER_K14_GEPP,
     dx, dy, dz, ds, dv = np.zeros(n, dt), np.zeros(m, dt), np.zeros(p, dt), np.zeros(p, dt), np.zeros(p, dt)
     dk = np.zeros(1, dt); ka = np.zeros(1, dt)
     nf = getattr(L, f"oracle_newton_step_{suf}")(n, m, p, *[_ptr(a) for a in data], *[_ptr(a) for a in it],
-                                                dt(kappa_target), solver, dt(floor_rel),
+                                                dt(kappa_target), solver, dt(floor_rel), partition_cap,
                                                 *[_ptr(a) for a in (dx, dy, dz, ds, dv, dk, ka)])
     return dict(dx=dx, dy=dy, dz=dz, ds=ds, dv=dv, dk=float(dk[0]), kappa=float(ka[0]), nfloor=nf)
 

@@ -55,6 +55,7 @@ typedef struct {
   int32_t formulation;    // orc::FORM_*
   double pivot_floor_rel; // LDL pivot floor theta = rel*max|diag| (Q12)
   double relax_tol;       // Alg. 2 residual tolerance (reading Q5b)
+  int32_t partition_cap;  // SOLVER_M_PART: most constraints kept in augmented form (reading Q12c); -1 = no cap
 } oracle_cfg;
 }
 
@@ -274,7 +275,7 @@ template <typename T> struct Factor {
 
 // precompute_kkt_factors (Alg. 1 line 12).
 template <typename T>
-static Factor<T> factor_kkt(const Prob<T>& P, const T* v, T kappa, int solver, T floor_rel) {
+static Factor<T> factor_kkt(const Prob<T>& P, const T* v, T kappa, int solver, T floor_rel, int pcap = -1) {
   const int n = P.n, m = P.m, p = P.p, N = n + p + m;
   Factor<T> F;
   F.kind = solver; F.N = N;
@@ -331,6 +332,18 @@ static Factor<T> factor_kkt(const Prob<T>& P, const T* v, T kappa, int solver, T
     F.act.clear();
     for (int i = 0; i < p; ++i)
       if (v[i] > T(0)) F.act.push_back(i);
+    // Reading Q12c: if more than pcap constraints have v_i > 0,
+    // keep only the pcap with the largest v_i (ties: smaller index first) and
+    // eliminate the others exactly like the v_i <= 0 ones (weight d+/d-).
+    if (pcap >= 0 && (int)F.act.size() > pcap) {
+      std::vector<int> order = F.act;
+      std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return v[a] > v[b]; });
+      order.resize(pcap);
+      std::sort(order.begin(), order.end());
+      F.act = order;
+    }
+    std::vector<char> kept(p, 0);
+    for (int i : F.act) kept[i] = 1;
     const int pa = (int)F.act.size(), Nr = n + pa + m;
     F.N = Nr;
     K.assign((size_t)Nr * Nr, 0);
@@ -339,7 +352,7 @@ static Factor<T> factor_kkt(const Prob<T>& P, const T* v, T kappa, int solver, T
       for (int j = 0; j < n; ++j) {
         T gg = 0;
         for (int k = 0; k < p; ++k) {
-          const T w = v[k] > T(0) ? F.dp[k] : F.dp[k] / F.dm[k];
+          const T w = kept[k] ? F.dp[k] : F.dp[k] / F.dm[k];
           gg += P.G[(size_t)k * n + i] * w * P.G[(size_t)k * n + j];
         }
         ar(i, j) = P.Q[(size_t)i * n + j] + gg;
@@ -508,7 +521,7 @@ static int solve_qp_implicit(const Prob<T>& P, const oracle_cfg& cfg, T* x, T* y
     *iters = k;
     if (converged_solve(R, tol)) return ST_CONVERGED;
     if (k == cfg.max_iter) return ST_MAX_ITER;
-    Factor<T> F = factor_kkt(P, v.data(), kappa, cfg.kkt_solver, fr);
+    Factor<T> F = factor_kkt(P, v.data(), kappa, cfg.kkt_solver, fr, cfg.partition_cap);
     if (!finite_all(F.dp) || !finite_all(F.dm) || !finite_all(F.c)) return ST_NUMERICAL_FAILURE | (STG_SCALING << 8);
     T kt = sigma * kappa;                 // kappa_target <- sigma kappa
     T rk = kappa - kt;                    // r_kappa = kappa - kappa_target
@@ -548,7 +561,7 @@ static int relax_qp_implicit(const Prob<T>& P, const oracle_cfg& cfg, T* x, T* y
     for (int i = 0; i < p; ++i) v[i] = z[i] - s[i];
     T kappa = mean_sz(s, z, p);
     residuals(P, x, y, z, s, kappa, true, R);
-    F = factor_kkt(P, v.data(), kappa, cfg.kkt_solver, fr);
+    F = factor_kkt(P, v.data(), kappa, cfg.kkt_solver, fr, cfg.partition_cap);
     *iters = k;
     if (!finite_all(F.dp) || !finite_all(F.dm) || !F.ok) return ST_NUMERICAL_FAILURE | (STG_RELAX << 8);
     bool kok = p == 0 || std::fabs(kappa / kr - T(1)) <= ktol;
@@ -909,14 +922,14 @@ static void backward_batch(const oracle_cfg& cfg, const BatchData<T>& D, int B, 
   extern "C" int oracle_newton_step_##SUF(int n, int m, int p, const T* Q, const T* q, const T* A,           \
                                           const T* b, const T* G, const T* h, const T* x, const T* y,        \
                                           const T* z, const T* s, T kappa_target, int solver, T floor_rel,   \
-                                          T* dx, T* dy, T* dz, T* ds, T* dv, T* dk, T* kappa_out) {          \
+                                          int pcap, T* dx, T* dy, T* dz, T* ds, T* dv, T* dk, T* kappa_out) {          \
     orc::Prob<T> P{n, m, p, Q, q, A, b, G, h};                                                               \
     std::vector<T> v(p);                                                                                     \
     for (int i = 0; i < p; ++i) v[i] = z[i] - s[i];                                                          \
     T kappa = orc::mean_sz(s, z, p);                                                                         \
     orc::Res<T> R;                                                                                           \
     orc::residuals(P, x, y, z, s, kappa, true, R);                                                           \
-    orc::Factor<T> F = orc::factor_kkt(P, v.data(), kappa, solver, floor_rel);                               \
+    orc::Factor<T> F = orc::factor_kkt(P, v.data(), kappa, solver, floor_rel, pcap);                         \
     T dkk;                                                                                                   \
     orc::newton_direction(P, F, R, kappa - kappa_target, dx, dy, dz, ds, dv, dkk);                           \
     *dk = dkk;                                                                                               \

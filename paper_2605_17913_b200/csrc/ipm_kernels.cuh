@@ -47,6 +47,7 @@ struct Args {
   float* kglob;              // per-CTA KKT workspaces in global memory (iterations with N > ncap)
   int tcf;                   // floats of the tensor-core staging area (large-N kernels; 0 = none)
   int rof;                   // entries of the row-offset table (path 1: N4max; 0 = none)
+  int pcap;                  // largest |A| the KKT buffer holds (reading Q12c; p = no cap)
 };
 
 // Algorithmic flops of one Newton iteration on the reduced system of size
@@ -103,7 +104,15 @@ __host__ __device__ inline Smem layout(float* base, int n4, int m, int p, int N4
   S.ds_x = q; q += n4 + m4;  // standard arm: predictor / centering Δx, Δy
   S.red = q; q += 160;
   S.scr = q; q += 16 * 17 + 16;
-  S.colscr = q; q += 4 * 4 * 64;  // residual column partial sums (≤ 4 groups × 4 sums × 64 columns)
+  // residual column partial sums (≤ 4 groups × 4 sums × 64 columns): used only
+  // inside residuals(), while the KKT buffer holds nothing live (the previous
+  // factor was consumed by its solve; the next assembly follows), so they
+  // alias the buffer when it is large enough
+  if (ksize >= 4 * 4 * 64) {
+    S.colscr = S.K;
+  } else {
+    S.colscr = q; q += 4 * 4 * 64;
+  }
   S.act = reinterpret_cast<int*>(q); q += p4;
   S.widx = reinterpret_cast<int*>(q); q += p4;
   S.flag = reinterpret_cast<int*>(q); q += 16;
@@ -161,17 +170,22 @@ __device__ __forceinline__ Prob prob_of(const Args& a, int bid) {
 }
 
 // ------------------------------------------------------------------------
-// Active-set compaction: act[0..pa) = {k : v_k > 0} in increasing order,
-// widx[k] = position in act or −1.  Returns pa (block-uniform).
+// Active-set compaction: act[0..pa) = the kept constraints in increasing
+// order, widx[k] = position in act or −1.  Returns pa (block-uniform).
+// Kept = {k : v_k > 0} (reading Q12b); when that set is larger than pcap
+// (reading Q12c: the shared-memory KKT buffer of this kernel holds at most
+// n4 + pcap + m rows), only the pcap constraints with the LARGEST v_k are
+// kept (ties: smaller k first) and the others are eliminated like those with
+// v_k ≤ 0, with weight ω_k = d₊/d₋.
 // ------------------------------------------------------------------------
-template <int NT>
-__device__ int compact_active(const Smem& S, int p, bool all_inactive) {
+template <int NT, class Pred>
+__device__ int compact_pass(const Smem& S, int p, Pred on_of) {
   constexpr int NW = NT / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int base = 0;
   for (int c0 = 0; c0 < p; c0 += NT) {
     const int k = c0 + tid;
-    const bool on = !all_inactive && k < p && S.v[k] > 0.f;
+    const bool on = k < p && on_of(k);
     const unsigned bal = __ballot_sync(0xffffffffu, on);
     __syncthreads();
     if (lane == 0) S.flag[warp] = __popc(bal);  // NW ≤ 16 counters
@@ -189,6 +203,21 @@ __device__ int compact_active(const Smem& S, int p, bool all_inactive) {
   }
   __syncthreads();
   return base;
+}
+
+template <int NT>
+__device__ int compact_active(const Smem& S, int p, bool all_inactive, int pcap) {
+  if (all_inactive) return compact_pass<NT>(S, p, [](int) { return false; });
+  const float* v = S.v;
+  const int pa = compact_pass<NT>(S, p, [v](int k) { return v[k] > 0.f; });
+  if (pa <= pcap) return pa;
+  return compact_pass<NT>(S, p, [v, p, pcap](int k) {
+    const float vk = v[k];
+    if (!(vk > 0.f)) return false;
+    int rank = 0;  // constraints ordered before k: larger v, or equal v and smaller index
+    for (int j = 0; j < p; ++j) rank += (v[j] > vk || (v[j] == vk && j < k)) ? 1 : 0;
+    return rank < pcap;
+  });
 }
 
 // ------------------------------------------------------------------------
@@ -408,11 +437,10 @@ __device__ Norms residuals(const Smem& S, const Args& a, const Prob& P, float ka
     const float dp = ret_db(vk, kappa), dm = ret_db(-vk, kappa);
     S.rz[k] = rz; S.rs[k] = rs; S.c[k] = ret_dk(vk, kappa);
     S.dp[k] = dp; S.dm[k] = dm;
-    S.om[k] = vk > 0.f ? dp : dp / dm;
     mz = fmaxf(mz, fabsf(zk)); ms = fmaxf(ms, fabsf(sk)); mh = fmaxf(mh, fabsf(__ldg(P.h + k)));
     mrzs = fmaxf(mrzs, fmaxf(fabsf(rz), fabsf(rs)));
   }
-  const int pa = compact_active<NT>(S, p, false);
+  const int pa = compact_active<NT>(S, p, false, a.pcap);
   // rows: r_i = Gx + s − h, r_e = Ax − b (warp per row); f2, t, rhs_w, rhs_y
   rowdots<NT>(P.G, p, n, S.x, S.gx);
   rowdots<NT>(P.A, m, n, S.x, S.gx + p);
@@ -420,8 +448,11 @@ __device__ Norms residuals(const Smem& S, const Args& a, const Prob& P, float ka
     const float ri = S.gx[k] + S.s[k] - __ldg(P.h + k);
     const float f2 = -(ri - S.rs[k] - S.c[k] * r_kappa);
     S.f2[k] = f2;
-    S.t[k] = fmaf(S.c[k], r_kappa, S.rz[k]) + (S.v[k] > 0.f ? 0.f : S.om[k] * f2);
     const int wi = S.widx[k];
+    // ω_k = d₊ for a kept constraint, d₊/d₋ for an eliminated one (Q12b, Q12c)
+    const float om = wi >= 0 ? S.dp[k] : S.dp[k] / S.dm[k];
+    S.om[k] = om;
+    S.t[k] = fmaf(S.c[k], r_kappa, S.rz[k]) + (wi >= 0 ? 0.f : om * f2);
     if (wi >= 0) S.rhs[n4 + wi] = f2;
   }
   for (int l = tid; l < m; l += NT) S.rhs[n4 + pa + l] = -(S.gx[p + l] - __ldg(P.b + l));
@@ -625,7 +656,7 @@ __device__ __forceinline__ void solve_problem(const Args& a, const Smem& S, cons
       // right-hand side (−q + Gᵀh, b); ẑ = Gx − h.
       for (int i = tid; i < p; i += NT) { S.om[i] = 1.f; S.v[i] = -1.f; }
       __syncthreads();
-      compact_active<NT>(S, p, true);
+      compact_active<NT>(S, p, true, p);
       for (int j = tid; j < n4; j += NT) {
         float acc = 0.f;
         if (j < n) {

@@ -30,6 +30,7 @@ constexpr size_t kMaxSmem = 232448;  // 227 KB opt-in dynamic shared memory per 
 struct Layout {
   int n4, Nmax, N4max;
   int ksmem, ncap;       // shared-memory KKT buffer and the largest reduced system it holds
+  int pcap;              // path 1: largest kept set |A| (reading Q12c; p = no cap)
   long long kglob;       // global workspace floats per CTA (worst case)
   bool big;              // some reduced systems may exceed 256 rows (factor_big compiled in)
   int threads, minb;     // kernel shape
@@ -41,6 +42,12 @@ int tc_floats(bool big) { return big ? qpb::tc::SMEM_BYTES / 4 : 0; }
 
 // entries of the shared-memory row-offset table (path 1 kernels only)
 int ro_ints(const Layout& L, bool big) { return big ? 0 : L.N4max; }
+
+// path 1 at buffer capacity ncap (the vectors sized for ncap as well)
+size_t path1_smem(const Layout& L, int m, int p, int ncap) {
+  const int N4 = (ncap + 3) & ~3;
+  return qpb::ipm_smem_bytes(L.n4, m, p, N4, qpb::KLayout::make(ncap, L.n4).size(), 0, N4);
+}
 
 size_t smem_for(const Layout& L, int m, int p, int ncap, bool big) {
   const int ks = ncap > 0 ? qpb::KLayout::make(ncap, L.n4).size() : 0;
@@ -59,25 +66,37 @@ Layout make_layout(int n, int m, int p, int formulation) {
   L.N4max = (L.Nmax + 3) & ~3;
   L.kglob = qpb::KLayout::make(L.Nmax, L.n4).size();
   L.big = false;
-  // The KKT buffer in smem holds reduced systems up to ncap; iterations with
-  // a larger active set use the CTA's global workspace.  Measured on config
-  // 2/3: more CTAs per SM do NOT pay when they shrink L1 (Q, G are re-read
-  // from L1 every iteration), so take the largest CTA count at which the
-  // buffer still holds the worst-case system; only when even one CTA cannot,
-  // run one CTA per SM with the largest buffer (hybrid).
+  // Path 1 (below) when the worst case has at most 256 rows and a buffer of
+  // the size it needs fits; otherwise the large-N kernels: one CTA per SM
+  // with the largest smem buffer, iterations with a larger reduced system in
+  // the CTA's global workspace (hybrid).
   int env_cap = -1;
   if (const char* e = getenv("QPB200_NCAP")) env_cap = atoi(e);
   int env_ctas = 0;
   if (const char* e = getenv("QPB200_CTAS")) env_ctas = atoi(e);
-  L.threads = 128; L.minb = 1; L.ncap = 0;
-  // path 1: the worst-case system fits the smem buffer and the register-panel
-  // factorisation (N4max ≤ 256) at some CTA count
+  L.threads = 128; L.minb = 1; L.ncap = 0; L.pcap = p;
+  // path 1: the KKT buffer and the register-panel factorisation (N4 ≤ 256).
+  // Take the largest CTA count (≤ 4) whose buffer holds either the worst case
+  // n4 + p + m or, with the kept set capped (reading Q12c), at least
+  // n4 + min(p, n4) + m rows: room for every constraint that can be strongly
+  // active at a solution satisfying LICQ (at most n of them), so the cap only
+  // ever eliminates constraints far from active.  More co-resident problems
+  // per SM is what pays on these latency-bound kernels.
   bool fit = false;
   if (L.N4max <= 256 && env_cap < 0 && !getenv("QPB200_FORCE_GLOBAL")) {
+    const int need = std::min(L.Nmax, L.n4 + std::min(p, L.n4) + m);
     const int want[4] = {4, 3, 2, 1};
     for (int w : want) {
       if (env_ctas && w != env_ctas) continue;
-      if (smem_for(L, m, p, L.Nmax, false) <= budget(w)) { L.ncap = L.Nmax; L.minb = w; fit = true; break; }
+      int ncap = L.Nmax;
+      while (ncap >= need && path1_smem(L, m, p, ncap) > budget(w)) --ncap;
+      if (ncap < need) continue;
+      if (ncap < L.Nmax && getenv("QPB200_NO_PCAP")) continue;  // A/B: worst case only
+      L.ncap = ncap; L.minb = w; fit = true;
+      L.pcap = formulation == QP_EXPLICIT ? p : std::min(p, ncap - L.n4 - m);
+      if (const char* e = getenv("QPB200_PCAP")) L.pcap = std::max(0, std::min(L.pcap, atoi(e)));  // tests
+      L.N4max = (ncap + 3) & ~3;
+      break;
     }
   }
   if (!fit) {
@@ -200,6 +219,7 @@ qpb::Args base_args(const qp_ctx* c) {
   a.B = c->d.batch; a.n = c->d.n; a.m = c->d.m_eq; a.p = c->d.p;
   a.n4 = c->L.n4; a.Nmax = c->L.Nmax; a.N4max = c->L.N4max;
   a.ksmem = c->L.ksmem; a.ncap = c->L.ncap; a.kglob_size = c->L.kglob;
+  a.pcap = c->L.big ? c->d.p : c->L.pcap;
   a.tcf = tc_floats(c->L.big);
   a.rof = ro_ints(c->L, c->L.big);
   a.sQ = c->d.bstride_Q; a.sq = c->d.bstride_q; a.sA = c->d.bstride_A;
@@ -338,7 +358,7 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     ctx->grid = std::min(d->batch, std::max(1, sms * std::max(1, ctx->ctas_per_sm)));
-    const bool need_glob = L.ncap < L.Nmax;
+    const bool need_glob = L.big && L.ncap < L.Nmax;
     if (need_glob && (e = dalloc(ctx, &ctx->kglob, (size_t)ctx->grid * (size_t)L.kglob)) != QP_OK) {
       free_all(ctx); delete ctx; return e;
     }
@@ -395,7 +415,8 @@ qp_err qp_set_stream(qp_ctx* c, void* stream) {
 
 qp_err qp_get_info(const qp_ctx* c, qp_info* info) {
   if (!c || !info) return QP_ERR_INVALID_ARG;
-  info->path = c->L.ncap >= c->L.Nmax ? 1 : (c->L.ncap > 0 ? 3 : 2);  // 1 smem, 2 global, 3 hybrid
+  info->path = !c->L.big ? 1 : (c->L.ncap > 0 ? 3 : 2);  // 1 smem, 2 global, 3 hybrid
+  info->partition_cap = c->L.big ? c->d.p : c->L.pcap;
   info->threads = c->ks.threads;
   info->smem_bytes = (int32_t)c->L.smem;
   info->ctas_per_sm = c->ctas_per_sm;

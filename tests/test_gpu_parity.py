@@ -13,9 +13,9 @@ from .helpers import (GRADS, TOL_GRAD, TOL_RES, TOL_X, bundle_norm, rel_err_rows
 pytestmark = pytest.mark.gpu
 
 
-def check_against_oracle(batch, g, iters_slack=1, grad_tol=TOL_GRAD):
+def check_against_oracle(batch, g, iters_slack=1, grad_tol=TOL_GRAD, cfg32=None):
     r64 = O.solve(batch, O.Cfg.f64(), "f64")
-    r32 = O.solve(batch, O.Cfg.f32(), "f32")
+    r32 = O.solve(batch, cfg32 or O.Cfg.f32(), "f32")
     assert np.all(r64["status"] == 0)
     ok32 = r32["status"] == 0
     # every instance the f32 oracle solves must be solved, without NaN/Inf
@@ -72,6 +72,20 @@ def test_cfg2_full_size_sampled():
     sub = b.subset(idx)
     gs = {k: (v[idx] if isinstance(v, np.ndarray) and v.shape[:1] == (b.batch,) else v) for k, v in g.items()}
     check_against_oracle(sub, gs)
+
+
+@pytest.mark.parametrize("cfg,batch,cap", [(2, 96, 52), (2, 64, 60), (3, 48, 90)])
+def test_partition_cap(monkeypatch, cfg, batch, cap):
+    """Reading Q12c with a cap far below the kernel's own (QPB200_PCAP): the
+    kept set is truncated in most iterations; parity with the f64 oracle
+    holds and the iteration counts follow the f32 oracle run with the same
+    cap (chosen here by the test)."""
+    monkeypatch.setenv("QPB200_PCAP", str(cap))
+    b = gen.make_config(cfg, batch=batch)
+    g = run_gpu(b)
+    assert g["info"]["path"] == 1 and g["info"]["partition_cap"] == cap, g["info"]
+    st = check_against_oracle(b, g, cfg32=O.Cfg.f32(partition_cap=cap))
+    assert st["iters_equal"] >= 0.5
 
 
 @pytest.mark.parametrize("n,m,p", [(1, 0, 1), (3, 1, 5), (7, 2, 0), (5, 0, 0), (13, 3, 17), (33, 5, 40),

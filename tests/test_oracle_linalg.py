@@ -71,6 +71,31 @@ def test_condensation_matches_dense_eq13(orc, seed):
             assert np.allclose(stm[k], st[k], rtol=1e-9, atol=1e-9 * max([1.0, *np.abs(st[k])])), (solver, k)
 
 
+@pytest.mark.parametrize("seed", range(20))
+def test_capped_partition_matches_dense_eq13(orc, seed):
+    """Reading Q12c: keeping only the pcap constraints with the largest v_i > 0
+    in augmented form (the rest eliminated with weight d+/d-) is still an
+    exact block elimination, so the step equals the dense Eq. 13 solve
+     for every cap, including 0 (every w_i eliminated)."""
+    rng = np.random.default_rng(1000 + seed)
+    n, m, p = int(rng.integers(2, 7)), int(rng.integers(0, 3)), int(rng.integers(4, 10))
+    prob = rand_qp(rng, n, m, p)
+    x, y = rng.standard_normal(n), rng.standard_normal(m)
+    z, s = rng.uniform(0.05, 2.0, p), rng.uniform(0.05, 2.0, p)
+    v = z - s
+    kappa = float(s @ z / p)
+    kt = 0.1 * kappa
+    r = orc.residuals(prob, n, m, p, x, y, z, s)
+    ret = orc.retract(v, kappa)
+    K, rhs = dense_eq13(prob, n, m, p, v, kappa, r, kappa - kt, ret["dp"], ret["dm"], ret["c"])
+    ref = np.linalg.solve(K, rhs)
+    for cap in range(0, int((v > 0).sum()) + 1):
+        st = orc.newton_step(prob, n, m, p, x, y, z, s, kt, solver=orc.SOLVER_M_PART, floor_rel=1e-14,
+                             partition_cap=cap)
+        sol = np.concatenate([st["dx"], st["dy"], st["dz"], st["ds"], st["dv"], [st["dk"]]])
+        assert np.allclose(sol, ref, rtol=1e-8, atol=1e-8 * np.abs(ref).max()), cap
+
+
 def test_zero_residual_zero_step(orc):
     """All residuals zero and kappa_target = kappa -> zero step."""
     n, p = 3, 2

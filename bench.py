@@ -257,10 +257,10 @@ def main():
     tpath = os.path.join(ROOT, "profiles", f"traffic_{c['key']}.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get("ipm_solve_kernel" if dom_solve else "ipm_backward_kernel")
+            traffic = json.load(open(tpath)).get("solve" if dom_solve else "backward")
         except Exception:
             traffic = None
-    roofline = {"bound": "alu", "kernel": "ipm_solve_kernel" if dom_solve else "ipm_backward_kernel",
+    roofline = {"bound": "alu", "kernel": "ipm_kernel (solve launch)" if dom_solve else "ipm_kernel (backward launch)",
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "traffic": traffic,
                 "peak_note": "FP32 FMA: SMs x 128 lanes x 2 flop x 1965 MHz (derived, DESIGN.md §6)",

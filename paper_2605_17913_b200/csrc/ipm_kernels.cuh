@@ -48,7 +48,34 @@ struct Args {
   int tcf;                   // floats of the tensor-core staging area (large-N kernels; 0 = none)
   int rof;                   // entries of the row-offset table (path 1: N4max; 0 = none)
   int pcap;                  // largest |A| the KKT buffer holds (reading Q12c; p = no cap)
+  int* sched;                // problem counter of this launch (dynamic assignment; zeroed by the host)
+  int* done;                 // per problem: epoch of the last solve that finished it
+  int epoch;                 // this solve's epoch (backward: the solve it differentiates)
+  int* status_out;           // solve: second copy of the status (the caller's array), nullptr = none
+  unsigned long long* tl;    // diagnostics (QPB200_TIMELINE): per problem {smid, t_start, t_end} (ns)
+  int bwd;                   // 0: solve launch (init + Alg. 1), 1: backward launch (Alg. 2 + Alg. 3)
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+  return r;
+}
+
+// Next problem for this CTA: problems are handed out in increasing order as
+// CTAs free up (one atomic per problem), so a CTA that drew short problems
+// takes more of them.  Block-uniform.
+__device__ __forceinline__ int next_problem(const Args& a, int* slot) {
+  __syncthreads();
+  if (threadIdx.x == 0) *slot = atomicAdd(a.sched, 1);
+  __syncthreads();
+  return *slot;
+}
 
 // Algorithmic flops of one Newton iteration on the reduced system of size
 // Nr = n + |A| + m: assembly p·n(n+1) + |A|·n, factorisation
@@ -630,130 +657,6 @@ __device__ bool newton_update(const Smem& S, const Args& a, const Prob& P, int p
   return true;
 }
 
-// ------------------------------------------------------------------------
-// Kernel: initialisation (Q11) + Algorithm 1.
-// The loop is written so that assemble / factor_qd / solve_qd have ONE call
-// site (iteration −1 is the initialisation): the kernel stays small enough for
-// the instruction cache.
-// ------------------------------------------------------------------------
-template <int NT, bool BIG>
-__device__ __forceinline__ void solve_problem(const Args& a, const Smem& S, const int bid) {
-  const int tid = threadIdx.x;
-  const Prob P = prob_of(a, bid);
-  const int n = a.n, n4 = a.n4, p = a.p, m = a.m;
-  int status = ST_CONVERGED, it = 0;
-  float fl = 0.f;  // algorithmic flops of this problem
-  unsigned long long tph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  long long t0 = clock64();
-  for (int k = -1;; ++k) {
-    const bool init = k < 0;
-    float kappa = 0.f, kt = 0.f;
-    int pa = 0;
-    const float *cw = S.om, *ev = S.om;
-    if (init) {
-      // [[Q, Gᵀ, Aᵀ], [G, −I, 0], [A, 0, 0]] (x, ẑ, y) = (−q, h, b); the congruence
-      // ẑ = Gx + w decouples w = −h: reduced matrix [[Q + GᵀG, Aᵀ], [A, 0]],
-      // right-hand side (−q + Gᵀh, b); ẑ = Gx − h.
-      for (int i = tid; i < p; i += NT) { S.om[i] = 1.f; S.v[i] = -1.f; }
-      __syncthreads();
-      compact_active<NT>(S, p, true, p);
-      for (int j = tid; j < n4; j += NT) {
-        float acc = 0.f;
-        if (j < n) {
-          acc = -__ldg(P.q + j);
-          for (int i = 0; i < p; ++i) acc = fmaf(__ldg(P.G + i * n + j), __ldg(P.h + i), acc);
-        }
-        S.rhs[j] = acc;
-      }
-      for (int l = tid; l < m; l += NT) S.rhs[n4 + l] = __ldg(P.b + l);
-      for (int j = n4 + m + tid; j < r4(n4 + m); j += NT) S.rhs[j] = 0.f;
-    } else {
-      kappa = manifold_coords<NT>(S, a);
-      kt = a.sigma * kappa;  // κ_target = σκ
-      const Norms R = residuals<NT>(S, a, P, kappa, kappa - kt);
-      long long t1 = clock64(); tph[0] += t1 - t0; t0 = t1;
-      it = k;
-      if (R.nonfin > 0.f) { status = ST_FAIL | (STG_SCALING << 8); break; }
-      fl += iter_flops(n, m, p, 0, true, false, false);
-      if (converged_solve(R, a.tol)) { status = ST_CONVERGED; break; }
-      if (k == a.max_iter) { status = ST_MAX_ITER; break; }
-      fl -= iter_flops(n, m, p, 0, true, false, false);  // counted again below with the step
-      pa = R.pa;
-      cw = S.dp; ev = S.dm;
-    }
-    const KLayout L = KLayout::make(n4 + pa + m, n4);
-    float* const K = kkt_ptr<BIG>(S, a, L);
-    tph[5] += pa; tph[6] += L.N; tph[7] = tph[7] > (unsigned long long)L.N ? tph[7] : (unsigned long long)L.N;
-    fl += iter_flops(n, m, p, pa, !init, true, true);
-    const float dmax = assemble<NT, BIG>(K, S, a, P, L, pa, S.om, cw, ev);
-    long long t1 = clock64(); tph[1] += t1 - t0; t0 = t1;
-    factor_any<NT, BIG>(K, S, L, a.floor_rel * dmax);
-    t1 = clock64(); tph[2] += t1 - t0; t0 = t1;
-    if constexpr (BIG) solve_qd<NT>(K, L, S.rinv, S.rhs);
-    else solve_qd<NT, true>(K, L, S.rinv, S.rhs, S.ro);
-    t1 = clock64(); tph[3] += t1 - t0; t0 = t1;
-    if (init) {
-      for (int j = tid; j < n; j += NT) S.x[j] = S.rhs[j];
-      for (int l = tid; l < m; l += NT) S.y[l] = S.rhs[n4 + l];
-      __syncthreads();
-      rowdots<NT>(P.G, p, n, S.x, S.dz);
-      for (int i = tid; i < p; i += NT) S.dz[i] -= __ldg(P.h + i);  // ẑ = Gx − h
-      float ap = -INFINITY, ad = -INFINITY, bad = 0.f;
-      for (int i = tid; i < p; i += NT) {
-        const float zh = S.dz[i];
-        ap = fmaxf(ap, zh); ad = fmaxf(ad, -zh);
-        if (!isfinite(zh)) bad = 1.f;
-      }
-      for (int j = tid; j < n; j += NT) if (!isfinite(S.x[j])) bad = 1.f;
-      float v[3] = {ap, ad, bad};
-      block_reduce<NT, 0, 3>(v, S.red);
-      ap = v[0]; ad = v[1];
-      for (int i = tid; i < p; i += NT) {  // s~ = −ẑ, z~ = ẑ, shifted into the interior (S:149)
-        const float zh = S.dz[i];
-        S.s[i] = ap >= 0.f ? -zh + (1.f + ap) : -zh;
-        S.z[i] = ad >= 0.f ? zh + (1.f + ad) : zh;
-      }
-      __syncthreads();
-      if (v[2] > 0.f) { status = ST_FAIL | (STG_INIT << 8); break; }
-    } else {
-      int stage = 0;
-      if (!newton_update<NT>(S, a, P, pa, kappa, kappa - kt, &stage)) { status = ST_FAIL | (stage << 8); break; }
-    }
-    t1 = clock64(); tph[4] += t1 - t0; t0 = t1;
-  }
-  if (a.prof && tid == 0) {
-    for (int i = 0; i < 8; ++i) a.prof[bid * 8 + i] = tph[i];
-  }
-  // ---- outputs
-  for (int j = tid; j < n; j += NT) a.x[(long long)bid * n + j] = S.x[j];
-  for (int l = tid; l < m; l += NT) a.y[(long long)bid * m + l] = S.y[l];
-  for (int i = tid; i < p; i += NT) {
-    a.z[(long long)bid * p + i] = S.z[i];
-    a.s[(long long)bid * p + i] = S.s[i];
-  }
-  if (tid == 0) {
-    a.iters[bid] = it;
-    a.status[bid] = status;
-    if (a.flops) a.flops[bid] = fl;
-  }
-  __syncthreads();
-}
-
-template <int NT, int MINB, bool BIG>
-__global__ void __launch_bounds__(NT, MINB) ipm_solve_kernel(const Args a) {
-  extern __shared__ __align__(16) float smem[];
-  const Smem S = carve(smem, a);
-  if constexpr (BIG) tc::tmem_alloc(tc::tc_state(S.tc));
-  for (int bid = blockIdx.x; bid < a.B; bid += gridDim.x) solve_problem<NT, BIG>(a, S, bid);
-  if constexpr (BIG) tc::tmem_free(*tc::tc_state(S.tc).tmem_slot);
-}
-
-// ------------------------------------------------------------------------
-// Kernel: Algorithm 2 (relax, exact Newton, factor-then-check: Q5, Q5b, Q6)
-// and Algorithm 3 (sign reading Q7, dz = d₊⊙dv: Q8).  One call
-// site each for assemble / factor_qd / solve_qd (the last solve is the
-// adjoint solve with the relaxed factorisation).
-// ------------------------------------------------------------------------
 // Alg. 3 parameter gradients from (x, y, z) and (dx, dy, dz) in
 // shared memory; coalesced stores; per-problem vectors for shared-field sums.
 template <int NT>
@@ -792,91 +695,218 @@ __device__ void write_gradients(const Smem& S, const Args& a, const int bid) {
   }
 }
 
+// ------------------------------------------------------------------------
+// One problem, either direction, in ONE Newton loop (so that the solve and
+// the backward launches run the same code: they share the instruction cache
+// when the backward grid overlaps the end of the solve grid).
+//   solve (bwd = false): CVXOPT initialisation (Q11; iteration −1) +
+//     Algorithm 1: κ_target = σκ, stop on the relative test (Q4).
+//   backward (bwd = true): Algorithm 2 (Q5, Q5b, Q6) from the
+//     solution: κ_target = κ_relax, Newton steps until the relax test holds;
+//     at that point the KKT matrix is assembled and factored once more at the
+//     relaxed point and Algorithm 3 (Q7, Q8) solves it with the
+//     right-hand side (−∇ₓℓ, 0, 0) — the factorisation Alg. 3 reuses sits
+//     at the relaxed point, as in factor-then-check (Q6).
+// assemble / factor / solve_qd have ONE call site.
+// ------------------------------------------------------------------------
 template <int NT, bool BIG>
-__device__ __forceinline__ void backward_problem(const Args& a, const Smem& S, const int bid) {
+__device__ __forceinline__ void ipm_problem(const Args& a, const Smem& S, const int bid, const bool bwd) {
   const int tid = threadIdx.x;
   const Prob P = prob_of(a, bid);
   const int n = a.n, n4 = a.n4, p = a.p, m = a.m;
-  for (int j = tid; j < n; j += NT) S.x[j] = a.x[(long long)bid * n + j];
-  for (int l = tid; l < m; l += NT) S.y[l] = a.y[(long long)bid * m + l];
-  for (int i = tid; i < p; i += NT) {
-    S.z[i] = a.z[(long long)bid * p + i];
-    S.s[i] = a.s[(long long)bid * p + i];
+  int status = ST_CONVERGED, it = 0;
+  bool ok = false;  // backward: gradients computed
+  float fl = 0.f;   // algorithmic flops of this problem
+  float phi_prev = INFINITY;
+  unsigned long long tph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long t0 = clock64();
+  if (bwd) {
+    // the solve's outputs (written by other SMs in this or the previous
+    // kernel): read past L1
+    for (int j = tid; j < n; j += NT) S.x[j] = __ldcg(a.x + (long long)bid * n + j);
+    for (int l = tid; l < m; l += NT) S.y[l] = __ldcg(a.y + (long long)bid * m + l);
+    for (int i = tid; i < p; i += NT) {
+      S.z[i] = __ldcg(a.z + (long long)bid * p + i);
+      S.s[i] = __ldcg(a.s + (long long)bid * p + i);
+    }
+    __syncthreads();
+    if ((__ldcg(a.status + bid) & 0xff) != ST_CONVERGED) status = ST_FAIL | (STG_RELAX << 8);
   }
-  __syncthreads();
-  int status = (a.status[bid] & 0xff) == ST_CONVERGED ? ST_CONVERGED : (ST_FAIL | (STG_RELAX << 8));
-  int it = 0;
-  bool ok = false;
-  float fl = 0.f;
-  if (status == ST_CONVERGED) {
-    float phi_prev = INFINITY;
-    for (int k = 0;; ++k) {
-      float kappa = manifold_coords<NT>(S, a);
-      const Norms R = residuals<NT>(S, a, P, kappa, kappa - a.kappa_relax);
-      const int pa = R.pa;
-      const KLayout L = KLayout::make(n4 + pa + m, n4);
-      float* const K = kkt_ptr<BIG>(S, a, L);
-      const float dmax = assemble<NT, BIG>(K, S, a, P, L, pa, S.om, S.dp, S.dm);
-      factor_any<NT, BIG>(K, S, L, a.floor_rel * dmax);
-      fl += iter_flops(n, m, p, pa, true, true, true);  // the adjoint solve replaces the last step's
+  for (int k = bwd ? 0 : -1; status == ST_CONVERGED; ++k) {
+    const bool init = k < 0;
+    float kappa = 0.f, kt = 0.f;
+    int pa = 0;
+    bool adj = false;  // backward: relaxed — this iteration's solve is Alg. 3's
+    const float *cw = S.om, *ev = S.om;
+    if (init) {
+      // [[Q, Gᵀ, Aᵀ], [G, −I, 0], [A, 0, 0]] (x, ẑ, y) = (−q, h, b); the congruence
+      // ẑ = Gx + w decouples w = −h: reduced matrix [[Q + GᵀG, Aᵀ], [A, 0]],
+      // right-hand side (−q + Gᵀh, b); ẑ = Gx − h.
+      for (int i = tid; i < p; i += NT) { S.om[i] = 1.f; S.v[i] = -1.f; }
+      __syncthreads();
+      compact_active<NT>(S, p, true, p);
+      for (int j = tid; j < n4; j += NT) {
+        float acc = 0.f;
+        if (j < n) {
+          acc = -__ldg(P.q + j);
+          for (int i = 0; i < p; ++i) acc = fmaf(__ldg(P.G + i * n + j), __ldg(P.h + i), acc);
+        }
+        S.rhs[j] = acc;
+      }
+      for (int l = tid; l < m; l += NT) S.rhs[n4 + l] = __ldg(P.b + l);
+      for (int j = n4 + m + tid; j < r4(n4 + m); j += NT) S.rhs[j] = 0.f;
+    } else {
+      kappa = manifold_coords<NT>(S, a);
+      kt = bwd ? a.kappa_relax : a.sigma * kappa;  // κ_target: κ_relax (Alg. 2) or σκ (Alg. 1)
+      const Norms R = residuals<NT>(S, a, P, kappa, kappa - kt);
+      long long t1 = clock64(); tph[0] += t1 - t0; t0 = t1;
       it = k;
-      if (R.nonfin > 0.f) { status = ST_FAIL | (STG_RELAX << 8); break; }
-      const bool kok = p == 0 || fabsf(kappa / a.kappa_relax - 1.f) <= a.relax_ktol;
-      const bool done = kok && relax_done(R, a.tol, a.relax_tol, phi_prev);
-      phi_prev = kok ? rel_phi(R) : INFINITY;
-      if (!done && k == a.relax_max_iter) { status = ST_MAX_ITER | (STG_RELAX << 8); break; }
-      if (done) {
-        // Algorithm 3: reduced system with right-hand side (−∇ₓℓ, 0, 0)
-        for (int j = tid; j < L.N4; j += NT) S.rhs[j] = j < n ? -__ldg(a.dl + (long long)bid * n + j) : 0.f;
-        __syncthreads();
+      if (R.nonfin > 0.f) { status = ST_FAIL | ((bwd ? STG_RELAX : STG_SCALING) << 8); break; }
+      if (!bwd) {
+        fl += iter_flops(n, m, p, 0, true, false, false);
+        if (converged_solve(R, a.tol)) break;
+        if (k == a.max_iter) { status = ST_MAX_ITER; break; }
+        fl -= iter_flops(n, m, p, 0, true, false, false);  // counted again below with the step
+      } else {
+        const bool kok = p == 0 || fabsf(kappa / a.kappa_relax - 1.f) <= a.relax_ktol;
+        adj = kok && relax_done(R, a.tol, a.relax_tol, phi_prev);
+        phi_prev = kok ? rel_phi(R) : INFINITY;
+        if (!adj && k == a.relax_max_iter) { status = ST_MAX_ITER | (STG_RELAX << 8); break; }
       }
-      if constexpr (BIG) solve_qd<NT>(K, L, S.rinv, S.rhs);
-      else solve_qd<NT, true>(K, L, S.rinv, S.rhs, S.ro);
-      if (done) {
-        // dv = G dx + w (w eliminated for v_i ≤ 0 with f2 = 0), dz = d₊ ⊙ dv
-        recover_dv<NT>(S, a, P, true);
-        for (int i = tid; i < p; i += NT) S.dz[i] = S.dp[i] * S.gx[i];
-        for (int j = tid; j < n; j += NT) S.dx[j] = S.rhs[j];
-        for (int l = tid; l < m; l += NT) S.dy[l] = S.rhs[n4 + pa + l];
-        __syncthreads();
-        float bad = 0.f;
-        for (int j = tid; j < n; j += NT) if (!isfinite(S.dx[j])) bad = 1.f;
-        for (int i = tid; i < p; i += NT) if (!isfinite(S.dz[i])) bad = 1.f;
-        for (int l = tid; l < m; l += NT) if (!isfinite(S.dy[l])) bad = 1.f;
-        float v[1] = {bad};
-        block_reduce<NT, 0, 1>(v, S.red);
-        ok = !(v[0] > 0.f);
-        if (!ok) status = ST_FAIL | (STG_BACKWARD << 8);
-        break;
+      pa = R.pa;
+      cw = S.dp; ev = S.dm;
+    }
+    const KLayout L = KLayout::make(n4 + pa + m, n4);
+    float* const K = kkt_ptr<BIG>(S, a, L);
+    tph[5] += pa; tph[6] += L.N; tph[7] = tph[7] > (unsigned long long)L.N ? tph[7] : (unsigned long long)L.N;
+    fl += iter_flops(n, m, p, pa, !init, true, true);
+    const float dmax = assemble<NT, BIG>(K, S, a, P, L, pa, S.om, cw, ev);
+    long long t1 = clock64(); tph[1] += t1 - t0; t0 = t1;
+    factor_any<NT, BIG>(K, S, L, a.floor_rel * dmax);
+    t1 = clock64(); tph[2] += t1 - t0; t0 = t1;
+    if (adj) {
+      // Algorithm 3: reduced system with right-hand side (−∇ₓℓ, 0, 0)
+      for (int j = tid; j < L.N4; j += NT) S.rhs[j] = j < n ? -__ldg(a.dl + (long long)bid * n + j) : 0.f;
+      __syncthreads();
+    }
+    if constexpr (BIG) solve_qd<NT>(K, L, S.rinv, S.rhs);
+    else solve_qd<NT, true>(K, L, S.rinv, S.rhs, S.ro);
+    t1 = clock64(); tph[3] += t1 - t0; t0 = t1;
+    if (init) {
+      for (int j = tid; j < n; j += NT) S.x[j] = S.rhs[j];
+      for (int l = tid; l < m; l += NT) S.y[l] = S.rhs[n4 + l];
+      __syncthreads();
+      rowdots<NT>(P.G, p, n, S.x, S.dz);
+      for (int i = tid; i < p; i += NT) S.dz[i] -= __ldg(P.h + i);  // ẑ = Gx − h
+      float ap = -INFINITY, ad = -INFINITY, bad = 0.f;
+      for (int i = tid; i < p; i += NT) {
+        const float zh = S.dz[i];
+        ap = fmaxf(ap, zh); ad = fmaxf(ad, -zh);
+        if (!isfinite(zh)) bad = 1.f;
       }
+      for (int j = tid; j < n; j += NT) if (!isfinite(S.x[j])) bad = 1.f;
+      float v[3] = {ap, ad, bad};
+      block_reduce<NT, 0, 3>(v, S.red);
+      ap = v[0]; ad = v[1];
+      for (int i = tid; i < p; i += NT) {  // s~ = −ẑ, z~ = ẑ, shifted into the interior (S:149)
+        const float zh = S.dz[i];
+        S.s[i] = ap >= 0.f ? -zh + (1.f + ap) : -zh;
+        S.z[i] = ad >= 0.f ? zh + (1.f + ad) : zh;
+      }
+      __syncthreads();
+      if (v[2] > 0.f) { status = ST_FAIL | (STG_INIT << 8); break; }
+    } else if (adj) {
+      // dv = G dx + w (w eliminated for v_i ≤ 0 with f2 = 0), dz = d₊ ⊙ dv
+      recover_dv<NT>(S, a, P, true);
+      for (int i = tid; i < p; i += NT) S.dz[i] = S.dp[i] * S.gx[i];
+      for (int j = tid; j < n; j += NT) S.dx[j] = S.rhs[j];
+      for (int l = tid; l < m; l += NT) S.dy[l] = S.rhs[n4 + pa + l];
+      __syncthreads();
+      float bad = 0.f;
+      for (int j = tid; j < n; j += NT) if (!isfinite(S.dx[j])) bad = 1.f;
+      for (int i = tid; i < p; i += NT) if (!isfinite(S.dz[i])) bad = 1.f;
+      for (int l = tid; l < m; l += NT) if (!isfinite(S.dy[l])) bad = 1.f;
+      float v[1] = {bad};
+      block_reduce<NT, 0, 1>(v, S.red);
+      ok = !(v[0] > 0.f);
+      if (!ok) status = ST_FAIL | (STG_BACKWARD << 8);
+      break;
+    } else {
       int stage = 0;
-      if (!newton_update<NT>(S, a, P, pa, kappa, kappa - a.kappa_relax, &stage)) {
-        status = ST_FAIL | (STG_RELAX << 8);
+      if (!newton_update<NT>(S, a, P, pa, kappa, kappa - kt, &stage)) {
+        status = ST_FAIL | ((bwd ? STG_RELAX : stage) << 8);
         break;
       }
     }
+    t1 = clock64(); tph[4] += t1 - t0; t0 = t1;
   }
-  if (!ok) {  // zero-filled gradients for failed problems
-    for (int j = tid; j < n; j += NT) { S.dx[j] = 0.f; S.x[j] = 0.f; }
-    for (int l = tid; l < m; l += NT) { S.dy[l] = 0.f; S.y[l] = 0.f; }
-    for (int i = tid; i < p; i += NT) { S.dz[i] = 0.f; S.z[i] = 0.f; }
-    __syncthreads();
-  }
-  write_gradients<NT>(S, a, bid);
-  if (tid == 0) {
-    if (a.riters) a.riters[bid] = it;
-    if (a.rstatus) a.rstatus[bid] = status;
-    if (a.flops) a.flops[bid] = fl + 2.f * (n * n + m * n + p * n);  // + gradient outer products
+  if (!bwd) {
+    if (a.prof && tid == 0)
+      for (int i = 0; i < 8; ++i) a.prof[bid * 8 + i] = tph[i];
+    for (int j = tid; j < n; j += NT) a.x[(long long)bid * n + j] = S.x[j];
+    for (int l = tid; l < m; l += NT) a.y[(long long)bid * m + l] = S.y[l];
+    for (int i = tid; i < p; i += NT) {
+      a.z[(long long)bid * p + i] = S.z[i];
+      a.s[(long long)bid * p + i] = S.s[i];
+    }
+    if (tid == 0) {
+      a.iters[bid] = it;
+      a.status[bid] = status;
+      if (a.status_out) a.status_out[bid] = status;
+      if (a.flops) a.flops[bid] = fl;
+    }
+  } else {
+    if (!ok) {  // zero-filled gradients for failed problems
+      for (int j = tid; j < n; j += NT) { S.dx[j] = 0.f; S.x[j] = 0.f; }
+      for (int l = tid; l < m; l += NT) { S.dy[l] = 0.f; S.y[l] = 0.f; }
+      for (int i = tid; i < p; i += NT) { S.dz[i] = 0.f; S.z[i] = 0.f; }
+      __syncthreads();
+    }
+    write_gradients<NT>(S, a, bid);
+    if (tid == 0) {
+      if (a.riters) a.riters[bid] = it;
+      if (a.rstatus) a.rstatus[bid] = status;
+      if (a.flops) a.flops[bid] = fl + 2.f * (n * n + m * n + p * n);  // + gradient outer products
+    }
   }
   __syncthreads();
 }
 
+// ------------------------------------------------------------------------
+// The kernel: persistent CTAs, problems handed out by next_problem.
+// a.bwd = 0: solve launch (qp_solve_batched); each finished problem is
+//   published in done[b] = epoch (release).
+// a.bwd = 1: backward launch (qp_backward_batched), possibly started while
+//   the solve grid drains (programmatic stream serialisation): each problem
+//   first waits for done[b] == epoch.
+// ------------------------------------------------------------------------
 template <int NT, int MINB, bool BIG>
-__global__ void __launch_bounds__(NT, MINB) ipm_backward_kernel(const Args a) {
+__global__ void __launch_bounds__(NT, MINB) ipm_kernel(const Args a) {
   extern __shared__ __align__(16) float smem[];
   const Smem S = carve(smem, a);
+  const bool bwd = a.bwd != 0;
+  // lets the next launch on the stream (the backward) start on SMs this grid leaves idle
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if constexpr (BIG) tc::tmem_alloc(tc::tc_state(S.tc));
-  for (int bid = blockIdx.x; bid < a.B; bid += gridDim.x) backward_problem<NT, BIG>(a, S, bid);
+  for (int bid = next_problem(a, S.flag + 12); bid < a.B; bid = next_problem(a, S.flag + 12)) {
+    if (bwd && a.done && threadIdx.x == 0) {
+      // relaxed polling (an acquire per poll would invalidate this SM's L1),
+      // one acquire fence once the flag is seen
+      int e;
+      for (;;) {
+        asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(e) : "l"(a.done + bid) : "memory");
+        if (e == a.epoch) break;
+        __nanosleep(256);
+      }
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    }
+    if (bwd) __syncthreads();
+    if (a.tl && threadIdx.x == 0) { a.tl[3 * bid] = smid(); a.tl[3 * bid + 1] = gtimer(); }
+    ipm_problem<NT, BIG>(a, S, bid, bwd);  // ends with a barrier after the output stores
+    if (a.tl && threadIdx.x == 0) a.tl[3 * bid + 2] = gtimer();
+    if (!bwd && a.done && threadIdx.x == 0)  // release (cumulative through the barrier): outputs before the flag
+      asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(a.done + bid), "r"(a.epoch) : "memory");
+  }
   if constexpr (BIG) tc::tmem_free(*tc::tc_state(S.tc).tmem_slot);
 }
 

@@ -137,12 +137,12 @@ KernelSet pick_kernels(const Layout& L, int formulation) {
     if (L.big) return {0, nullptr, nullptr};
     return {128, qpb::xpm_solve_kernel<128, 1>, qpb::xpm_backward_kernel<128, 1>};
   }
-  if (L.big) return {256, qpb::ipm_solve_kernel<256, 1, true>, qpb::ipm_backward_kernel<256, 1, true>};
+  if (L.big) return {256, qpb::ipm_kernel<256, 1, true>, qpb::ipm_kernel<256, 1, true>};
   switch (L.minb) {
-    case 5: return {128, qpb::ipm_solve_kernel<128, 5, false>, qpb::ipm_backward_kernel<128, 5, false>};
-    case 4: return {128, qpb::ipm_solve_kernel<128, 4, false>, qpb::ipm_backward_kernel<128, 4, false>};
-    case 3: return {128, qpb::ipm_solve_kernel<128, 3, false>, qpb::ipm_backward_kernel<128, 3, false>};
-    default: return {128, qpb::ipm_solve_kernel<128, 1, false>, qpb::ipm_backward_kernel<128, 1, false>};
+    case 5: return {128, qpb::ipm_kernel<128, 5, false>, qpb::ipm_kernel<128, 5, false>};
+    case 4: return {128, qpb::ipm_kernel<128, 4, false>, qpb::ipm_kernel<128, 4, false>};
+    case 3: return {128, qpb::ipm_kernel<128, 3, false>, qpb::ipm_kernel<128, 3, false>};
+    default: return {128, qpb::ipm_kernel<128, 1, false>, qpb::ipm_kernel<128, 1, false>};
   }
 }
 
@@ -175,6 +175,15 @@ struct qp_ctx {
   int grid = 0;               // CTAs per launch (persistent over problems on path 2)
   float* kglob = nullptr;     // path 2 workspaces
   unsigned long long* prof = nullptr;  // QPB200_PHASE_PROFILE diagnostics
+  // dynamic problem assignment and solve -> backward hand-off (path 1 and
+  // large-N kernels): sched[0..15] solve launch counters, sched[16..31]
+  // backward launch counters (one per pipeline chunk), zeroed by each solve;
+  // done[b] = epoch of the last solve that finished problem b
+  int* sched = nullptr;
+  int* done = nullptr;
+  unsigned long long* tl = nullptr;  // QPB200_TIMELINE diagnostics: [2][B][3]
+  int epoch = 0;
+  bool bwd_dirty = true;  // backward counters used since the last solve zeroed them
   float* flops_solve = nullptr;        // per-problem algorithmic flops of the last calls
   float* flops_bwd = nullptr;
   // host-memory mode, path 1: the batch runs in kPipe chunks on their own
@@ -201,7 +210,7 @@ qp_err dalloc(qp_ctx* c, T** p, size_t count) {
 size_t field_elems(int64_t stride, int32_t B, size_t per) { return stride == 0 ? per : (size_t)B * per; }
 
 void free_all(qp_ctx* c) {
-  void* ptrs[] = {c->kglob, c->flops_solve, c->flops_bwd, c->prof, c->own_status, c->wx, c->wy, c->wz, c->wdx, c->wdy, c->wdz, c->dQ_, c->dq_, c->dA_, c->db_,
+  void* ptrs[] = {c->tl, c->sched, c->done, c->kglob, c->flops_solve, c->flops_bwd, c->prof, c->own_status, c->wx, c->wy, c->wz, c->wdx, c->wdy, c->wdz, c->dQ_, c->dq_, c->dA_, c->db_,
                   c->dG_, c->dh_, c->dx_, c->ds_, c->dz_, c->dy_, c->ddl_, c->dit_, c->dst_, c->gQ_, c->gq_,
                   c->gA_, c->gb_, c->gG_, c->gh_};
   for (void* p : ptrs)
@@ -239,6 +248,8 @@ qpb::Args chunk_args(qpb::Args a, int b0, int nb) {
   a.x += o * n; a.y += o * m; a.z += o * p; a.s += o * p;
   if (a.iters) a.iters += o;
   if (a.status) a.status += o;
+  if (a.status_out) a.status_out += o;
+  if (a.done) a.done += o;
   if (a.dl) a.dl += o * n;
   if (a.gQ) a.gQ += o * n * n;
   if (a.gq) a.gq += o * n;
@@ -365,8 +376,12 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
   }
   const int B = d->batch, n = d->n, m = d->m_eq, p = d->p;
   if ((e = dalloc(ctx, &ctx->own_status, B)) || (e = dalloc(ctx, &ctx->flops_solve, B)) ||
-      (e = dalloc(ctx, &ctx->flops_bwd, B))) {
+      (e = dalloc(ctx, &ctx->flops_bwd, B)) || (e = dalloc(ctx, &ctx->sched, 32)) ||
+      (e = dalloc(ctx, &ctx->done, std::max(B, 1)))) {
     free_all(ctx); delete ctx; return e;
+  }
+  if (cudaMemset(ctx->done, 0, sizeof(int) * std::max(B, 1)) != cudaSuccess) {  // epochs start at 1
+    free_all(ctx); delete ctx; return QP_ERR_CUDA;
   }
   if (any_shared(*d)) {
     if ((e = dalloc(ctx, &ctx->wx, (size_t)B * n)) || (e = dalloc(ctx, &ctx->wdx, (size_t)B * n)) ||
@@ -470,6 +485,18 @@ qp_err qp_solve_batched(qp_ctx* c, const float* Q, const float* q, const float* 
   a.x = c->x; a.y = c->y ? c->y : dummy; a.z = c->z ? c->z : dummy; a.s = c->s ? c->s : dummy;
   a.iters = host ? c->dit_ : iters;
   a.status = c->own_status;
+  a.status_out = host ? nullptr : status;
+  const bool implicit = c->c.formulation != QP_EXPLICIT;
+  if (implicit) {
+    // zero every launch counter of this solve and of the backward that follows
+    if ((e = cuda_ok(cudaMemsetAsync(c->sched, 0, sizeof(int) * 32, c->stream))) != QP_OK) return e;
+    c->bwd_dirty = false;
+    a.sched = c->sched;
+    a.done = c->done;
+    a.epoch = ++c->epoch;
+    if (getenv("QPB200_TIMELINE") && !c->tl) cudaMalloc(&c->tl, sizeof(unsigned long long) * 6 * (size_t)B);
+    a.tl = c->tl;
+  }
   if (getenv("QPB200_PHASE_PROFILE") && !c->prof) {
     cudaMalloc(&c->prof, sizeof(unsigned long long) * 8 * B);
     int on = 1;
@@ -498,7 +525,8 @@ qp_err qp_solve_batched(qp_ctx* c, const float* Q, const float* q, const float* 
                                          sizeof(float) * (size_t)nb * bstr[f], cudaMemcpyHostToDevice, st))) !=
                 QP_OK)
           return e;
-      const qpb::Args ac = chunk_args(a, b0, nb);
+      qpb::Args ac = chunk_args(a, b0, nb);
+      if (implicit) ac.sched = c->sched + ch;
       c->ks.solve<<<std::min(c->grid, nb), c->ks.threads, c->L.smem, st>>>(ac);
       if ((e = cuda_ok(cudaGetLastError())) != QP_OK) return e;
       auto o2h = [&](auto* dst, const auto* dsrc, size_t per_prob) -> qp_err {
@@ -525,11 +553,11 @@ qp_err qp_solve_batched(qp_ctx* c, const float* Q, const float* q, const float* 
         (e = d2h(c, iters, c->dit_, (size_t)B)) || (e = d2h(c, status, c->own_status, (size_t)B)))
       return e;
     if ((e = cuda_ok(cudaStreamSynchronize(c->stream))) != QP_OK) return e;
-  } else {
+  } else if (!implicit) {
     if ((e = cuda_ok(cudaMemcpyAsync(status, c->own_status, sizeof(int32_t) * B, cudaMemcpyDeviceToDevice,
                                      c->stream))) != QP_OK)
       return e;
-  }
+  }  // (implicit kernels write the caller's status array themselves)
   c->solved = true;
   if (c->prof) {
     cudaStreamSynchronize(c->stream);
@@ -586,6 +614,7 @@ qp_err qp_backward_batched(qp_ctx* c, const float* dl_dx, float* dQ, float* dq, 
   a.x = c->x; a.y = c->y ? c->y : dummy; a.z = c->z ? c->z : dummy; a.s = c->s ? c->s : dummy;
   a.status = c->own_status;
   a.dl = dl;
+  a.bwd = 1;
   // per-problem gradients for non-shared fields; shared fields via batch sums
   a.gQ = d.bstride_Q ? oQ : nullptr;
   a.gq = d.bstride_q ? oq : nullptr;
@@ -603,6 +632,17 @@ qp_err qp_backward_batched(qp_ctx* c, const float* dl_dx, float* dQ, float* dq, 
   a.rstatus = ost;
   a.flops = c->flops_bwd;
   a.kglob = c->kglob;
+  const bool implicit = c->c.formulation != QP_EXPLICIT;
+  if (implicit) {
+    if (c->bwd_dirty &&
+        (e = cuda_ok(cudaMemsetAsync(c->sched + 16, 0, sizeof(int) * 16, c->stream))) != QP_OK)
+      return e;
+    c->bwd_dirty = true;
+    a.sched = c->sched + 16;
+    a.done = c->done;
+    a.epoch = c->epoch;
+    a.tl = c->tl ? c->tl + 3 * (size_t)B : nullptr;
+  }
   if (pipe) {
     // chunk ch on stream pst[ch]: H2D of its cotangents, its kernel, D2H of its
     // per-problem gradients; shared-field sums follow on c->stream
@@ -620,7 +660,8 @@ qp_err qp_backward_batched(qp_ctx* c, const float* dl_dx, float* dQ, float* dq, 
       if ((e = cuda_ok(cudaMemcpyAsync(c->ddl_ + (size_t)b0 * n, dl_dx + (size_t)b0 * n, sizeof(float) * (size_t)nb * n,
                                        cudaMemcpyHostToDevice, st))) != QP_OK)
         return e;
-      const qpb::Args ac = chunk_args(a, b0, nb);
+      qpb::Args ac = chunk_args(a, b0, nb);
+      if (implicit) ac.sched = c->sched + 16 + ch;
       c->ks.backward<<<std::min(c->grid, nb), c->ks.threads, c->L.smem, st>>>(ac);
       if ((e = cuda_ok(cudaGetLastError())) != QP_OK) return e;
       for (int f = 0; f < 6; ++f)  // per-problem gradients (a.g* is null for shared / skipped fields)
@@ -638,6 +679,25 @@ qp_err qp_backward_batched(qp_ctx* c, const float* dl_dx, float* dQ, float* dq, 
       if ((e = cuda_ok(cudaEventRecord(c->pev[ch], st))) != QP_OK) return e;
       if ((e = cuda_ok(cudaStreamWaitEvent(c->stream, c->pev[ch], 0))) != QP_OK) return e;
     }
+  } else if (implicit && !c->L.big && !getenv("QPB200_NO_PDL")) {
+    // programmatic stream serialisation: the backward grid may start while the
+    // solve grid drains (each CTA waits on done[b] for its problem), so the
+    // solve's last, partly occupied wave overlaps backward work.  Both
+    // launches run the same kernel (ipm_kernel), so mixed SMs share its
+    // instruction cache (two separate kernels made the overlap a net loss).
+    // Not on the large-N path: its per-CTA global KKT workspaces are indexed
+    // by blockIdx, which a solve CTA and a backward CTA would share.
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(c->grid);
+    lc.blockDim = dim3(c->ks.threads);
+    lc.dynamicSmemBytes = c->L.smem;
+    lc.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    if ((e = cuda_ok(cudaLaunchKernelEx(&lc, c->ks.backward, a))) != QP_OK) return e;
   } else {
     c->ks.backward<<<c->grid, c->ks.threads, c->L.smem, c->stream>>>(a);
     if ((e = cuda_ok(cudaGetLastError())) != QP_OK) return e;
@@ -679,6 +739,15 @@ qp_err qp_backward_batched(qp_ctx* c, const float* dl_dx, float* dQ, float* dq, 
         (status && (e = d2h(c, status, c->dst_, (size_t)B))))
       return e;
     if ((e = cuda_ok(cudaStreamSynchronize(c->stream))) != QP_OK) return e;
+  }
+  if (c->tl) {  // diagnostics: append {smid, start, end} of every problem (solve, then backward) to the file
+    cudaStreamSynchronize(c->stream);
+    std::vector<unsigned long long> h(6 * (size_t)B);
+    cudaMemcpy(h.data(), c->tl, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost);
+    if (FILE* fp = fopen(getenv("QPB200_TIMELINE"), "ab")) {
+      fwrite(h.data(), sizeof(unsigned long long), h.size(), fp);
+      fclose(fp);
+    }
   }
   return QP_OK;
 }

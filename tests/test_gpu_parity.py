@@ -299,3 +299,31 @@ def test_cfg4_full_size_sampled_and_batch_sums():
         ref = sums[k].cpu().numpy()
         err = np.linalg.norm(g[k] - ref) / np.linalg.norm(ref)
         assert err <= 1e-5, (k, err)
+
+
+@pytest.mark.parametrize("cfg,batch", [(2, 200), (3, 48), (None, 2)])
+def test_backward_overlapping_solve(cfg, batch):
+    """qp_backward_batched launched right behind qp_solve_batched on the same
+    stream (no host synchronisation: on path 1 the backward grid starts while
+    the solve grid drains and waits per problem on the solve's done flags)
+    gives bitwise the same outputs as a run with a synchronisation between
+    the two calls; two consecutive steps (epochs) as well."""
+    import torch
+    from paper_2605_17913_b200.solver import QPSolver
+    b = gen.make_config(cfg, batch=batch) if cfg else gen.g_rand(2, 2, 130, 0, 200)
+    S = QPSolver(b.batch, b.n, b.m, b.p, device=0)
+    data = [torch.from_numpy(np.ascontiguousarray(getattr(b, f))).cuda() for f in ("Q", "q", "A", "b", "G", "h")]
+    dl = torch.from_numpy(b.dl_dx).cuda()
+    res = []
+    for sync in (True, False, False):
+        out = S.solve(*data)
+        if sync:
+            torch.cuda.synchronize()
+        g = S.backward(dl)
+        torch.cuda.synchronize()
+        res.append({k: v.cpu().numpy().copy() for k, v in {**out, **{"g" + k: v for k, v in g.items()}}.items()})
+    S.close()
+    assert np.all(res[0]["status"] == 0) and np.all(res[0]["gstatus"] == 0)
+    for r in res[1:]:
+        for k in res[0]:
+            assert np.array_equal(res[0][k], r[k]), k

@@ -10,5 +10,8 @@ python bench.py --no-cpu --no-e2e --steps 2 --warmup 1 > gpurun_out/plain_${TAG}
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_${TAG}.csv \
     python bench.py --no-cpu --no-e2e --steps 2 --warmup 1 > gpurun_out/ncu_launch_${TAG}.log 2>&1; echo "launch_rc=$?"
 python bench.py --no-cpu --no-e2e --steps 1 --warmup 1 > gpurun_out/plain2_${TAG}.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:ipm_ -s 2 -c 2 -o gpurun_out/prof_${TAG} \
+ncu --set full --clock-control none --import-source on -k regex:ipm_kernel -s 2 -c 1 -o gpurun_out/prof_${TAG} \
     python bench.py --no-cpu --no-e2e --steps 1 --warmup 1 > gpurun_out/ncu_full_${TAG}.log 2>&1; echo "ncu_rc=$?"
+# the same kernel serves both calls (solve launch first, backward launch second)
+ncu --set full --clock-control none --import-source on -k regex:ipm_kernel -s 3 -c 1 -o gpurun_out/prof_${TAG}_bwd \
+    python bench.py --no-cpu --no-e2e --steps 1 --warmup 1 > gpurun_out/ncu_full_bwd_${TAG}.log 2>&1; echo "ncu_bwd_rc=$?"

@@ -323,18 +323,21 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
     __syncthreads();
     { const long long t = clock64(); tpan += t - tc0; tc0 = t; }
     // ---- (2) trailing update A22 −= L21 S_b L21ᵀ --------------------------------
+    //      32-row × 16-column tiles of the lower triangle, one warp each
+    //      (8×2 strided register tile per lane): twice as many tiles as 32×32
+    //      ones, so the 4 warps stay balanced on the small trailing matrices
+    //      of path 1 (T = 3 row blocks: 12 tiles instead of 6).
     if (k1 < N4) {
-      const int T = (N4 - k1 + 31) >> 5;
-      const int nst = T * (T + 1) / 2;
+      const int Tn = N4 - k1;
+      const int T = (Tn + 31) >> 5, T16 = (Tn + 15) >> 4;
+      const int nst = T * (T + 1) - (2 * T - T16);  // Σ_I min(2I + 2, T16)
       const int ty = lane >> 3, tx = lane & 7;
       for (int st = warp; st < nst; st += NW) {
-        int I = (int)((sqrtf(8.f * st + 1.f) - 1.f) * 0.5f);
-        while ((I + 1) * (I + 2) / 2 <= st) ++I;
-        while (I * (I + 1) / 2 > st) --I;
-        const int J = st - I * (I + 1) / 2;
-        const int rb = k1 + 32 * I + ty, cb = k1 + 32 * J + tx;
-        int roff[8], coff[4];
-        bool rok[8], cok[4];
+        int I = 0, J = st;
+        while (J >= min(2 * I + 2, T16)) { J -= min(2 * I + 2, T16); ++I; }
+        const int rb = k1 + 32 * I + ty, cb = k1 + 16 * J + tx;
+        int roff[8], coff[2];
+        bool rok[8], cok[2];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const int r = rb + 4 * q;
@@ -342,23 +345,24 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
           roff[q] = rok[q] ? row_off<TAB>(L, tab, r) : 0;
         }
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < 2; ++c) {
           const int cc = cb + 8 * c;
           cok[c] = cc < N4;
           coff[c] = cok[c] ? row_off<TAB>(L, tab, cc) : 0;
         }
-        float acc[8][4];
+        float acc[8][2];
 #pragma unroll
         for (int q = 0; q < 8; ++q)
 #pragma unroll
-          for (int c = 0; c < 4; ++c) acc[q][c] = (rok[q] && cok[c]) ? K[roff[q] + cb + 8 * c] : 0.f;
+          for (int c = 0; c < 2; ++c)
+            acc[q][c] = (rok[q] && cok[c] && cb + 8 * c <= rb + 4 * q) ? K[roff[q] + cb + 8 * c] : 0.f;
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
           // S_b applied to the column operand (npos is a multiple of 4)
           const float sq = k0 + 4 * q4 < npos ? -1.f : 1.f;
-          float4 lc[4];
+          float4 lc[2];
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
+          for (int c = 0; c < 2; ++c) {
             float4 t = cok[c] ? *reinterpret_cast<const float4*>(K + coff[c] + k0 + 4 * q4)
                               : make_float4(0, 0, 0, 0);
             t.x *= sq; t.y *= sq; t.z *= sq; t.w *= sq;
@@ -369,7 +373,7 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
             const float4 lr = rok[q] ? *reinterpret_cast<const float4*>(K + roff[q] + k0 + 4 * q4)
                                      : make_float4(0, 0, 0, 0);
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < 2; ++c) {
               float t = acc[q][c];
               t = fmaf(lr.x, lc[c].x, t);
               t = fmaf(lr.y, lc[c].y, t);
@@ -382,7 +386,7 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
 #pragma unroll
         for (int q = 0; q < 8; ++q)
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
+          for (int c = 0; c < 2; ++c) {
             const int cc = cb + 8 * c;
             // lower triangle only (a diagonal block's upper part is never touched)
             if (rok[q] && cok[c] && cc <= rb + 4 * q) K[roff[q] + cc] = acc[q][c];

@@ -56,6 +56,7 @@ typedef struct {
   double pivot_floor_rel; // LDL pivot floor theta = rel*max|diag| (Q12)
   double relax_tol;       // Alg. 2 residual tolerance (reading Q5b)
   int32_t partition_cap;  // SOLVER_M_PART: most constraints kept in augmented form (reading Q12c); -1 = no cap
+  int32_t relax_mode;     // 0: Alg. 2 by exact Newton (Q6); 1: chord steps with Alg. 1's factor nearest kappa_relax (N2(i))
 } oracle_cfg;
 }
 
@@ -507,7 +508,9 @@ template <typename T> static T mean_sz(const T* s, const T* z, int p) {
 // iters = number of Newton steps taken.
 // ---------------------------------------------------------------------------
 template <typename T>
-static int solve_qp_implicit(const Prob<T>& P, const oracle_cfg& cfg, T* x, T* y, T* z, T* s, int* iters) {
+static int solve_qp_implicit(const Prob<T>& P, const oracle_cfg& cfg, T* x, T* y, T* z, T* s, int* iters,
+                             Factor<T>* cache = nullptr) {
+  bool cached = false;
   const int n = P.n, m = P.m, p = P.p;
   const T tol = T(cfg.tol), sigma = T(cfg.sigma), tau = T(cfg.tau), fr = T(cfg.pivot_floor_rel);
   *iters = 0;
@@ -523,6 +526,9 @@ static int solve_qp_implicit(const Prob<T>& P, const oracle_cfg& cfg, T* x, T* y
     if (k == cfg.max_iter) return ST_MAX_ITER;
     Factor<T> F = factor_kkt(P, v.data(), kappa, cfg.kkt_solver, fr, cfg.partition_cap);
     if (!finite_all(F.dp) || !finite_all(F.dm) || !finite_all(F.c)) return ST_NUMERICAL_FAILURE | (STG_SCALING << 8);
+    // N2(i): keep the factorisation of the first iterate with kappa below
+    // sqrt(10) kappa_relax (the iterates pass kappa_relax about one decade per step)
+    if (cache && !cached && kappa < std::sqrt(T(10)) * T(cfg.kappa_relax)) { *cache = F; cached = true; }
     T kt = sigma * kappa;                 // kappa_target <- sigma kappa
     T rk = kappa - kt;                    // r_kappa = kappa - kappa_target
     T dk;
@@ -550,7 +556,7 @@ static int solve_qp_implicit(const Prob<T>& P, const oracle_cfg& cfg, T* x, T* y
 // ---------------------------------------------------------------------------
 template <typename T>
 static int relax_qp_implicit(const Prob<T>& P, const oracle_cfg& cfg, T* x, T* y, T* z, T* s, int* iters,
-                             Factor<T>& F) {
+                             Factor<T>& F, const Factor<T>* chord = nullptr) {
   const int n = P.n, m = P.m, p = P.p;
   const T tol = T(cfg.tol), tau = T(cfg.tau), kr = T(cfg.kappa_relax), ktol = T(cfg.relax_ktol),
           fr = T(cfg.pivot_floor_rel), rtol = T(cfg.relax_tol);
@@ -561,16 +567,21 @@ static int relax_qp_implicit(const Prob<T>& P, const oracle_cfg& cfg, T* x, T* y
     for (int i = 0; i < p; ++i) v[i] = z[i] - s[i];
     T kappa = mean_sz(s, z, p);
     residuals(P, x, y, z, s, kappa, true, R);
-    F = factor_kkt(P, v.data(), kappa, cfg.kkt_solver, fr, cfg.partition_cap);
     *iters = k;
-    if (!finite_all(F.dp) || !finite_all(F.dm) || !F.ok) return ST_NUMERICAL_FAILURE | (STG_RELAX << 8);
     bool kok = p == 0 || std::fabs(kappa / kr - T(1)) <= ktol;
-    if (kok && relax_done(R, tol, rtol, phi_prev)) return ST_CONVERGED;
+    const bool done = kok && relax_done(R, tol, rtol, phi_prev);
+    if (!chord || done) {
+      // exact Newton (or the final factorisation at the relaxed point, for Alg. 3)
+      F = factor_kkt(P, v.data(), kappa, cfg.kkt_solver, fr, cfg.partition_cap);
+      if (!finite_all(F.dp) || !finite_all(F.dm) || !F.ok) return ST_NUMERICAL_FAILURE | (STG_RELAX << 8);
+    }
+    if (done) return ST_CONVERGED;
     phi_prev = kok ? rel_phi(R) : std::numeric_limits<T>::infinity();
     if (k == cfg.relax_max_iter) return ST_MAX_ITER | (STG_RELAX << 8);
     T rk = kappa - kr;  // kappa_target = kappa_relax
     T dk;
-    newton_direction(P, F, R, rk, dx.data(), dy.data(), dz.data(), ds.data(), dv.data(), dk);
+    // chord step (N2(i)): the Newton system of Alg. 1's cached factorisation, current residuals
+    newton_direction(P, chord ? *chord : F, R, rk, dx.data(), dy.data(), dz.data(), ds.data(), dv.data(), dk);
     if (!finite_all(dx) || !finite_all(dv) || !finite_all(dz) || !finite_all(ds))
       return ST_NUMERICAL_FAILURE | (STG_RELAX << 8);
     T alpha = linesearch(s, z, ds.data(), dz.data(), p, tau);
@@ -859,8 +870,18 @@ static void backward_batch(const oracle_cfg& cfg, const BatchData<T>& D, int B, 
       st = relax_qp_explicit(P, cfg, xi, yi, zi, si, &riters[i], F);
       if ((st & 0xff) == ST_CONVERGED) grads_explicit(P, F, xi, yi, zi, si, dl + (size_t)i * n, gQi, gqi, gAi, gbi, gGi, ghi);
     } else {
-      Factor<T> F;
-      st = relax_qp_implicit(P, cfg, xi, yi, zi, si, &riters[i], F);
+      Factor<T> F, C;
+      const Factor<T>* chord = nullptr;
+      if (cfg.relax_mode == 1) {
+        // N2(i): the factorisation Alg. 1 computed nearest kappa_relax, recomputed
+        // here by re-running the (deterministic) forward solve
+        std::vector<T> xs(n), ys(m), zs(p), ss(p);
+        int it0;
+        C.N = -1;
+        solve_qp_implicit(P, cfg, xs.data(), ys.data(), zs.data(), ss.data(), &it0, &C);
+        if (C.N >= 0) chord = &C;
+      }
+      st = relax_qp_implicit(P, cfg, xi, yi, zi, si, &riters[i], F, chord);
       if ((st & 0xff) == ST_CONVERGED) grads_from_factor(P, F, xi, yi, zi, dl + (size_t)i * n, gQi, gqi, gAi, gbi, gGi, ghi);
     }
     if ((st & 0xff) == ST_CONVERGED) {

@@ -150,3 +150,21 @@ def test_relax_reaches_kappa_relax(orc):
         zs = g["relaxed"]["z"].astype(float) * g["relaxed"]["s"].astype(float)
         assert np.all(np.abs(zs / cfg.kappa_relax - 1) <= rel)
         assert np.all(g["relax_iters"] >= 1)
+
+
+def test_chord_relax_same_relaxed_map_f64(orc):
+    """N2(i) evaluation harness (relax_mode=1: Alg. 2 steps with the Alg. 1
+    factorisation nearest kappa_relax, final factorisation at the
+    relaxed point for Alg. 3): the relaxed point is the unique central-path
+    point at kappa_relax, so the gradients equal the exact-Newton relax's to
+    1e-7 in f64 wherever the chord iteration converges."""
+    b = gen.make_config(2, batch=8)
+    c0, c1 = orc.Cfg.f64(), orc.Cfg.f64(relax_mode=1)
+    r = orc.solve(b, c0, "f64")
+    g0, g1 = orc.backward(b, r, c0, "f64"), orc.backward(b, r, c1, "f64")
+    ok = g1["status"] == 0
+    assert np.all(g0["status"] == 0) and ok.sum() >= 6
+    for k in FIELDS:
+        a, ref = g1[k].reshape(8, -1)[ok], g0[k].reshape(8, -1)[ok]
+        err = np.linalg.norm(a - ref, axis=1) / np.maximum(np.linalg.norm(ref, axis=1), 1e-30)
+        assert err.max() <= 1e-7, (k, err.max())

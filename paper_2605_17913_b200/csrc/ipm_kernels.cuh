@@ -710,7 +710,8 @@ __device__ void write_gradients(const Smem& S, const Args& a, const int bid) {
 // assemble / factor / solve_qd have ONE call site.
 // ------------------------------------------------------------------------
 template <int NT, bool BIG>
-__device__ __forceinline__ void ipm_problem(const Args& a, const Smem& S, const int bid, const bool bwd) {
+__device__ __forceinline__ void ipm_problem(const Args& a, const Smem& S, const int bid, const bool bwd,
+                                            const bool lost = false) {
   const int tid = threadIdx.x;
   const Prob P = prob_of(a, bid);
   const int n = a.n, n4 = a.n4, p = a.p, m = a.m;
@@ -730,7 +731,8 @@ __device__ __forceinline__ void ipm_problem(const Args& a, const Smem& S, const 
       S.s[i] = __ldcg(a.s + (long long)bid * p + i);
     }
     __syncthreads();
-    if ((__ldcg(a.status + bid) & 0xff) != ST_CONVERGED) status = ST_FAIL | (STG_RELAX << 8);
+    if (lost) status = ST_FAIL | (STG_BACKWARD << 8);
+    else if ((__ldcg(a.status + bid) & 0xff) != ST_CONVERGED) status = ST_FAIL | (STG_RELAX << 8);
   }
   for (int k = bwd ? 0 : -1; status == ST_CONVERGED; ++k) {
     const bool init = k < 0;
@@ -889,20 +891,26 @@ __global__ void __launch_bounds__(NT, MINB) ipm_kernel(const Args a) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if constexpr (BIG) tc::tmem_alloc(tc::tc_state(S.tc));
   for (int bid = next_problem(a, S.flag + 12); bid < a.B; bid = next_problem(a, S.flag + 12)) {
-    if (bwd && a.done && threadIdx.x == 0) {
-      // relaxed polling (an acquire per poll would invalidate this SM's L1),
-      // one acquire fence once the flag is seen
-      int e;
-      for (;;) {
-        asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(e) : "l"(a.done + bid) : "memory");
-        if (e == a.epoch) break;
-        __nanosleep(256);
+    bool lost = false;  // backward: the solve never published this problem (watchdog)
+    if (bwd && a.done) {
+      if (threadIdx.x == 0) {
+        // relaxed polling (an acquire per poll would invalidate this SM's L1),
+        // one acquire fence once the flag is seen; after 20 s without the
+        // flag the problem is reported failed instead of hanging the GPU
+        int e;
+        const unsigned long long t0 = gtimer();
+        for (;;) {
+          asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(e) : "l"(a.done + bid) : "memory");
+          if (e == a.epoch) break;
+          if (gtimer() - t0 > 20000000000ull) { lost = true; break; }
+          __nanosleep(256);
+        }
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
       }
-      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      lost = __syncthreads_or(lost);
     }
-    if (bwd) __syncthreads();
     if (a.tl && threadIdx.x == 0) { a.tl[3 * bid] = smid(); a.tl[3 * bid + 1] = gtimer(); }
-    ipm_problem<NT, BIG>(a, S, bid, bwd);  // ends with a barrier after the output stores
+    ipm_problem<NT, BIG>(a, S, bid, bwd, lost);  // ends with a barrier after the output stores
     if (a.tl && threadIdx.x == 0) a.tl[3 * bid + 2] = gtimer();
     if (!bwd && a.done && threadIdx.x == 0)  // release (cumulative through the barrier): outputs before the flag
       asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(a.done + bid), "r"(a.epoch) : "memory");

@@ -489,6 +489,7 @@ qp_err qp_solve_batched(qp_ctx* c, const float* Q, const float* q, const float* 
   const bool implicit = c->c.formulation != QP_EXPLICIT;
   if (implicit) {
     // zero every launch counter of this solve and of the backward that follows
+    c->solved = false;  // a backward must not wait on an epoch whose solve was never launched
     if ((e = cuda_ok(cudaMemsetAsync(c->sched, 0, sizeof(int) * 32, c->stream))) != QP_OK) return e;
     c->bwd_dirty = false;
     a.sched = c->sched;

@@ -272,7 +272,7 @@ def main():
     # ---- e2e: host buffers through the C ABI, H2D/D2H inside the timed region
     e2e = None
     if not a.no_e2e:
-        Sh = QPSolver(B, n, m, p, shared=shared, device=local, mem="host", **c["solver"])
+        Sh = QPSolver(B, n, m, p, shared=shared, device=local, mem="host_async", **c["solver"])
         hdata = [torch.from_numpy(np.ascontiguousarray(getattr(batch, f)[0] if f in shared else getattr(batch, f)))
                  .pin_memory() for f in FIELDS]
         hdl = torch.from_numpy(batch.dl_dx).pin_memory()

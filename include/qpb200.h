@@ -24,7 +24,12 @@
  *     stream; the caller synchronises.  QP_MEM_HOST: every pointer is host
  *     memory (ideally pinned); the library copies in and out through its own
  *     device staging buffers and the call returns after the results are back
- *     in host memory.
+ *     in host memory.  QP_MEM_HOST_ASYNC: as QP_MEM_HOST, but the calls only
+ *     enqueue their copies and kernels on the ctx stream (and, on path 1, its
+ *     four chunk streams, joined back into the ctx stream); host outputs are
+ *     valid, and host inputs may be modified, once the ctx stream has been
+ *     synchronised.  A backward call may then start on the problems whose
+ *     solve chunk has finished while later chunks still run.
  *   - All buffers are caller-owned.  The ctx owns its workspaces only.
  *   - qp_backward_batched reuses the problem data and the solution of the
  *     LAST qp_solve_batched call on the same ctx: with QP_MEM_DEVICE the
@@ -67,7 +72,7 @@ enum {
 };
 
 enum { QP_IMPLICIT = 0, QP_EXPLICIT = 1 };   /* formulation: Eq. 14 or Eq. 8 */
-enum { QP_MEM_DEVICE = 0, QP_MEM_HOST = 1 };
+enum { QP_MEM_DEVICE = 0, QP_MEM_HOST = 1, QP_MEM_HOST_ASYNC = 2 };
 
 typedef struct {
   int32_t batch;   /* B ≥ 1                                                     */
@@ -87,7 +92,7 @@ typedef struct {
   int32_t relax_max_iter; /* Alg. 2 iterations (Q22); default 50                           */
   int32_t formulation;    /* QP_IMPLICIT (default) | QP_EXPLICIT (config-3 standard arm)   */
   float pivot_floor_rel;  /* LDLᵀ pivot floor θ = rel·max|diag| (Q12); default √ε_f32     */
-  int32_t mem_kind;       /* QP_MEM_DEVICE (default) | QP_MEM_HOST                         */
+  int32_t mem_kind;       /* QP_MEM_DEVICE (default) | QP_MEM_HOST | QP_MEM_HOST_ASYNC     */
   float relax_tol;        /* Alg. 2 residual tolerance (Q5b); default 1e-6; the relax loop */
                           /* also stops at the f32 floor (φ ≤ tol and no 10% progress)     */
 } qp_config;

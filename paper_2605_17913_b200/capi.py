@@ -16,7 +16,7 @@ ERRORS = {0: "ok", -1: "invalid argument", -2: "unsupported shape", -3: "pointer
           -7: "unsupported option"}
 QP_CONVERGED, QP_MAX_ITER, QP_NUMERICAL_FAILURE = 0, 2, 3
 QP_IMPLICIT, QP_EXPLICIT = 0, 1
-QP_MEM_DEVICE, QP_MEM_HOST = 0, 1
+QP_MEM_DEVICE, QP_MEM_HOST, QP_MEM_HOST_ASYNC = 0, 1, 2
 
 
 class QpDims(C.Structure):

@@ -105,7 +105,9 @@ Layout make_layout(int n, int m, int p, int formulation) {
     // area; iterations whose reduced system is larger use the CTA's global
     // workspace (hybrid)
     L.big = true;
-    const size_t bud = budget(1);
+    int bctas = 1;
+    if (const char* e = getenv("QPB200_BIG_CTAS")) bctas = std::max(1, std::min(2, atoi(e)));  // experiments
+    const size_t bud = budget(bctas);
     int lo = 0, hi = L.Nmax;
     if (smem_for(L, m, p, 0, true) > bud) {
       lo = 0;  // vectors alone do not fit: qp_create reports QP_ERR_SHAPE
@@ -118,7 +120,7 @@ Layout make_layout(int n, int m, int p, int formulation) {
     L.ncap = lo;
     if (env_cap >= 0) L.ncap = std::min(env_cap, L.ncap);
     if (getenv("QPB200_FORCE_GLOBAL")) L.ncap = 0;
-    L.threads = 256; L.minb = 1;
+    L.threads = 256; L.minb = bctas;
   }
   if (const char* e = getenv("QPB200_THREADS"); e && !L.big) L.threads = atoi(e);  // experiments: 128|256
   L.ksmem = L.ncap > 0 ? qpb::KLayout::make(L.ncap, L.n4).size() : 0;
@@ -137,9 +139,11 @@ KernelSet pick_kernels(const Layout& L, int formulation) {
     if (L.big) return {0, nullptr, nullptr};
     return {128, qpb::xpm_solve_kernel<128, 1>, qpb::xpm_backward_kernel<128, 1>};
   }
-  if (L.big) return {256, qpb::ipm_kernel<256, 1, true>, qpb::ipm_kernel<256, 1, true>};
+  if (L.big) {
+    if (L.minb == 2) return {256, qpb::ipm_kernel<256, 2, true>, qpb::ipm_kernel<256, 2, true>};
+    return {256, qpb::ipm_kernel<256, 1, true>, qpb::ipm_kernel<256, 1, true>};
+  }
   switch (L.minb) {
-    case 5: return {128, qpb::ipm_kernel<128, 5, false>, qpb::ipm_kernel<128, 5, false>};
     case 4: return {128, qpb::ipm_kernel<128, 4, false>, qpb::ipm_kernel<128, 4, false>};
     case 3: return {128, qpb::ipm_kernel<128, 3, false>, qpb::ipm_kernel<128, 3, false>};
     default: return {128, qpb::ipm_kernel<128, 1, false>, qpb::ipm_kernel<128, 1, false>};
@@ -335,7 +339,7 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
   if (!(c.tol > 0.f) || c.max_iter < 0 || !(c.sigma > 0.f && c.sigma < 1.f) || !(c.tau > 0.f && c.tau <= 1.f) ||
       !(c.kappa_relax > 0.f) || !(c.relax_ktol > 0.f) || !(c.relax_tol > 0.f) || c.relax_max_iter < 0 || !(c.pivot_floor_rel >= 0.f) ||
       (c.formulation != QP_IMPLICIT && c.formulation != QP_EXPLICIT) ||
-      (c.mem_kind != QP_MEM_DEVICE && c.mem_kind != QP_MEM_HOST))
+      (c.mem_kind != QP_MEM_DEVICE && c.mem_kind != QP_MEM_HOST && c.mem_kind != QP_MEM_HOST_ASYNC))
     return QP_ERR_INVALID_ARG;
   const int64_t strides[6] = {d->bstride_Q, d->bstride_q, d->bstride_A, d->bstride_b, d->bstride_G, d->bstride_h};
   const int64_t need[6] = {(int64_t)d->n * d->n, d->n, (int64_t)d->m_eq * d->n, d->m_eq, (int64_t)d->p * d->n,
@@ -390,7 +394,7 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
       free_all(ctx); delete ctx; return e;
     }
   }
-  if (c.mem_kind == QP_MEM_HOST) {
+  if (c.mem_kind != QP_MEM_DEVICE) {
     if ((e = dalloc(ctx, &ctx->dQ_, field_elems(d->bstride_Q, B, (size_t)n * n))) ||
         (e = dalloc(ctx, &ctx->dq_, field_elems(d->bstride_q, B, n))) ||
         (e = dalloc(ctx, &ctx->dA_, field_elems(d->bstride_A, B, (size_t)m * n))) ||
@@ -462,7 +466,8 @@ qp_err qp_solve_batched(qp_ctx* c, const float* Q, const float* q, const float* 
     if (pp && !aligned4(pp)) return QP_ERR_ALIGN;
   if (cudaSetDevice(c->device) != cudaSuccess) return QP_ERR_CUDA;
   qp_err e;
-  const bool host = c->c.mem_kind == QP_MEM_HOST;
+  const bool host = c->c.mem_kind != QP_MEM_DEVICE;
+  const bool hsync = c->c.mem_kind == QP_MEM_HOST;  // QP_MEM_HOST_ASYNC: the caller synchronises
   // host mode: device copies of the six fields (stride 0 = shared, one copy)
   float* const stage[6] = {c->dQ_, c->dq_, c->dA_, c->db_, c->dG_, c->dh_};
   const float* const src[6] = {Q, q, A, b, G, h};
@@ -541,7 +546,7 @@ qp_err qp_solve_batched(qp_ctx* c, const float* Q, const float* q, const float* 
       if ((e = cuda_ok(cudaEventRecord(c->pev[ch], st))) != QP_OK) return e;
       if ((e = cuda_ok(cudaStreamWaitEvent(c->stream, c->pev[ch], 0))) != QP_OK) return e;
     }
-    if ((e = cuda_ok(cudaStreamSynchronize(c->stream))) != QP_OK) return e;
+    if (hsync && (e = cuda_ok(cudaStreamSynchronize(c->stream))) != QP_OK) return e;
   } else {
     c->ks.solve<<<c->grid, c->ks.threads, c->L.smem, c->stream>>>(a);
     if ((e = cuda_ok(cudaGetLastError())) != QP_OK) return e;
@@ -553,7 +558,7 @@ qp_err qp_solve_batched(qp_ctx* c, const float* Q, const float* q, const float* 
         (e = d2h(c, z, c->dz_, (size_t)B * p)) || (e = d2h(c, y, c->dy_, (size_t)B * m)) ||
         (e = d2h(c, iters, c->dit_, (size_t)B)) || (e = d2h(c, status, c->own_status, (size_t)B)))
       return e;
-    if ((e = cuda_ok(cudaStreamSynchronize(c->stream))) != QP_OK) return e;
+    if (hsync && (e = cuda_ok(cudaStreamSynchronize(c->stream))) != QP_OK) return e;
   } else if (!implicit) {
     if ((e = cuda_ok(cudaMemcpyAsync(status, c->own_status, sizeof(int32_t) * B, cudaMemcpyDeviceToDevice,
                                      c->stream))) != QP_OK)
@@ -596,7 +601,8 @@ qp_err qp_backward_batched(qp_ctx* c, const float* dl_dx, float* dQ, float* dq, 
   if (cudaSetDevice(c->device) != cudaSuccess) return QP_ERR_CUDA;
   const qp_dims& d = c->d;
   const int B = d.batch, n = d.n, m = d.m_eq, p = d.p;
-  const bool host = c->c.mem_kind == QP_MEM_HOST;
+  const bool host = c->c.mem_kind != QP_MEM_DEVICE;
+  const bool hsync = c->c.mem_kind == QP_MEM_HOST;  // QP_MEM_HOST_ASYNC: the caller synchronises
   qp_err e;
   const float* dl = dl_dx;
   float *oQ = dQ, *oq = dq, *oA = dA, *ob = db, *oG = dG, *oh = dh;
@@ -657,7 +663,10 @@ qp_err qp_backward_batched(qp_ctx* c, const float* dl_dx, float* dQ, float* dq, 
       const int b0 = ch * cs, nb = std::min(cs, B - b0);
       if (nb <= 0) break;
       cudaStream_t st = c->pst[ch];
-      if ((e = cuda_ok(cudaStreamWaitEvent(st, c->pev[KP], 0))) != QP_OK) return e;
+      // QP_MEM_HOST: after all earlier work on the ctx stream.  QP_MEM_HOST_ASYNC:
+      // chunk ch follows the solve's chunk ch on its own stream only, so the
+      // first backward chunks overlap the last solve chunks
+      if (hsync && (e = cuda_ok(cudaStreamWaitEvent(st, c->pev[KP], 0))) != QP_OK) return e;
       if ((e = cuda_ok(cudaMemcpyAsync(c->ddl_ + (size_t)b0 * n, dl_dx + (size_t)b0 * n, sizeof(float) * (size_t)nb * n,
                                        cudaMemcpyHostToDevice, st))) != QP_OK)
         return e;
@@ -728,7 +737,7 @@ qp_err qp_backward_batched(qp_ctx* c, const float* dl_dx, float* dQ, float* dq, 
     const size_t gper[6] = {(size_t)n * n, (size_t)n, (size_t)m * n, (size_t)m, (size_t)p * n, (size_t)p};
     for (int f = 0; f < 6; ++f)
       if (bstr[f] == 0 && ghost[f] && (e = d2h(c, ghost[f], gst[f], gper[f])) != QP_OK) return e;
-    if ((e = cuda_ok(cudaStreamSynchronize(c->stream))) != QP_OK) return e;
+    if (hsync && (e = cuda_ok(cudaStreamSynchronize(c->stream))) != QP_OK) return e;
   } else if (host) {
     if ((dQ && (e = d2h(c, dQ, c->gQ_, field_elems(d.bstride_Q, B, (size_t)n * n)))) ||
         (dq && (e = d2h(c, dq, c->gq_, field_elems(d.bstride_q, B, n)))) ||
@@ -739,7 +748,7 @@ qp_err qp_backward_batched(qp_ctx* c, const float* dl_dx, float* dQ, float* dq, 
         (relax_iters && (e = d2h(c, relax_iters, c->dit_, (size_t)B))) ||
         (status && (e = d2h(c, status, c->dst_, (size_t)B))))
       return e;
-    if ((e = cuda_ok(cudaStreamSynchronize(c->stream))) != QP_OK) return e;
+    if (hsync && (e = cuda_ok(cudaStreamSynchronize(c->stream))) != QP_OK) return e;
   }
   if (c->tl) {  // diagnostics: append {smid, start, end} of every problem (solve, then backward) to the file
     cudaStreamSynchronize(c->stream);

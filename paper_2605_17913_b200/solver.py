@@ -38,7 +38,11 @@ class QPSolver:
         for k, v in cfg.items():
             setattr(c, k, v)
         c.formulation = capi.QP_EXPLICIT if formulation == "explicit" else capi.QP_IMPLICIT
-        c.mem_kind = capi.QP_MEM_HOST if mem == "host" else capi.QP_MEM_DEVICE
+        # "host": host buffers, each call returns with its results in host memory;
+        # "host_async": host buffers, the caller synchronises the device (copies
+        # and kernels of consecutive calls overlap)
+        c.mem_kind = {"device": capi.QP_MEM_DEVICE, "host": capi.QP_MEM_HOST,
+                      "host_async": capi.QP_MEM_HOST_ASYNC}[mem]
         self.cfg = c
         stream = torch.cuda.current_stream(device).cuda_stream if mem == "device" else None
         self.h = capi.qp_create(self.dims, c, device, stream)
@@ -72,7 +76,7 @@ class QPSolver:
             raise ValueError(f"{f}: need contiguous float32")
         if self.mem == "device" and (not t.is_cuda or t.device.index != self.device):
             raise ValueError(f"{f}: must live on cuda:{self.device}")
-        if self.mem == "host" and t.is_cuda:
+        if self.mem != "device" and t.is_cuda:
             raise ValueError(f"{f}: host mode takes CPU tensors")
 
     def _alloc(self, shape, dtype=torch.float32):

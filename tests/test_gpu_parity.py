@@ -140,6 +140,32 @@ def test_host_memory_pipelined_chunks_match_device(cfg, B):
         assert np.array_equal(gd[k], gh[k]), k
 
 
+@pytest.mark.parametrize("cfg,B", [(1, 16), (2, 301), (4, 130)])
+def test_host_async_mode_matches_device(cfg, B):
+    """QP_MEM_HOST_ASYNC: solve and backward enqueued back to back with no
+    synchronisation in between (on path 1 the backward chunk i only follows
+    the solve chunk i on its stream), one device synchronisation at the end:
+    bitwise the device-mode results."""
+    import torch
+    from paper_2605_17913_b200.solver import QPSolver
+    b = gen.make_config(cfg, batch=B)
+    gd = run_gpu(b)
+    shared = [k for k, v in b.shared.items() if v]
+    S = QPSolver(b.batch, b.n, b.m, b.p, shared=shared, mem="host_async")
+    data = [torch.from_numpy(np.ascontiguousarray(getattr(b, f)[0] if f in shared else getattr(b, f))).pin_memory()
+            for f in ("Q", "q", "A", "b", "G", "h")]
+    dl = torch.from_numpy(b.dl_dx).pin_memory()
+    for _ in range(2):  # second round reuses the output buffers, as a training loop would
+        out = S.solve(*data) if _ == 0 else S.solve(*data, out=out)
+        g = S.backward(dl) if _ == 0 else S.backward(dl, out=g)
+        torch.cuda.synchronize()
+        res = {k: v.numpy().copy() for k, v in out.items()}
+        res.update({k: v.numpy().copy() for k, v in g.items() if k != "status"})
+        for k in ("x", "z", "s", "y", "iters", "status", "dQ", "dq", "dG", "dh"):
+            assert np.array_equal(gd[k], res[k]), k
+    S.close()
+
+
 def test_deterministic():
     b = gen.make_config(2, batch=32)
     g1, g2 = run_gpu(b), run_gpu(b)

@@ -26,7 +26,7 @@
  *     device staging buffers and the call returns after the results are back
  *     in host memory.  QP_MEM_HOST_ASYNC: as QP_MEM_HOST, but the calls only
  *     enqueue their copies and kernels on the ctx stream (and, on path 1, its
- *     four chunk streams, joined back into the ctx stream); host outputs are
+ *     eight chunk streams, joined back into the ctx stream); host outputs are
  *     valid, and host inputs may be modified, once the ctx stream has been
  *     synchronised.  A backward call may then start on the problems whose
  *     solve chunk has finished while later chunks still run.

@@ -192,7 +192,7 @@ struct qp_ctx {
   float* flops_bwd = nullptr;
   // host-memory mode, path 1: the batch runs in kPipe chunks on their own
   // streams, so chunk i's kernel overlaps chunk i+1's H2D and chunk i−1's D2H
-  static constexpr int kPipe = 4;
+  static constexpr int kPipe = 8;
   bool pipe = false;
   cudaStream_t pst[kPipe] = {};
   cudaEvent_t pev[kPipe + 1] = {};

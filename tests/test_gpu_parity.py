@@ -130,7 +130,7 @@ def test_host_memory_mode_matches_device():
 
 @pytest.mark.parametrize("cfg,B", [(2, 301), (4, 130)])
 def test_host_memory_pipelined_chunks_match_device(cfg, B):
-    """Host mode with B >= 128 runs the batch in 4 chunks on 4 streams (H2D /
+    """Host mode with B >= 128 runs the batch in 8 chunks on 8 streams (H2D /
     kernel / D2H overlap; ragged last chunk for B = 301; shared fields for
     config 4): bitwise the device-mode results."""
     b = gen.make_config(cfg, batch=B)

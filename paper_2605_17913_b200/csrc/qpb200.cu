@@ -83,12 +83,16 @@ Layout make_layout(int n, int m, int p, int formulation) {
   // ever eliminates constraints far from active.  More co-resident problems
   // per SM is what pays on these latency-bound kernels.
   bool fit = false;
-  if (L.N4max <= 256 && env_cap < 0 && !getenv("QPB200_FORCE_GLOBAL")) {
+  // Shapes whose worst case exceeds 256 rows also take path 1 when the
+  // capped buffer fits at least 2 CTAs per SM (e.g. the Bézier workloads);
+  // otherwise the large-N kernels (tensor-core assembly) are the better fit.
+  if (env_cap < 0 && !getenv("QPB200_FORCE_GLOBAL")) {
     const int need = std::min(L.Nmax, L.n4 + std::min(p, L.n4) + m);
     const int want[4] = {4, 3, 2, 1};
     for (int w : want) {
       if (env_ctas && w != env_ctas) continue;
-      int ncap = L.Nmax;
+      if (L.N4max > 256 && w < 2) continue;
+      int ncap = std::min(L.Nmax, 256);
       while (ncap >= need && path1_smem(L, m, p, ncap) > budget(w)) --ncap;
       if (ncap < need) continue;
       if (ncap < L.Nmax && getenv("QPB200_NO_PCAP")) continue;  // A/B: worst case only

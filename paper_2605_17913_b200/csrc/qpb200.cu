@@ -109,9 +109,7 @@ Layout make_layout(int n, int m, int p, int formulation) {
     // area; iterations whose reduced system is larger use the CTA's global
     // workspace (hybrid)
     L.big = true;
-    int bctas = 1;
-    if (const char* e = getenv("QPB200_BIG_CTAS")) bctas = std::max(1, std::min(2, atoi(e)));  // experiments
-    const size_t bud = budget(bctas);
+    const size_t bud = budget(1);
     int lo = 0, hi = L.Nmax;
     if (smem_for(L, m, p, 0, true) > bud) {
       lo = 0;  // vectors alone do not fit: qp_create reports QP_ERR_SHAPE
@@ -124,7 +122,7 @@ Layout make_layout(int n, int m, int p, int formulation) {
     L.ncap = lo;
     if (env_cap >= 0) L.ncap = std::min(env_cap, L.ncap);
     if (getenv("QPB200_FORCE_GLOBAL")) L.ncap = 0;
-    L.threads = 256; L.minb = bctas;
+    L.threads = 256; L.minb = 1;
   }
   if (const char* e = getenv("QPB200_THREADS"); e && !L.big) L.threads = atoi(e);  // experiments: 128|256
   L.ksmem = L.ncap > 0 ? qpb::KLayout::make(L.ncap, L.n4).size() : 0;
@@ -143,10 +141,7 @@ KernelSet pick_kernels(const Layout& L, int formulation) {
     if (L.big) return {0, nullptr, nullptr};
     return {128, qpb::xpm_solve_kernel<128, 1>, qpb::xpm_backward_kernel<128, 1>};
   }
-  if (L.big) {
-    if (L.minb == 2) return {256, qpb::ipm_kernel<256, 2, true>, qpb::ipm_kernel<256, 2, true>};
-    return {256, qpb::ipm_kernel<256, 1, true>, qpb::ipm_kernel<256, 1, true>};
-  }
+  if (L.big) return {256, qpb::ipm_kernel<256, 1, true>, qpb::ipm_kernel<256, 1, true>};
   switch (L.minb) {
     case 4: return {128, qpb::ipm_kernel<128, 4, false>, qpb::ipm_kernel<128, 4, false>};
     case 3: return {128, qpb::ipm_kernel<128, 3, false>, qpb::ipm_kernel<128, 3, false>};

@@ -202,11 +202,11 @@ __device__ __forceinline__ void invert_diag_block(float* __restrict__ K, const K
 // A pivot on the wrong side of ±θ is replaced by ±θ (reading Q12) and
 // counted.  On exit K holds L (M = L S Lᵀ) and rinv[k] = 1/L[k][k].
 // ------------------------------------------------------------------------
-template <int NT, bool TAB = false>
+template <int NT, bool TAB = false, int MAXN4 = 256>
 __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float theta, float* __restrict__ rinv,
                          int* __restrict__ flag, float* __restrict__ colT, const int* __restrict__ tab = nullptr) {
   constexpr int NW = NT / 32;
-  constexpr int RPT = (256 + NT - 1) / NT;  // rows per thread (N4 ≤ 256)
+  constexpr int RPT = (MAXN4 + NT - 1) / NT;  // rows per thread (N4 ≤ MAXN4)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int N4 = L.N4, npos = L.npos;
   int nfloor = 0;

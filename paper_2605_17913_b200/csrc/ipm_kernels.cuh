@@ -171,7 +171,7 @@ __device__ __forceinline__ float* kkt_ptr(const Smem& S, const Args& a, const KL
 
 // factor_qd keeps up to 256/NT panel rows per thread in registers; larger
 // systems stream their panel rows (factor_big).
-template <int NT, bool BIG>
+template <int NT, bool BIG, int MAXN4 = 256>
 __device__ __forceinline__ int factor_any(float* K, const Smem& S, const KLayout& L, float theta) {
   if constexpr (BIG) {
     // large N: tensor-core left-looking panels (QPB200_NO_TC_FACTOR: FP32 factor_big, for A/B)
@@ -182,7 +182,7 @@ __device__ __forceinline__ int factor_any(float* K, const Smem& S, const KLayout
 #endif
   }
   if constexpr (BIG) return factor_qd<NT>(K, L, theta, S.rinv, S.flag, S.scr);
-  else return factor_qd<NT, true>(K, L, theta, S.rinv, S.flag, S.scr, S.ro);
+  else return factor_qd<NT, true, MAXN4>(K, L, theta, S.rinv, S.flag, S.scr, S.ro);
 }
 
 struct Prob {
@@ -709,7 +709,7 @@ __device__ void write_gradients(const Smem& S, const Args& a, const int bid) {
 //     at the relaxed point, as in factor-then-check (Q6).
 // assemble / factor / solve_qd have ONE call site.
 // ------------------------------------------------------------------------
-template <int NT, bool BIG>
+template <int NT, bool BIG, int MAXN4 = 256>
 __device__ __forceinline__ void ipm_problem(const Args& a, const Smem& S, const int bid, const bool bwd,
                                             const bool lost = false) {
   const int tid = threadIdx.x;
@@ -784,7 +784,7 @@ __device__ __forceinline__ void ipm_problem(const Args& a, const Smem& S, const 
     fl += iter_flops(n, m, p, pa, !init, true, true);
     const float dmax = assemble<NT, BIG>(K, S, a, P, L, pa, S.om, cw, ev);
     long long t1 = clock64(); tph[1] += t1 - t0; t0 = t1;
-    factor_any<NT, BIG>(K, S, L, a.floor_rel * dmax);
+    factor_any<NT, BIG, MAXN4>(K, S, L, a.floor_rel * dmax);
     t1 = clock64(); tph[2] += t1 - t0; t0 = t1;
     if (adj) {
       // Algorithm 3: reduced system with right-hand side (−∇ₓℓ, 0, 0)
@@ -876,13 +876,16 @@ __device__ __forceinline__ void ipm_problem(const Args& a, const Smem& S, const 
 
 // ------------------------------------------------------------------------
 // The kernel: persistent CTAs, problems handed out by next_problem.
+// NT = 128 (path 1, reduced systems ≤ MAXN4 = 256 rows), NT = 256 (large-N
+// kernels), NT = 64 (small-n path: two warps own one QP, systems ≤ 64 rows,
+// up to 8 problems per SM).
 // a.bwd = 0: solve launch (qp_solve_batched); each finished problem is
 //   published in done[b] = epoch (release).
 // a.bwd = 1: backward launch (qp_backward_batched), possibly started while
 //   the solve grid drains (programmatic stream serialisation): each problem
 //   first waits for done[b] == epoch.
 // ------------------------------------------------------------------------
-template <int NT, int MINB, bool BIG>
+template <int NT, int MINB, bool BIG, int MAXN4 = 256>
 __global__ void __launch_bounds__(NT, MINB) ipm_kernel(const Args a) {
   extern __shared__ __align__(16) float smem[];
   const Smem S = carve(smem, a);
@@ -910,7 +913,7 @@ __global__ void __launch_bounds__(NT, MINB) ipm_kernel(const Args a) {
       lost = __syncthreads_or(lost);
     }
     if (a.tl && threadIdx.x == 0) { a.tl[3 * bid] = smid(); a.tl[3 * bid + 1] = gtimer(); }
-    ipm_problem<NT, BIG>(a, S, bid, bwd, lost);  // ends with a barrier after the output stores
+    ipm_problem<NT, BIG, MAXN4>(a, S, bid, bwd, lost);  // ends with a barrier after the output stores
     if (a.tl && threadIdx.x == 0) a.tl[3 * bid + 2] = gtimer();
     if (!bwd && a.done && threadIdx.x == 0)  // release (cumulative through the barrier): outputs before the flag
       asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(a.done + bid), "r"(a.epoch) : "memory");

@@ -57,7 +57,7 @@ size_t smem_for(const Layout& L, int m, int p, int ncap, bool big) {
 // Shared-memory budget per CTA (dynamic part) for `ctas` CTAs per SM.
 size_t budget(int ctas) { return std::min(kMaxSmem, (size_t)(233472 / ctas) - 1024); }
 
-Layout make_layout(int n, int m, int p, int formulation) {
+Layout make_layout(int n, int m, int p, int formulation, int batch = 0, int sms = 148) {
   Layout L;
   L.n4 = (n + 3) & ~3;
   // implicit: reduced system n4 + |A| + m with |A| <= p; standard arm: every
@@ -83,10 +83,31 @@ Layout make_layout(int n, int m, int p, int formulation) {
   // ever eliminates constraints far from active.  More co-resident problems
   // per SM is what pays on these latency-bound kernels.
   bool fit = false;
+  // Small n (the kept set capped, reading Q12c, so that every reduced system
+  // has at most 64 rows) and a batch larger than the 4 CTAs/SM of path 1
+  // hold: 64-thread CTAs (two warps per QP, one panel row per thread), up to
+  // 8 per SM (128 registers per thread), so twice as many problems are in
+  // flight.  Measured (one B200, 4096 problems): cbf7 620 K → 744 K QP/s,
+  // cbf9 464 K → 571 K; one warp per QP (16 per SM) 726 K / 482 K.
+  if (formulation != QP_EXPLICIT && env_cap < 0 && !getenv("QPB200_FORCE_GLOBAL") && !getenv("QPB200_NO_SMALL") &&
+      env_ctas == 0 && batch > 4 * sms) {
+    const int need = std::min(L.Nmax, L.n4 + std::min(p, L.n4) + m);
+    const int ncap = std::min(L.Nmax, 64);
+    if (need <= ncap) {
+      const size_t sm = path1_smem(L, m, p, ncap);
+      const int ctas = std::min<int>(8, (int)(233472 / (sm + 1024)));
+      if (ctas >= 6) {
+        L.threads = 64; L.minb = 8; L.ncap = ncap; fit = true;
+        L.pcap = std::min(p, ncap - L.n4 - m);
+        if (const char* e = getenv("QPB200_PCAP")) L.pcap = std::max(0, std::min(L.pcap, atoi(e)));  // tests
+        L.N4max = (ncap + 3) & ~3;
+      }
+    }
+  }
   // Shapes whose worst case exceeds 256 rows also take path 1 when the
   // capped buffer fits at least 2 CTAs per SM (e.g. the Bézier workloads);
   // otherwise the large-N kernels (tensor-core assembly) are the better fit.
-  if (env_cap < 0 && !getenv("QPB200_FORCE_GLOBAL")) {
+  if (!fit && env_cap < 0 && !getenv("QPB200_FORCE_GLOBAL")) {
     const int need = std::min(L.Nmax, L.n4 + std::min(p, L.n4) + m);
     const int want[4] = {4, 3, 2, 1};
     for (int w : want) {
@@ -124,7 +145,6 @@ Layout make_layout(int n, int m, int p, int formulation) {
     if (getenv("QPB200_FORCE_GLOBAL")) L.ncap = 0;
     L.threads = 256; L.minb = 1;
   }
-  if (const char* e = getenv("QPB200_THREADS"); e && !L.big) L.threads = atoi(e);  // experiments: 128|256
   L.ksmem = L.ncap > 0 ? qpb::KLayout::make(L.ncap, L.n4).size() : 0;
   L.smem = qpb::ipm_smem_bytes(L.n4, m, p, L.N4max, L.ksmem, tc_floats(L.big), ro_ints(L, L.big));
   return L;
@@ -142,6 +162,7 @@ KernelSet pick_kernels(const Layout& L, int formulation) {
     return {128, qpb::xpm_solve_kernel<128, 1>, qpb::xpm_backward_kernel<128, 1>};
   }
   if (L.big) return {256, qpb::ipm_kernel<256, 1, true>, qpb::ipm_kernel<256, 1, true>};
+  if (L.threads == 64) return {64, qpb::ipm_kernel<64, 8, false, 64>, qpb::ipm_kernel<64, 8, false, 64>};
   switch (L.minb) {
     case 4: return {128, qpb::ipm_kernel<128, 4, false>, qpb::ipm_kernel<128, 4, false>};
     case 3: return {128, qpb::ipm_kernel<128, 3, false>, qpb::ipm_kernel<128, 3, false>};
@@ -350,6 +371,11 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) return QP_ERR_CUDA;
   if (cudaSetDevice(device) != cudaSuccess) return QP_ERR_CUDA;
+  {
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return QP_ERR_CUDA;
+    L = make_layout(d->n, d->m_eq, d->p, c.formulation, d->batch, sms);
+  }
   qp_ctx* ctx = new (std::nothrow) qp_ctx();
   if (!ctx) return QP_ERR_OOM;
   ctx->d = *d; ctx->c = c; ctx->device = device; ctx->stream = static_cast<cudaStream_t>(stream); ctx->L = L;

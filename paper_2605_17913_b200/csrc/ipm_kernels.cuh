@@ -17,6 +17,8 @@
 // off A: every entry stays bounded (the property the paper's method rests
 // on), and the size drops from n+p+m to n+|A|+m.
 #pragma once
+#include <type_traits>
+
 #include "ipm_cta.cuh"
 #include "tc_factor.cuh"
 #include "tc_syrk.cuh"
@@ -346,44 +348,56 @@ __device__ float assemble(float* K, const Smem& S, const Args& a, const Prob& P,
         const int i = i0 + u, j = j0 + w;
         acc[u][w] = (i < n && j < n) ? __ldg(P.Q + i * n + j) : (i == j ? 1.f : 0.f);
       }
-    // 4 rows of G in flight per step (loads issued before the FMAs)
-    int k = 0;
-    for (; k + 4 <= p; k += 4) {
-      float gi[4][4], gj[4][4];
+    // 4 rows of G in flight per step (loads issued before the FMAs); for even
+    // n the rows are 8-byte aligned and each 4-wide strip is two float2 loads
+    auto kloop = [&](auto even_t) {
+      constexpr bool EVEN = decltype(even_t)::value;
+      auto ld4 = [&](const float* g, int c0, float (&o)[4]) {
+        if constexpr (EVEN) {  // c0 % 4 == 0, n even: c0 < n ⇒ c0 + 1 < n
+          const float2 a = c0 < n ? __ldg(reinterpret_cast<const float2*>(g + c0)) : make_float2(0.f, 0.f);
+          const float2 b = c0 + 2 < n ? __ldg(reinterpret_cast<const float2*>(g + c0 + 2)) : make_float2(0.f, 0.f);
+          o[0] = a.x; o[1] = a.y; o[2] = b.x; o[3] = b.y;
+        } else {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float* g = P.G + (k + q) * n;
+          for (int u = 0; u < 4; ++u) o[u] = c0 + u < n ? __ldg(g + c0 + u) : 0.f;
+        }
+      };
+      int k = 0;
+      for (; k + 4 <= p; k += 4) {
+        float gi[4][4], gj[4][4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          gi[q][u] = i0 + u < n ? __ldg(g + i0 + u) : 0.f;
-          gj[q][u] = j0 + u < n ? __ldg(g + j0 + u) : 0.f;
+        for (int q = 0; q < 4; ++q) {
+          const float* g = P.G + (k + q) * n;
+          ld4(g, i0, gi[q]);
+          ld4(g, j0, gj[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float w = om[k + q];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) gj[q][u] *= w;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int w2 = 0; w2 < 4; ++w2) acc[u][w2] = fmaf(gi[q][u], gj[q][w2], acc[u][w2]);
         }
       }
+      for (; k < p; ++k) {
+        const float* g = P.G + k * n;
+        const float w = om[k];
+        float gi[4], gj[4];
+        ld4(g, i0, gi);
+        ld4(g, j0, gj);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float w = om[k + q];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) gj[q][u] *= w;
+        for (int u = 0; u < 4; ++u) gj[u] *= w;
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
-          for (int w2 = 0; w2 < 4; ++w2) acc[u][w2] = fmaf(gi[q][u], gj[q][w2], acc[u][w2]);
+          for (int w2 = 0; w2 < 4; ++w2) acc[u][w2] = fmaf(gi[u], gj[w2], acc[u][w2]);
       }
-    }
-    for (; k < p; ++k) {
-      const float* g = P.G + k * n;
-      const float w = om[k];
-      float gi[4], gj[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        gi[u] = i0 + u < n ? __ldg(g + i0 + u) : 0.f;
-        gj[u] = j0 + u < n ? w * __ldg(g + j0 + u) : 0.f;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int w2 = 0; w2 < 4; ++w2) acc[u][w2] = fmaf(gi[u], gj[w2], acc[u][w2]);
-    }
+    };
+    if ((n & 1) == 0) kloop(std::true_type{});
+    else kloop(std::false_type{});
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       float* row = K + row_off<!TC>(L, S.ro, i0 + u) + j0;

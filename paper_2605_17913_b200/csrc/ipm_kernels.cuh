@@ -278,6 +278,10 @@ __device__ float assemble(float* K, const Smem& S, const Args& a, const Prob& P,
     // (path 1 keeps one: measured 1.5 % faster there)
     constexpr int UB = TC ? 4 : 1;
     const int tot = nrow * n;
+    // (row, column) of this thread's element, advanced by NT elements per
+    // step without a division: NT = drr rows + dj columns
+    const int drr = NT / n, dj = NT - drr * n;
+    int rr = tid / n, j = tid - rr * n;
     for (int base = 0; base < tot; base += UB * NT) {
       float val[UB];
       int dst[UB];
@@ -287,7 +291,6 @@ __device__ float assemble(float* K, const Smem& S, const Args& a, const Prob& P,
         dst[u] = -1;
         val[u] = 0.f;
         if (idx < tot) {
-          const int rr = idx / n, j = idx - rr * n;
           if (rr < pa) {
             const int k = S.act[rr];
             val[u] = cw[k] * __ldg(P.G + k * n + j);
@@ -296,6 +299,8 @@ __device__ float assemble(float* K, const Smem& S, const Args& a, const Prob& P,
           }
           dst[u] = row_off<!TC>(L, S.ro, n4 + rr) + j;
         }
+        rr += drr; j += dj;
+        if (j >= n) { j -= n; ++rr; }
       }
 #pragma unroll
       for (int u = 0; u < UB; ++u)
@@ -678,28 +683,25 @@ __device__ void write_gradients(const Smem& S, const Args& a, const int bid) {
   const int tid = threadIdx.x;
   const int n = a.n, p = a.p, m = a.m;
   const long long bb = bid;
+  // (row, column) of element e = tid + s·NT advanced without a division
+  const int drr = NT / n, dj = NT - drr * n, r0 = tid / n, j0 = tid - r0 * n;
+  auto adv = [&](int& r, int& j) { r += drr; j += dj; if (j >= n) { j -= n; ++r; } };
   if (a.gQ) {
     float* o = a.gQ + bb * n * n;
-    for (int e = tid; e < n * n; e += NT) {
-      const int i = e / n, j = e - i * n;
-      o[e] = 0.5f * (S.dx[i] * S.x[j] + S.x[i] * S.dx[j]);
-    }
+    int i = r0, j = j0;
+    for (int e = tid; e < n * n; e += NT, adv(i, j)) o[e] = 0.5f * (S.dx[i] * S.x[j] + S.x[i] * S.dx[j]);
   }
   if (a.gq) for (int j = tid; j < n; j += NT) a.gq[bb * n + j] = S.dx[j];
   if (a.gA) {
     float* o = a.gA + bb * m * n;
-    for (int e = tid; e < m * n; e += NT) {
-      const int l = e / n, j = e - l * n;
-      o[e] = S.dy[l] * S.x[j] + S.y[l] * S.dx[j];
-    }
+    int l = r0, j = j0;
+    for (int e = tid; e < m * n; e += NT, adv(l, j)) o[e] = S.dy[l] * S.x[j] + S.y[l] * S.dx[j];
   }
   if (a.gb) for (int l = tid; l < m; l += NT) a.gb[bb * m + l] = -S.dy[l];
   if (a.gG) {
     float* o = a.gG + bb * p * n;
-    for (int e = tid; e < p * n; e += NT) {
-      const int i = e / n, j = e - i * n;
-      o[e] = S.dz[i] * S.x[j] + S.z[i] * S.dx[j];
-    }
+    int i = r0, j = j0;
+    for (int e = tid; e < p * n; e += NT, adv(i, j)) o[e] = S.dz[i] * S.x[j] + S.z[i] * S.dx[j];
   }
   if (a.gh) for (int i = tid; i < p; i += NT) a.gh[bb * p + i] = -S.dz[i];
   if (a.wx) {

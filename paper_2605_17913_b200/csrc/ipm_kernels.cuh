@@ -892,8 +892,8 @@ __device__ __forceinline__ void ipm_problem(const Args& a, const Smem& S, const 
 
 // ------------------------------------------------------------------------
 // The kernel: persistent CTAs, problems handed out by next_problem.
-// NT = 128 (path 1, reduced systems ≤ MAXN4 = 256 rows), NT = 256 (large-N
-// kernels), NT = 64 (small-n path: two warps own one QP, systems ≤ 64 rows,
+// NT = 128 (path 1 at 3-4 CTAs/SM, reduced systems ≤ MAXN4 = 256 rows),
+// NT = 256 (path 1 at 1-2 CTAs/SM, and the large-N kernels), NT = 64 (small-n path: two warps own one QP, systems ≤ 64 rows,
 // up to 8 problems per SM).
 // a.bwd = 0: solve launch (qp_solve_batched); each finished problem is
 //   published in done[b] = epoch (release).

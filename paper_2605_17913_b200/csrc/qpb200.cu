@@ -105,14 +105,15 @@ Layout make_layout(int n, int m, int p, int formulation, int batch = 0, int sms 
     }
   }
   // Shapes whose worst case exceeds 256 rows also take path 1 when the
-  // capped buffer fits at least 2 CTAs per SM (e.g. the Bézier workloads);
-  // otherwise the large-N kernels (tensor-core assembly) are the better fit.
+  // capped buffer (≤ 256 rows) still holds n4 + min(p, n4) + m (bezier4:
+  // 110 K → 255 K QP/s at 4 CTAs/SM; bezier8: 25.6 K → 32.2 K at 1 CTA/SM of
+  // 256 threads, against the large-N kernels); only larger systems need the
+  // large-N kernels.
   if (!fit && env_cap < 0 && !getenv("QPB200_FORCE_GLOBAL")) {
     const int need = std::min(L.Nmax, L.n4 + std::min(p, L.n4) + m);
     const int want[4] = {4, 3, 2, 1};
     for (int w : want) {
       if (env_ctas && w != env_ctas) continue;
-      if (L.N4max > 256 && w < 2) continue;
       int ncap = std::min(L.Nmax, 256);
       while (ncap >= need && path1_smem(L, m, p, ncap) > budget(w)) --ncap;
       if (ncap < need) continue;
@@ -121,6 +122,9 @@ Layout make_layout(int n, int m, int p, int formulation, int batch = 0, int sms 
       L.pcap = formulation == QP_EXPLICIT ? p : std::min(p, ncap - L.n4 - m);
       if (const char* e = getenv("QPB200_PCAP")) L.pcap = std::max(0, std::min(L.pcap, atoi(e)));  // tests
       L.N4max = (ncap + 3) & ~3;
+      // at ≤ 2 CTAs/SM the registers allow 256 threads per QP (128 per thread
+      // at 2 CTAs): config 3 73 K → 89 K QP/s
+      if (w <= 2) L.threads = 256;
       break;
     }
   }
@@ -163,6 +167,8 @@ KernelSet pick_kernels(const Layout& L, int formulation) {
   }
   if (L.big) return {256, qpb::ipm_kernel<256, 1, true>, qpb::ipm_kernel<256, 1, true>};
   if (L.threads == 64) return {64, qpb::ipm_kernel<64, 8, false, 64>, qpb::ipm_kernel<64, 8, false, 64>};
+  if (L.threads == 256 && L.minb == 2) return {256, qpb::ipm_kernel<256, 2, false>, qpb::ipm_kernel<256, 2, false>};
+  if (L.threads == 256) return {256, qpb::ipm_kernel<256, 1, false>, qpb::ipm_kernel<256, 1, false>};
   switch (L.minb) {
     case 4: return {128, qpb::ipm_kernel<128, 4, false>, qpb::ipm_kernel<128, 4, false>};
     case 3: return {128, qpb::ipm_kernel<128, 3, false>, qpb::ipm_kernel<128, 3, false>};

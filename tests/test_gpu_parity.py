@@ -181,9 +181,10 @@ def test_zero_cotangent():
 
 
 def test_large_n_global_path():
-    """Path 2 (KKT in a global workspace): n=120, m=4, p=200 does not fit the
-    shared-memory budget."""
-    b = gen.g_rand(13, 8, 120, 4, 200)
+    """Large-N kernels (KKT in shared memory when it fits, else in a global
+    workspace): n=130, m=4, p=200 needs more than the 256 rows path 1 holds
+    (n4 + min(p, n4) + m = 266)."""
+    b = gen.g_rand(13, 8, 130, 4, 200)
     g = run_gpu(b)
     assert g["info"]["path"] in (2, 3)
     check_against_oracle(b, g)

@@ -328,7 +328,7 @@ def test_cfg4_full_size_sampled_and_batch_sums():
         assert err <= 1e-5, (k, err)
 
 
-@pytest.mark.parametrize("cfg,batch", [(2, 200), (3, 48), (None, 2)])
+@pytest.mark.parametrize("cfg,batch", [(2, 200), (3, 48), (None, 2), ("cbf7", 1024)])
 def test_backward_overlapping_solve(cfg, batch):
     """qp_backward_batched launched right behind qp_solve_batched on the same
     stream (no host synchronisation: on path 1 the backward grid starts while
@@ -337,7 +337,10 @@ def test_backward_overlapping_solve(cfg, batch):
     the two calls; two consecutive steps (epochs) as well."""
     import torch
     from paper_2605_17913_b200.solver import QPSolver
-    b = gen.make_config(cfg, batch=batch) if cfg else gen.g_rand(2, 2, 130, 0, 200)
+    if isinstance(cfg, str):
+        b = gen.make_workload(cfg, batch=batch)  # small-n path (64-thread CTAs)
+    else:
+        b = gen.make_config(cfg, batch=batch) if cfg else gen.g_rand(2, 2, 130, 0, 200)
     S = QPSolver(b.batch, b.n, b.m, b.p, device=0)
     data = [torch.from_numpy(np.ascontiguousarray(getattr(b, f))).cuda() for f in ("Q", "q", "A", "b", "G", "h")]
     dl = torch.from_numpy(b.dl_dx).cuda()

@@ -159,3 +159,24 @@ def test_explicit_f32_breaks_down_implicit_does_not(orc):
     assert fails.sum() >= 3
     stages = set((rx["status"][fails] >> 8).tolist())
     assert stages <= {2, 4, 5}  # predictor / corrector / line search
+
+
+@pytest.mark.parametrize("cap", [52, 60, 78])
+def test_capped_partition_same_solution_f64(orc, cap):
+    """Reading Q12c end to end: with at most `cap` ≥ n constraints kept in
+    augmented form (the rest eliminated with weight d+/d-) every Newton step
+    is the same exact step (pinned against dense Eq. 13), so the f64 solve
+    with the partitioned solver lands on the same x*, and the relaxed
+    gradients agree, as without the cap (the paper-literal Eq. 14 solver)."""
+    b = gen.make_config(2, batch=6)
+    ref = orc.solve(b, orc.Cfg.f64(), "f64")
+    gref = orc.backward(b, ref, orc.Cfg.f64(), "f64")
+    c = orc.Cfg.f64(kkt_solver=orc.SOLVER_M_PART, partition_cap=cap)
+    r = orc.solve(b, c, "f64")
+    g = orc.backward(b, r, c, "f64")
+    assert np.all(r["status"] == 0) and np.all(g["status"] == 0)
+    assert np.abs(r["x"] - ref["x"]).max() <= 1e-8 * max(1.0, np.abs(ref["x"]).max())
+    for k in ("dQ", "dq", "dG", "dh"):
+        a, e = g[k].reshape(6, -1), gref[k].reshape(6, -1)
+        err = np.linalg.norm(a - e, axis=1) / np.maximum(np.linalg.norm(e, axis=1), 1e-30)
+        assert err.max() <= 1e-7, (k, err.max())

@@ -63,6 +63,12 @@ def test_validation_without_gpu(lib):
     # 227 KB of shared memory for the per-constraint vectors alone
     big = capi.QpDims(4, 1024, 0, 8192, 1024 * 1024, 1024, 0, 0, 8192 * 1024, 8192)
     assert lib.qp_create(C.byref(h), C.byref(big), C.byref(cfg), 0, None) == -2
+    # mem_kind: QP_MEM_DEVICE / QP_MEM_HOST / QP_MEM_HOST_ASYNC pass validation
+    # (then fail on the missing device), anything else is an invalid config
+    for mk, want in ((capi.QP_MEM_HOST_ASYNC, -4), (3, -1)):
+        cfg.mem_kind = mk
+        assert lib.qp_create(C.byref(h), C.byref(good), C.byref(cfg), 0, None) == want, mk
+    cfg = capi.default_config()
     assert lib.qp_error_string(-4) == b"CUDA error"
     assert lib.qp_solve_batched(*([None] * 13)) == -1
     assert lib.qp_backward_batched(*([None] * 10)) == -1

@@ -542,6 +542,7 @@ qp_err qp_solve_batched(qp_ctx* c, const float* Q, const float* q, const float* 
   if (c->prof) {
     unsigned long long z[4] = {0, 0, 0, 0};
     cudaMemcpyToSymbolAsync(qpb::g_fac_cycles, z, sizeof(z), 0, cudaMemcpyHostToDevice, c->stream);
+    cudaMemcpyToSymbolAsync(qpb::g_tcf_cycles, z, sizeof(z), 0, cudaMemcpyHostToDevice, c->stream);
   }
   a.prof = c->prof;
   a.flops = c->flops_solve;
@@ -618,6 +619,10 @@ qp_err qp_solve_batched(qp_ctx* c, const float* Q, const float* q, const float* 
     cudaMemcpyFromSymbol(fc, qpb::g_fac_cycles, sizeof(fc));
     if (fc[3]) fprintf(stderr, "[qpb200 factor sub-phases per factorisation] panel %.0f syrk %.0f inverses %.0f\n",
                        (double)fc[0] / fc[3], (double)fc[1] / fc[3], (double)fc[2] / fc[3]);
+    cudaMemcpyFromSymbol(fc, qpb::g_tcf_cycles, sizeof(fc));
+    if (fc[3])
+      fprintf(stderr, "[qpb200 tensor-core factorisations: %llu] tc updates %.0f panels %.0f inverses %.0f cycles each\n",
+              fc[3], (double)fc[0] / fc[3], (double)fc[1] / fc[3], (double)fc[2] / fc[3]);
   }
   return QP_OK;
 }

@@ -22,6 +22,7 @@
 namespace qpb {
 
 __device__ int g_tc_w;  // panel width override (QPB200_TC_W experiments; 0 = default)
+__device__ unsigned long long g_tcf_cycles[4];  // diagnostics: tensor-core updates, panels, inverses, count
 
 // kind::tf32 instruction descriptor for M = 128, N = nn (multiple of 16, ≤ 256)
 __device__ __forceinline__ uint32_t tc_idesc_n(int nn) {
@@ -35,6 +36,7 @@ __device__ void tc_left_update(const tc::TcState& s, float* __restrict__ K, cons
   using namespace tc;
   constexpr int UA = (TK / 4) * TM / NT;   // A units (one row, 4 consecutive k) per thread
   constexpr int UB = (TK / 4) * 128 / NT;  // B units per thread (w ≤ 128)
+  constexpr int PF = 3;                     // L2 prefetch distance in K chunks
   const int tid = threadIdx.x;
   const int N4 = L.N4, npos = L.npos;
   const uint32_t tmem = *s.tmem_slot;
@@ -54,6 +56,24 @@ __device__ void tc_left_update(const tc::TcState& s, float* __restrict__ K, cons
       const int j = c0 + c, k = k0 + 4 * kc;
       rb[u] = (kc < TK / 4 && j < N4 && k < c0) ? *reinterpret_cast<const float4*>(K + L.off(j) + k)
                                                 : make_float4(0, 0, 0, 0);
+    }
+  };
+  // the operand rows of chunk k0 into L2 (the workspace of a large system does
+  // not stay L2-resident: config 5's is 19 MB per CTA)
+  auto prefetch = [&](int k0) {
+#pragma unroll
+    for (int u = 0; u < UA; ++u) {
+      const int unit = tid + u * NT, kc = unit / TM, m = unit - kc * TM;
+      const int i = i0 + m, k = k0 + 4 * kc;
+      if (i < N4 && k < c0 && (k & 31) == 0)  // one prefetch per 128-B row segment
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(K + L.off(i) + k));
+    }
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      const int unit = tid + u * NT, kc = unit / w, c = unit - kc * w;
+      const int j = c0 + c, k = k0 + 4 * kc;
+      if (kc < TK / 4 && j < N4 && k < c0 && (k & 31) == 0)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(K + L.off(j) + k));
     }
   };
   auto split = [](float4 v, float4& hi, float4& lo) {
@@ -105,6 +125,7 @@ __device__ void tc_left_update(const tc::TcState& s, float* __restrict__ K, cons
       commit(s.mbar);
     }
     if (k0 + TK < c0) load(k0 + TK);  // overlaps the MMAs of this chunk
+    if (k0 + PF * TK < c0) prefetch(k0 + PF * TK);  // L2 prefetch PF chunks ahead (no registers held)
     mbar_wait(s.mbar, phase);
     phase ^= 1u;
     tc_fence_after();
@@ -148,15 +169,24 @@ __device__ int factor_tc(float* __restrict__ K, const KLayout& L, const float th
   const int N4 = L.N4;
   const int w = g_tc_w > 0 ? g_tc_w : 64;  // measured: config 4 best at 64 (16: -20 %, 32: -5 %), config 5 flat for 64-128
   int nfloor = 0;
+  long long t0 = clock64(), tup = 0, tpan = 0;
   for (int c0 = 0; c0 < N4; c0 += w) {
     const int c1 = c0 + w < N4 ? c0 + w : N4;
     if (c0 > 0) {
       const int wn = (c1 - c0 + 15) & ~15;  // MMA N (columns ≥ N4 are zero)
       for (int i0 = c0; i0 < N4; i0 += tc::TM) tc_left_update<NT>(ts, K, L, c0, wn, i0);
     }
+    { const long long t = clock64(); tup += t - t0; t0 = t; }
     nfloor += factor_big_range<NT>(K, L, theta, rinv, scr, c0, c1);
+    { const long long t = clock64(); tpan += t - t0; t0 = t; }
   }
   for (int b = threadIdx.x >> 5; b < L.NB; b += NT / 32) invert_diag_block(K, L, b, rinv);
+  if (threadIdx.x == 0 && g_fac_on) {  // diagnostics (QPB200_PHASE_PROFILE)
+    atomicAdd(&g_tcf_cycles[0], (unsigned long long)tup);
+    atomicAdd(&g_tcf_cycles[1], (unsigned long long)tpan);
+    atomicAdd(&g_tcf_cycles[2], (unsigned long long)(clock64() - t0));
+    atomicAdd(&g_tcf_cycles[3], 1ull);
+  }
   if (threadIdx.x == 0) *flag = nfloor;
   __syncthreads();
   const int r = *flag;

@@ -234,6 +234,18 @@ __device__ void syrk_tile(const TcState& s, const float* __restrict__ G, const f
       commit(s.mbar);
     }
     if (k0 + TK < p) load(k0 + TK);  // overlaps the MMAs of this chunk
+    {
+      // L2 prefetch of the G rows 3 chunks ahead (config 5's G, 8 MB per
+      // problem, does not stay in L2): 32 rows × (4 + 4) 128-B lines of the
+      // i0 and j0 column ranges, one line per thread and round
+      const int kp = k0 + 3 * TK;
+#pragma unroll
+      for (int e = tid; e < TK * 8; e += NT) {
+        const int r = e >> 3, sg = e & 7;
+        const int k = kp + r, c = (sg < 4 ? i0 : j0) + 32 * (sg & 3);
+        if (k < p && c < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(G + (size_t)k * n + c));
+      }
+    }
     mbar_wait(s.mbar, phase);
     phase ^= 1u;
     tc_fence_after();

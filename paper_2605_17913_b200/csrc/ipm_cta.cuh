@@ -429,8 +429,20 @@ __device__ int factor_qd(float* __restrict__ K, const KLayout& L, const float th
 // every row below them, and the trailing update touches only columns < c1
 // (factor_tc's tensor-core left-looking update brings later columns up to
 // date).  Returns the number of floored pivots (thread 0's count).
-template <int NT>
-__device__ int factor_big_range(float* __restrict__ K, const KLayout& L, const float theta, float* __restrict__ rinv,
+// A column panel [c0, c0 + S') of the packed matrix copied to a dense
+// shared-memory array: row i (≥ c0) at (i − c0)·S, column j at j − c0 (the
+// caller offsets the base pointer by −c0).  Same interface as KLayout for
+// factor_big_range.
+struct PanelLayout {
+  int N4, NB, npos, c0, S;
+  KLayout base;
+  __device__ __forceinline__ int off(int i) const { return (i - c0) * S; }
+  __device__ __forceinline__ int len(int) const { return S; }
+  __device__ __forceinline__ int bw(int b) const { return base.bw(b); }
+};
+
+template <int NT, class LT = KLayout>
+__device__ int factor_big_range(float* __restrict__ K, const LT& L, const float theta, float* __restrict__ rinv,
                                 float* __restrict__ scr, const int c0, const int c1) {
   constexpr int NW = NT / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

@@ -173,12 +173,17 @@ __device__ __forceinline__ float* kkt_ptr(const Smem& S, const Args& a, const KL
 
 // factor_qd keeps up to 256/NT panel rows per thread in registers; larger
 // systems stream their panel rows (factor_big).
+// floats of the shared-memory KKT buffer (it ends where rinv starts)
+__device__ __forceinline__ int ksmem_of(const Smem& S) { return (int)(S.rinv - S.K); }
+
 template <int NT, bool BIG, int MAXN4 = 256>
 __device__ __forceinline__ int factor_any(float* K, const Smem& S, const KLayout& L, float theta) {
   if constexpr (BIG) {
     // large N: tensor-core left-looking panels (QPB200_NO_TC_FACTOR: FP32 factor_big, for A/B)
 #ifndef QPB200_NO_TC_FACTOR
-    if (L.N4 > 256) return factor_tc<NT>(K, L, theta, S.rinv, S.flag, S.scr, tc::tc_state(S.tc));
+    if (L.N4 > 256)  // K lives in the global workspace: the smem KKT buffer stages the panels
+      return factor_tc<NT>(K, L, theta, S.rinv, S.flag, S.scr, tc::tc_state(S.tc), K == S.K ? nullptr : S.K,
+                           K == S.K ? 0 : ksmem_of(S));
 #else
     if (L.N4 > 256) return factor_big<NT>(K, L, theta, S.rinv, S.flag, S.scr);
 #endif

@@ -165,7 +165,8 @@ __device__ void tc_left_update(const tc::TcState& s, float* __restrict__ K, cons
 // same output contract as factor_qd / factor_big.
 template <int NT>
 __device__ int factor_tc(float* __restrict__ K, const KLayout& L, const float theta, float* __restrict__ rinv,
-                         int* __restrict__ flag, float* __restrict__ scr, const tc::TcState& ts) {
+                         int* __restrict__ flag, float* __restrict__ scr, const tc::TcState& ts,
+                         float* __restrict__ pbuf = nullptr, int pcap = 0) {
   const int N4 = L.N4;
   const int w = g_tc_w > 0 ? g_tc_w : 64;  // measured: config 4 best at 64 (16: -20 %, 32: -5 %), config 5 flat for 64-128
   int nfloor = 0;
@@ -177,7 +178,32 @@ __device__ int factor_tc(float* __restrict__ K, const KLayout& L, const float th
       for (int i0 = c0; i0 < N4; i0 += tc::TM) tc_left_update<NT>(ts, K, L, c0, wn, i0);
     }
     { const long long t = clock64(); tup += t - t0; t0 = t; }
-    nfloor += factor_big_range<NT>(K, L, theta, rinv, scr, c0, c1);
+    // the panel's rows [c0, N4) × columns [c0, c1) are factored in shared
+    // memory when they fit the (otherwise idle: K lives in the global
+    // workspace) smem KKT buffer `pbuf`; else in place in global memory
+    constexpr int PS = 68;  // panel row stride: 64 columns + 4 (rows 16-B aligned, odd multiple of 16 B)
+    if (pbuf && c1 - c0 <= 64 && (N4 - c0) * PS <= pcap) {
+      const int nr = N4 - c0, wc = c1 - c0;
+      for (int e = threadIdx.x; e < nr * (wc >> 2); e += NT) {
+        const int r = e / (wc >> 2), q = e - r * (wc >> 2);
+        const int i = c0 + r, j = c0 + 4 * q;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (j <= i) v = *reinterpret_cast<const float4*>(K + L.off(i) + j);  // (j ≤ i: within row i)
+        *reinterpret_cast<float4*>(pbuf + r * PS + 4 * q) = v;
+      }
+      __syncthreads();
+      PanelLayout P;
+      P.N4 = L.N4; P.NB = L.NB; P.npos = L.npos; P.c0 = c0; P.S = PS; P.base = L;
+      nfloor += factor_big_range<NT>(pbuf - c0, P, theta, rinv, scr, c0, c1);
+      for (int e = threadIdx.x; e < nr * (wc >> 2); e += NT) {
+        const int r = e / (wc >> 2), q = e - r * (wc >> 2);
+        const int i = c0 + r, j = c0 + 4 * q;
+        if (j <= i) *reinterpret_cast<float4*>(K + L.off(i) + j) = *reinterpret_cast<const float4*>(pbuf + r * PS + 4 * q);
+      }
+      __syncthreads();
+    } else {
+      nfloor += factor_big_range<NT>(K, L, theta, rinv, scr, c0, c1);
+    }
     { const long long t = clock64(); tpan += t - t0; t0 = t; }
   }
   for (int b = threadIdx.x >> 5; b < L.NB; b += NT / 32) invert_diag_block(K, L, b, rinv);

@@ -11,7 +11,11 @@
 //       subtraction done in a coalesced epilogue;
 //   (2) factor the panel with factor_big_range (16-wide blocks: warp-factored
 //       diagonal block, TRSM of the rows below, FP32 trailing update confined
-//       to the panel's columns).
+//       to the panel's columns) — on a dense copy of the panel in the shared-
+//       memory KKT buffer when K lives in the global workspace and the panel
+//       fits, else in place.
+// The operand loads of both loops are backed by L2 prefetches three K chunks
+// ahead (config 5's workspace, 19 MB per CTA, does not stay in L2).
 // Traffic: each panel's update reads the rows [i][0:c0] once (≈ N³/(6w)
 // floats in total) instead of the right-looking read-modify-write of the
 // whole trailing matrix per 16 columns (≈ N³/24 floats).

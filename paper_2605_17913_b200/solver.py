@@ -44,16 +44,23 @@ class QPSolver:
         c.mem_kind = {"device": capi.QP_MEM_DEVICE, "host": capi.QP_MEM_HOST,
                       "host_async": capi.QP_MEM_HOST_ASYNC}[mem]
         self.cfg = c
+        self._saved = None
+        if batch == 0:  # empty batch: nothing to solve, no ctx (the C ABI takes B >= 1)
+            self.h = None
+            return
         stream = torch.cuda.current_stream(device).cuda_stream if mem == "device" else None
         self.h = capi.qp_create(self.dims, c, device, stream)
-        self._saved = None
 
     def info(self) -> dict:
+        if self.h is None:
+            return {}
         i = capi.qp_get_info(self.h)
         return {k: getattr(i, k) for k, _ in i._fields_}
 
     def last_flops(self):
         """(solve, backward) algorithmic flops of the last calls."""
+        if self.h is None:
+            return (0.0, 0.0)
         return capi.qp_last_flops(self.h)
 
     def close(self):
@@ -80,6 +87,9 @@ class QPSolver:
             raise ValueError(f"{f}: host mode takes CPU tensors")
 
     def _alloc(self, shape, dtype=torch.float32):
+        if self.B == 0:  # empty outputs; shared-field gradients are sums over no problems
+            dev = f"cuda:{self.device}" if self.mem == "device" else "cpu"
+            return torch.zeros(shape, dtype=dtype, device=dev)
         if self.mem == "device":
             return torch.empty(shape, dtype=dtype, device=f"cuda:{self.device}")
         return torch.empty(shape, dtype=dtype, pin_memory=True)  # no staging copy
@@ -93,13 +103,16 @@ class QPSolver:
         data = dict(Q=Q, q=q, A=A, b=b, G=G, h=h)
         for f, t in data.items():
             self._check(f, t)
-        if self.mem == "device":
+        if self.mem == "device" and self.h is not None:
             capi.qp_set_stream(self.h, torch.cuda.current_stream(self.device).cuda_stream)
         B, n, m, p = self.B, self.n, self.m, self.p
         if out is None:
             out = dict(x=self._alloc((B, n)), s=self._alloc((B, p)), z=self._alloc((B, p)), y=self._alloc((B, m)),
                        iters=self._alloc((B,), torch.int32), status=self._alloc((B,), torch.int32))
         P = self._ptr
+        if self.B == 0:
+            self._saved = (data, out)
+            return out
         capi.qp_solve_batched(self.h, *[P(data[f]) for f in FIELDS], P(out["x"]), P(out["s"]), P(out["z"]),
                               P(out["y"]), P(out["iters"]), P(out["status"]))
         self._saved = (data, out)  # keep alive for backward (C-ABI contract)
@@ -107,7 +120,7 @@ class QPSolver:
 
     def backward(self, dl_dx, out=None, need=GRADS):
         self._check_dl(dl_dx)
-        if self.mem == "device":
+        if self.mem == "device" and self.h is not None:
             capi.qp_set_stream(self.h, torch.cuda.current_stream(self.device).cuda_stream)
         if out is None:
             out = {}
@@ -117,6 +130,10 @@ class QPSolver:
             out["relax_iters"] = self._alloc((self.B,), torch.int32)
             out["status"] = self._alloc((self.B,), torch.int32)
         P = self._ptr
+        if self.B == 0:
+            if self._saved is None:
+                raise RuntimeError("QP_ERR_NOT_SOLVED: backward before solve")
+            return out
         capi.qp_backward_batched(self.h, P(dl_dx), *[P(out.get(g)) for g in GRADS], P(out["relax_iters"]),
                                  P(out["status"]))
         return out

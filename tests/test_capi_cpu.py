@@ -81,3 +81,23 @@ def test_product_path_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "qp_oracle" not in txt, f
+
+
+def test_empty_batch_binding_cpu():
+    """Degenerate case B = 0 (host buffers, no GPU needed): the binding returns
+    empty outputs without creating a ctx (the C ABI itself takes B >= 1 and
+    answers QP_ERR_SHAPE, checked above); gradients of shared fields are sums
+    over no problems, i.e. zero."""
+    import torch
+    from paper_2605_17913_b200.solver import QPSolver
+    n, m, p = 5, 2, 3
+    s = QPSolver(0, n, m, p, shared=("G", "h"), mem="host")
+    f = lambda *sh: torch.zeros(*sh, dtype=torch.float32)
+    out = s.solve(f(0, n, n), f(0, n), f(0, m, n), f(0, m), f(p, n), f(p))
+    assert out["x"].shape == (0, n) and out["z"].shape == (0, p) and out["iters"].shape == (0,)
+    g = s.backward(f(0, n))
+    assert g["dQ"].shape == (0, n, n) and g["dG"].shape == (p, n) and g["dh"].shape == (p,)
+    assert float(g["dG"].abs().sum()) == 0.0 and float(g["dh"].abs().sum()) == 0.0
+    assert s.info() == {} and s.last_flops() == (0.0, 0.0)
+    with pytest.raises(RuntimeError):
+        QPSolver(0, n, m, p, mem="host").backward(f(0, n))

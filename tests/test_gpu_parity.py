@@ -387,3 +387,20 @@ def test_small_n_path(monkeypatch, cfg_or_shape, B):
     d = np.abs(g["iters"].astype(int) - g2["iters"].astype(int))
     assert d.max() <= 2 and np.mean(d == 0) >= 0.9
     assert x_rel(g["x"], g2["x"]).max() <= 2 * TOL_X
+
+
+def test_empty_batch_device():
+    """B = 0 on the device (degenerate case): empty outputs, zero shared-field
+    gradients, no kernel launched; a B = 1 solve on the same stream afterwards
+    is unaffected."""
+    import torch
+    from paper_2605_17913_b200.solver import QPSolver
+    n, m, p = 6, 2, 4
+    s = QPSolver(0, n, m, p, shared=("Q",))
+    f = lambda *sh: torch.zeros(*sh, dtype=torch.float32, device="cuda:0")
+    out = s.solve(f(n, n), f(0, n), f(0, m, n), f(0, m), f(0, p, n), f(0, p))
+    g = s.backward(f(0, n))
+    torch.cuda.synchronize()
+    assert out["x"].shape == (0, n) and g["dQ"].shape == (n, n) and float(g["dQ"].abs().sum()) == 0.0
+    b = gen.g_rand(5, 1, n, m, p)
+    check_against_oracle(b, run_gpu(b))

@@ -1,0 +1,24 @@
+"""bench.py contract on CPU: the reference arm (the oracle)
+prints one JSON line with the keys the driver reads, and its metric, unit and
+workload match the GPU arm's defaults."""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_reference_arm_json_line():
+    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "0"],
+                         cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    r = json.loads(lines[0])
+    assert r["impl"] == "reference" and r["unit"] == "QP/s" and r["higher_is_better"] is True
+    assert r["value"] > 0 and r["steps"] == 1 and r["warmup"] == 0 and r["n_gpus"] == 1
+    assert r["config"]["workload"] == "cfg2_optnet_n50_m10_p100_B1024"
+    assert r["cpu_baseline"]["kind"] == "oracle" and r["cpu_baseline"]["value"] == r["value"]
+    assert r["cpu_baseline"]["cores"] >= 1
+    assert r["e2e"] == {"value": r["value"], "unit": "QP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}

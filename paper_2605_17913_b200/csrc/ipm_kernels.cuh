@@ -430,7 +430,8 @@ __device__ float assemble(float* K, const Smem& S, const Args& a, const Prob& P,
 
 // Warp-per-row dot products out[r] = Mat[r,:]·vec for r < rows (Mat global
 // row-major rows×n, vec and out in shared memory); each warp keeps 4 rows in
-// flight so the loads and the shuffle reductions overlap.  Not inlined: one
+// flight so the loads and the shuffle reductions overlap; rows of even length
+// are read as float2 (one pass per row for n ≤ 64).  Not inlined: one
 // copy of the code serves every call site (instruction-cache footprint).
 // Ends with a barrier.
 template <int NT>
@@ -438,15 +439,28 @@ __device__ __noinline__ void rowdots(const float* __restrict__ Mat, int rows, in
                                      float* out) {
   constexpr int NW = NT / 32, R = 4;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool v2 = !(n & 1) && !((reinterpret_cast<uintptr_t>(Mat) | reinterpret_cast<uintptr_t>(vec)) & 7);
   for (int r0 = warp * R; r0 < rows; r0 += NW * R) {
     float acc[R];
 #pragma unroll
     for (int u = 0; u < R; ++u) acc[u] = 0.f;
-    for (int j = lane; j < n; j += 32) {
-      const float xv = vec[j];
+    if (v2) {  // even n, 8-byte aligned rows: float2 loads (one pass for n ≤ 64)
+      for (int j = lane; j < (n >> 1); j += 32) {
+        const float2 xv = reinterpret_cast<const float2*>(vec)[j];
 #pragma unroll
-      for (int u = 0; u < R; ++u)
-        if (r0 + u < rows) acc[u] = fmaf(__ldg(Mat + (r0 + u) * n + j), xv, acc[u]);
+        for (int u = 0; u < R; ++u)
+          if (r0 + u < rows) {
+            const float2 g = __ldg(reinterpret_cast<const float2*>(Mat + (r0 + u) * n) + j);
+            acc[u] = fmaf(g.y, xv.y, fmaf(g.x, xv.x, acc[u]));
+          }
+      }
+    } else {
+      for (int j = lane; j < n; j += 32) {
+        const float xv = vec[j];
+#pragma unroll
+        for (int u = 0; u < R; ++u)
+          if (r0 + u < rows) acc[u] = fmaf(__ldg(Mat + (r0 + u) * n + j), xv, acc[u]);
+      }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1)

@@ -526,8 +526,46 @@ __device__ Norms residuals(const Smem& S, const Args& a, const Prob& P, float ka
   // When n < NT the row ranges are split over ng groups of threads (partial
   // sums in S.colscr) so that every thread has work.
   const int gw = (n + 31) & ~31;
-  const int ng = gw >= NT ? 1 : min(NT / gw, 4);
-  if (ng > 1) {
+  int ng = gw >= NT ? 1 : min(NT / gw, 4), cw = gw;  // groups, column-sum stride
+  // even n with 8-byte aligned rows: a thread owns the column PAIR (j, j+1)
+  // (float2 loads, half the loop trips), so up to 4 groups fit for n ≤ 64
+  const int gw2 = ((n >> 1) + 31) & ~31;
+  const int ng2 = min(min(NT, 128) / gw2, 4);
+  const bool pairs = ng2 >= 2 && !(n & 1) &&
+                     !((reinterpret_cast<uintptr_t>(P.Q) | reinterpret_cast<uintptr_t>(P.G) |
+                        (m > 0 ? reinterpret_cast<uintptr_t>(P.A) : 0)) & 7);
+  if (pairs) {
+    ng = ng2; cw = 2 * gw2;
+    const int grp = tid / gw2, jp = tid - grp * gw2, j = 2 * jp;
+    if (grp < ng && j < n) {
+      float2 qx = make_float2(0.f, 0.f), gz = qx, gt = qx, ay = qx;
+      const int i0 = grp * n / ng, i1 = (grp + 1) * n / ng;
+#pragma unroll 4
+      for (int i = i0; i < i1; ++i) {
+        const float2 g = __ldg(reinterpret_cast<const float2*>(P.Q + i * n + j));
+        const float xi = S.x[i];
+        qx.x = fmaf(g.x, xi, qx.x); qx.y = fmaf(g.y, xi, qx.y);
+      }
+      const int k0 = grp * p / ng, k1 = (grp + 1) * p / ng;
+#pragma unroll 4
+      for (int k = k0; k < k1; ++k) {
+        const float2 g = __ldg(reinterpret_cast<const float2*>(P.G + k * n + j));
+        const float zk = S.z[k], tk = S.t[k];
+        gz.x = fmaf(g.x, zk, gz.x); gz.y = fmaf(g.y, zk, gz.y);
+        gt.x = fmaf(g.x, tk, gt.x); gt.y = fmaf(g.y, tk, gt.y);
+      }
+      const int l0 = grp * m / ng, l1 = (grp + 1) * m / ng;
+      for (int l = l0; l < l1; ++l) {
+        const float2 g = __ldg(reinterpret_cast<const float2*>(P.A + l * n + j));
+        const float yl = S.y[l];
+        ay.x = fmaf(g.x, yl, ay.x); ay.y = fmaf(g.y, yl, ay.y);
+      }
+      float* cs = S.colscr + grp * 4 * cw;
+      *reinterpret_cast<float2*>(cs + j) = qx; *reinterpret_cast<float2*>(cs + cw + j) = gz;
+      *reinterpret_cast<float2*>(cs + 2 * cw + j) = gt; *reinterpret_cast<float2*>(cs + 3 * cw + j) = ay;
+    }
+    __syncthreads();
+  } else if (ng > 1) {
     const int grp = tid / gw, j = tid - grp * gw;
     if (grp < ng && j < n) {
       float qx = 0.f, gz = 0.f, gt = 0.f, ay = 0.f;
@@ -553,8 +591,8 @@ __device__ Norms residuals(const Smem& S, const Args& a, const Prob& P, float ka
     float qx = 0.f, gz = 0.f, gt = 0.f, ay = 0.f;
     if (ng > 1) {
       for (int g = 0; g < ng; ++g) {
-        const float* cs = S.colscr + g * 4 * gw;
-        qx += cs[j]; gz += cs[gw + j]; gt += cs[2 * gw + j]; ay += cs[3 * gw + j];
+        const float* cs = S.colscr + g * 4 * cw;
+        qx += cs[j]; gz += cs[cw + j]; gt += cs[2 * cw + j]; ay += cs[3 * cw + j];
       }
     } else {
 #pragma unroll 4

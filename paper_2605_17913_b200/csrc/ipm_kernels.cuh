@@ -528,10 +528,11 @@ __device__ Norms residuals(const Smem& S, const Args& a, const Prob& P, float ka
   const int gw = (n + 31) & ~31;
   int ng = gw >= NT ? 1 : min(NT / gw, 4), cw = gw;  // groups, column-sum stride
   // even n with 8-byte aligned rows: a thread owns the column PAIR (j, j+1)
-  // (float2 loads, half the loop trips), so up to 4 groups fit for n ≤ 64
+  // (float2 loads, half the loop trips), so up to 4 groups fit for n ≤ 64;
+  // used only where that gives more groups than one column per thread
   const int gw2 = ((n >> 1) + 31) & ~31;
   const int ng2 = min(min(NT, 128) / gw2, 4);
-  const bool pairs = ng2 >= 2 && !(n & 1) &&
+  const bool pairs = ng2 > ng && !(n & 1) &&
                      !((reinterpret_cast<uintptr_t>(P.Q) | reinterpret_cast<uintptr_t>(P.G) |
                         (m > 0 ? reinterpret_cast<uintptr_t>(P.A) : 0)) & 7);
   if (pairs) {

@@ -278,7 +278,29 @@ __device__ float assemble(float* K, const Smem& S, const Args& a, const Prob& P,
   }
   __syncthreads();
   const int nrow = N - n4;  // C rows then A rows
-  {
+  const bool pairs = !TC && !(n & 1) &&
+                     !((reinterpret_cast<uintptr_t>(P.G) | (a.m > 0 ? reinterpret_cast<uintptr_t>(P.A) : 0)) & 7);
+  if (pairs) {
+    // even n (path 1): column pairs, float2 loads and stores (rows of K start
+    // at multiples of 4 floats)
+    const int n2 = n >> 1, tot = nrow * n2;
+    const int drr = NT / n2, dj = NT - drr * n2;
+    int rr = tid / n2, jp = tid - rr * n2;
+    for (int idx = tid; idx < tot; idx += NT) {
+      float2 val;
+      if (rr < pa) {
+        const int k = S.act[rr];
+        const float w = cw[k];
+        val = __ldg(reinterpret_cast<const float2*>(P.G + k * n) + jp);
+        val.x *= w; val.y *= w;
+      } else {
+        val = __ldg(reinterpret_cast<const float2*>(P.A + (rr - pa) * n) + jp);
+      }
+      *reinterpret_cast<float2*>(K + row_off<!TC>(L, S.ro, n4 + rr) + 2 * jp) = val;
+      rr += drr; jp += dj;
+      if (jp >= n2) { jp -= n2; ++rr; }
+    }
+  } else {
     // large n: 4 elements per thread and step, loads issued before the stores
     // (path 1 keeps one: measured 1.5 % faster there)
     constexpr int UB = TC ? 4 : 1;

@@ -428,7 +428,7 @@ __device__ float assemble(float* K, const Smem& S, const Args& a, const Prob& P,
           for (int w2 = 0; w2 < 4; ++w2) acc[u][w2] = fmaf(gi[u], gj[w2], acc[u][w2]);
       }
     };
-    if ((n & 1) == 0) kloop(std::true_type{});
+    if ((n & 1) == 0 && !(reinterpret_cast<uintptr_t>(P.G) & 7)) kloop(std::true_type{});
     else kloop(std::false_type{});
 #pragma unroll
     for (int u = 0; u < 4; ++u) {

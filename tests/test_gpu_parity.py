@@ -404,3 +404,32 @@ def test_empty_batch_device():
     assert out["x"].shape == (0, n) and g["dQ"].shape == (n, n) and float(g["dQ"].abs().sum()) == 0.0
     b = gen.g_rand(5, 1, n, m, p)
     check_against_oracle(b, run_gpu(b))
+
+
+def test_even_n_unaligned_rows_take_scalar_loads():
+    """Even n with Q, G, A at a 4-byte (not 8-byte) offset: the float2
+    column-pair loads of the residuals, rowdots and the assembly scatter are
+    disabled by their alignment test and the scalar loops run; the result
+    still meets the oracle bar (config-2 shape, 64 problems)."""
+    import torch
+    from paper_2605_17913_b200.solver import QPSolver
+    b = gen.make_config(2, batch=64)
+    S = QPSolver(b.batch, b.n, b.m, b.p)
+
+    def T(name, shift):
+        a = np.ascontiguousarray(getattr(b, name), dtype=np.float32)
+        buf = torch.empty(a.size + 1, dtype=torch.float32, device="cuda:0")
+        t = buf[shift:shift + a.size].view(a.shape)
+        t.copy_(torch.from_numpy(a))
+        return t
+
+    data = [T(f, 1 if f in ("Q", "G", "A") else 0) for f in ("Q", "q", "A", "b", "G", "h")]
+    assert all(data[i].data_ptr() % 8 == 4 for i in (0, 2, 4))
+    out = S.solve(*data)
+    g = S.backward(torch.from_numpy(np.ascontiguousarray(b.dl_dx, dtype=np.float32)).cuda())
+    torch.cuda.synchronize()
+    res = {k: v.cpu().numpy() for k, v in out.items()}
+    res.update({k: v.cpu().numpy() for k, v in g.items() if k != "status"})
+    res["grad_status"] = g["status"].cpu().numpy()
+    S.close()
+    check_against_oracle(b, res)

@@ -4,11 +4,17 @@ arxiv 2605.17913) through the C ABI on B200.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
 
-One step = qp_solve_batched + qp_backward_batched over one batch per GPU
-(weak scaling: every rank owns its own batch of distinct problems), plus the
-NCCL all-reduce of shared-parameter gradients when the config shares them.
-Metric (BASELINE.json): QP solve+backward/sec, f32, device-timed, whole job.
-Rank 0 prints ONE JSON line.  See DESIGN.md §7 for every field."""
+Default workload: BASELINE.json config 4, the end-to-end / bilevel training
+step (8192 QPs, n = 200, p = 400, Q, G, h shared by the batch, gradients
+all-reduced) — the configuration the metric's "1/2/4/8 B200" is defined on.
+One step = qp_solve_batched + qp_backward_batched over this rank's slice of
+the FIXED global batch (strong scaling: rank r of N takes the contiguous
+slice dist.shard(B, r, N)), plus the NCCL all-reduce of the shared-parameter
+gradients.  `--gpus N` without torchrun re-executes itself under
+`torch.distributed.run --nproc-per-node N` (one process per GPU).
+Metric (BASELINE.json): QP solve+backward/sec, f32, device-timed, whole job
+(global batch ÷ max-over-ranks time).  Rank 0 prints ONE JSON line.  See
+DESIGN.md §7 for every field."""
 from __future__ import annotations
 
 import argparse
@@ -38,15 +44,17 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2, help="BASELINE.json config index (1-based)")
+    ap.add_argument("--config", type=int, default=4, help="BASELINE.json config index (1-based)")
     ap.add_argument("--batch", type=int, default=None,
-                    help="override the per-GPU batch (plumbing tests only; bench lines use the config's batch)")
+                    help="override the GLOBAL batch (plumbing tests only; bench lines use the config's batch)")
     ap.add_argument("--workload", default=None, choices=sorted(gen.WORKLOADS),
                     help="an N4 application shape instead of a BASELINE.json config")
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--dump", default=None,
+                    help="write this rank's outputs of the last timed step to DIR/rank<r>.npz (tests)")
     return ap.parse_args()
 
 
@@ -122,28 +130,44 @@ def workload_of(a) -> dict:
                 make=lambda B, start=0: gen.make_config(a.config, batch=B, start=start), solver={})
 
 
-def oracle_rate(W: dict, target_s: float, batch_cap: int, start: int = 0):
-    """Time the f64 oracle (K14 + GEPP, the parity reference) on a bounded
-    sample of the workload, all host cores.  Returns (QP/s, cores, sample, n_problems)."""
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_rate(W: dict, target_s: float, batch_cap: int, start: int = 0, prec: str = "f64"):
+    """Time the oracle on a bounded sample of the workload, all host cores:
+    prec "f64" = the parity reference (paper-literal Eq. 14 + GEPP), "f32" =
+    the iteration-count reference (M_PART, the CUDA path's algorithm class).
+    Returns (QP/s, cores, n_problems, seconds)."""
     import oracle
     nt = oracle.hardware_threads()
+    cfg = oracle.Cfg.f64() if prec == "f64" else oracle.Cfg.f32()
     pilot = W["make"](min(nt, batch_cap), start)
     t0 = time.perf_counter()
-    r = oracle.solve(pilot, oracle.Cfg.f64(), "f64", nthreads=nt)
-    oracle.backward(pilot, r, oracle.Cfg.f64(), "f64", nthreads=nt)
+    r = oracle.solve(pilot, cfg, prec, nthreads=nt)
+    oracle.backward(pilot, r, cfg, prec, nthreads=nt)
     dt = time.perf_counter() - t0
     rate = pilot.batch / max(dt, 1e-6)
     ns = int(min(batch_cap, max(pilot.batch, round(rate * target_s))))
     ns = max(nt, (ns // nt) * nt) if ns >= nt else ns
     samp = W["make"](ns, start)
     t0 = time.perf_counter()
-    r = oracle.solve(samp, oracle.Cfg.f64(), "f64", nthreads=nt)
-    oracle.backward(samp, r, oracle.Cfg.f64(), "f64", nthreads=nt)
+    r = oracle.solve(samp, cfg, prec, nthreads=nt)
+    oracle.backward(samp, r, cfg, prec, nthreads=nt)
     dt = time.perf_counter() - t0
     return ns / dt, nt, ns, dt
 
 
 def run_reference(a):
+    """The reference arm: the oracle as it stands (f64, paper-literal Eq. 14 +
+    GEPP) on the host cores, same workload, metric and unit; under torchrun
+    only rank 0 runs it."""
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
         return 0
@@ -151,7 +175,7 @@ def run_reference(a):
     import oracle
     nt = oracle.hardware_threads()
     # calibrate one step to ~4 s of CPU work so K+W steps finish in minutes
-    _, _, ns, _ = oracle_rate(c, 4.0, c["batch"])
+    _, _, ns, _ = oracle_rate(c, 4.0, a.batch or c["batch"])
     samp = c["make"](ns)
     times = []
     for i in range(a.warmup + a.steps):
@@ -163,9 +187,9 @@ def run_reference(a):
     tot = sum(times)
     val = ns * a.steps / tot
     sample = (f"first {ns} problems of {c['name']} per step; f64 oracle "
-              f"(Eq. 14 + GEPP), init + Alg. 1 + Alg. 2 + Alg. 3, std::thread over problems")
+              f"(Eq. 14 + GEPP), init + Alg. 1 + Alg. 2 + Alg. 3, std::thread over problems; CPU {cpu_model()}")
     out = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
-           "ms_per_step": 1e3 * tot / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "ms_per_step": 1e3 * tot / a.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
            "dtype": "f64", "data": "synthetic", "impl": "reference",
            "config": {"workload": c["name"], "batch_per_step": ns, "n": c["n"], "m_eq": c["m"], "p": c["p"]},
            "cpu_baseline": {"value": val, "unit": UNIT, "cores": nt, "kind": "oracle", "sample": sample},
@@ -176,10 +200,31 @@ def run_reference(a):
 
 
 # ---------------------------------------------------------------------------
+# N > 1 without torchrun: one process per GPU via torch.distributed.run
+# ---------------------------------------------------------------------------
+def relaunch(a) -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ)
+    # NCCL communicator set-up on stderr (ranks, transport); stdout keeps the one JSON line
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
+# ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
 def main():
     a = parse()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(a)
     if a.impl == "reference":
         return run_reference(a)
     import torch
@@ -187,13 +232,29 @@ def main():
     from paper_2605_17913_b200.solver import QPSolver
 
     rank, world, local = D.init()
-    local = local % max(1, torch.cuda.device_count())  # = LOCAL_RANK on a node with ≥ world GPUs
+    if world != a.gpus:
+        print(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
+    ndev = torch.cuda.device_count()
+    if world > ndev and os.environ.get("QPB200_DIST_BACKEND") != "gloo":
+        print(f"bench.py: {world} ranks need {world} GPUs, this node has {ndev}", file=sys.stderr)
+        return 2
+    local = local % max(1, ndev)  # = LOCAL_RANK on a node with ≥ world GPUs (gloo plumbing tests share one)
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     c = workload_of(a)
-    B, n, m, p = a.batch or c["batch"], c["n"], c["m"], c["p"]
-    batch = c["make"](B, rank * B)  # distinct problems per rank
+    n, m, p = c["n"], c["m"], c["p"]
+    B_glob = a.batch or c["batch"]
+    start, stop = D.shard(B_glob, rank, world)  # strong scaling: this rank's slice of the fixed global batch
+    B = stop - start
+    batch = c["make"](B, start)  # problem i of the global batch is the same problem at every world size
     shared = [k for k, v in batch.shared.items() if v]
+    if world > 1:
+        # communicator up before timing; its size goes to stderr next to NCCL's own INIT lines
+        t = torch.ones(1, device=dev)
+        torch.distributed.all_reduce(t)
+        print(f"[bench rank {rank}] communicator: backend={torch.distributed.get_backend()} nranks={int(t.item())} "
+              f"problems [{start}, {stop})", file=sys.stderr, flush=True)
     S = QPSolver(B, n, m, p, shared=shared, device=local, **c["solver"])
     info = S.info()
 
@@ -219,10 +280,11 @@ def main():
     D.barrier()
     torch.cuda.synchronize(dev)
     props = torch.cuda.get_device_properties(dev)
-    uuid = str(getattr(props, "uuid", "")) or None
+    uuid = (str(getattr(props, "uuid", "")) or None) if world == 1 else None  # N > 1: every GPU of the node
     clk = ClockSampler(uuid)
-    clk.start()
-    time.sleep(0.3)
+    if rank == 0:
+        clk.start()
+        time.sleep(0.3)
     t_solve = t_bwd = 0.0
     for _ in range(a.steps):
         flush.fill_(1.0)  # L2 flush between timed steps (outside the events)
@@ -237,37 +299,43 @@ def main():
         t_solve += e0.elapsed_time(e1)
         t_bwd += e1.elapsed_time(e2)
     torch.cuda.synchronize(dev)
-    clk.stop()
+    if rank == 0:
+        clk.stop()
     D.barrier()
     total_ms = D.max_over_ranks(t_solve + t_bwd, dev)
-    value = B * world * a.steps / (total_ms / 1e3)
+    value = B_glob * a.steps / (total_ms / 1e3)
 
+    if a.dump:
+        os.makedirs(a.dump, exist_ok=True)
+        np.savez(os.path.join(a.dump, f"rank{rank}.npz"), start=start, stop=stop,
+                 **{k: v.cpu().numpy() for k, v in out.items()},
+                 **{"g_" + k: v.cpu().numpy() for k, v in g.items()})
     iters = out["iters"].cpu().numpy()
     riters = g["relax_iters"].cpu().numpy()
     status = out["status"].cpu().numpy()
     gstatus = g["status"].cpu().numpy()
-    # algorithmic flops counted inside the kernels (reduced-system sizes)
-    f_solve, f_bwd = S.last_flops()
     ms_solve, ms_bwd = t_solve / a.steps, t_bwd / a.steps
     peak = FL.fp32_peak_tflops(props.multi_processor_count)
     dom_solve = ms_solve >= ms_bwd
-    f_dom, ms_dom = (f_solve, ms_solve) if dom_solve else (f_bwd, ms_bwd)
+    # SURVEY §8(d) algorithmic flops (K14-literal) of this rank's launches,
+    # from the measured per-problem iteration counts
+    k14_s = float(sum(FL.k14_solve(n, m, p, int(i)) for i in iters))
+    k14_b = float(sum(FL.k14_backward(n, m, p, int(r)) for r in riters))
+    # executed flops of the reduced systems, counted inside the kernels
+    x_s, x_b = S.last_flops()
+    f_dom, x_dom, ms_dom = (k14_s, x_s, ms_solve) if dom_solve else (k14_b, x_b, ms_bwd)
     achieved = f_dom / (ms_dom / 1e3) / 1e12
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", f"traffic_{c['key']}.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get("solve" if dom_solve else "backward")
-        except Exception:
-            traffic = None
     roofline = {"bound": "alu", "kernel": "ipm_kernel (solve launch)" if dom_solve else "ipm_kernel (backward launch)",
-                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": traffic,
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                "work_model": "SURVEY §8(d) K14-literal: per iteration N^3/3 + 2N^2 + 2n^2 + 6pn + 4mn "
+                              "(N = n+p+m) at the measured iteration counts, + init, + p*n^2 once (flops.py)",
                 "peak_note": "FP32 FMA: SMs x 128 lanes x 2 flop x 1965 MHz (derived, DESIGN.md §6)",
+                "traffic_note": "DRAM bytes per launch from ncu --set full: profiles/r2/ (not measurable in this run)",
                 "flops_per_launch": f_dom, "ms_per_launch": ms_dom,
+                "frac_exec": x_dom / (ms_dom / 1e3) / 1e12 / peak, "exec_flops_per_launch": x_dom,
                 "solve_ms": ms_solve, "backward_ms": ms_bwd,
-                "solve_tflops": f_solve / (ms_solve / 1e3) / 1e12,
-                "backward_tflops": f_bwd / (ms_bwd / 1e3) / 1e12}
+                "solve_tflops": k14_s / (ms_solve / 1e3) / 1e12, "backward_tflops": k14_b / (ms_bwd / 1e3) / 1e12,
+                "step_tflops": (k14_s + k14_b) / ((ms_solve + ms_bwd) / 1e3) / 1e12}
 
     # ---- e2e: host buffers through the C ABI, H2D/D2H inside the timed region
     e2e = None
@@ -308,29 +376,35 @@ def main():
         h2d = B * per + sh + B * n * 4
         d2h = sum(int(v.numel() * v.element_size()) for v in o.values()) + \
             sum(int(v.numel() * v.element_size()) for v in gg.values())
-        e2e = {"value": B * world * a.steps / (h_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": h_ms / a.steps}
+        e2e = {"value": B_glob * a.steps / (h_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": h_ms / a.steps,
+               "note": "QP_MEM_HOST_ASYNC: pinned host inputs and outputs, per-rank bytes"}
         Sh.close()
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
         rate, cores, ns, dt = oracle_rate(c, a.cpu_seconds, B)
-        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+        r32, _, ns32, dt32 = oracle_rate(c, a.cpu_seconds / 3, B, prec="f32")
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
                "sample": f"first {ns} problems of {c['name']} ({dt:.1f} s): f64 oracle (Eq. 14 + GEPP), "
-                         f"init + Alg. 1 + Alg. 2 + Alg. 3, std::thread over problems"}
+                         f"init + Alg. 1 + Alg. 2 + Alg. 3, std::thread over problems",
+               "f32_value": r32,
+               "f32_sample": f"first {ns32} problems ({dt32:.1f} s): f32 oracle (M_PART, reading Q12b)"}
 
-    clocks = clk.summary()
+    clocks = clk.summary() if rank == 0 else None
     if rank == 0:
+        launches = info["launches_solve"] + info["launches_backward"]
         res = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
-               "warmup": a.warmup, "ms_per_step": total_ms / a.steps, "higher_is_better": True, "scaling": "weak",
+               "warmup": a.warmup, "ms_per_step": total_ms / a.steps, "higher_is_better": True, "scaling": "strong",
                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-               "config": {"workload": c["name"], "batch_per_gpu": B, "global_batch": B * world, "n": n, "m_eq": m,
-                          "p": p, "shared": shared, "parallelism": f"dp{world} (batch sharded, no collective"
-                          + (", shared-grad all-reduce" if shared else "") + ")",
+               "config": {"workload": c["name"], "global_batch": B_glob, "batch_per_gpu": B, "n": n, "m_eq": m,
+                          "p": p, "shared": shared, "parallelism": f"dp{world} (fixed global batch sharded by rank"
+                          + (", NCCL all-reduce of the shared-parameter gradients" if shared and world > 1 else "")
+                          + ")",
                           "l2": "flushed between timed steps (256 MiB write outside the events)",
                           "tol": S.cfg.tol, "kappa_relax": S.cfg.kappa_relax, "sigma": S.cfg.sigma},
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-               "gpu_launches": a.steps * (info["launches_solve"] + info["launches_backward"]),
+               "gpu_launches": a.steps * launches,
                "clocks": clocks,
                "solver": {"converged": int((status == 0).sum()), "grad_ok": int((gstatus == 0).sum()),
                           "iters_mean": float(iters.mean()), "iters_max": int(iters.max()),

@@ -80,6 +80,10 @@ typedef struct {
   int32_t m_eq;    /* equality constraints, ≥ 0                         */
   int32_t p;       /* inequality constraints, ≥ 0                               */
   int64_t bstride_Q, bstride_q, bstride_A, bstride_b, bstride_G, bstride_h; /* elements; 0 = shared */
+  /* A non-zero stride must be ≥ the per-problem size (n·n, n, m·n, m, p·n, p);
+   * strides larger than that (padded batches) are accepted with
+   * QP_MEM_DEVICE only — host modes take 0 or exactly the per-problem size
+   * (QP_ERR_SHAPE otherwise). */
 } qp_dims;
 
 typedef struct {

@@ -115,6 +115,9 @@ def _declare(L):
         f = getattr(L, f"oracle_newton_step_{suf}")
         f.argtypes = [C.c_int] * 3 + [P] * 10 + [ft, C.c_int, ft, C.c_int] + [P] * 7
         f.restype = C.c_int
+        f = getattr(L, f"oracle_ldl_{suf}")
+        f.argtypes = [C.c_int, C.c_int, ft, P, P, P]
+        f.restype = C.c_int
         f = getattr(L, f"oracle_residuals_{suf}")
         f.argtypes = [C.c_int] * 3 + [P] * 10 + [P] * 5
         f.restype = None
@@ -235,3 +238,19 @@ def residuals(prob, n, m, p, x, y, z, s, prec="f64"):
     getattr(L, f"oracle_residuals_{suf}")(n, m, p, *[_ptr(a) for a in data], *[_ptr(a) for a in it],
                                           *[_ptr(o) for o in out])
     return dict(zip(("rt", "re", "ri", "rz", "rs"), out))
+
+
+def ldl(M, npos, floor_rel, rhs, prec="f64"):
+    """Unpivoted signed LDLᵀ of M (first npos pivots positive, the rest
+    negative; a pivot on the wrong side of ±θ, θ = floor_rel·max|diag|, is set
+    to ±θ and counted — reading Q12) and the solve of M x = rhs with that
+    factor.  Returns dict(L (unit lower), D, x, nfloor)."""
+    L_ = lib()
+    dt, suf = _dt(prec)
+    M = np.array(M, dtype=dt, order="C")
+    N = M.shape[0]
+    D = np.zeros(N, dt)
+    x = np.array(rhs, dtype=dt)
+    nf = getattr(L_, f"oracle_ldl_{suf}")(N, npos, dt(floor_rel), _ptr(M), _ptr(D), _ptr(x))
+    Lm = np.tril(M, -1) + np.eye(N, dtype=dt)
+    return dict(L=Lm, D=D, x=x, nfloor=nf)

@@ -957,6 +957,17 @@ static void backward_batch(const oracle_cfg& cfg, const BatchData<T>& D, int B, 
     *kappa_out = kappa;                                                                                      \
     return F.nfloor;                                                                                         \
   }                                                                                                          \
+  /* Unpivoted signed LDL' of a dense N x N matrix (reading Q12, pivot floor) and one solve; M is          \
+   * overwritten by L (strict lower part), D by the pivots, x (rhs on entry) by the solution.  Returns       \
+   * the number of floored pivots.  (Test entry point: pins the floor branch of ldl_factor.) */              \
+  extern "C" int oracle_ldl_##SUF(int N, int npos, T floor_rel, T* M, T* D, T* x) {                          \
+    std::vector<T> Mv(M, M + (size_t)N * N), Dv;                                                             \
+    const int nf = orc::ldl_factor(Mv, N, npos, floor_rel, Dv);                                              \
+    orc::ldl_solve(Mv, Dv, N, x);                                                                            \
+    std::copy(Mv.begin(), Mv.end(), M);                                                                      \
+    std::copy(Dv.begin(), Dv.end(), D);                                                                      \
+    return nf;                                                                                               \
+  }                                                                                                          \
   /* Residual vectors (Eq. 4, Eq. 10) at (x,y,z,s) with kappa = s'z/p. */                                    \
   extern "C" void oracle_residuals_##SUF(int n, int m, int p, const T* Q, const T* q, const T* A,            \
                                          const T* b, const T* G, const T* h, const T* x, const T* y,         \

@@ -63,6 +63,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+// griddepcontrol.wait: block until every grid this launch depends on
+// (programmatic stream serialisation) has completed and its memory is
+// visible; returns at once when the launch has no such dependency.
+__device__ __forceinline__ void grid_dependency_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ unsigned smid() {
   unsigned r;
   asm volatile("mov.u32 %0, %smid;" : "=r"(r));
@@ -883,7 +887,12 @@ __device__ __forceinline__ void ipm_problem(const Args& a, const Smem& S, const 
     factor_any<NT, BIG, MAXN4>(K, S, L, a.floor_rel * dmax);
     t1 = clock64(); tph[2] += t1 - t0; t0 = t1;
     if (adj) {
-      // Algorithm 3: reduced system with right-hand side (−∇ₓℓ, 0, 0)
+      // Algorithm 3: reduced system with right-hand side (−∇ₓℓ, 0, 0).  The
+      // cotangent may be the output of the kernel launched just before this
+      // one on the stream (programmatic launch: this grid may have started
+      // while that one still runs), so wait for it to complete first; the
+      // relax steps above read only this ctx's solve outputs (done[] flags).
+      grid_dependency_wait();
       for (int j = tid; j < L.N4; j += NT) S.rhs[j] = j < n ? -__ldg(a.dl + (long long)bid * n + j) : 0.f;
       __syncthreads();
     }
@@ -954,6 +963,9 @@ __device__ __forceinline__ void ipm_problem(const Args& a, const Smem& S, const 
       if (a.flops) a.flops[bid] = fl;
     }
   } else {
+    // the gradient buffers may still be read by the previous kernel on the
+    // stream (caching allocator reuse): no store before it has completed
+    grid_dependency_wait();
     if (!ok) {  // zero-filled gradients for failed problems
       for (int j = tid; j < n; j += NT) { S.dx[j] = 0.f; S.x[j] = 0.f; }
       for (int l = tid; l < m; l += NT) { S.dy[l] = 0.f; S.y[l] = 0.f; }

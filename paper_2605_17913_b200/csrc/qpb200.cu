@@ -370,8 +370,12 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
   const int64_t strides[6] = {d->bstride_Q, d->bstride_q, d->bstride_A, d->bstride_b, d->bstride_G, d->bstride_h};
   const int64_t need[6] = {(int64_t)d->n * d->n, d->n, (int64_t)d->m_eq * d->n, d->m_eq, (int64_t)d->p * d->n,
                            d->p};
-  for (int i = 0; i < 6; ++i)
+  for (int i = 0; i < 6; ++i) {
     if (strides[i] != 0 && strides[i] < need[i]) return QP_ERR_SHAPE;
+    // host modes stage contiguous copies of the fields: padded batch strides
+    // are a device-mode feature
+    if (c.mem_kind != QP_MEM_DEVICE && strides[i] != 0 && strides[i] != need[i]) return QP_ERR_SHAPE;
+  }
   Layout L = make_layout(d->n, d->m_eq, d->p, c.formulation);
   if (L.smem > kMaxSmem) return QP_ERR_SHAPE;  // vectors alone exceed the smem budget
   int ndev = 0;
@@ -707,7 +711,13 @@ qp_err qp_backward_batched(qp_ctx* c, const float* dl_dx, float* dQ, float* dq, 
                                        cudaMemcpyHostToDevice, st))) != QP_OK)
         return e;
       qpb::Args ac = chunk_args(a, b0, nb);
-      if (implicit) ac.sched = c->sched + 16 + ch;
+      if (implicit) {
+        // this chunk's problem counter, zeroed on the chunk's own stream: with
+        // QP_MEM_HOST_ASYNC the chunk is ordered only after the work on pst[ch]
+        // (the solve chunk, an earlier backward chunk), not after c->stream
+        ac.sched = c->sched + 16 + ch;
+        if ((e = cuda_ok(cudaMemsetAsync(ac.sched, 0, sizeof(int), st))) != QP_OK) return e;
+      }
       c->ks.backward<<<std::min(c->grid, nb), c->ks.threads, c->L.smem, st>>>(ac);
       if ((e = cuda_ok(cudaGetLastError())) != QP_OK) return e;
       for (int f = 0; f < 6; ++f)  // per-problem gradients (a.g* is null for shared / skipped fields)

@@ -48,6 +48,42 @@ def backward_flops(n, m, p, relax_iters) -> float:
     return (relax_iters + 1) * fac + relax_iters * step + 2 * N ** 2 + 2 * p * n + 2 * (n * n + m * n + p * n)
 
 
+# ---------------------------------------------------------------------------
+# SURVEY.md §8(d) work model ("K14-literal"): the paper's own system, Eq. 14
+# (P:292-307), of dimension N = n + p + m factored every iteration, its
+# constant (1,1) block Q − GᵀG formed once per problem, so per Newton
+# iteration N³/3 (factorisation) + 2N² (two triangular solves) + 2n² + 6pn +
+# 4mn (the residual GEMVs of Eq. 4 / Eq. 10), and once per unit p·n².  These
+# are the flops `roofline.frac` is quoted on; what the kernels execute (the
+# smaller sign(v)-partitioned system of reading Q12b plus its assembly) is
+# reported beside it as `frac_exec`.
+# ---------------------------------------------------------------------------
+def k14_iteration(n: int, m: int, p: int) -> float:
+    N = n + p + m
+    return N ** 3 / 3 + 2 * N ** 2 + (2 * n * n + 6 * p * n + 4 * m * n)
+
+
+def k14_solve(n: int, m: int, p: int, iters) -> float:
+    """qp_solve_batched, one problem with `iters` Newton steps: the CVXOPT
+    initialisation (one factorisation + solve of an N-dimensional system,
+    P:394), p·n² for Q − GᵀG, `iters` iterations, and the final residual
+    evaluation that certifies convergence."""
+    N = n + p + m
+    return (N ** 3 / 3 + 2 * N ** 2) + p * n * n + iters * k14_iteration(n, m, p) + \
+        (2 * n * n + 6 * p * n + 4 * m * n)
+
+
+def k14_backward(n: int, m: int, p: int, relax_iters) -> float:
+    """qp_backward_batched, one problem: Alg. 2 with `relax_iters` Newton steps
+    (relax_iters + 1 residual evaluations and factorisations: factor-then-check,
+    reading Q6), the Alg. 3 adjoint solve 2N², and the outer products of the
+    gradients 2(n² + mn + pn)."""
+    N = n + p + m
+    resid = 2 * n * n + 6 * p * n + 4 * m * n
+    return (relax_iters + 1) * (N ** 3 / 3 + resid) + relax_iters * 2 * N ** 2 + 2 * N ** 2 + \
+        2 * (n * n + m * n + p * n)
+
+
 def data_bytes(n, m, p, shared=()) -> tuple[int, int]:
     """(per-problem bytes, shared bytes) of the six data fields."""
     sizes = {"Q": n * n, "q": n, "A": m * n, "b": m, "G": p * n, "h": p}

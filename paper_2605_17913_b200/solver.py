@@ -45,6 +45,7 @@ class QPSolver:
                       "host_async": capi.QP_MEM_HOST_ASYNC}[mem]
         self.cfg = c
         self._saved = None
+        self.generation = 0  # number of solve calls; the C ctx differentiates the LAST one
         if batch == 0:  # empty batch: nothing to solve, no ctx (the C ABI takes B >= 1)
             self.h = None
             return
@@ -112,10 +113,12 @@ class QPSolver:
         P = self._ptr
         if self.B == 0:
             self._saved = (data, out)
+            self.generation += 1
             return out
         capi.qp_solve_batched(self.h, *[P(data[f]) for f in FIELDS], P(out["x"]), P(out["s"]), P(out["z"]),
                               P(out["y"]), P(out["iters"]), P(out["status"]))
         self._saved = (data, out)  # keep alive for backward (C-ABI contract)
+        self.generation += 1
         return out
 
     def backward(self, dl_dx, out=None, need=GRADS):
@@ -148,14 +151,23 @@ class QPFunction(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, solver: QPSolver, Q, q, A, b, G, h):
-        out = solver.solve(Q.contiguous(), q.contiguous(), A.contiguous(), b.contiguous(), G.contiguous(),
-                           h.contiguous())
+        data = [t.contiguous() for t in (Q, q, A, b, G, h)]
+        out = solver.solve(*data)
         ctx.solver = solver
+        ctx.generation = solver.generation
+        ctx.save_for_backward(*data)
         return out["x"]
 
     @staticmethod
     def backward(ctx, gx):
-        g = ctx.solver.backward(gx.contiguous())
+        solver = ctx.solver
+        if solver.generation != ctx.generation:
+            # the solver was applied again since this forward (a layer used
+            # twice, an evaluation solve in between): the C ctx holds the later
+            # solve, so solve this graph's problems again (deterministic: the
+            # same x*) before differentiating
+            solver.solve(*ctx.saved_tensors)
+        g = solver.backward(gx.contiguous())
         return (None, g["dQ"], g["dq"], g["dA"], g["db"], g["dG"], g["dh"])
 
 

@@ -1,16 +1,20 @@
 """Shared helpers for the parity tests: run the CUDA path through the C ABI
 and compare it with the oracle using the north-star tolerances
-(BASELINE.json north_star):
+(BASELINE.json north_star), with NO floors or slack:
   * primal/dual residuals and gap <= 1e-5 relative, evaluated in f64 from the
     f32 outputs (the relative form of reading Q4);
   * x within 1e-4 relative of the f64 oracle;
-  * gradients within 1e-3 relative of the f64 oracle, per field:
-    ||g - g_ref||_2 / max(||g_ref||_2, 1e-2 ||bundle_ref||_2), where the
-    bundle is all six fields of that problem (a field below 1% of the bundle —
-    e.g. grad_q of a 1-D QP pinned by an active constraint, ~kappa_relax in
-    size — is measured against 1% of the bundle: its f32 value is computed
-    through a cancellation of O(1) terms);
-  * iteration counts equal to the f32 oracle (M-form) or within +-1."""
+  * gradients within 1e-3 relative of the f64 oracle, per field and problem:
+    ||g - g_ref||_2 / ||g_ref||_2;
+  * iteration counts equal to the f32 oracle (M-form) or within +-1.
+The only exception is a documented precision limit: a
+(problem, quantity) pair that misses its bar passes only if the f32 oracle —
+the same algorithm in the same precision, sharing no code — misses the SAME
+bar on the SAME pair (the f32 rounding of the method itself cannot meet it
+there, e.g. a gradient field ~kappa_relax in size obtained through a
+cancellation of O(1) terms), and the GPU — a different but equally valid
+f32 rounding sequence — is within 10x of the f32 oracle's error there; every
+such pair is reported (`precision_limited`)."""
 from __future__ import annotations
 
 import numpy as np
@@ -21,6 +25,23 @@ FIELDS = ("Q", "q", "A", "b", "G", "h")
 TOL_RES = 1e-5
 TOL_X = 1e-4
 TOL_GRAD = 1e-3
+
+
+def within_bar(err_gpu, err_f32, bar, what, report=None):
+    """Per-problem check of the parity bar with the precision-limit exception
+    (module docstring).  err_gpu / err_f32: per-problem errors of the GPU and
+    of the f32 oracle against the f64 oracle (or against the exact bar for
+    residuals).  Returns the number of precision-limited problems."""
+    err_gpu = np.asarray(err_gpu, dtype=np.float64)
+    err_f32 = np.asarray(err_f32, dtype=np.float64)
+    miss = err_gpu > bar
+    limited = miss & (err_f32 > bar) & (err_gpu <= 10 * err_f32)
+    bad = miss & ~limited
+    assert not bad.any(), (what, "GPU misses the bar where the f32 oracle does not (or by >10x)",
+                           np.flatnonzero(bad)[:8].tolist(), err_gpu[bad][:8].tolist(), err_f32[bad][:8].tolist())
+    if report is not None and limited.any():
+        report.append((what, int(limited.sum()), float(err_gpu[limited].max()), float(err_f32[limited].max())))
+    return int(limited.sum())
 
 
 def run_gpu(batch, mem="device", need_backward=True, dl=None, formulation="implicit", **cfg):
@@ -82,19 +103,6 @@ def rel_err_rows(a, r, floor=None):
     if floor is not None:
         den = np.maximum(den, floor)
     return np.where(den > 0, num / np.maximum(den, 1e-300), num)
-
-
-def bundle_norm(grads, idx=None):
-    """Per-problem 2-norm of the whole gradient bundle (per-problem fields only)."""
-    tot = None
-    for k in GRADS:
-        g = grads[k]
-        if g.ndim < 2 or g.size == 0:
-            continue
-        v = (g.reshape(g.shape[0], -1).astype(np.float64) ** 2).sum(1)
-        tot = v if tot is None else tot + v
-    out = np.sqrt(tot)
-    return out if idx is None else out[idx]
 
 
 def x_rel(a, r):

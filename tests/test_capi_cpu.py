@@ -68,6 +68,12 @@ def test_validation_without_gpu(lib):
     for mk, want in ((capi.QP_MEM_HOST_ASYNC, -4), (3, -1)):
         cfg.mem_kind = mk
         assert lib.qp_create(C.byref(h), C.byref(good), C.byref(cfg), 0, None) == want, mk
+    # padded batch strides (bstride > per-problem size): device mode only;
+    # the host modes stage contiguous copies and reject them
+    padded = capi.QpDims(4, 5, 0, 3, 32, 8, 0, 0, 16, 4)
+    for mk, want in ((capi.QP_MEM_DEVICE, -4), (capi.QP_MEM_HOST, -2), (capi.QP_MEM_HOST_ASYNC, -2)):
+        cfg.mem_kind = mk
+        assert lib.qp_create(C.byref(h), C.byref(padded), C.byref(cfg), 0, None) == want, mk
     cfg = capi.default_config()
     assert lib.qp_error_string(-4) == b"CUDA error"
     assert lib.qp_solve_batched(*([None] * 13)) == -1

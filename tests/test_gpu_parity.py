@@ -7,40 +7,52 @@ import oracle as O
 from paper_2605_17913_b200 import generators as gen
 from paper_2605_17913_b200.generators import QPBatch
 
-from .helpers import (GRADS, TOL_GRAD, TOL_RES, TOL_X, bundle_norm, rel_err_rows, rel_residuals, run_gpu,
-                      shared_sum, x_rel)
+from .helpers import (GRADS, TOL_GRAD, TOL_RES, TOL_X, rel_err_rows, rel_residuals, run_gpu, shared_sum,
+                      within_bar, x_rel)
 
 pytestmark = pytest.mark.gpu
 
 
 def check_against_oracle(batch, g, iters_slack=1, grad_tol=TOL_GRAD, cfg32=None):
+    """The north-star bar, unfloored (tests/helpers.py): residuals <= 1e-5,
+    x <= 1e-4, every gradient field <= 1e-3 per problem, iterations within
+    +-1 of the f32 oracle; a miss passes only where the f32 oracle misses the
+    same bar on the same problem (precision limit, reported)."""
+    c32 = cfg32 or O.Cfg.f32()
     r64 = O.solve(batch, O.Cfg.f64(), "f64")
-    r32 = O.solve(batch, cfg32 or O.Cfg.f32(), "f32")
+    r32 = O.solve(batch, c32, "f32")
     assert np.all(r64["status"] == 0)
     ok32 = r32["status"] == 0
     # every instance the f32 oracle solves must be solved, without NaN/Inf
     assert np.all(g["status"][ok32] == 0), (g["status"], r32["status"])
     for k in ("x", "s", "z", "y"):
         assert np.all(np.isfinite(g[k][ok32]))
-    res = rel_residuals(batch, g["x"], g["y"], g["z"], g["s"])
-    assert res[ok32].max() <= 2 * TOL_RES, res.max(axis=0)
-    assert x_rel(g["x"], r64["x"])[ok32].max() <= TOL_X
+    report = []
+    res = rel_residuals(batch, g["x"], g["y"], g["z"], g["s"])[ok32]
+    res32 = rel_residuals(batch, r32["x"], r32["y"], r32["z"], r32["s"])[ok32]
+    for j, nm in enumerate(("r_t", "r_e", "r_i", "gap")):
+        within_bar(res[:, j], res32[:, j], TOL_RES, nm, report)
+    within_bar(x_rel(g["x"], r64["x"])[ok32], x_rel(r32["x"], r64["x"])[ok32], TOL_X, "x", report)
     d_it = np.abs(g["iters"].astype(int) - r32["iters"].astype(int))
     assert d_it[ok32].max() <= iters_slack, (g["iters"], r32["iters"])
     b64 = O.backward(batch, r64, O.Cfg.f64(), "f64")
+    b32 = O.backward(batch, r32, c32, "f32")
     ref = shared_sum(batch, b64)
+    ref32 = shared_sum(batch, b32)
     assert np.all(g["grad_status"][ok32] == 0)
-    floor = 1e-2 * bundle_norm(b64)[ok32]
     for k in GRADS:
         if ref[k].size == 0:
             continue
         if ref[k].ndim == g[k].ndim and g[k].shape[0] == batch.batch and not batch.shared.get(k[1:], False):
-            err = rel_err_rows(g[k][ok32], ref[k][ok32], floor)
-            assert err.max() <= grad_tol, (k, err.max())
-        else:
-            err = np.linalg.norm(g[k] - ref[k]) / max(np.linalg.norm(ref[k]), 1e-30)
-            assert err <= grad_tol, (k, err)
-    return dict(r64=r64, r32=r32, iters_equal=float(np.mean(d_it == 0)))
+            within_bar(rel_err_rows(g[k][ok32], ref[k][ok32]), rel_err_rows(b32[k][ok32], ref[k][ok32]),
+                       grad_tol, k, report)
+        else:  # batch-summed gradient of a shared field
+            nr = max(np.linalg.norm(ref[k]), 1e-30)
+            within_bar([np.linalg.norm(g[k] - ref[k]) / nr], [np.linalg.norm(ref32[k] - ref[k]) / nr],
+                       grad_tol, k, report)
+    if report:
+        print("precision-limited (quantity, problems, GPU err, f32-oracle err):", report)
+    return dict(r64=r64, r32=r32, iters_equal=float(np.mean(d_it == 0)), precision_limited=report)
 
 
 def test_cfg1_full_batch():
@@ -217,7 +229,9 @@ def test_standard_arm_config3_ablation():
     sizeable fraction of instances — like the f32 oracle of the same arm —
     with the failure first seen in the predictor/corrector/line search, while
     the bounded (implicit) f32 arm solves every instance.  Where the standard
-    arm converges, its x agrees with the f64 oracle."""
+    arm converges, its x agrees with the f64 oracle (1e-4, or the precision
+    limit of tests/helpers.py where the f32 oracle's own standard arm misses
+    1e-4 on the same problem)."""
     b = gen.make_config(3, batch=60)
     gi = run_gpu(b)
     assert np.all(gi["status"] == 0)
@@ -230,8 +244,10 @@ def test_standard_arm_config3_ablation():
     assert abs(int(fail_gpu.sum()) - int(fail_orc.sum())) <= 0.25 * len(fail_gpu)
     assert set((gx["status"][fail_gpu] >> 8).tolist()) <= {2, 3, 4, 5}
     r64 = O.solve(b, O.Cfg.f64(), "f64")
-    ok = gx["status"] == 0
-    assert x_rel(gx["x"][ok], r64["x"][ok]).max() <= 2e-3
+    # where both f32 arms converge: x at the north-star 1e-4, unless the f32
+    # oracle's standard arm misses it on the same problem (precision limit)
+    ok = (gx["status"] == 0) & (ox["status"] == 0)
+    within_bar(x_rel(gx["x"], r64["x"])[ok], x_rel(ox["x"], r64["x"])[ok], TOL_X, "standard-arm x")
 
 
 def test_standard_arm_matches_oracle_where_stable():
@@ -306,7 +322,7 @@ def test_cfg4_full_size_sampled_and_batch_sums():
     r64 = O.solve(sub, O.Cfg.f64(), "f64")
     assert x_rel(g["x"][idx], r64["x"]).max() <= TOL_X
     b64 = O.backward(sub, r64, O.Cfg.f64(), "f64")
-    err = rel_err_rows(g["dq"][idx], b64["dq"], 1e-2 * bundle_norm(b64))
+    err = rel_err_rows(g["dq"][idx], b64["dq"])
     assert err.max() <= TOL_GRAD, err.max()
     # replicated run in chunks of 1024 problems: per-problem dQ, dG, dh summed on the device
     dev = "cuda:0"
@@ -433,3 +449,64 @@ def test_even_n_unaligned_rows_take_scalar_loads():
     res["grad_status"] = g["status"].cpu().numpy()
     S.close()
     check_against_oracle(b, res)
+
+
+@pytest.mark.parametrize("case", ["constructed", "cfg2"])
+def test_initialization_point_matches_oracle(case):
+    """Row a1 (reading Q11 = S:149) observed on its own: with
+    max_iter = 0 the solve returns the CVXOPT initial point (status
+    MAX_ITER).  Constructed case: the closed-form shifts of
+    tests/test_oracle_linalg.py::test_initialization_shift_constructed
+    (no shift when α < 0, shift by exactly 1 + α otherwise); config 2: 64
+    problems against the f64 oracle's initialisation (f32 precision limit
+    against its own f32 initialisation, tests/helpers.py)."""
+    if case == "constructed":
+        G = np.array([[1.0], [-1.0]], np.float32)
+        qs = np.array([[-2.0], [0.0]], np.float32)
+        hs = np.array([[3.0, 5.0], [4.0, -2.0]], np.float32)
+        b = QPBatch(1, 0, 2, np.ones((2, 1, 1), np.float32), qs, np.zeros((2, 0, 1), np.float32),
+                    np.zeros((2, 0), np.float32), np.stack([G, G]), hs, np.zeros((2, 1), np.float32), 2)
+        g = run_gpu(b, need_backward=False, max_iter=0)
+        assert np.all((g["status"] & 0xFF) == 2)
+        assert np.allclose(g["x"][:, 0], [0.0, 2.0], atol=1e-6)
+        assert np.allclose(g["s"], [[3.0, 5.0], [3.0, 1.0]], atol=1e-6), g["s"]
+        assert np.allclose(g["z"], [[3.0, 1.0], [1.0, 3.0]], atol=1e-6), g["z"]
+        return
+    b = gen.make_config(2, batch=64)
+    g = run_gpu(b, need_backward=False, max_iter=0)
+    ref = [O.initialize(b.problem(i), b.n, b.m, b.p, prec="f64") for i in range(b.batch)]
+    r32 = [O.initialize(b.problem(i), b.n, b.m, b.p, prec="f32") for i in range(b.batch)]
+    for k in ("x", "y", "z", "s"):
+        R = np.stack([r[k] for r in ref])
+        R32 = np.stack([r[k] for r in r32])
+        within_bar(x_rel(g[k], R), x_rel(R32, R), TOL_X, "init " + k)
+
+
+@pytest.mark.parametrize("cfg,B", [(1, 16), (3, 60)])
+def test_standard_arm_backward_matches_oracle(cfg, B):
+    """Row a13's backward (the OptNet-style adjoint of Eq. 8):
+    GPU xpm_backward_kernel gradients against the f64 oracle's explicit-arm
+    gradients (grads_explicit) on every problem where the GPU arm, the f32
+    oracle arm and the f64 oracle arm all converge; x at 1e-4 and every
+    gradient field at 1e-3 relative, unfloored, with the f32 precision-limit
+    exception (the same arm in the f32 oracle misses the same bar on the same
+    problem — the paper's point about this formulation)."""
+    b = gen.make_config(cfg, batch=B)
+    gx = run_gpu(b, formulation="explicit")
+    c32 = O.Cfg.f32(formulation=O.FORM_EXPLICIT, kkt_solver=O.SOLVER_NORMAL_CHOL)
+    c64 = O.Cfg.f64(formulation=O.FORM_EXPLICIT)
+    r32, r64 = O.solve(b, c32, "f32"), O.solve(b, c64, "f64")
+    g32, g64 = O.backward(b, r32, c32, "f32"), O.backward(b, r64, c64, "f64")
+    both = ((gx["status"] == 0) & (gx["grad_status"] == 0) & (r32["status"] == 0) & (g32["status"] == 0) &
+            (r64["status"] == 0) & (g64["status"] == 0))
+    # the f32 standard arm fails its relaxation on most config-1 problems (the
+    # paper's Table 1 pattern, P:1007-1043): few problems are comparable there
+    assert both.sum() >= (2 if cfg == 1 else 10), both.sum()
+    report = []
+    within_bar(x_rel(gx["x"], r64["x"])[both], x_rel(r32["x"], r64["x"])[both], TOL_X, "x", report)
+    for k in GRADS:
+        if g64[k].size == 0:
+            continue
+        within_bar(rel_err_rows(gx[k][both], g64[k][both]), rel_err_rows(g32[k][both], g64[k][both]), TOL_GRAD,
+                   k, report)
+    print(f"standard arm cfg{cfg}: {both.sum()} of {B} compared; precision-limited: {report}")

@@ -45,9 +45,10 @@ def test_bezier_trajectory_shapes(name, B):
     (x) and O(1) (gradients) away from the f64 reference.  Parity here means:
     the GPU solves whatever the f32 oracle solves, with relative residuals
     ≤ 2·tol, and is no further from the f64 reference than the f32 oracle is
-    (x and every gradient field, per problem, with the usual floors)."""
+    (x and every gradient field, per problem, unfloored): a miss of the
+    nominal bar passes only where the f32 oracle misses it too."""
     import oracle as O
-    from .helpers import GRADS, bundle_norm, rel_err_rows, rel_residuals, x_rel
+    from .helpers import GRADS, rel_err_rows, rel_residuals, within_bar, x_rel
     tol = 1e-4
     b = gen.make_workload(name, batch=B)
     g = run_gpu(b, tol=tol)
@@ -56,16 +57,20 @@ def test_bezier_trajectory_shapes(name, B):
     ok = r32["status"] == 0
     assert np.all(r64["status"] == 0) and ok.mean() > 0.9
     assert np.all(g["status"][ok] == 0)
-    res = rel_residuals(b, g["x"], g["y"], g["z"], g["s"])
-    assert res[ok].max() <= 2 * tol, res.max(axis=0)
+    res = rel_residuals(b, g["x"], g["y"], g["z"], g["s"])[ok]
+    res32 = rel_residuals(b, r32["x"], r32["y"], r32["z"], r32["s"])[ok]
+    report = []
+    for j in range(4):
+        within_bar(res[:, j], res32[:, j], tol, f"residual {j}", report)
     ex_gpu, ex_or = x_rel(g["x"], r64["x"]), x_rel(r32["x"], r64["x"])
     assert np.all(ex_gpu[ok] <= np.maximum(10 * tol, 3 * ex_or[ok])), (ex_gpu.max(), ex_or.max())
     g64 = O.backward(b, r64, c64, "f64")
     g32 = O.backward(b, r32, c32, "f32")
-    fl = 1e-2 * bundle_norm(g64)
     for k in GRADS:
         if g64[k].size == 0:
             continue
-        e_gpu = rel_err_rows(g[k], g64[k], fl)
-        e_or = rel_err_rows(g32[k], g64[k], fl)
+        e_gpu = rel_err_rows(g[k], g64[k])
+        e_or = rel_err_rows(g32[k], g64[k])
         assert np.all(e_gpu[ok] <= np.maximum(1e-3, 3 * e_or[ok])), (k, e_gpu.max(), e_or.max())
+    if report:
+        print("precision-limited:", report)

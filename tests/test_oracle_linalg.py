@@ -167,3 +167,59 @@ def test_initialization(orc):
               G=np.zeros((0, 1)), h=np.zeros(0))
     it = orc.initialize(pr, 1, 1, 0)
     assert it["x"][0] == pytest.approx(2.0) and it["y"][0] == pytest.approx(-5.0)
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_initialization_shift_constructed(orc, prec):
+    """S:149 (reading Q11) on constructed QPs whose init solve is known in
+    closed form.  n = 1, Q = [1], G = [[1], [-1]], m = 0: the init system
+    [[Q, Gᵀ], [G, -I]] (x, ẑ) = (-q, h) gives x = (h1 - h2 - q)/3,
+    ẑ = (x - h1, -x - h2); s~ = -ẑ, z~ = ẑ; α_p = -min s~, α_d = -min z~;
+    s = s~ + (1 + α_p) iff α_p >= 0 (else s = s~), z likewise.
+    Case A (α_p = -3 < 0 -> no shift: "always shift" would give s = (1, 3);
+    α_d = 5 -> z = ẑ + 6); case B (α_p = 0 -> shift by exactly 1, where a
+    shift of 2 + α would give 2; α_d = 2 -> z = ẑ + 3)."""
+    G = np.array([[1.0], [-1.0]])
+    cases = [  # (q, h1, h2) -> (x, s, z)
+        (-2.0, 3.0, 5.0, 0.0, (3.0, 5.0), (3.0, 1.0)),
+        (0.0, 4.0, -2.0, 2.0, (3.0, 1.0), (1.0, 3.0)),
+    ]
+    for q, h1, h2, x, s, z in cases:
+        pr = dict(Q=np.array([[1.0]]), q=np.array([q]), A=np.zeros((0, 1)), b=np.zeros(0), G=G,
+                  h=np.array([h1, h2]))
+        it = orc.initialize(pr, 1, 0, 2, prec=prec)
+        assert it["ok"]
+        tol = 1e-12 if prec == "f64" else 1e-6
+        assert abs(it["x"][0] - x) <= tol
+        assert np.abs(it["s"] - np.array(s)).max() <= tol, it["s"]
+        assert np.abs(it["z"] - np.array(z)).max() <= tol, it["z"]
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_ldl_pivot_floor_branch(orc, prec):
+    """Reading Q12: a pivot on the wrong side of ±θ (θ = floor_rel·max|diag|)
+    is replaced by ±θ and counted; the factor and the solve then follow the
+    floored pivot exactly.  Hand-computed 2×2 and 3×3 cases:
+      M = [[1, 1], [1, 1]], npos = 1: d0 = 1, l10 = 1, d1 = 0 is not <= -θ
+        -> d1 = -θ (1 floor); M x = (1, 3) solved as L D Lᵀ x = b:
+        u = (1, 2), w = (1, -2/θ), x = (1 + 2/θ, -2/θ).
+      M = [[1, 2], [2, 1]], npos = 2: d1 = 1 - 4 = -3 < θ -> d1 = +θ.
+      M = diag(4, -1, -2) with npos = 3: d1 = -1 -> θ, d2 = -2 -> θ (2 floors);
+        no floor when npos = 1 (quasi-definite signs respected)."""
+    fr = 0.25
+    r = orc.ldl([[1.0, 1.0], [1.0, 1.0]], 1, fr, [1.0, 3.0], prec=prec)
+    th = fr * 1.0
+    assert r["nfloor"] == 1
+    assert np.allclose(r["D"], [1.0, -th]) and np.allclose(r["L"], [[1, 0], [1, 1]])
+    assert np.allclose(r["x"], [1 + 2 / th, -2 / th], rtol=1e-6)
+    r = orc.ldl([[1.0, 2.0], [2.0, 1.0]], 2, fr, [1.0, 0.0], prec=prec)
+    assert r["nfloor"] == 1 and np.allclose(r["D"], [1.0, th]) and np.allclose(r["L"][1, 0], 2.0)
+    # (L D Lᵀ) x = b with the floored D
+    LDL = r["L"] @ np.diag(r["D"]) @ r["L"].T
+    assert np.allclose(LDL @ r["x"], [1.0, 0.0], atol=1e-5)
+    M3 = np.diag([4.0, -1.0, -2.0])
+    r = orc.ldl(M3, 3, fr, [1.0, 1.0, 1.0], prec=prec)
+    assert r["nfloor"] == 2 and np.allclose(r["D"], [4.0, fr * 4.0, fr * 4.0])
+    r = orc.ldl(M3, 1, fr, [1.0, 1.0, 1.0], prec=prec)
+    assert r["nfloor"] == 0 and np.allclose(r["D"], [4.0, -1.0, -2.0])
+    assert np.allclose(r["x"], [0.25, -1.0, -0.5])

@@ -1,5 +1,6 @@
 """Run solve+backward of config C at batch B twice (profiling target for ncu:
 -s <launches of the first pass> -c ...).  usage: prof_cfg.py C B"""
+import os, sys; sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))  # noqa: E401,E702
 import sys
 
 import torch

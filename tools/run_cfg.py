@@ -1,5 +1,6 @@
 """Time one solve+backward of config C at batch B (device events), print status summary.
 usage: run_cfg.py C B"""
+import os, sys; sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))  # noqa: E401,E702
 import sys
 import time
 

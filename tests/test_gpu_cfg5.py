@@ -35,7 +35,7 @@ def test_cfg5_full_size_properties():
     assert np.all(st == 0), st
     x, y, z, s = (out[k].cpu().numpy() for k in ("x", "y", "z", "s"))
     res = rel_residuals(pb, x, y, z, s)
-    assert res.max() <= 2 * TOL_RES, res
+    assert res.max() <= TOL_RES, res
     rng = np.random.default_rng(5)
     d1 = rng.standard_normal((B, pb.n)).astype(np.float32)
     d2 = rng.standard_normal((B, pb.n)).astype(np.float32)
@@ -67,3 +67,41 @@ def test_cfg5_full_size_properties():
         u = J1[i] / np.linalg.norm(J1[i])
         resid = R - np.outer(R @ u, u)                          # remove the rank-1 dq part
         assert np.linalg.norm(resid) <= 1e-2 * np.linalg.norm(dG[i]), np.linalg.norm(resid) / np.linalg.norm(dG[i])
+
+
+def test_cfg5_against_oracle_golden():
+    """Config 5 at full size (n = 1024, p = 2048) against the CPU oracle.  The
+    oracle needs tens of minutes per problem here, so its results for
+    problems 0 and 1 were written once by tools/make_cfg5_golden.py (which
+    calls only oracle/ — f64 with the M_PART solver, reading Q12b, pinned
+    equal to the paper-literal Eq. 14 solve) into tests/golden/cfg5_oracle.npz.
+    North-star bar, unfloored: x within 1e-4 of f64, residuals ≤ 1e-5, every
+    gradient field within 1e-3 (∇Q, ∇G expanded from the oracle's Alg. 3
+    vectors by P:559-575's outer products), iterations within ±1 of the f32
+    oracle (problem 0); precision-limit exception of tests/helpers.py where
+    the f32 oracle result exists (problem 0)."""
+    import os
+    from .helpers import TOL_GRAD, TOL_X, run_gpu, within_bar, x_rel
+    gold = dict(np.load(os.path.join(os.path.dirname(__file__), "golden", "cfg5_oracle.npz")))
+    pb = gen.make_config(5, batch=2)
+    g = run_gpu(pb)
+    assert np.all(g["status"] == 0) and np.all(g["grad_status"] == 0)
+    assert np.all(gold["status"] == 0) and np.all(gold["gstatus"] == 0)
+    inf = np.array([np.inf])
+    ex32 = np.concatenate([x_rel(gold["x32"], gold["x"][:1]), inf])      # f32 oracle only for problem 0
+    within_bar(x_rel(g["x"], gold["x"]), ex32, TOL_X, "x")
+    res = rel_residuals(pb, g["x"], g["y"], g["z"], g["s"])
+    sub = pb.subset([0])
+    res32 = rel_residuals(sub, gold["x32"], np.zeros((1, 0), np.float32), gold["z32"], gold["s32"])
+    for j in range(4):
+        within_bar(res[:, j], np.concatenate([res32[:, j], [0.0]]), TOL_RES, f"residual {j}")
+    assert abs(int(g["iters"][0]) - int(gold["iters32"][0])) <= 1, (g["iters"], gold["iters32"])
+    dx, dz, xr, zr = (gold[k].astype(np.float64) for k in ("dx", "dz", "xr", "zr"))
+    ref = {"dq": dx, "dh": -dz,
+           "dQ": 0.5 * (np.einsum("bi,bj->bij", dx, xr) + np.einsum("bi,bj->bij", xr, dx)),
+           "dG": np.einsum("bi,bj->bij", dz, xr) + np.einsum("bi,bj->bij", zr, dx)}
+    for k, r in ref.items():
+        a = g[k].reshape(2, -1).astype(np.float64)
+        r = r.reshape(2, -1)
+        err = np.linalg.norm(a - r, axis=1) / np.linalg.norm(r, axis=1)
+        assert err.max() <= TOL_GRAD, (k, err)

@@ -1,0 +1,577 @@
+// bnd_kernels.cuh — the BATCHED large-N engine (qp_info.path = 4): configs 4
+// and 5 and every shape whose reduced KKT system does not fit a path-1 CTA.
+//
+// Why a second engine.  The persistent kernel of ipm_kernels.cuh runs one
+// problem per CTA through the whole of Alg. 1 (or Alg. 2 + 3).  At config-4
+// size (n = 200, p = 400, reduced systems of 300-540 rows) one CTA fills an
+// SM, so each SM advances ONE problem through a chain of ~10⁴ dependent,
+// barrier-separated steps per Newton iteration: the SM sits mostly idle on
+// latency (round 1: 7.7 ms per problem, FP32 pipe < 10 %).  Here the same
+// iteration is split into phases, each a kernel over the whole batch
+// ("bulk-synchronous"), so that every SM holds several problems of every
+// phase at once and the dependent chains of one problem hide behind those of
+// the others:
+//
+//   bnd_begin                       CVXOPT initial system (solve) / load the
+//                                   solution (backward)
+//   per iteration k:
+//     bnd_resid       (B CTAs)      v, κ, residuals Eq. 4 / Eq. 10, stop or
+//                                   relax test, d±, c, ω, kept set, RHS
+//     bnd_assemble    (tiles × B)   H = Q + Gᵀ diag(ω) G on tcgen05 (3×TF32)
+//                                   tiles + the C / A rows and the diagonal
+//     per 64-column panel c0:
+//       bnd_tc_update (row tiles × B)  left-looking Schur update of the panel
+//                                   on tcgen05 (3×TF32): K[i][c0:c1] −=
+//                                   L[i][0:c0] S L[c0:c1][0:c0]ᵀ
+//       bnd_panel     (B CTAs)      16-wide blocked signed Cholesky of the
+//                                   panel + its diagonal-block inverses
+//     bnd_solve       (B CTAs)      the two triangular solves (solve_qd)
+//     bnd_update      (B CTAs)      Δv recovery, fraction-to-boundary step,
+//                                   retraction — or, on the relaxed
+//                                   iteration of the backward, Alg. 3
+//
+// Every phase calls the SAME device building blocks as the persistent kernel
+// (residuals, compact_active, syrk_tile, tc_left_update, factor_big_range,
+// invert_diag_block, solve_qd, recover_dv, newton_update, write_gradients),
+// so the arithmetic of a Newton step is unchanged; only the schedule differs.
+// Per-problem state (the iterate and the per-constraint vectors — the
+// persistent kernel's shared-memory carve-up, Smem) lives in a global state
+// block per problem, copied into shared memory by the phases that compute on
+// it; the KKT matrix lives in a per-problem global workspace in the packed
+// 16-row-block layout of ipm_cta.cuh.  DESIGN.md §5.
+#pragma once
+#include "ipm_kernels.cuh"
+#include "kr_gemm.cuh"
+
+namespace qpb {
+
+enum { BM_DONE = 0, BM_INIT = 1, BM_NEWTON = 2, BM_ADJ = 3 };
+
+// Per-problem scalars: the first 16 words of every state block.
+struct BScal {
+  float kappa, kt, fl, phi_prev;
+  float dmax;  // max |diag| of this iteration's KKT matrix (pivot floor θ = floor_rel·dmax)
+  int mode, pa, it, status, ok;
+  int pad[6];
+};
+static_assert(sizeof(BScal) == 64, "BScal: 16 words");
+
+struct BArgs {
+  Args a;               // problem data, outputs, settings (as for ipm_kernel)
+  float* st;            // state blocks [B][st_stride]: BScal, then the Smem layout (no KKT buffer)
+  long long st_stride;  // floats per state block (multiple of 4)
+  float* kw;            // KKT workspaces [B][kstride] (packed layout of capacity Nmax)
+  long long kstride;
+  int* ctl;             // [0] problems still iterating after bnd_resid, [1] largest N4 among them
+  int k;                // iteration index (bnd_resid)
+  int c0, w;            // panel (bnd_tc_update, bnd_panel)
+  int ntiles;           // H tiles of the assembly (lower triangle of ⌈n4/128⌉² tiles; 0 = kr_gemm assembles H)
+  // shared G (kr_gemm.cuh): this iteration's Ω rows (hi/lo tf32 split) of
+  // the iterating problems by slot, and slot -> problem
+  float *whi, *wlo;
+  int* slotmap;
+  int kr;
+};
+
+__device__ __forceinline__ float* st_of(const BArgs& b, int bid) { return b.st + (long long)bid * b.st_stride; }
+__device__ __forceinline__ BScal& scal_of(float* st) { return *reinterpret_cast<BScal*>(st); }
+__device__ __forceinline__ Smem carve_state(float* st, const Args& a) {
+  return layout(st + 16, a.n4, a.m, a.p, a.N4max, 0, 0, 0);
+}
+__host__ inline long long bnd_state_floats(int n4, int m, int p, int N4max) {
+  return (16 + (long long)(ipm_smem_bytes(n4, m, p, N4max, 0, 0, 0) / 4) + 3) & ~3LL;
+}
+
+// float4 copy of a state block (global ↔ shared), whole CTA, then a barrier
+template <int NT>
+__device__ __forceinline__ void copy_block(float* __restrict__ dst, const float* __restrict__ src, long long nf) {
+  const float4* s4 = reinterpret_cast<const float4*>(src);
+  float4* d4 = reinterpret_cast<float4*>(dst);
+  for (long long i = threadIdx.x; i < (nf >> 2); i += NT) d4[i] = s4[i];
+  __syncthreads();
+}
+
+// The problem's KKT layout of this iteration: N = n4 + |kept| + m.
+__device__ __forceinline__ KLayout bnd_layout(const Args& a, int pa) { return KLayout::make(a.n4 + pa + a.m, a.n4); }
+
+// Solve finished (converged / failed / max_iter): outputs to the caller.
+template <int NT>
+__device__ void bnd_finish_solve(const Args& a, const Smem& S, BScal& h, int bid) {
+  const int tid = threadIdx.x, n = a.n, m = a.m, p = a.p;
+  for (int j = tid; j < n; j += NT) a.x[(long long)bid * n + j] = S.x[j];
+  for (int l = tid; l < m; l += NT) a.y[(long long)bid * m + l] = S.y[l];
+  for (int i = tid; i < p; i += NT) {
+    a.z[(long long)bid * p + i] = S.z[i];
+    a.s[(long long)bid * p + i] = S.s[i];
+  }
+  if (tid == 0) {
+    a.iters[bid] = h.it;
+    a.status[bid] = h.status;
+    if (a.status_out) a.status_out[bid] = h.status;
+    if (a.flops) a.flops[bid] = h.fl;
+    h.mode = BM_DONE;
+  }
+}
+
+// Backward finished: gradients (zero-filled unless h.ok) and counters.
+template <int NT>
+__device__ void bnd_finish_backward(const Args& a, const Smem& S, BScal& h, int bid) {
+  const int tid = threadIdx.x, n = a.n, m = a.m, p = a.p;
+  __syncthreads();
+  if (!h.ok) {
+    for (int j = tid; j < n; j += NT) { S.dx[j] = 0.f; S.x[j] = 0.f; }
+    for (int l = tid; l < m; l += NT) { S.dy[l] = 0.f; S.y[l] = 0.f; }
+    for (int i = tid; i < p; i += NT) { S.dz[i] = 0.f; S.z[i] = 0.f; }
+    __syncthreads();
+  }
+  write_gradients<NT>(S, a, bid);
+  if (tid == 0) {
+    if (a.riters) a.riters[bid] = h.it;
+    if (a.rstatus) a.rstatus[bid] = h.status;
+    if (a.flops) a.flops[bid] = h.fl + 2.f * (n * n + m * n + p * n);
+    h.mode = BM_DONE;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// bnd_begin: solve — the CVXOPT initial system (reading Q11; the
+// persistent kernel's iteration −1): ω = 1, nothing kept, right-hand side
+// (−q + Gᵀh, b).  Backward — the solution of the last solve and its status.
+// ---------------------------------------------------------------------------
+template <int NT>
+__global__ void __launch_bounds__(NT) bnd_begin(const BArgs ba) {
+  extern __shared__ __align__(16) float sm[];
+  const Args& a = ba.a;
+  const int bid = blockIdx.x, tid = threadIdx.x;
+  const int n = a.n, n4 = a.n4, m = a.m, p = a.p;
+  float* gst = st_of(ba, bid);
+  const Smem S = carve_state(sm, a);
+  BScal& h = scal_of(sm);
+  const Prob P = prob_of(a, bid);
+  if (tid == 0) {
+    h.kappa = 0.f; h.kt = 0.f; h.fl = 0.f; h.phi_prev = INFINITY; h.dmax = 0.f;
+    h.pa = 0; h.it = 0; h.status = ST_CONVERGED; h.ok = 0;
+  }
+  if (!a.bwd) {
+    for (int i = tid; i < p; i += NT) { S.om[i] = 1.f; S.v[i] = -1.f; }
+    __syncthreads();
+    compact_active<NT>(S, p, true, p);
+    for (int j = tid; j < n4; j += NT) {
+      float acc = 0.f;
+      if (j < n) {
+        acc = -__ldg(P.q + j);
+        for (int i = 0; i < p; ++i) acc = fmaf(__ldg(P.G + i * n + j), __ldg(P.h + i), acc);
+      }
+      S.rhs[j] = acc;
+    }
+    for (int l = tid; l < m; l += NT) S.rhs[n4 + l] = __ldg(P.b + l);
+    for (int j = n4 + m + tid; j < r4(n4 + m); j += NT) S.rhs[j] = 0.f;
+    if (tid == 0) {
+      h.mode = BM_INIT;
+      h.fl = iter_flops(n, m, p, 0, false, true, true);
+    }
+    if (ba.kr) {  // Ω row of the initial system: ω = 1
+      __shared__ int slot0;
+      if (tid == 0) { slot0 = atomicAdd(ba.ctl, 1); ba.slotmap[slot0] = bid; }
+      __syncthreads();
+      kr::write_omega<NT>(ba.whi, ba.wlo, slot0, S.om, p, true);
+    }
+  } else {
+    for (int j = tid; j < n; j += NT) S.x[j] = a.x[(long long)bid * n + j];
+    for (int l = tid; l < m; l += NT) S.y[l] = a.y[(long long)bid * m + l];
+    for (int i = tid; i < p; i += NT) {
+      S.z[i] = a.z[(long long)bid * p + i];
+      S.s[i] = a.s[(long long)bid * p + i];
+    }
+    const bool solved = (a.status[bid] & 0xff) == ST_CONVERGED;
+    if (tid == 0) {
+      h.mode = BM_NEWTON;  // bnd_resid decides
+      if (!solved) h.status = ST_FAIL | (STG_RELAX << 8);
+    }
+    __syncthreads();
+    if (!solved) bnd_finish_backward<NT>(a, S, h, bid);
+  }
+  __syncthreads();
+  copy_block<NT>(gst, sm, ba.st_stride);
+}
+
+// ---------------------------------------------------------------------------
+// bnd_resid (iteration k ≥ 0): manifold coordinates, residuals and the
+// stopping test (solve: Q4; backward: the relax test Q5/Q5b), then the data
+// of this iteration's Newton system — exactly the head of the persistent
+// kernel's loop body.
+// ---------------------------------------------------------------------------
+template <int NT>
+__global__ void __launch_bounds__(NT) bnd_resid(const BArgs ba) {
+  extern __shared__ __align__(16) float sm[];
+  const Args& a = ba.a;
+  const int bid = blockIdx.x, tid = threadIdx.x;
+  const int n = a.n, n4 = a.n4, m = a.m, p = a.p;
+  float* gst = st_of(ba, bid);
+  if (scal_of(gst).mode == BM_DONE) return;
+  copy_block<NT>(sm, gst, ba.st_stride);
+  const Smem S = carve_state(sm, a);
+  BScal& h = scal_of(sm);
+  const Prob P = prob_of(a, bid);
+  const bool bwd = a.bwd != 0;
+  const int k = ba.k;
+  const float kappa = manifold_coords<NT>(S, a);
+  const float kt = bwd ? a.kappa_relax : a.sigma * kappa;
+  const Norms R = residuals<NT>(S, a, P, kappa, kappa - kt);
+  bool fin = false, adj = false;
+  int status = ST_CONVERGED;
+  float fl = h.fl, phi_prev = h.phi_prev;
+  if (R.nonfin > 0.f) {
+    status = ST_FAIL | ((bwd ? STG_RELAX : STG_SCALING) << 8);
+    fin = true;
+  } else if (!bwd) {
+    if (converged_solve(R, a.tol)) {
+      fl += iter_flops(n, m, p, 0, true, false, false);
+      fin = true;
+    } else if (k == a.max_iter) {
+      fl += iter_flops(n, m, p, 0, true, false, false);
+      status = ST_MAX_ITER;
+      fin = true;
+    }
+  } else {
+    const bool kok = p == 0 || fabsf(kappa / a.kappa_relax - 1.f) <= a.relax_ktol;
+    adj = kok && relax_done(R, a.tol, a.relax_tol, phi_prev);
+    phi_prev = kok ? rel_phi(R) : INFINITY;
+    if (!adj && k == a.relax_max_iter) {
+      status = ST_MAX_ITER | (STG_RELAX << 8);
+      fin = true;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    h.it = k; h.status = status; h.fl = fl; h.phi_prev = phi_prev;
+    h.kappa = kappa; h.kt = kt; h.pa = R.pa; h.dmax = 0.f; h.ok = 0;
+  }
+  if (fin) {
+    __syncthreads();
+    if (!bwd) bnd_finish_solve<NT>(a, S, h, bid);
+    else bnd_finish_backward<NT>(a, S, h, bid);
+  } else {
+    if (adj)  // Algorithm 3: the relaxed system with right-hand side (−∇ₓℓ, 0, 0)
+      for (int j = tid; j < a.N4max; j += NT) S.rhs[j] = j < n ? -__ldg(a.dl + (long long)bid * n + j) : 0.f;
+    __shared__ int slot;
+    if (tid == 0) {
+      h.mode = adj ? BM_ADJ : BM_NEWTON;
+      h.fl = fl + iter_flops(n, m, p, R.pa, true, true, true);
+      slot = atomicAdd(ba.ctl, 1);
+      atomicMax(ba.ctl + 1, r4(n4 + R.pa + m));
+      if (ba.kr) ba.slotmap[slot] = bid;
+    }
+    if (ba.kr) {  // this problem's Ω row for the batched assembly GEMM
+      __syncthreads();
+      kr::write_omega<NT>(ba.whi, ba.wlo, slot, S.om, p, false);
+    }
+  }
+  __syncthreads();
+  copy_block<NT>(gst, sm, ba.st_stride);
+}
+
+// ---------------------------------------------------------------------------
+// bnd_assemble: grid (ntiles + 1, B).  CTA x < ntiles: one 128×128 tile of
+// H = Q + Gᵀ diag(ω) G (tcgen05, 3×TF32; tc_syrk.cuh), lower triangle, the
+// epilogue adding Q (identity on the padding rows n..n4).  CTA x = ntiles:
+// the rows ≥ n4 — zeroed, then the kept C rows d₊ₖ gₖ, the A rows and the
+// diagonal (−d₋ on the kept rows, 0 for y, −1 on padding).  Both record
+// max|diag| (θ of the pivot floor) with an atomic max.
+// ---------------------------------------------------------------------------
+template <int NT>
+__global__ void __launch_bounds__(NT) bnd_assemble(const BArgs ba) {
+  extern __shared__ __align__(128) float smtc[];
+  float* sm = smtc;
+  const Args& a = ba.a;
+  const int bid = blockIdx.y, tid = threadIdx.x;
+  const int n = a.n, n4 = a.n4, p = a.p;
+  float* gst = st_of(ba, bid);
+  BScal& h = scal_of(gst);
+  if (h.mode == BM_DONE) return;
+  const Smem S = carve_state(gst, a);  // global state (read only here)
+  const int pa = h.pa;
+  const KLayout L = bnd_layout(a, pa);
+  float* K = ba.kw + (long long)bid * ba.kstride;
+  const Prob P = prob_of(a, bid);
+  const int N = L.N, N4 = L.N4;
+  float dmax = 0.f;
+  if ((int)blockIdx.x == ba.ntiles) {
+    if (n4 < N4) {
+      float4* K4 = reinterpret_cast<float4*>(K);
+      for (int i = (L.off(n4) >> 2) + tid; i < (L.size() >> 2); i += NT) K4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncthreads();
+    // one warp per row: coalesced row segments of G / A into row n4 + rr
+    const int nrow = N - n4;
+    for (int rr = tid >> 5; rr < nrow; rr += NT / 32) {
+      const float* src;
+      float w = 1.f;
+      if (rr < pa) {
+        const int kk = S.act[rr];
+        src = P.G + (size_t)kk * n;
+        w = S.dp[kk];
+      } else {
+        src = P.A + (size_t)(rr - pa) * n;
+      }
+      float* dst = K + L.off(n4 + rr);
+      for (int j = tid & 31; j < n; j += 32) dst[j] = w * __ldg(src + j);
+    }
+    for (int r = n4 + tid; r < N4; r += NT) {
+      float d;
+      if (r < n4 + pa) {
+        const float e = S.dm[S.act[r - n4]];
+        d = -e;
+        dmax = fmaxf(dmax, fabsf(e));
+      } else {
+        d = r < N ? 0.f : -1.f;
+      }
+      K[L.off(r) + r] = d;
+    }
+  } else {
+    int I = 0, t = blockIdx.x;
+    while (t > I) { t -= I + 1; ++I; }
+    const int i0 = tc::TM * I, j0 = tc::TN * t;
+    const tc::TcState ts = tc::tc_state(sm);
+    tc::tmem_alloc(ts);
+    tc::syrk_tile<NT>(ts, P.G, S.om, p, n, i0, j0, [&](int row0, int j, const float* tt) {
+      float qv[32];
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        const int i = row0 + r;
+        qv[r] = (i < n && j < n && j <= i) ? __ldg(P.Q + (size_t)i * n + j) : 0.f;
+      }
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        const int i = row0 + r;
+        if (i < n4 && j <= i) {
+          const float val = (i < n && j < n) ? qv[r] + tt[33 * r] : (i == j ? 1.f : 0.f);
+          K[L.off(i) + j] = val;
+          if (i == j && i < n) dmax = fmaxf(dmax, fabsf(val));
+        }
+      }
+    });
+    tc::tmem_free(*ts.tmem_slot);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+  if ((tid & 31) == 0 && dmax > 0.f) atomicMax(reinterpret_cast<int*>(&h.dmax), __float_as_int(dmax));
+}
+
+// ---------------------------------------------------------------------------
+// bnd_tc_update: grid (row tiles, B), panel [c0, c0 + w), c0 > 0: rows
+// [c0 + 128·x, +128) of the panel brought up to date with every earlier
+// column on tcgen05 (tc_factor.cuh tc_left_update, 3×TF32).
+// ---------------------------------------------------------------------------
+template <int NT>
+__global__ void __launch_bounds__(NT) bnd_tc_update(const BArgs ba) {
+  extern __shared__ __align__(128) float smtc[];
+  float* sm = smtc;
+  const Args& a = ba.a;
+  const int bid = blockIdx.y;
+  const BScal& h = scal_of(st_of(ba, bid));
+  if (h.mode == BM_DONE) return;
+  const KLayout L = bnd_layout(a, h.pa);
+  const int c0 = ba.c0, i0 = c0 + tc::TM * (int)blockIdx.x;
+  if (c0 >= L.N4 || i0 >= L.N4) return;
+  const int c1 = min(c0 + ba.w, L.N4);
+  float* K = ba.kw + (long long)bid * ba.kstride;
+  const tc::TcState ts = tc::tc_state(sm);
+  tc::tmem_alloc(ts);
+  tc_left_update<NT>(ts, K, L, c0, (c1 - c0 + 15) & ~15, i0);
+  tc::tmem_free(*ts.tmem_slot);
+}
+
+// ---------------------------------------------------------------------------
+// bnd_panel: grid B, panel [c0, c0 + w) (w = 64 except the last panel):
+//   1. the w×w diagonal block is copied to shared memory and factored there
+//      (factor_big_range on a dense PanelLayout: warp-factored 16×16
+//      diagonal blocks, TRSM, update; pivot floor θ = floor_rel·max|diag|,
+//      reading Q12), its 16×16 diagonal-block inverses W_b formed (solve_qd),
+//      and the block written back;
+//   2. every row i below the block is finished by ONE thread in registers:
+//      forward substitution of its 64 panel entries against the factored
+//      block, x_k = a_k / L_kk, a_j −= x_k L_jk (j > k), stored L_ik = S_k x_k
+//      — the TRSM and the in-panel Schur updates of all four 16-column blocks
+//      in one pass over the row (64 loads, 2016 FMAs, 64 stores).
+// ---------------------------------------------------------------------------
+template <int NT>
+__global__ void __launch_bounds__(NT, 2) bnd_panel(const BArgs ba) {
+  constexpr int W = 64, DS = 68;  // panel width, dense row stride (odd multiple of 16 B)
+  __shared__ __align__(16) float D[W * DS];
+  __shared__ __align__(16) float DT[W * DS];  // DT[k][j] = L[j][k]: column k contiguous (float4 broadcasts)
+  __shared__ float scr[16 * 17 + 16];
+  __shared__ float rl[W];
+  const Args& a = ba.a;
+  const int bid = blockIdx.x, tid = threadIdx.x;
+  float* gst = st_of(ba, bid);
+  const BScal& h = scal_of(gst);
+  if (h.mode == BM_DONE) return;
+  const KLayout L = bnd_layout(a, h.pa);
+  const int c0 = ba.c0, N4 = L.N4;
+  if (c0 >= N4) return;
+  const int c1 = min(c0 + W, N4), w = c1 - c0;
+  float* K = ba.kw + (long long)bid * ba.kstride;
+  float* rinv = carve_state(gst, a).rinv;
+  // 1. diagonal block → smem (lower part, zeros above), factor, inverses, back
+  for (int e = tid; e < w * (W / 4); e += NT) {
+    const int r = e / (W / 4), q = e - r * (W / 4), i = c0 + r, j = c0 + 4 * q;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (4 * q < w && j <= i) v = *reinterpret_cast<const float4*>(K + L.off(i) + j);
+    *reinterpret_cast<float4*>(D + r * DS + 4 * q) = v;
+  }
+  __syncthreads();
+  PanelLayout P;
+  P.N4 = c1; P.NB = L.NB; P.npos = L.npos; P.c0 = c0; P.S = DS; P.base = L;
+  factor_big_range<NT>(D - c0, P, a.floor_rel * h.dmax, rinv, scr, c0, c1);
+  __syncthreads();
+  for (int b = c0 / KB + (tid >> 5); KB * b < c1; b += NT / 32) invert_diag_block(D - c0, P, b, rinv);
+  for (int k = tid; k < w; k += NT) rl[k] = rinv[c0 + k];
+  __syncthreads();
+  for (int e = tid; e < W * W; e += NT) {
+    const int j = e / W, k = e - j * W;
+    DT[k * DS + j] = (j < w && k < j) ? D[j * DS + k] : 0.f;
+  }
+  __syncthreads();
+  for (int e = tid; e < w * (W / 4); e += NT) {  // row i keeps columns up to the end of its 16-block
+    const int r = e / (W / 4), q = e - r * (W / 4), i = c0 + r, j = c0 + 4 * q;
+    if (4 * q < w && j < ((i >> 4) + 1) * KB)
+      *reinterpret_cast<float4*>(K + L.off(i) + j) = *reinterpret_cast<const float4*>(D + r * DS + 4 * q);
+  }
+  if (c1 >= N4) return;
+  // 2. rows below: one thread per row, the whole 64-column forward substitution in registers
+  for (int i = c1 + tid; i < N4; i += NT) {
+    float* row = K + L.off(i) + c0;
+    float x[W];
+#pragma unroll
+    for (int q = 0; q < W / 4; ++q) {
+      const float4 t = reinterpret_cast<const float4*>(row)[q];
+      x[4 * q] = t.x; x[4 * q + 1] = t.y; x[4 * q + 2] = t.z; x[4 * q + 3] = t.w;
+    }
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      x[k] *= rl[k];
+      const float xk = -x[k];
+#pragma unroll
+      for (int j4 = (k + 1) >> 2; j4 < W / 4; ++j4) {
+        const float4 d = *reinterpret_cast<const float4*>(DT + k * DS + 4 * j4);
+        if (4 * j4 > k) x[4 * j4] = fmaf(xk, d.x, x[4 * j4]);
+        if (4 * j4 + 1 > k) x[4 * j4 + 1] = fmaf(xk, d.y, x[4 * j4 + 1]);
+        if (4 * j4 + 2 > k) x[4 * j4 + 2] = fmaf(xk, d.z, x[4 * j4 + 2]);
+        x[4 * j4 + 3] = fmaf(xk, d.w, x[4 * j4 + 3]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < W / 4; ++q) {
+      const float s0 = sgn_of(c0 + 4 * q, L.npos);  // S_k (npos is a multiple of 4)
+      reinterpret_cast<float4*>(row)[q] =
+          make_float4(s0 * x[4 * q], s0 * x[4 * q + 1], s0 * x[4 * q + 2], s0 * x[4 * q + 3]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// bnd_solve: grid B — forward and backward substitution with the factor
+// (solve_qd), right-hand side staged in shared memory.
+// ---------------------------------------------------------------------------
+template <int NT>
+__global__ void __launch_bounds__(NT) bnd_solve(const BArgs ba) {
+  extern __shared__ __align__(16) float sm[];
+  const Args& a = ba.a;
+  const int bid = blockIdx.x;
+  float* gst = st_of(ba, bid);
+  const BScal& h = scal_of(gst);
+  if (h.mode == BM_DONE) return;
+  const KLayout L = bnd_layout(a, h.pa);
+  const Smem G = carve_state(gst, a);
+  const float* K = ba.kw + (long long)bid * ba.kstride;
+  copy_block<NT>(sm, G.rhs, L.N4);
+  solve_qd<NT>(K, L, G.rinv, sm);
+  __syncthreads();
+  copy_block<NT>(G.rhs, sm, L.N4);
+}
+
+// ---------------------------------------------------------------------------
+// bnd_update: grid B — the tail of the loop body: the initial point (INIT),
+// the Newton step with its fraction-to-boundary step length and retraction
+// (NEWTON), or Alg. 3's gradients from the relaxed factorisation (ADJ).
+// ---------------------------------------------------------------------------
+template <int NT>
+__global__ void __launch_bounds__(NT) bnd_update(const BArgs ba) {
+  extern __shared__ __align__(16) float sm[];
+  const Args& a = ba.a;
+  const int bid = blockIdx.x, tid = threadIdx.x;
+  const int n = a.n, n4 = a.n4, m = a.m, p = a.p;
+  float* gst = st_of(ba, bid);
+  if (scal_of(gst).mode == BM_DONE) return;
+  copy_block<NT>(sm, gst, ba.st_stride);
+  const Smem S = carve_state(sm, a);
+  BScal& h = scal_of(sm);
+  const Prob P = prob_of(a, bid);
+  const bool bwd = a.bwd != 0;
+  const int mode = h.mode, pa = h.pa;
+  if (mode == BM_INIT) {
+    for (int j = tid; j < n; j += NT) S.x[j] = S.rhs[j];
+    for (int l = tid; l < m; l += NT) S.y[l] = S.rhs[n4 + l];
+    __syncthreads();
+    rowdots<NT>(P.G, p, n, S.x, S.dz);
+    for (int i = tid; i < p; i += NT) S.dz[i] -= __ldg(P.h + i);  // ẑ = Gx − h
+    __syncthreads();
+    float ap = -INFINITY, ad = -INFINITY, bad = 0.f;
+    for (int i = tid; i < p; i += NT) {
+      const float zh = S.dz[i];
+      ap = fmaxf(ap, zh); ad = fmaxf(ad, -zh);
+      if (!isfinite(zh)) bad = 1.f;
+    }
+    for (int j = tid; j < n; j += NT) if (!isfinite(S.x[j])) bad = 1.f;
+    float v[3] = {ap, ad, bad};
+    block_reduce<NT, 0, 3>(v, S.red);
+    for (int i = tid; i < p; i += NT) {  // s~ = −ẑ, z~ = ẑ, shifted into the interior
+      const float zh = S.dz[i];
+      S.s[i] = v[0] >= 0.f ? -zh + (1.f + v[0]) : -zh;
+      S.z[i] = v[1] >= 0.f ? zh + (1.f + v[1]) : zh;
+    }
+    __syncthreads();
+    if (v[2] > 0.f) {
+      if (tid == 0) { h.status = ST_FAIL | (STG_INIT << 8); h.it = 0; }
+      __syncthreads();
+      bnd_finish_solve<NT>(a, S, h, bid);
+    } else if (tid == 0) {
+      h.mode = BM_NEWTON;
+    }
+  } else if (mode == BM_NEWTON) {
+    float kappa = h.kappa;
+    int stage = 0;
+    const bool okstep = newton_update<NT>(S, a, P, pa, kappa, kappa - h.kt, &stage);
+    if (!okstep) {
+      if (tid == 0) h.status = ST_FAIL | ((bwd ? STG_RELAX : stage) << 8);
+      __syncthreads();
+      if (!bwd) bnd_finish_solve<NT>(a, S, h, bid);
+      else bnd_finish_backward<NT>(a, S, h, bid);
+    } else if (tid == 0) {
+      h.kappa = kappa;
+    }
+  } else {  // BM_ADJ: dv = G dx + w (f2 = 0), dz = d₊ ⊙ dv (reading Q8), Alg. 3 outer products
+    recover_dv<NT>(S, a, P, true);
+    for (int i = tid; i < p; i += NT) S.dz[i] = S.dp[i] * S.gx[i];
+    for (int j = tid; j < n; j += NT) S.dx[j] = S.rhs[j];
+    for (int l = tid; l < m; l += NT) S.dy[l] = S.rhs[n4 + pa + l];
+    __syncthreads();
+    float bad = 0.f;
+    for (int j = tid; j < n; j += NT) if (!isfinite(S.dx[j])) bad = 1.f;
+    for (int i = tid; i < p; i += NT) if (!isfinite(S.dz[i])) bad = 1.f;
+    for (int l = tid; l < m; l += NT) if (!isfinite(S.dy[l])) bad = 1.f;
+    float v[1] = {bad};
+    block_reduce<NT, 0, 1>(v, S.red);
+    if (tid == 0) {
+      h.ok = !(v[0] > 0.f);
+      if (!h.ok) h.status = ST_FAIL | (STG_BACKWARD << 8);
+    }
+    __syncthreads();
+    bnd_finish_backward<NT>(a, S, h, bid);
+  }
+  __syncthreads();
+  copy_block<NT>(gst, sm, ba.st_stride);
+}
+
+}  // namespace qpb

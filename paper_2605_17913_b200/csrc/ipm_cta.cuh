@@ -154,7 +154,8 @@ __device__ __forceinline__ float block_min(float a, float* red) {
 // diag(W) = rinv.  Used by solve_qd to turn the serial diagonal-block
 // substitutions into 16×16 matrix-vector products.
 // ------------------------------------------------------------------------
-__device__ __forceinline__ void invert_diag_block(float* __restrict__ K, const KLayout& L, int b,
+template <class LT = KLayout>
+__device__ __forceinline__ void invert_diag_block(float* __restrict__ K, const LT& L, int b,
                                                   const float* __restrict__ rinv) {
   const int lane = threadIdx.x & 31;
   const int k0 = KB * b, kb = L.bw(b);

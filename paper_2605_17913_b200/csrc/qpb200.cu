@@ -19,6 +19,7 @@
 #include "../../include/qpb200.h"
 #include "xpm_kernels.cuh"
 #include "tc_syrk.cuh"
+#include "bnd_kernels.cuh"
 
 namespace {
 
@@ -33,6 +34,7 @@ struct Layout {
   int pcap;              // path 1: largest kept set |A| (reading Q12c; p = no cap)
   long long kglob;       // global workspace floats per CTA (worst case)
   bool big;              // some reduced systems may exceed 256 rows (factor_big compiled in)
+  bool batched;          // big shapes: the batched phase engine (bnd_kernels.cuh, path 4)
   int threads, minb;     // kernel shape
   size_t smem;
 };
@@ -66,6 +68,7 @@ Layout make_layout(int n, int m, int p, int formulation, int batch = 0, int sms 
   L.N4max = (L.Nmax + 3) & ~3;
   L.kglob = qpb::KLayout::make(L.Nmax, L.n4).size();
   L.big = false;
+  L.batched = false;
   // Path 1 (below) when the worst case has at most 256 rows and a buffer of
   // the size it needs fits; otherwise the large-N kernels: one CTA per SM
   // with the largest smem buffer, iterations with a larger reduced system in
@@ -148,6 +151,9 @@ Layout make_layout(int n, int m, int p, int formulation, int batch = 0, int sms 
     if (env_cap >= 0) L.ncap = std::min(env_cap, L.ncap);
     if (getenv("QPB200_FORCE_GLOBAL")) L.ncap = 0;
     L.threads = 256; L.minb = 1;
+    // the batched phase engine (path 4) unless the persistent large-N kernel
+    // is asked for (A/B experiments, parity tests of that kernel)
+    L.batched = formulation != QP_EXPLICIT && !getenv("QPB200_PERSISTENT_BIG");
   }
   L.ksmem = L.ncap > 0 ? qpb::KLayout::make(L.ncap, L.n4).size() : 0;
   L.smem = qpb::ipm_smem_bytes(L.n4, m, p, L.N4max, L.ksmem, tc_floats(L.big), ro_ints(L, L.big));
@@ -218,6 +224,18 @@ struct qp_ctx {
   float* flops_bwd = nullptr;
   // host-memory mode, path 1: the batch runs in kPipe chunks on their own
   // streams, so chunk i's kernel overlaps chunk i+1's H2D and chunk i−1's D2H
+  // batched phase engine (path 4): per-problem state blocks and KKT
+  // workspaces for `bchunk` problems at a time, the iteration counters
+  float* bst = nullptr;
+  long long bst_stride = 0;
+  int bchunk = 0;
+  int* bctl = nullptr;       // device: [0] problems iterating, [1] largest N4
+  int* hctl = nullptr;       // pinned host copy
+  int blaunch[2] = {0, 0};   // kernel launches of the last solve / backward
+  // shared G: the assembly as one batched GEMM (kr_gemm.cuh)
+  bool kr = false;
+  float *whi = nullptr, *wlo = nullptr, *gghi = nullptr, *gglo = nullptr;
+  int* slotmap = nullptr;
   static constexpr int kPipe = 8;
   bool pipe = false;
   cudaStream_t pst[kPipe] = {};
@@ -240,7 +258,8 @@ qp_err dalloc(qp_ctx* c, T** p, size_t count) {
 size_t field_elems(int64_t stride, int32_t B, size_t per) { return stride == 0 ? per : (size_t)B * per; }
 
 void free_all(qp_ctx* c) {
-  void* ptrs[] = {c->tl, c->sched, c->done, c->kglob, c->flops_solve, c->flops_bwd, c->prof, c->own_status, c->wx, c->wy, c->wz, c->wdx, c->wdy, c->wdz, c->dQ_, c->dq_, c->dA_, c->db_,
+  if (c->hctl) cudaFreeHost(c->hctl);
+  void* ptrs[] = {c->whi, c->wlo, c->gghi, c->gglo, c->slotmap, c->bst, c->bctl, c->tl, c->sched, c->done, c->kglob, c->flops_solve, c->flops_bwd, c->prof, c->own_status, c->wx, c->wy, c->wz, c->wdx, c->wdy, c->wdz, c->dQ_, c->dq_, c->dA_, c->db_,
                   c->dG_, c->dh_, c->dx_, c->ds_, c->dz_, c->dy_, c->ddl_, c->dit_, c->dst_, c->gQ_, c->gq_,
                   c->gA_, c->gb_, c->gG_, c->gh_};
   for (void* p : ptrs)
@@ -313,6 +332,106 @@ template <typename T>
 static qp_err d2h(qp_ctx* c, T* dst, const T* src, size_t count) {
   if (count == 0 || !dst) return QP_OK;
   return cuda_ok(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+}
+
+constexpr int kBT = 128;  // threads of the batched-engine kernels
+constexpr int kBW = 64;   // panel width of the batched factorisation
+
+// smem attributes of the batched-engine kernels (once per process and shape)
+qp_err bnd_setup(const qp_ctx* c) {
+  const int sst = (int)(c->bst_stride * 4), ssv = (int)(c->L.N4max * 4);
+  const int stc = qpb::tc::SMEM_BYTES;
+  if (cudaFuncSetAttribute(qpb::bnd_begin<kBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sst) ||
+      cudaFuncSetAttribute(qpb::bnd_resid<kBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sst) ||
+      cudaFuncSetAttribute(qpb::bnd_update<kBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sst) ||
+      cudaFuncSetAttribute(qpb::bnd_solve<kBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, ssv) ||
+      cudaFuncSetAttribute(qpb::bnd_assemble<kBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, stc) ||
+      cudaFuncSetAttribute(qpb::bnd_tc_update<kBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, stc) ||
+      cudaFuncSetAttribute(qpb::kr::kr_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, qpb::kr::SMEM_BYTES))
+    return QP_ERR_CUDA;
+  return QP_OK;
+}
+
+// One call (solve: init + Alg. 1; backward: Alg. 2 + Alg. 3) on the batched
+// phase engine: chunks of c->bchunk problems, per chunk the host loop over
+// Newton iterations of bnd_kernels.cuh.  After bnd_resid the host reads back
+// how many problems still iterate (and their largest padded system size,
+// which bounds the panel loop), so the call returns once every problem has
+// finished (the stream is synchronised at each iteration).
+qp_err run_batched(qp_ctx* c, const qpb::Args& a0, bool bwd) {
+  const int B = a0.B;
+  const int n4 = c->L.n4, m = c->d.m_eq;
+  const int T = (n4 + qpb::tc::TM - 1) / qpb::tc::TM;
+  const int sst = (int)(c->bst_stride * 4), ssv = (int)(c->L.N4max * 4);
+  const int stc = qpb::tc::SMEM_BYTES;
+  int launches = 0;
+  cudaStream_t st = c->stream;
+  for (int b0 = 0; b0 < B; b0 += c->bchunk) {
+    const int nb = std::min(c->bchunk, B - b0);
+    qpb::BArgs ba;
+    std::memset(&ba, 0, sizeof(ba));
+    ba.a = chunk_args(a0, b0, nb);
+    ba.a.bwd = bwd ? 1 : 0;
+    ba.st = c->bst; ba.st_stride = c->bst_stride;
+    ba.kw = c->kglob; ba.kstride = c->L.kglob;
+    ba.ctl = c->bctl;
+    ba.ntiles = c->kr ? 0 : T * (T + 1) / 2;
+    ba.w = kBW;
+    ba.kr = c->kr ? 1 : 0;
+    ba.whi = c->whi; ba.wlo = c->wlo; ba.slotmap = c->slotmap;
+    qpb::kr::GemmArgs ga;
+    const int krN = (qpb::kr::npairs(n4) + qpb::kr::BN - 1) / qpb::kr::BN;
+    if (c->kr) {
+      ga.whi = c->whi; ga.wlo = c->wlo; ga.gghi = c->gghi; ga.gglo = c->gglo;
+      ga.count = c->bctl; ga.slotmap = c->slotmap;
+      ga.kw = c->kglob; ga.kstride = c->L.kglob; ga.st = c->bst; ga.st_stride = c->bst_stride;
+      ga.Q = ba.a.Q; ga.sQ = ba.a.sQ;
+      ga.n = c->d.n; ga.n4 = n4; ga.m = m; ga.p = c->d.p;
+      if (b0 == 0) {  // GG = the Khatri-Rao square of the shared G, once per call
+        qpb::kr::kr_prep<<<4 * 148, 256, 0, st>>>(a0.G, c->d.n, n4, c->d.p, c->gghi, c->gglo);
+        ++launches;
+      }
+    }
+    if (cudaMemsetAsync(c->bctl, 0, 2 * sizeof(int), st) != cudaSuccess) return QP_ERR_CUDA;
+    qpb::bnd_begin<kBT><<<nb, kBT, sst, st>>>(ba);
+    ++launches;
+    int N4cur = bwd ? 0 : qpb::r4(n4 + m);  // the initial system (solve)
+    const int kmax = bwd ? c->c.relax_max_iter : c->c.max_iter;
+    for (int k = bwd ? 0 : -1; k <= kmax + 1; ++k) {
+      if (k >= 0) {
+        if (cudaMemsetAsync(c->bctl, 0, 2 * sizeof(int), st) != cudaSuccess) return QP_ERR_CUDA;
+        ba.k = k;
+        qpb::bnd_resid<kBT><<<nb, kBT, sst, st>>>(ba);
+        ++launches;
+        if (cudaMemcpyAsync(c->hctl, c->bctl, 2 * sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess)
+          return QP_ERR_CUDA;
+        if (c->hctl[0] == 0) break;
+        N4cur = c->hctl[1];
+      }
+      qpb::bnd_assemble<kBT><<<dim3(ba.ntiles + 1, nb), kBT, ba.ntiles ? stc : 0, st>>>(ba);
+      ++launches;
+      if (c->kr) {
+        qpb::kr::kr_gemm<<<dim3(krN, (nb + qpb::kr::BM - 1) / qpb::kr::BM), 128, qpb::kr::SMEM_BYTES, st>>>(ga);
+        ++launches;
+      }
+      for (int c0 = 0; c0 < N4cur; c0 += kBW) {
+        ba.c0 = c0;
+        if (c0 > 0) {
+          qpb::bnd_tc_update<kBT><<<dim3((N4cur - c0 + qpb::tc::TM - 1) / qpb::tc::TM, nb), kBT, stc, st>>>(ba);
+          ++launches;
+        }
+        qpb::bnd_panel<kBT><<<nb, kBT, 0, st>>>(ba);
+        ++launches;
+      }
+      qpb::bnd_solve<kBT><<<nb, kBT, ssv, st>>>(ba);
+      qpb::bnd_update<kBT><<<nb, kBT, sst, st>>>(ba);
+      launches += 2;
+    }
+    if (cudaGetLastError() != cudaSuccess) return QP_ERR_CUDA;
+  }
+  c->blaunch[bwd ? 1 : 0] = launches;
+  return QP_OK;
 }
 
 }  // namespace
@@ -408,9 +527,40 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     ctx->grid = std::min(d->batch, std::max(1, sms * std::max(1, ctx->ctas_per_sm)));
-    const bool need_glob = L.big && L.ncap < L.Nmax;
+    const bool need_glob = L.big && L.ncap < L.Nmax && !L.batched;
     if (need_glob && (e = dalloc(ctx, &ctx->kglob, (size_t)ctx->grid * (size_t)L.kglob)) != QP_OK) {
       free_all(ctx); delete ctx; return e;
+    }
+  }
+  if (L.batched) {
+    // per problem: a state block and a KKT workspace of capacity Nmax, for
+    // up to half of the free device memory's worth of problems at a time
+    ctx->bst_stride = qpb::bnd_state_floats(L.n4, d->m_eq, d->p, L.N4max);
+    const size_t per = 4 * ((size_t)ctx->bst_stride + (size_t)L.kglob);
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    long long cap = (long long)(fr / 2 / per);
+    if (const char* e2 = getenv("QPB200_BCHUNK")) cap = atoll(e2);  // tests: force several chunks
+    ctx->bchunk = (int)std::max(1LL, std::min<long long>(d->batch, cap));
+    if ((e = dalloc(ctx, &ctx->bst, (size_t)ctx->bchunk * ctx->bst_stride)) != QP_OK ||
+        (e = dalloc(ctx, &ctx->kglob, (size_t)ctx->bchunk * (size_t)L.kglob)) != QP_OK ||
+        (e = dalloc(ctx, &ctx->bctl, 4)) != QP_OK) {
+      free_all(ctx); delete ctx; return e;
+    }
+    if (cudaMallocHost(&ctx->hctl, 4 * sizeof(int)) != cudaSuccess || bnd_setup(ctx) != QP_OK) {
+      free_all(ctx); delete ctx; return QP_ERR_CUDA;
+    }
+    // shared G: the assembly runs as one GEMM over the batch (kr_gemm.cuh)
+    ctx->kr = d->bstride_G == 0 && d->p > 0 && !getenv("QPB200_NO_KR");
+    if (ctx->kr) {
+      const size_t kpad = (size_t)qpb::kr::nkc(d->p) * qpb::kr::BK;
+      const size_t mrows = (size_t)((ctx->bchunk + qpb::kr::BM - 1) / qpb::kr::BM) * qpb::kr::BM;
+      const size_t nrows = (size_t)((qpb::kr::npairs(L.n4) + qpb::kr::BN - 1) / qpb::kr::BN) * qpb::kr::BN;
+      if ((e = dalloc(ctx, &ctx->whi, mrows * kpad)) || (e = dalloc(ctx, &ctx->wlo, mrows * kpad)) ||
+          (e = dalloc(ctx, &ctx->gghi, nrows * kpad)) || (e = dalloc(ctx, &ctx->gglo, nrows * kpad)) ||
+          (e = dalloc(ctx, &ctx->slotmap, ctx->bchunk))) {
+        free_all(ctx); delete ctx; return e;
+      }
     }
   }
   const int B = d->batch, n = d->n, m = d->m_eq, p = d->p;
@@ -469,7 +619,7 @@ qp_err qp_set_stream(qp_ctx* c, void* stream) {
 
 qp_err qp_get_info(const qp_ctx* c, qp_info* info) {
   if (!c || !info) return QP_ERR_INVALID_ARG;
-  info->path = !c->L.big ? 1 : (c->L.ncap > 0 ? 3 : 2);  // 1 smem, 2 global, 3 hybrid
+  info->path = !c->L.big ? 1 : c->L.batched ? 4 : (c->L.ncap > 0 ? 3 : 2);  // 1 smem, 2 global, 3 hybrid, 4 batched
   info->partition_cap = c->L.big ? c->d.p : c->L.pcap;
   info->threads = c->ks.threads;
   info->smem_bytes = (int32_t)c->L.smem;
@@ -485,6 +635,10 @@ qp_err qp_get_info(const qp_ctx* c, qp_info* info) {
   if (d.bstride_G == 0 && d.p > 0) ++extra;
   if (d.bstride_h == 0 && d.p > 0) ++extra;
   info->launches_backward = 1 + extra;
+  if (c->L.batched) {  // phase kernels: counted by the last calls
+    info->launches_solve = c->blaunch[0];
+    info->launches_backward = c->blaunch[1] + extra;
+  }
   info->workspace_bytes = c->workspace;
   return QP_OK;
 }
@@ -583,6 +737,8 @@ qp_err qp_solve_batched(qp_ctx* c, const float* Q, const float* q, const float* 
       if ((e = cuda_ok(cudaStreamWaitEvent(c->stream, c->pev[ch], 0))) != QP_OK) return e;
     }
     if (hsync && (e = cuda_ok(cudaStreamSynchronize(c->stream))) != QP_OK) return e;
+  } else if (c->L.batched) {
+    if ((e = run_batched(c, a, false)) != QP_OK) return e;
   } else {
     c->ks.solve<<<c->grid, c->ks.threads, c->L.smem, c->stream>>>(a);
     if ((e = cuda_ok(cudaGetLastError())) != QP_OK) return e;
@@ -735,6 +891,8 @@ qp_err qp_backward_batched(qp_ctx* c, const float* dl_dx, float* dQ, float* dq, 
       if ((e = cuda_ok(cudaEventRecord(c->pev[ch], st))) != QP_OK) return e;
       if ((e = cuda_ok(cudaStreamWaitEvent(c->stream, c->pev[ch], 0))) != QP_OK) return e;
     }
+  } else if (c->L.batched) {
+    if ((e = run_batched(c, a, true)) != QP_OK) return e;
   } else if (implicit && !c->L.big && !getenv("QPB200_NO_PDL")) {
     // programmatic stream serialisation: the backward grid may start while the
     // solve grid drains (each CTA waits on done[b] for its problem), so the

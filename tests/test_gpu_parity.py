@@ -198,7 +198,7 @@ def test_large_n_global_path():
     (n4 + min(p, n4) + m = 266)."""
     b = gen.g_rand(13, 8, 130, 4, 200)
     g = run_gpu(b)
-    assert g["info"]["path"] in (2, 3)
+    assert g["info"]["path"] == 4  # batched phase engine
     check_against_oracle(b, g)
 
 
@@ -207,20 +207,46 @@ def test_cfg4_shared_subset():
     batch-summed shared gradients."""
     b = gen.make_config(4, batch=16)
     g = run_gpu(b)
-    assert g["info"]["path"] in (2, 3)
+    assert g["info"]["path"] == 4  # batched phase engine
     check_against_oracle(b, g)
 
 
-def test_global_path_forced_matches_smem_path(monkeypatch):
-    """The same problems through path 1 and (forced) path 2 agree closely."""
+@pytest.mark.parametrize("engine", ["batched", "persistent"])
+def test_global_path_forced_matches_smem_path(monkeypatch, engine):
+    """The same problems through path 1 and, forced off it (QPB200_FORCE_GLOBAL),
+    through the batched phase engine (path 4) or the persistent large-N kernel
+    with its KKT matrix in the global workspace (path 2): close agreement and
+    the oracle bar."""
     b = gen.make_config(2, batch=32)
     g1 = run_gpu(b)
     monkeypatch.setenv("QPB200_FORCE_GLOBAL", "1")
+    if engine == "persistent":
+        monkeypatch.setenv("QPB200_PERSISTENT_BIG", "1")
     g2 = run_gpu(b)
-    assert g1["info"]["path"] in (1, 3) and g2["info"]["path"] == 2
+    assert g1["info"]["path"] == 1 and g2["info"]["path"] == (4 if engine == "batched" else 2)
     assert np.abs(g1["x"] - g2["x"]).max() <= 1e-4
     assert np.abs(g1["iters"] - g2["iters"]).max() <= 1
     check_against_oracle(b, g2)
+
+
+@pytest.mark.parametrize("chunk", [None, 5])
+def test_batched_engine_matches_persistent_large_n(monkeypatch, chunk):
+    """Config-4 shapes (16 problems, shared Q, G, h) on the batched phase
+    engine (path 4; with QPB200_BCHUNK = 5 in chunks of 5 problems, a ragged
+    last chunk) and on the persistent large-N kernel (path 3): the same Newton
+    arithmetic in a different schedule — iterations within ±1, x within 1e-4,
+    and both at the oracle bar."""
+    b = gen.make_config(4, batch=16)
+    if chunk:
+        monkeypatch.setenv("QPB200_BCHUNK", str(chunk))
+    g4 = run_gpu(b)
+    monkeypatch.setenv("QPB200_PERSISTENT_BIG", "1")
+    g3 = run_gpu(b)
+    assert g4["info"]["path"] == 4 and g3["info"]["path"] in (2, 3)
+    assert np.abs(g4["iters"].astype(int) - g3["iters"].astype(int)).max() <= 1
+    assert x_rel(g4["x"], g3["x"]).max() <= TOL_X
+    check_against_oracle(b, g4)
+    check_against_oracle(b, g3)
 
 
 def test_standard_arm_config3_ablation():

@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(NT) bnd_tc_update(const BArgs ba) {
 //      in one pass over the row (64 loads, 2016 FMAs, 64 stores).
 // ---------------------------------------------------------------------------
 template <int NT>
-__global__ void __launch_bounds__(NT, 2) bnd_panel(const BArgs ba) {
+__global__ void __launch_bounds__(NT, 4) bnd_panel(const BArgs ba) {
   constexpr int W = 64, DS = 68;  // panel width, dense row stride (odd multiple of 16 B)
   __shared__ __align__(16) float D[W * DS];
   __shared__ __align__(16) float DT[W * DS];  // DT[k][j] = L[j][k]: column k contiguous (float4 broadcasts)

@@ -23,8 +23,10 @@
 //       bnd_tc_update (row tiles × B)  left-looking Schur update of the panel
 //                                   on tcgen05 (3×TF32): K[i][c0:c1] −=
 //                                   L[i][0:c0] S L[c0:c1][0:c0]ᵀ
-//       bnd_panel     (B CTAs)      16-wide blocked signed Cholesky of the
-//                                   panel + its diagonal-block inverses
+//       bnd_pdiag     (B warps)     the panel's diagonal block: 16-wide
+//                                   blocked signed Cholesky + inverses
+//       bnd_prows     (row tiles × B)  the rows below it: per-thread
+//                                   register forward substitution
 //     bnd_solve       (B CTAs)      the two triangular solves (solve_qd)
 //     bnd_update      (B CTAs)      Δv recovery, fraction-to-boundary step,
 //                                   retraction — or, on the relaxed
@@ -64,13 +66,14 @@ struct BArgs {
   long long kstride;
   int* ctl;             // [0] problems still iterating after bnd_resid, [1] largest N4 among them
   int k;                // iteration index (bnd_resid)
-  int c0, w;            // panel (bnd_tc_update, bnd_panel)
+  int c0, w;            // panel (bnd_tc_update, bnd_pdiag, bnd_prows)
   int ntiles;           // H tiles of the assembly (lower triangle of ⌈n4/128⌉² tiles; 0 = kr_gemm assembles H)
   // shared G (kr_gemm.cuh): this iteration's Ω rows (hi/lo tf32 split) of
   // the iterating problems by slot, and slot -> problem
   float *whi, *wlo;
   int* slotmap;
   int kr;
+  float* dtg;           // [B][64·64]: the current panel's factored diagonal block, transposed (bnd_pdiag → bnd_prows)
 };
 
 __device__ __forceinline__ float* st_of(const BArgs& b, int bid) { return b.st + (long long)bid * b.st_stride; }
@@ -272,6 +275,64 @@ __global__ void __launch_bounds__(NT) bnd_resid(const BArgs ba) {
 }
 
 // ---------------------------------------------------------------------------
+// bnd_scatter: grid B — the rows ≥ n4 of the KKT matrix (zeroed, then the
+// kept C rows d₊ₖ gₖ, the A rows, the diagonal −d₋ / 0 / −1) when H comes
+// from kr_gemm (shared G); bnd_assemble's last CTA does the same otherwise.
+// ---------------------------------------------------------------------------
+template <int NT>
+__device__ __forceinline__ void scatter_rows(const Args& a, const Smem& S, const KLayout& L, float* K, const Prob& P,
+                                             int pa, float& dmax) {
+  const int tid = threadIdx.x, n = a.n, n4 = a.n4, N = L.N, N4 = L.N4;
+  if (n4 < N4) {
+    float4* K4 = reinterpret_cast<float4*>(K);
+    for (int i = (L.off(n4) >> 2) + tid; i < (L.size() >> 2); i += NT) K4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  __syncthreads();
+  // one warp per row: coalesced row segments of G / A into row n4 + rr
+  const int nrow = N - n4;
+  for (int rr = tid >> 5; rr < nrow; rr += NT / 32) {
+    const float* src;
+    float w = 1.f;
+    if (rr < pa) {
+      const int kk = S.act[rr];
+      src = P.G + (size_t)kk * n;
+      w = S.dp[kk];
+    } else {
+      src = P.A + (size_t)(rr - pa) * n;
+    }
+    float* dst = K + L.off(n4 + rr);
+    for (int j = tid & 31; j < n; j += 32) dst[j] = w * __ldg(src + j);
+  }
+  for (int r = n4 + tid; r < N4; r += NT) {
+    float d;
+    if (r < n4 + pa) {
+      const float e = S.dm[S.act[r - n4]];
+      d = -e;
+      dmax = fmaxf(dmax, fabsf(e));
+    } else {
+      d = r < N ? 0.f : -1.f;
+    }
+    K[L.off(r) + r] = d;
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) bnd_scatter(const BArgs ba) {
+  const Args& a = ba.a;
+  const int bid = blockIdx.x;
+  float* gst = st_of(ba, bid);
+  BScal& h = scal_of(gst);
+  if (h.mode == BM_DONE) return;
+  const int pa = h.pa;
+  const KLayout L = bnd_layout(a, pa);
+  float dmax = 0.f;
+  scatter_rows<NT>(a, carve_state(gst, a), L, ba.kw + (long long)bid * ba.kstride, prob_of(a, bid), pa, dmax);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+  if ((threadIdx.x & 31) == 0 && dmax > 0.f) atomicMax(reinterpret_cast<int*>(&h.dmax), __float_as_int(dmax));
+}
+
+// ---------------------------------------------------------------------------
 // bnd_assemble: grid (ntiles + 1, B).  CTA x < ntiles: one 128×128 tile of
 // H = Q + Gᵀ diag(ω) G (tcgen05, 3×TF32; tc_syrk.cuh), lower triangle, the
 // epilogue adding Q (identity on the padding rows n..n4).  CTA x = ntiles:
@@ -297,37 +358,7 @@ __global__ void __launch_bounds__(NT) bnd_assemble(const BArgs ba) {
   const int N = L.N, N4 = L.N4;
   float dmax = 0.f;
   if ((int)blockIdx.x == ba.ntiles) {
-    if (n4 < N4) {
-      float4* K4 = reinterpret_cast<float4*>(K);
-      for (int i = (L.off(n4) >> 2) + tid; i < (L.size() >> 2); i += NT) K4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    __syncthreads();
-    // one warp per row: coalesced row segments of G / A into row n4 + rr
-    const int nrow = N - n4;
-    for (int rr = tid >> 5; rr < nrow; rr += NT / 32) {
-      const float* src;
-      float w = 1.f;
-      if (rr < pa) {
-        const int kk = S.act[rr];
-        src = P.G + (size_t)kk * n;
-        w = S.dp[kk];
-      } else {
-        src = P.A + (size_t)(rr - pa) * n;
-      }
-      float* dst = K + L.off(n4 + rr);
-      for (int j = tid & 31; j < n; j += 32) dst[j] = w * __ldg(src + j);
-    }
-    for (int r = n4 + tid; r < N4; r += NT) {
-      float d;
-      if (r < n4 + pa) {
-        const float e = S.dm[S.act[r - n4]];
-        d = -e;
-        dmax = fmaxf(dmax, fabsf(e));
-      } else {
-        d = r < N ? 0.f : -1.f;
-      }
-      K[L.off(r) + r] = d;
-    }
+    scatter_rows<NT>(a, S, L, K, P, pa, dmax);
   } else {
     int I = 0, t = blockIdx.x;
     while (t > I) { t -= I + 1; ++I; }
@@ -383,25 +414,30 @@ __global__ void __launch_bounds__(NT) bnd_tc_update(const BArgs ba) {
 }
 
 // ---------------------------------------------------------------------------
-// bnd_panel: grid B, panel [c0, c0 + w) (w = 64 except the last panel):
-//   1. the w×w diagonal block is copied to shared memory and factored there
-//      (factor_big_range on a dense PanelLayout: warp-factored 16×16
-//      diagonal blocks, TRSM, update; pivot floor θ = floor_rel·max|diag|,
-//      reading Q12), its 16×16 diagonal-block inverses W_b formed (solve_qd),
-//      and the block written back;
-//   2. every row i below the block is finished by ONE thread in registers:
-//      forward substitution of its 64 panel entries against the factored
-//      block, x_k = a_k / L_kk, a_j −= x_k L_jk (j > k), stored L_ik = S_k x_k
-//      — the TRSM and the in-panel Schur updates of all four 16-column blocks
-//      in one pass over the row (64 loads, 2016 FMAs, 64 stores).
+// The panel [c0, c0 + w) (w = 64 except the last panel) after its Schur
+// update, in two kernels:
+//   bnd_pdiag (grid B, ONE warp per problem): the w×w diagonal block in
+//     shared memory, factored (factor_big_range on a dense PanelLayout:
+//     16×16 diagonal blocks with a register window, TRSM, update; pivot floor
+//     θ = floor_rel·max|diag|, reading Q12), its 16×16 diagonal-block
+//     inverses W_b formed (for solve_qd) and the block written back.  The
+//     pivot chain of a panel is inherently serial; one warp per problem keeps
+//     up to 12 such chains in flight per SM instead of one per 128 threads.
+//   bnd_prows (grid (128-row tiles, B)): every row i below the block finished
+//     by ONE thread in registers — forward substitution of its 64 panel
+//     entries against the factored block, x_k = a_k / L_kk, a_j −= x_k L_jk
+//     (j > k), stored L_ik = S_k x_k: the TRSM and the in-panel Schur updates
+//     of all four 16-column blocks in one pass over the row.
 // ---------------------------------------------------------------------------
+namespace pnl {
+constexpr int W = 64, DS = 68;  // panel width, dense row stride (odd multiple of 16 B)
+}
+
 template <int NT>
-__global__ void __launch_bounds__(NT, 4) bnd_panel(const BArgs ba) {
-  constexpr int W = 64, DS = 68;  // panel width, dense row stride (odd multiple of 16 B)
+__global__ void __launch_bounds__(NT) bnd_pdiag(const BArgs ba) {
+  using namespace pnl;
   __shared__ __align__(16) float D[W * DS];
-  __shared__ __align__(16) float DT[W * DS];  // DT[k][j] = L[j][k]: column k contiguous (float4 broadcasts)
   __shared__ float scr[16 * 17 + 16];
-  __shared__ float rl[W];
   const Args& a = ba.a;
   const int bid = blockIdx.x, tid = threadIdx.x;
   float* gst = st_of(ba, bid);
@@ -413,7 +449,6 @@ __global__ void __launch_bounds__(NT, 4) bnd_panel(const BArgs ba) {
   const int c1 = min(c0 + W, N4), w = c1 - c0;
   float* K = ba.kw + (long long)bid * ba.kstride;
   float* rinv = carve_state(gst, a).rinv;
-  // 1. diagonal block → smem (lower part, zeros above), factor, inverses, back
   for (int e = tid; e < w * (W / 4); e += NT) {
     const int r = e / (W / 4), q = e - r * (W / 4), i = c0 + r, j = c0 + 4 * q;
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -426,47 +461,71 @@ __global__ void __launch_bounds__(NT, 4) bnd_panel(const BArgs ba) {
   factor_big_range<NT>(D - c0, P, a.floor_rel * h.dmax, rinv, scr, c0, c1);
   __syncthreads();
   for (int b = c0 / KB + (tid >> 5); KB * b < c1; b += NT / 32) invert_diag_block(D - c0, P, b, rinv);
-  for (int k = tid; k < w; k += NT) rl[k] = rinv[c0 + k];
-  __syncthreads();
-  for (int e = tid; e < W * W; e += NT) {
-    const int j = e / W, k = e - j * W;
-    DT[k * DS + j] = (j < w && k < j) ? D[j * DS + k] : 0.f;
-  }
   __syncthreads();
   for (int e = tid; e < w * (W / 4); e += NT) {  // row i keeps columns up to the end of its 16-block
     const int r = e / (W / 4), q = e - r * (W / 4), i = c0 + r, j = c0 + 4 * q;
     if (4 * q < w && j < ((i >> 4) + 1) * KB)
       *reinterpret_cast<float4*>(K + L.off(i) + j) = *reinterpret_cast<const float4*>(D + r * DS + 4 * q);
   }
-  if (c1 >= N4) return;
-  // 2. rows below: one thread per row, the whole 64-column forward substitution in registers
-  for (int i = c1 + tid; i < N4; i += NT) {
-    float* row = K + L.off(i) + c0;
-    float x[W];
-#pragma unroll
-    for (int q = 0; q < W / 4; ++q) {
-      const float4 t = reinterpret_cast<const float4*>(row)[q];
-      x[4 * q] = t.x; x[4 * q + 1] = t.y; x[4 * q + 2] = t.z; x[4 * q + 3] = t.w;
+  if (c1 < N4) {  // rows below follow: the strictly lower part, transposed, for bnd_prows
+    float* dt = ba.dtg + (long long)bid * (W * W);
+    for (int e = tid; e < W * W; e += NT) {
+      const int k = e / W, j = e - k * W;
+      dt[e] = k < j ? D[j * DS + k] : 0.f;
     }
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT, 4) bnd_prows(const BArgs ba) {
+  using namespace pnl;
+  __shared__ __align__(16) float DT[W * DS];  // DT[k][j] = L[j][k] (j > k): column k contiguous (float4 broadcasts)
+  __shared__ float rl[W];
+  const Args& a = ba.a;
+  const int bid = blockIdx.y, tid = threadIdx.x;
+  float* gst = st_of(ba, bid);
+  const BScal& h = scal_of(gst);
+  if (h.mode == BM_DONE) return;
+  const KLayout L = bnd_layout(a, h.pa);
+  const int c0 = ba.c0, N4 = L.N4, c1 = c0 + W;
+  const int r0 = c1 + NT * (int)blockIdx.x;
+  if (c1 >= N4 || r0 >= N4) return;  // (rows below a panel exist only when it is 64 wide)
+  float* K = ba.kw + (long long)bid * ba.kstride;
+  const float* rinv = carve_state(gst, a).rinv;
+  const float4* dt = reinterpret_cast<const float4*>(ba.dtg + (long long)bid * (W * W));
+  for (int e = tid; e < W * W / 4; e += NT) {
+    const int k = e / (W / 4), q = e - k * (W / 4);
+    *reinterpret_cast<float4*>(DT + k * DS + 4 * q) = dt[e];
+  }
+  for (int k = tid; k < W; k += NT) rl[k] = rinv[c0 + k];
+  __syncthreads();
+  const int i = r0 + tid;
+  if (i >= N4) return;
+  float* row = K + L.off(i) + c0;
+  float x[W];
 #pragma unroll
-    for (int k = 0; k < W; ++k) {
-      x[k] *= rl[k];
-      const float xk = -x[k];
+  for (int q = 0; q < W / 4; ++q) {
+    const float4 t = reinterpret_cast<const float4*>(row)[q];
+    x[4 * q] = t.x; x[4 * q + 1] = t.y; x[4 * q + 2] = t.z; x[4 * q + 3] = t.w;
+  }
 #pragma unroll
-      for (int j4 = (k + 1) >> 2; j4 < W / 4; ++j4) {
-        const float4 d = *reinterpret_cast<const float4*>(DT + k * DS + 4 * j4);
-        if (4 * j4 > k) x[4 * j4] = fmaf(xk, d.x, x[4 * j4]);
-        if (4 * j4 + 1 > k) x[4 * j4 + 1] = fmaf(xk, d.y, x[4 * j4 + 1]);
-        if (4 * j4 + 2 > k) x[4 * j4 + 2] = fmaf(xk, d.z, x[4 * j4 + 2]);
-        x[4 * j4 + 3] = fmaf(xk, d.w, x[4 * j4 + 3]);
-      }
+  for (int k = 0; k < W; ++k) {
+    x[k] *= rl[k];
+    const float xk = -x[k];
+#pragma unroll
+    for (int j4 = (k + 1) >> 2; j4 < W / 4; ++j4) {
+      const float4 d = *reinterpret_cast<const float4*>(DT + k * DS + 4 * j4);
+      if (4 * j4 > k) x[4 * j4] = fmaf(xk, d.x, x[4 * j4]);
+      if (4 * j4 + 1 > k) x[4 * j4 + 1] = fmaf(xk, d.y, x[4 * j4 + 1]);
+      if (4 * j4 + 2 > k) x[4 * j4 + 2] = fmaf(xk, d.z, x[4 * j4 + 2]);
+      x[4 * j4 + 3] = fmaf(xk, d.w, x[4 * j4 + 3]);
     }
+  }
 #pragma unroll
-    for (int q = 0; q < W / 4; ++q) {
-      const float s0 = sgn_of(c0 + 4 * q, L.npos);  // S_k (npos is a multiple of 4)
-      reinterpret_cast<float4*>(row)[q] =
-          make_float4(s0 * x[4 * q], s0 * x[4 * q + 1], s0 * x[4 * q + 2], s0 * x[4 * q + 3]);
-    }
+  for (int q = 0; q < W / 4; ++q) {
+    const float s0 = sgn_of(c0 + 4 * q, L.npos);  // S_k (npos is a multiple of 4)
+    reinterpret_cast<float4*>(row)[q] =
+        make_float4(s0 * x[4 * q], s0 * x[4 * q + 1], s0 * x[4 * q + 2], s0 * x[4 * q + 3]);
   }
 }
 
@@ -486,7 +545,7 @@ __global__ void __launch_bounds__(NT) bnd_solve(const BArgs ba) {
   const Smem G = carve_state(gst, a);
   const float* K = ba.kw + (long long)bid * ba.kstride;
   copy_block<NT>(sm, G.rhs, L.N4);
-  solve_qd<NT>(K, L, G.rinv, sm);
+  solve_qd<NT, false, true>(K, L, G.rinv, sm);
   __syncthreads();
   copy_block<NT>(G.rhs, sm, L.N4);
 }

@@ -610,7 +610,7 @@ __device__ int factor_big(float* __restrict__ K, const KLayout& L, const float t
 //   backward (per block b, last first):  x_b = W_bᵀ r_b;  r_j −= L_bjᵀ x_b above
 // rhs has N4 entries (padding entries must be 0 on entry).
 // ------------------------------------------------------------------------
-template <int NT, bool TAB = false>
+template <int NT, bool TAB = false, bool UNR = false>
 __device__ void solve_qd(const float* __restrict__ K, const KLayout& L, const float* __restrict__ rinv,
                          float* __restrict__ rhs, const int* __restrict__ tab = nullptr) {
   const int tid = threadIdx.x;
@@ -683,7 +683,16 @@ __device__ void solve_qd(const float* __restrict__ K, const KLayout& L, const fl
       const float* Bk = K + row_off<TAB>(L, tab, k0);
       for (int j = tid; j < k0; j += NT) {
         float acc = rhs[j];
-        for (int i = 0; i < kb; ++i) acc = fmaf(-Bk[i * Lb + j], rhs[k0 + i], acc);
+        if constexpr (UNR) {
+          // (batched engine, K in global memory) all 16 loads in flight
+          float lv[KB];
+#pragma unroll
+          for (int i = 0; i < KB; ++i) lv[i] = i < kb ? Bk[i * Lb + j] : 0.f;
+#pragma unroll
+          for (int i = 0; i < KB; ++i) acc = fmaf(-lv[i], i < kb ? rhs[k0 + i] : 0.f, acc);
+        } else {
+          for (int i = 0; i < kb; ++i) acc = fmaf(-Bk[i * Lb + j], rhs[k0 + i], acc);
+        }
         rhs[j] = acc;
       }
       __syncthreads();

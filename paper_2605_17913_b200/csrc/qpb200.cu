@@ -236,6 +236,7 @@ struct qp_ctx {
   bool kr = false;
   float *whi = nullptr, *wlo = nullptr, *gghi = nullptr, *gglo = nullptr;
   int* slotmap = nullptr;
+  float* dtg = nullptr;  // [bchunk][64·64] panel diagonal blocks (bnd_pdiag → bnd_prows)
   static constexpr int kPipe = 8;
   bool pipe = false;
   cudaStream_t pst[kPipe] = {};
@@ -259,7 +260,7 @@ size_t field_elems(int64_t stride, int32_t B, size_t per) { return stride == 0 ?
 
 void free_all(qp_ctx* c) {
   if (c->hctl) cudaFreeHost(c->hctl);
-  void* ptrs[] = {c->whi, c->wlo, c->gghi, c->gglo, c->slotmap, c->bst, c->bctl, c->tl, c->sched, c->done, c->kglob, c->flops_solve, c->flops_bwd, c->prof, c->own_status, c->wx, c->wy, c->wz, c->wdx, c->wdy, c->wdz, c->dQ_, c->dq_, c->dA_, c->db_,
+  void* ptrs[] = {c->dtg, c->whi, c->wlo, c->gghi, c->gglo, c->slotmap, c->bst, c->bctl, c->tl, c->sched, c->done, c->kglob, c->flops_solve, c->flops_bwd, c->prof, c->own_status, c->wx, c->wy, c->wz, c->wdx, c->wdy, c->wdz, c->dQ_, c->dq_, c->dA_, c->db_,
                   c->dG_, c->dh_, c->dx_, c->ds_, c->dz_, c->dy_, c->ddl_, c->dit_, c->dst_, c->gQ_, c->gq_,
                   c->gA_, c->gb_, c->gG_, c->gh_};
   for (void* p : ptrs)
@@ -334,16 +335,17 @@ static qp_err d2h(qp_ctx* c, T* dst, const T* src, size_t count) {
   return cuda_ok(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
 }
 
-constexpr int kBT = 128;  // threads of the batched-engine kernels
+constexpr int kBT = 128;  // threads of the batched-engine tensor-core / panel kernels
+constexpr int kBS = 256;  // threads of the per-problem state kernels (resid, solve, update)
 constexpr int kBW = 64;   // panel width of the batched factorisation
 
 // smem attributes of the batched-engine kernels (once per process and shape)
 qp_err bnd_setup(const qp_ctx* c) {
   const int sst = (int)(c->bst_stride * 4), ssv = (int)(c->L.N4max * 4);
   const int stc = qpb::tc::SMEM_BYTES;
-  if (cudaFuncSetAttribute(qpb::bnd_begin<kBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sst) ||
-      cudaFuncSetAttribute(qpb::bnd_resid<kBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sst) ||
-      cudaFuncSetAttribute(qpb::bnd_update<kBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sst) ||
+  if (cudaFuncSetAttribute(qpb::bnd_begin<kBS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sst) ||
+      cudaFuncSetAttribute(qpb::bnd_resid<kBS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sst) ||
+      cudaFuncSetAttribute(qpb::bnd_update<kBS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sst) ||
       cudaFuncSetAttribute(qpb::bnd_solve<kBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, ssv) ||
       cudaFuncSetAttribute(qpb::bnd_assemble<kBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, stc) ||
       cudaFuncSetAttribute(qpb::bnd_tc_update<kBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, stc) ||
@@ -378,7 +380,7 @@ qp_err run_batched(qp_ctx* c, const qpb::Args& a0, bool bwd) {
     ba.ntiles = c->kr ? 0 : T * (T + 1) / 2;
     ba.w = kBW;
     ba.kr = c->kr ? 1 : 0;
-    ba.whi = c->whi; ba.wlo = c->wlo; ba.slotmap = c->slotmap;
+    ba.whi = c->whi; ba.wlo = c->wlo; ba.slotmap = c->slotmap; ba.dtg = c->dtg;
     qpb::kr::GemmArgs ga;
     const int krN = (qpb::kr::npairs(n4) + qpb::kr::BN - 1) / qpb::kr::BN;
     if (c->kr) {
@@ -393,7 +395,7 @@ qp_err run_batched(qp_ctx* c, const qpb::Args& a0, bool bwd) {
       }
     }
     if (cudaMemsetAsync(c->bctl, 0, 2 * sizeof(int), st) != cudaSuccess) return QP_ERR_CUDA;
-    qpb::bnd_begin<kBT><<<nb, kBT, sst, st>>>(ba);
+    qpb::bnd_begin<kBS><<<nb, kBS, sst, st>>>(ba);
     ++launches;
     int N4cur = bwd ? 0 : qpb::r4(n4 + m);  // the initial system (solve)
     const int kmax = bwd ? c->c.relax_max_iter : c->c.max_iter;
@@ -401,7 +403,7 @@ qp_err run_batched(qp_ctx* c, const qpb::Args& a0, bool bwd) {
       if (k >= 0) {
         if (cudaMemsetAsync(c->bctl, 0, 2 * sizeof(int), st) != cudaSuccess) return QP_ERR_CUDA;
         ba.k = k;
-        qpb::bnd_resid<kBT><<<nb, kBT, sst, st>>>(ba);
+        qpb::bnd_resid<kBS><<<nb, kBS, sst, st>>>(ba);
         ++launches;
         if (cudaMemcpyAsync(c->hctl, c->bctl, 2 * sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
             cudaStreamSynchronize(st) != cudaSuccess)
@@ -409,7 +411,8 @@ qp_err run_batched(qp_ctx* c, const qpb::Args& a0, bool bwd) {
         if (c->hctl[0] == 0) break;
         N4cur = c->hctl[1];
       }
-      qpb::bnd_assemble<kBT><<<dim3(ba.ntiles + 1, nb), kBT, ba.ntiles ? stc : 0, st>>>(ba);
+      if (c->kr) qpb::bnd_scatter<kBS><<<nb, kBS, 0, st>>>(ba);
+      else qpb::bnd_assemble<kBT><<<dim3(ba.ntiles + 1, nb), kBT, stc, st>>>(ba);
       ++launches;
       if (c->kr) {
         qpb::kr::kr_gemm<<<dim3(krN, (nb + qpb::kr::BM - 1) / qpb::kr::BM), 128, qpb::kr::SMEM_BYTES, st>>>(ga);
@@ -421,11 +424,13 @@ qp_err run_batched(qp_ctx* c, const qpb::Args& a0, bool bwd) {
           qpb::bnd_tc_update<kBT><<<dim3((N4cur - c0 + qpb::tc::TM - 1) / qpb::tc::TM, nb), kBT, stc, st>>>(ba);
           ++launches;
         }
-        qpb::bnd_panel<kBT><<<nb, kBT, 0, st>>>(ba);
-        ++launches;
+        qpb::bnd_pdiag<32><<<nb, 32, 0, st>>>(ba);
+        if (c0 + kBW < N4cur)
+          qpb::bnd_prows<kBT><<<dim3((N4cur - c0 - kBW + kBT - 1) / kBT, nb), kBT, 0, st>>>(ba);
+        launches += 2;
       }
       qpb::bnd_solve<kBT><<<nb, kBT, ssv, st>>>(ba);
-      qpb::bnd_update<kBT><<<nb, kBT, sst, st>>>(ba);
+      qpb::bnd_update<kBS><<<nb, kBS, sst, st>>>(ba);
       launches += 2;
     }
     if (cudaGetLastError() != cudaSuccess) return QP_ERR_CUDA;
@@ -536,7 +541,7 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
     // per problem: a state block and a KKT workspace of capacity Nmax, for
     // up to half of the free device memory's worth of problems at a time
     ctx->bst_stride = qpb::bnd_state_floats(L.n4, d->m_eq, d->p, L.N4max);
-    const size_t per = 4 * ((size_t)ctx->bst_stride + (size_t)L.kglob);
+    const size_t per = 4 * ((size_t)ctx->bst_stride + (size_t)L.kglob + 64 * 64);
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
     long long cap = (long long)(fr / 2 / per);
@@ -544,7 +549,8 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
     ctx->bchunk = (int)std::max(1LL, std::min<long long>(d->batch, cap));
     if ((e = dalloc(ctx, &ctx->bst, (size_t)ctx->bchunk * ctx->bst_stride)) != QP_OK ||
         (e = dalloc(ctx, &ctx->kglob, (size_t)ctx->bchunk * (size_t)L.kglob)) != QP_OK ||
-        (e = dalloc(ctx, &ctx->bctl, 4)) != QP_OK) {
+        (e = dalloc(ctx, &ctx->bctl, 4)) != QP_OK ||
+        (e = dalloc(ctx, &ctx->dtg, (size_t)ctx->bchunk * 64 * 64)) != QP_OK) {
       free_all(ctx); delete ctx; return e;
     }
     if (cudaMallocHost(&ctx->hctl, 4 * sizeof(int)) != cudaSuccess || bnd_setup(ctx) != QP_OK) {

@@ -74,6 +74,8 @@ struct BArgs {
   int* slotmap;
   int kr;
   float* dtg;           // [B][64·64]: the current panel's factored diagonal block, transposed (bnd_pdiag → bnd_prows)
+  float* ug;            // [B][ustride]: the panel's Schur update U[i − c0][0:64] (bnd_tc_update → bnd_pdiag / bnd_prows)
+  long long ustride;
 };
 
 __device__ __forceinline__ float* st_of(const BArgs& b, int bid) { return b.st + (long long)bid * b.st_stride; }
@@ -390,27 +392,121 @@ __global__ void __launch_bounds__(NT) bnd_assemble(const BArgs ba) {
 }
 
 // ---------------------------------------------------------------------------
-// bnd_tc_update: grid (row tiles, B), panel [c0, c0 + w), c0 > 0: rows
-// [c0 + 128·x, +128) of the panel brought up to date with every earlier
-// column on tcgen05 (tc_factor.cuh tc_left_update, 3×TF32).
+// bnd_tc_update: grid (row tiles, B), panel [c0, c0 + 64), c0 > 0: for rows
+// [c0 + 128·x, +128) the Schur update of the panel from every earlier column
+//     U[i][c] = Σ_{k<c0} L[i][k] S_k L[c0+c][k]
+// on tcgen05 (3×TF32 split, TMEM accumulator 128 × 64): each thread stages
+// 12 fixed 16-byte row pieces per 32-deep K chunk (row offsets computed
+// once) in registers, the next chunk's loads in flight while the MMAs of
+// this one run.  The result goes to the per-problem buffer U (each thread
+// writes its TMEM lane's 32-column row segments); bnd_pdiag / bnd_prows
+// subtract it when they load the panel — K itself is read here only as the
+// operands, never read-modified-written.
 // ---------------------------------------------------------------------------
 template <int NT>
-__global__ void __launch_bounds__(NT) bnd_tc_update(const BArgs ba) {
+__global__ void __launch_bounds__(NT, 3) bnd_tc_update(const BArgs ba) {
+  static_assert(NT == 128, "bnd_tc_update: 128 threads (16 rows x 8 K-quads per pass)");
+  using tc::TK;
+  constexpr int TM = 128, BW = 64, SA = TM / 16, SB = BW / 16;  // row passes of A and B per thread
   extern __shared__ __align__(128) float smtc[];
-  float* sm = smtc;
   const Args& a = ba.a;
-  const int bid = blockIdx.y;
+  const int bid = blockIdx.y, tid = threadIdx.x;
   const BScal& h = scal_of(st_of(ba, bid));
   if (h.mode == BM_DONE) return;
   const KLayout L = bnd_layout(a, h.pa);
-  const int c0 = ba.c0, i0 = c0 + tc::TM * (int)blockIdx.x;
-  if (c0 >= L.N4 || i0 >= L.N4) return;
-  const int c1 = min(c0 + ba.w, L.N4);
-  float* K = ba.kw + (long long)bid * ba.kstride;
-  const tc::TcState ts = tc::tc_state(sm);
+  const int c0 = ba.c0, i0 = c0 + TM * (int)blockIdx.x, N4 = L.N4, npos = L.npos;
+  if (c0 >= N4 || i0 >= N4) return;
+  const int c1 = min(c0 + BW, N4), wn = (c1 - c0 + 15) & ~15;
+  const float* K = ba.kw + (long long)bid * ba.kstride;
+  const tc::TcState ts = tc::tc_state(smtc);
   tc::tmem_alloc(ts);
-  tc_left_update<NT>(ts, K, L, c0, (c1 - c0 + 15) & ~15, i0);
-  tc::tmem_free(*ts.tmem_slot);
+  const uint32_t tmem = *ts.tmem_slot;
+  uint32_t phase = *ts.phase_slot;
+  const uint32_t idesc = tc_idesc_n(wn);
+  // thread → (row, K quad): lanes 8h..8h+7 take rows 8·warp + [0, 8) at quad h (+4): a
+  // quarter-warp stores one core-matrix column of 8 rows (conflict-free) and
+  // the four quarter-warps read 64 contiguous bytes of each row (whole sectors)
+  const int warp = tid >> 5, lane = tid & 31, rl8 = lane & 7, qq = lane >> 3;
+  int ro[SA / 2 + SB / 2];  // rows 8·warp + rl8 + 32·s: A s < 4, B s < 2
+#pragma unroll
+  for (int s2 = 0; s2 < SA / 2; ++s2) { const int i = i0 + 8 * warp + rl8 + 32 * s2; ro[s2] = i < N4 ? L.off(i) : -1; }
+#pragma unroll
+  for (int s2 = 0; s2 < SB / 2; ++s2) { const int j = c0 + 8 * warp + rl8 + 32 * s2; ro[SA / 2 + s2] = j < c1 ? L.off(j) : -1; }
+  float4 rg[SA + SB];  // [2 quads][rows]: index h·(SA/2 + SB/2) + s
+  constexpr int NR = SA / 2 + SB / 2;
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const int k = k0 + 4 * (qq + 4 * h2);
+#pragma unroll
+      for (int s2 = 0; s2 < NR; ++s2)
+        rg[h2 * NR + s2] = (ro[s2] >= 0 && k < c0) ? *reinterpret_cast<const float4*>(K + ro[s2] + k)
+                                                    : make_float4(0, 0, 0, 0);
+    }
+  };
+  auto split4 = [](float4 v, float4& hi, float4& lo) {
+    hi.x = tc::to_tf32(v.x); lo.x = tc::to_tf32(v.x - hi.x);
+    hi.y = tc::to_tf32(v.y); lo.y = tc::to_tf32(v.y - hi.y);
+    hi.z = tc::to_tf32(v.z); lo.z = tc::to_tf32(v.z - hi.z);
+    hi.w = tc::to_tf32(v.w); lo.w = tc::to_tf32(v.w - hi.w);
+  };
+  load(0);
+  for (int k0 = 0; k0 < c0; k0 += TK) {
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const int qd = qq + 4 * h2;
+      const bool neg = k0 + 4 * qd >= npos;  // S_k on the B operand (npos is a multiple of 4)
+#pragma unroll
+      for (int s2 = 0; s2 < NR; ++s2) {
+        float4 v = rg[h2 * NR + s2], hi, lo;
+        const bool isb = s2 >= SA / 2;
+        if (isb && neg) { v.x = -v.x; v.y = -v.y; v.z = -v.z; v.w = -v.w; }
+        split4(v, hi, lo);
+        const int sr = isb ? s2 - SA / 2 : s2;
+        const int o = ((warp + 4 * sr) * (TK / 4) + qd) * 32 + rl8 * 4;  // canonical K-major (op_offset)
+        *reinterpret_cast<float4*>((isb ? ts.bhi : ts.ahi) + o) = hi;
+        *reinterpret_cast<float4*>((isb ? ts.blo : ts.alo) + o) = lo;
+      }
+    }
+    tc::fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tc::tc_fence_after();
+      const uint32_t ahi = tc::smem_u32(ts.ahi), alo = tc::smem_u32(ts.alo);
+      const uint32_t bhi = tc::smem_u32(ts.bhi), blo = tc::smem_u32(ts.blo);
+#pragma unroll
+      for (int ks = 0; ks < TK / 8; ++ks) {
+        const uint32_t off = ks * 2 * 128;
+        const uint32_t acc0 = (k0 > 0 || ks > 0) ? 1u : 0u;
+        tc::mma_tf32(tmem, tc::make_desc(ahi + off), tc::make_desc(bhi + off), idesc, acc0);
+        tc::mma_tf32(tmem, tc::make_desc(ahi + off), tc::make_desc(blo + off), idesc, 1u);
+        tc::mma_tf32(tmem, tc::make_desc(alo + off), tc::make_desc(bhi + off), idesc, 1u);
+      }
+      tc::commit(ts.mbar);
+    }
+    if (k0 + TK < c0) load(k0 + TK);  // in flight while the MMAs run
+    tc::mbar_wait(ts.mbar, phase);
+    phase ^= 1u;
+    tc::tc_fence_after();
+  }
+  // epilogue: TMEM lane = row i0 + 32·warp + lane → registers → per-warp
+  // transpose (the operand tiles are idle now) → coalesced 128-byte rows of U
+  float* T = ts.ahi + warp * (32 * 33);
+  float* U = ba.ug + (long long)bid * ba.ustride;
+  for (int cc = 0; cc < wn; cc += 32) {
+    float v[32];
+    tc::tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)cc, v);
+#pragma unroll
+    for (int c = 0; c < 32; ++c) T[lane * 33 + c] = v[c];
+    __syncwarp();
+#pragma unroll 4
+    for (int r = 0; r < 32; ++r) {
+      const int i = i0 + 32 * warp + r;
+      if (i < N4) U[(long long)(i - c0) * BW + cc + lane] = T[r * 33 + lane];
+    }
+    __syncwarp();
+  }
+  tc::tmem_free(tmem);
 }
 
 // ---------------------------------------------------------------------------
@@ -452,7 +548,13 @@ __global__ void __launch_bounds__(NT) bnd_pdiag(const BArgs ba) {
   for (int e = tid; e < w * (W / 4); e += NT) {
     const int r = e / (W / 4), q = e - r * (W / 4), i = c0 + r, j = c0 + 4 * q;
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (4 * q < w && j <= i) v = *reinterpret_cast<const float4*>(K + L.off(i) + j);
+    if (4 * q < w && j <= i) {
+      v = *reinterpret_cast<const float4*>(K + L.off(i) + j);
+      if (c0 > 0) {  // the panel's Schur update from bnd_tc_update
+        const float4 u = *reinterpret_cast<const float4*>(ba.ug + (long long)bid * ba.ustride + r * W + 4 * q);
+        v.x -= u.x; v.y -= u.y; v.z -= u.z; v.w -= u.w;
+      }
+    }
     *reinterpret_cast<float4*>(D + r * DS + 4 * q) = v;
   }
   __syncthreads();
@@ -503,9 +605,14 @@ __global__ void __launch_bounds__(NT, 4) bnd_prows(const BArgs ba) {
   if (i >= N4) return;
   float* row = K + L.off(i) + c0;
   float x[W];
+  const float4* urow = reinterpret_cast<const float4*>(ba.ug + (long long)bid * ba.ustride + (long long)(i - c0) * W);
 #pragma unroll
   for (int q = 0; q < W / 4; ++q) {
-    const float4 t = reinterpret_cast<const float4*>(row)[q];
+    float4 t = reinterpret_cast<const float4*>(row)[q];
+    if (c0 > 0) {  // the panel's Schur update from bnd_tc_update
+      const float4 u = urow[q];
+      t.x -= u.x; t.y -= u.y; t.z -= u.z; t.w -= u.w;
+    }
     x[4 * q] = t.x; x[4 * q + 1] = t.y; x[4 * q + 2] = t.z; x[4 * q + 3] = t.w;
   }
 #pragma unroll

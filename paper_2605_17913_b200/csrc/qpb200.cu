@@ -237,6 +237,7 @@ struct qp_ctx {
   float *whi = nullptr, *wlo = nullptr, *gghi = nullptr, *gglo = nullptr;
   int* slotmap = nullptr;
   float* dtg = nullptr;  // [bchunk][64·64] panel diagonal blocks (bnd_pdiag → bnd_prows)
+  float* ug = nullptr;   // [bchunk][N4max·64] panel Schur updates (bnd_tc_update → bnd_pdiag / bnd_prows)
   static constexpr int kPipe = 8;
   bool pipe = false;
   cudaStream_t pst[kPipe] = {};
@@ -260,7 +261,7 @@ size_t field_elems(int64_t stride, int32_t B, size_t per) { return stride == 0 ?
 
 void free_all(qp_ctx* c) {
   if (c->hctl) cudaFreeHost(c->hctl);
-  void* ptrs[] = {c->dtg, c->whi, c->wlo, c->gghi, c->gglo, c->slotmap, c->bst, c->bctl, c->tl, c->sched, c->done, c->kglob, c->flops_solve, c->flops_bwd, c->prof, c->own_status, c->wx, c->wy, c->wz, c->wdx, c->wdy, c->wdz, c->dQ_, c->dq_, c->dA_, c->db_,
+  void* ptrs[] = {c->ug, c->dtg, c->whi, c->wlo, c->gghi, c->gglo, c->slotmap, c->bst, c->bctl, c->tl, c->sched, c->done, c->kglob, c->flops_solve, c->flops_bwd, c->prof, c->own_status, c->wx, c->wy, c->wz, c->wdx, c->wdy, c->wdz, c->dQ_, c->dq_, c->dA_, c->db_,
                   c->dG_, c->dh_, c->dx_, c->ds_, c->dz_, c->dy_, c->ddl_, c->dit_, c->dst_, c->gQ_, c->gq_,
                   c->gA_, c->gb_, c->gG_, c->gh_};
   for (void* p : ptrs)
@@ -381,6 +382,7 @@ qp_err run_batched(qp_ctx* c, const qpb::Args& a0, bool bwd) {
     ba.w = kBW;
     ba.kr = c->kr ? 1 : 0;
     ba.whi = c->whi; ba.wlo = c->wlo; ba.slotmap = c->slotmap; ba.dtg = c->dtg;
+    ba.ug = c->ug; ba.ustride = (long long)c->L.N4max * 64;
     qpb::kr::GemmArgs ga;
     const int krN = (qpb::kr::npairs(n4) + qpb::kr::BN - 1) / qpb::kr::BN;
     if (c->kr) {
@@ -541,7 +543,7 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
     // per problem: a state block and a KKT workspace of capacity Nmax, for
     // up to half of the free device memory's worth of problems at a time
     ctx->bst_stride = qpb::bnd_state_floats(L.n4, d->m_eq, d->p, L.N4max);
-    const size_t per = 4 * ((size_t)ctx->bst_stride + (size_t)L.kglob + 64 * 64);
+    const size_t per = 4 * ((size_t)ctx->bst_stride + (size_t)L.kglob + 64 * 64 + (size_t)L.N4max * 64);
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
     long long cap = (long long)(fr / 2 / per);
@@ -550,7 +552,8 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
     if ((e = dalloc(ctx, &ctx->bst, (size_t)ctx->bchunk * ctx->bst_stride)) != QP_OK ||
         (e = dalloc(ctx, &ctx->kglob, (size_t)ctx->bchunk * (size_t)L.kglob)) != QP_OK ||
         (e = dalloc(ctx, &ctx->bctl, 4)) != QP_OK ||
-        (e = dalloc(ctx, &ctx->dtg, (size_t)ctx->bchunk * 64 * 64)) != QP_OK) {
+        (e = dalloc(ctx, &ctx->dtg, (size_t)ctx->bchunk * 64 * 64)) != QP_OK ||
+        (e = dalloc(ctx, &ctx->ug, (size_t)ctx->bchunk * L.N4max * 64)) != QP_OK) {
       free_all(ctx); delete ctx; return e;
     }
     if (cudaMallocHost(&ctx->hctl, 4 * sizeof(int)) != cudaSuccess || bnd_setup(ctx) != QP_OK) {

@@ -310,6 +310,8 @@ def main():
         np.savez(os.path.join(a.dump, f"rank{rank}.npz"), start=start, stop=stop,
                  **{k: v.cpu().numpy() for k, v in out.items()},
                  **{"g_" + k: v.cpu().numpy() for k, v in g.items()})
+    info = S.info()  # after the calls: the batched engine counts its launches per call
+    path4 = info.get("path") == 4
     iters = out["iters"].cpu().numpy()
     riters = g["relax_iters"].cpu().numpy()
     status = out["status"].cpu().numpy()
@@ -325,7 +327,12 @@ def main():
     x_s, x_b = S.last_flops()
     f_dom, x_dom, ms_dom = (k14_s, x_s, ms_solve) if dom_solve else (k14_b, x_b, ms_bwd)
     achieved = f_dom / (ms_dom / 1e3) / 1e12
-    roofline = {"bound": "alu", "kernel": "ipm_kernel (solve launch)" if dom_solve else "ipm_kernel (backward launch)",
+    if path4:  # batched phase engine: one call = a sequence of phase kernels
+        kname = (f"qp_solve_batched ({info['launches_solve']} launches of the batched engine)" if dom_solve else
+                 f"qp_backward_batched ({info['launches_backward']} launches of the batched engine)")
+    else:
+        kname = "ipm_kernel (solve launch)" if dom_solve else "ipm_kernel (backward launch)"
+    roofline = {"bound": "alu", "kernel": kname,
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
                 "work_model": "SURVEY §8(d) K14-literal: per iteration N^3/3 + 2N^2 + 2n^2 + 6pn + 4mn "
                               "(N = n+p+m) at the measured iteration counts, + init, + p*n^2 once (flops.py)",

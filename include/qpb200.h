@@ -37,6 +37,11 @@
  *     (autograd saved-tensor semantics); with QP_MEM_HOST the ctx keeps device
  *     copies itself.
  *
+ *   - Path 4 (qp_info.path, the batched engine for large shapes) reads back,
+ *     after each Newton iteration, how many problems still iterate: its calls
+ *     return when the work is complete (the ctx stream is synchronised), still
+ *     stream-ordered after earlier work on that stream.
+ *
  * Errors: an API-level qp_err return covers argument, shape and CUDA errors.
  * The numerical outcome is per problem in status[] and never aborts a call
  * (S:262): a failed problem keeps its last finite iterate, its gradients are
@@ -104,14 +109,20 @@ typedef struct {
 typedef struct qp_ctx qp_ctx;
 
 typedef struct {
-  int32_t path;            /* CTA per QP; KKT matrix in 1 = shared memory, 2 = a global    */
-                           /* workspace (L2), 3 = shared memory when the reduced system    */
-                           /* fits (most iterations), else the global workspace            */
-  int32_t threads;         /* threads per CTA                                              */
-  int32_t smem_bytes;      /* dynamic shared memory per CTA                                */
-  int32_t ctas_per_sm;     /* occupancy of the chosen kernel                               */
+  int32_t path;            /* 1-3: one CTA per QP for the whole call; KKT matrix in        */
+                           /* 1 = shared memory, 2 = a global workspace (L2), 3 = shared   */
+                           /* memory when the reduced system fits, else the workspace;     */
+                           /* 4 = the batched phase engine (large shapes, the default for  */
+                           /* everything path 1 cannot hold): one kernel per phase of a     */
+                           /* Newton iteration over the whole batch, KKT matrices in        */
+                           /* per-problem global workspaces, tensor-core assembly (one GEMM */
+                           /* over the batch when G is shared) and Schur updates            */
+  int32_t threads;         /* threads per CTA (path 4: of the per-problem phase kernels)   */
+  int32_t smem_bytes;      /* dynamic shared memory per CTA (path 4: per-problem state)    */
+  int32_t ctas_per_sm;     /* occupancy of the chosen kernel (path 4: 0, varies by phase)  */
   int32_t kkt_dim;         /* N = n4 + p + m (n4 = n rounded up to 4)                      */
-  int32_t launches_solve;  /* kernel launches per qp_solve_batched                         */
+  int32_t launches_solve;  /* kernel launches per qp_solve_batched (path 4: of the last    */
+                           /* call — the count depends on the iterations it took)          */
   int32_t launches_backward;
   int64_t workspace_bytes;
   int32_t partition_cap;   /* largest number of constraints kept in augmented form in one */

@@ -570,10 +570,11 @@ __global__ void __launch_bounds__(NT) bnd_pdiag(const BArgs ba) {
       *reinterpret_cast<float4*>(K + L.off(i) + j) = *reinterpret_cast<const float4*>(D + r * DS + 4 * q);
   }
   if (c1 < N4) {  // rows below follow: the strictly lower part, transposed, for bnd_prows
-    float* dt = ba.dtg + (long long)bid * (W * W);
-    for (int e = tid; e < W * W; e += NT) {
-      const int k = e / W, j = e - k * W;
-      dt[e] = k < j ? D[j * DS + k] : 0.f;
+    float4* dt = reinterpret_cast<float4*>(ba.dtg + (long long)bid * (W * W));
+    for (int e = tid; e < W * W / 4; e += NT) {
+      const int k = e / (W / 4), j = 4 * (e - k * (W / 4));
+      dt[e] = make_float4(k < j ? D[j * DS + k] : 0.f, k < j + 1 ? D[(j + 1) * DS + k] : 0.f,
+                          k < j + 2 ? D[(j + 2) * DS + k] : 0.f, k < j + 3 ? D[(j + 3) * DS + k] : 0.f);
     }
   }
 }

@@ -647,6 +647,9 @@ qp_err qp_get_info(const qp_ctx* c, qp_info* info) {
   if (c->L.batched) {  // phase kernels: counted by the last calls
     info->launches_solve = c->blaunch[0];
     info->launches_backward = c->blaunch[1] + extra;
+    info->threads = kBS;
+    info->smem_bytes = (int32_t)(c->bst_stride * 4);  // state block of the per-problem phases
+    info->ctas_per_sm = 0;                            // varies by phase kernel
   }
   info->workspace_bytes = c->workspace;
   return QP_OK;

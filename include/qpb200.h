@@ -127,6 +127,8 @@ typedef struct {
   int64_t workspace_bytes;
   int32_t partition_cap;   /* largest number of constraints kept in augmented form in one */
                            /* reduced system (reading Q12c); p = no cap                    */
+  int32_t handed_solve;    /* problems the last solve / backward handed to the uncapped    */
+  int32_t handed_backward; /* large-N kernel (reading Q12c guard); synchronises the stream */
 } qp_info;
 
 /* Fill *cfg with the defaults listed above. */

@@ -36,7 +36,7 @@ class QpInfo(C.Structure):
     _fields_ = [("path", C.c_int32), ("threads", C.c_int32), ("smem_bytes", C.c_int32),
                 ("ctas_per_sm", C.c_int32), ("kkt_dim", C.c_int32), ("launches_solve", C.c_int32),
                 ("launches_backward", C.c_int32), ("workspace_bytes", C.c_int64),
-                ("partition_cap", C.c_int32)]
+                ("partition_cap", C.c_int32), ("handed_solve", C.c_int32), ("handed_backward", C.c_int32)]
 
 
 EXPORTS = ("qp_config_default", "qp_create", "qp_set_stream", "qp_get_info", "qp_max_kkt_dim",

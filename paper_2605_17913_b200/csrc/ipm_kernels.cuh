@@ -56,6 +56,15 @@ struct Args {
   int* status_out;           // solve: second copy of the status (the caller's array), nullptr = none
   unsigned long long* tl;    // diagnostics (QPB200_TIMELINE): per problem {smid, t_start, t_end} (ns)
   int bwd;                   // 0: solve launch (init + Alg. 1), 1: backward launch (Alg. 2 + Alg. 3)
+  // Reading Q12c guard (path 1): a problem whose capped elimination would put
+  // a weight ω > fb_bound on an eliminated v_i > 0 constraint is handed to the
+  // uncapped large-N kernel (the fallback launch that follows on the stream)
+  float fb_bound;            // 0 = no check (large-N kernels, uncapped)
+  int* fb_flag;              // [B] solve: 1 = handed over (read by the backward)
+  int* fb_list;              // this call's hand-over list (chunk-local problem indices)
+  int* fb_count;             // its length
+  const int* plist;          // list-driven launch (the fallback): problems plist[i], i < *pcount
+  const int* pcount;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -78,7 +87,10 @@ __device__ __forceinline__ unsigned smid() {
 // takes more of them.  Block-uniform.
 __device__ __forceinline__ int next_problem(const Args& a, int* slot) {
   __syncthreads();
-  if (threadIdx.x == 0) *slot = atomicAdd(a.sched, 1);
+  if (threadIdx.x == 0) {
+    const int i = atomicAdd(a.sched, 1);
+    *slot = !a.plist ? i : (i < *a.pcount ? a.plist[i] : a.B);  // the fallback walks its list
+  }
   __syncthreads();
   return *slot;
 }
@@ -244,11 +256,13 @@ __device__ int compact_pass(const Smem& S, int p, Pred on_of) {
 }
 
 template <int NT>
-__device__ int compact_active(const Smem& S, int p, bool all_inactive, int pcap) {
+__device__ int compact_active(const Smem& S, int p, bool all_inactive, int pcap, bool* capped = nullptr) {
+  if (capped) *capped = false;
   if (all_inactive) return compact_pass<NT>(S, p, [](int) { return false; });
   const float* v = S.v;
   const int pa = compact_pass<NT>(S, p, [v](int k) { return v[k] > 0.f; });
   if (pa <= pcap) return pa;
+  if (capped) *capped = true;
   return compact_pass<NT>(S, p, [v, p, pcap](int k) {
     const float vk = v[k];
     if (!(vk > 0.f)) return false;
@@ -515,6 +529,7 @@ struct Norms {
   float gap, obj, nonfin;
   float nrt, nre, nri, nrzs, sQx, sq, sGz, sAy, sAx, sb, sGx, ss, sh, sz;
   int pa;
+  bool spill;  // reading Q12c guard: the capped elimination would exceed fb_bound
 };
 
 template <int NT>
@@ -531,7 +546,21 @@ __device__ Norms residuals(const Smem& S, const Args& a, const Prob& P, float ka
     mz = fmaxf(mz, fabsf(zk)); ms = fmaxf(ms, fabsf(sk)); mh = fmaxf(mh, fabsf(__ldg(P.h + k)));
     mrzs = fmaxf(mrzs, fmaxf(fabsf(rz), fabsf(rs)));
   }
-  const int pa = compact_active<NT>(S, p, false, a.pcap);
+  bool capped;
+  const int pa = compact_active<NT>(S, p, false, a.pcap, &capped);
+  // Reading Q12c guard: when the cap bound, no eliminated constraint with
+  // v_k > 0 may carry a weight ω_k = d₊/d₋ above fb_bound (every factored
+  // entry stays bounded); otherwise the problem goes to the
+  // uncapped fallback (block-uniform: capped is)
+  bool spill = false;
+  if (capped && a.fb_bound > 0.f) {
+    float w = 0.f;
+    for (int k = tid; k < p; k += NT)
+      if (S.v[k] > 0.f && S.widx[k] < 0) w = fmaxf(w, S.dp[k] / S.dm[k]);
+    float vv[1] = {w};
+    block_reduce<NT, 0, 1>(vv, S.red);
+    spill = vv[0] > a.fb_bound;
+  }
   // rows: r_i = Gx + s − h, r_e = Ax − b (warp per row); f2, t, rhs_w, rhs_y
   rowdots<NT>(P.G, p, n, S.x, S.gx);
   rowdots<NT>(P.A, m, n, S.x, S.gx + p);
@@ -662,6 +691,7 @@ __device__ Norms residuals(const Smem& S, const Args& a, const Prob& P, float ka
   R.sQx = v[7]; R.sq = v[8]; R.sGz = v[9]; R.sAy = v[10]; R.sAx = v[11]; R.sb = v[12]; R.sGx = v[13];
   R.ss = v[14]; R.sh = v[15]; R.sz = v[16];
   R.pa = pa;
+  R.spill = spill;
   return R;
 }
 
@@ -821,6 +851,15 @@ __device__ __forceinline__ void ipm_problem(const Args& a, const Smem& S, const 
   float phi_prev = INFINITY;
   unsigned long long tph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long t0 = clock64();
+  bool handed = false;  // reading Q12c guard: this problem goes to the fallback launch
+  if (a.fb_bound > 0.f) {
+    if (!bwd) {
+      if (tid == 0) a.fb_flag[bid] = 0;
+    } else if (__ldcg(a.fb_flag + bid)) {  // the solve handed it over: so does the backward
+      if (tid == 0) a.fb_list[atomicAdd(a.fb_count, 1)] = bid;
+      return;
+    }
+  }
   if (bwd) {
     // the solve's outputs (written by other SMs in this or the previous
     // kernel): read past L1
@@ -863,6 +902,15 @@ __device__ __forceinline__ void ipm_problem(const Args& a, const Smem& S, const 
       const Norms R = residuals<NT>(S, a, P, kappa, kappa - kt);
       long long t1 = clock64(); tph[0] += t1 - t0; t0 = t1;
       it = k;
+      if (R.spill) {
+        handed = true;
+        status = ST_FAIL;  // (placeholder: the fallback launch overwrites this problem's outputs)
+        if (tid == 0) {
+          if (!bwd) a.fb_flag[bid] = 1;
+          a.fb_list[atomicAdd(a.fb_count, 1)] = bid;
+        }
+        break;
+      }
       if (R.nonfin > 0.f) { status = ST_FAIL | ((bwd ? STG_RELAX : STG_SCALING) << 8); break; }
       if (!bwd) {
         fl += iter_flops(n, m, p, 0, true, false, false);
@@ -963,6 +1011,10 @@ __device__ __forceinline__ void ipm_problem(const Args& a, const Smem& S, const 
       if (a.flops) a.flops[bid] = fl;
     }
   } else {
+    if (handed) {  // the fallback launch writes this problem's gradients
+      __syncthreads();
+      return;
+    }
     // the gradient buffers may still be read by the previous kernel on the
     // stream (caching allocator reuse): no store before it has completed
     grid_dependency_wait();
@@ -1026,6 +1078,10 @@ __global__ void __launch_bounds__(NT, MINB) ipm_kernel(const Args a) {
     if (!bwd && a.done && threadIdx.x == 0)  // release (cumulative through the barrier): outputs before the flag
       asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(a.done + bid), "r"(a.epoch) : "memory");
   }
+  // a programmatically launched backward completes only after the grid it
+  // depends on (so that work ordered after it, e.g. the fallback launch,
+  // also follows that grid)
+  if (bwd) grid_dependency_wait();
   if constexpr (BIG) tc::tmem_free(*tc::tc_state(S.tc).tmem_slot);
 }
 

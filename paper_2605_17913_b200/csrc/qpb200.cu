@@ -59,7 +59,7 @@ size_t smem_for(const Layout& L, int m, int p, int ncap, bool big) {
 // Shared-memory budget per CTA (dynamic part) for `ctas` CTAs per SM.
 size_t budget(int ctas) { return std::min(kMaxSmem, (size_t)(233472 / ctas) - 1024); }
 
-Layout make_layout(int n, int m, int p, int formulation, int batch = 0, int sms = 148) {
+Layout make_layout(int n, int m, int p, int formulation, int batch = 0, int sms = 148, bool force_big = false) {
   Layout L;
   L.n4 = (n + 3) & ~3;
   // implicit: reduced system n4 + |A| + m with |A| <= p; standard arm: every
@@ -92,7 +92,8 @@ Layout make_layout(int n, int m, int p, int formulation, int batch = 0, int sms 
   // 8 per SM (128 registers per thread), so twice as many problems are in
   // flight.  Measured (one B200, 4096 problems): cbf7 620 K → 744 K QP/s,
   // cbf9 464 K → 571 K; one warp per QP (16 per SM) 726 K / 482 K.
-  if (formulation != QP_EXPLICIT && env_cap < 0 && !getenv("QPB200_FORCE_GLOBAL") && !getenv("QPB200_NO_SMALL") &&
+  if (force_big) env_cap = -2;  // the fallback kernel of reading Q12c's guard: large-N layout
+  if (formulation != QP_EXPLICIT && env_cap == -1 && !getenv("QPB200_FORCE_GLOBAL") && !getenv("QPB200_NO_SMALL") &&
       env_ctas == 0 && batch > 4 * sms) {
     const int need = std::min(L.Nmax, L.n4 + std::min(p, L.n4) + m);
     const int ncap = std::min(L.Nmax, 64);
@@ -112,7 +113,7 @@ Layout make_layout(int n, int m, int p, int formulation, int batch = 0, int sms 
   // 110 K → 255 K QP/s at 4 CTAs/SM; bezier8: 25.6 K → 32.2 K at 1 CTA/SM of
   // 256 threads, against the large-N kernels); only larger systems need the
   // large-N kernels.
-  if (!fit && env_cap < 0 && !getenv("QPB200_FORCE_GLOBAL")) {
+  if (!fit && env_cap == -1 && !getenv("QPB200_FORCE_GLOBAL")) {
     const int need = std::min(L.Nmax, L.n4 + std::min(p, L.n4) + m);
     const int want[4] = {4, 3, 2, 1};
     for (int w : want) {
@@ -149,11 +150,12 @@ Layout make_layout(int n, int m, int p, int formulation, int batch = 0, int sms 
     }
     L.ncap = lo;
     if (env_cap >= 0) L.ncap = std::min(env_cap, L.ncap);
+    if (force_big) { L.threads = 256; L.minb = 1; L.batched = false; }
     if (getenv("QPB200_FORCE_GLOBAL")) L.ncap = 0;
     L.threads = 256; L.minb = 1;
     // the batched phase engine (path 4) unless the persistent large-N kernel
     // is asked for (A/B experiments, parity tests of that kernel)
-    L.batched = formulation != QP_EXPLICIT && !getenv("QPB200_PERSISTENT_BIG");
+    L.batched = formulation != QP_EXPLICIT && !getenv("QPB200_PERSISTENT_BIG") && !force_big;
   }
   L.ksmem = L.ncap > 0 ? qpb::KLayout::make(L.ncap, L.n4).size() : 0;
   L.smem = qpb::ipm_smem_bytes(L.n4, m, p, L.N4max, L.ksmem, tc_floats(L.big), ro_ints(L, L.big));
@@ -238,6 +240,17 @@ struct qp_ctx {
   int* slotmap = nullptr;
   float* dtg = nullptr;  // [bchunk][64·64] panel diagonal blocks (bnd_pdiag → bnd_prows)
   float* ug = nullptr;   // [bchunk][N4max·64] panel Schur updates (bnd_tc_update → bnd_pdiag / bnd_prows)
+  // reading Q12c guard (path 1 with a kept-set cap): problems whose capped
+  // elimination would exceed fb_bound go to the uncapped large-N kernel,
+  // launched (list-driven) right after each path-1 launch
+  bool fb = false;
+  float fb_bound = 0.f;
+  Layout Lf{};
+  int gridf = 0;
+  float* kglobf = nullptr;
+  int* fb_flag = nullptr;   // [B]
+  int* fb_list = nullptr;   // [2B]: solve list, backward list (chunk segments at b0)
+  int* fb_ctl = nullptr;    // [2][kPipe][2]: count, launch counter per call and chunk
   static constexpr int kPipe = 8;
   bool pipe = false;
   cudaStream_t pst[kPipe] = {};
@@ -261,7 +274,7 @@ size_t field_elems(int64_t stride, int32_t B, size_t per) { return stride == 0 ?
 
 void free_all(qp_ctx* c) {
   if (c->hctl) cudaFreeHost(c->hctl);
-  void* ptrs[] = {c->ug, c->dtg, c->whi, c->wlo, c->gghi, c->gglo, c->slotmap, c->bst, c->bctl, c->tl, c->sched, c->done, c->kglob, c->flops_solve, c->flops_bwd, c->prof, c->own_status, c->wx, c->wy, c->wz, c->wdx, c->wdy, c->wdz, c->dQ_, c->dq_, c->dA_, c->db_,
+  void* ptrs[] = {c->kglobf, c->fb_flag, c->fb_list, c->fb_ctl, c->ug, c->dtg, c->whi, c->wlo, c->gghi, c->gglo, c->slotmap, c->bst, c->bctl, c->tl, c->sched, c->done, c->kglob, c->flops_solve, c->flops_bwd, c->prof, c->own_status, c->wx, c->wy, c->wz, c->wdx, c->wdy, c->wdz, c->dQ_, c->dq_, c->dA_, c->db_,
                   c->dG_, c->dh_, c->dx_, c->ds_, c->dz_, c->dy_, c->ddl_, c->dit_, c->dst_, c->gQ_, c->gq_,
                   c->gA_, c->gb_, c->gG_, c->gh_};
   for (void* p : ptrs)
@@ -312,6 +325,8 @@ qpb::Args chunk_args(qpb::Args a, int b0, int nb) {
   if (a.riters) a.riters += o;
   if (a.rstatus) a.rstatus += o;
   if (a.flops) a.flops += o;
+  if (a.fb_flag) a.fb_flag += o;
+  if (a.fb_list) a.fb_list += o;
   if (a.prof) a.prof += 8 * o;
   return a;
 }
@@ -334,6 +349,38 @@ template <typename T>
 static qp_err d2h(qp_ctx* c, T* dst, const T* src, size_t count) {
   if (count == 0 || !dst) return QP_OK;
   return cuda_ok(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+}
+
+// Reading Q12c guard: path-1 arguments of one launch (chunk ch; the list and
+// its counters are per call and chunk).
+void set_fb(const qp_ctx* c, qpb::Args& a, bool bwd, int ch) {
+  if (!c->fb) return;
+  a.fb_bound = c->fb_bound;
+  a.fb_flag = c->fb_flag;
+  a.fb_list = c->fb_list + (bwd ? c->d.batch : 0);
+  a.fb_count = c->fb_ctl + 2 * (ch + (bwd ? qp_ctx::kPipe : 0));
+}
+
+// The fallback launch after a path-1 launch `ap` (chunk ch of nch, stream st):
+// the uncapped large-N persistent kernel over the problems the path-1 launch
+// handed over (list-driven; its CTAs exit at once when the list is empty).
+qp_err launch_fallback(const qp_ctx* c, const qpb::Args& ap, bool bwd, int ch, int nch, cudaStream_t st) {
+  if (!c->fb) return QP_OK;
+  qpb::Args a = ap;
+  const Layout& L = c->Lf;
+  a.n4 = L.n4; a.Nmax = L.Nmax; a.N4max = L.N4max;
+  a.ksmem = L.ksmem; a.ncap = L.ncap; a.kglob_size = L.kglob;
+  a.pcap = c->d.p; a.tcf = qpb::tc::SMEM_BYTES / 4; a.rof = 0;
+  a.fb_bound = 0.f; a.fb_flag = nullptr; a.fb_list = nullptr; a.fb_count = nullptr;
+  a.plist = ap.fb_list;
+  a.pcount = ap.fb_count;
+  a.sched = ap.fb_count + 1;
+  a.done = nullptr;  // stream-ordered after the path-1 launch: nothing to poll
+  a.prof = nullptr; a.tl = nullptr;
+  const int g = std::max(1, c->gridf / nch);
+  a.kglob = c->kglobf + (size_t)ch * g * (size_t)L.kglob;  // this chunk's CTA workspaces
+  qpb::ipm_kernel<256, 1, true><<<g, 256, L.smem, st>>>(a);
+  return cuda_ok(cudaGetLastError());
 }
 
 constexpr int kBT = 128;  // threads of the batched-engine tensor-core / panel kernels
@@ -539,6 +586,29 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
       free_all(ctx); delete ctx; return e;
     }
   }
+  if (!L.big && c.formulation == QP_IMPLICIT && L.pcap < d->p && !getenv("QPB200_NO_FALLBACK")) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    ctx->fb = true;
+    ctx->fb_bound = 1e3f;
+    if (const char* e2 = getenv("QPB200_FB_BOUND")) ctx->fb_bound = (float)atof(e2);  // tests
+    ctx->Lf = make_layout(d->n, d->m_eq, d->p, c.formulation, d->batch, sms, true);
+    ctx->gridf = sms;
+    if (ctx->Lf.smem > kMaxSmem ||
+        cudaFuncSetAttribute(qpb::ipm_kernel<256, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)ctx->Lf.smem) != cudaSuccess) {
+      free_all(ctx); delete ctx; return QP_ERR_CUDA;
+    }
+    if ((e = dalloc(ctx, &ctx->kglobf, (size_t)ctx->gridf * (size_t)ctx->Lf.kglob)) ||
+        (e = dalloc(ctx, &ctx->fb_flag, (size_t)d->batch)) || (e = dalloc(ctx, &ctx->fb_list, 2 * (size_t)d->batch)) ||
+        (e = dalloc(ctx, &ctx->fb_ctl, 4 * (size_t)qp_ctx::kPipe))) {
+      free_all(ctx); delete ctx; return e;
+    }
+    if (cudaMemset(ctx->fb_flag, 0, sizeof(int) * d->batch) != cudaSuccess ||
+        cudaMemset(ctx->fb_ctl, 0, sizeof(int) * 4 * qp_ctx::kPipe) != cudaSuccess) {
+      free_all(ctx); delete ctx; return QP_ERR_CUDA;
+    }
+  }
   if (L.batched) {
     // per problem: a state block and a KKT workspace of capacity Nmax, for
     // up to half of the free device memory's worth of problems at a time
@@ -652,6 +722,17 @@ qp_err qp_get_info(const qp_ctx* c, qp_info* info) {
     info->ctas_per_sm = 0;                            // varies by phase kernel
   }
   info->workspace_bytes = c->workspace;
+  info->handed_solve = info->handed_backward = 0;
+  if (c->fb) {  // reading Q12c guard: hand-over counts of the last calls (all chunks)
+    int h[4 * qp_ctx::kPipe];
+    if (cudaStreamSynchronize(c->stream) != cudaSuccess ||
+        cudaMemcpy(h, c->fb_ctl, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess)
+      return QP_ERR_CUDA;
+    for (int ch = 0; ch < qp_ctx::kPipe; ++ch) {
+      info->handed_solve += h[2 * ch];
+      info->handed_backward += h[2 * (ch + qp_ctx::kPipe)];
+    }
+  }
   return QP_OK;
 }
 
@@ -717,6 +798,7 @@ qp_err qp_solve_batched(qp_ctx* c, const float* Q, const float* q, const float* 
   a.prof = c->prof;
   a.flops = c->flops_solve;
   a.kglob = c->kglob;
+  if (implicit) set_fb(c, a, false, 0);
   if (pipe) {
     // chunk ch on stream pst[ch]: H2D of its problems, its kernel, D2H of its outputs
     constexpr int KP = qp_ctx::kPipe;
@@ -735,8 +817,13 @@ qp_err qp_solve_batched(qp_ctx* c, const float* Q, const float* q, const float* 
           return e;
       qpb::Args ac = chunk_args(a, b0, nb);
       if (implicit) ac.sched = c->sched + ch;
+      if (c->fb) {
+        ac.fb_count = c->fb_ctl + 2 * ch;
+        if ((e = cuda_ok(cudaMemsetAsync(ac.fb_count, 0, 2 * sizeof(int), st))) != QP_OK) return e;
+      }
       c->ks.solve<<<std::min(c->grid, nb), c->ks.threads, c->L.smem, st>>>(ac);
       if ((e = cuda_ok(cudaGetLastError())) != QP_OK) return e;
+      if ((e = launch_fallback(c, ac, false, ch, KP, st)) != QP_OK) return e;
       auto o2h = [&](auto* dst, const auto* dsrc, size_t per_prob) -> qp_err {
         if (!dst || per_prob == 0) return QP_OK;
         return cuda_ok(cudaMemcpyAsync(dst + (size_t)b0 * per_prob, dsrc + (size_t)b0 * per_prob,
@@ -752,8 +839,10 @@ qp_err qp_solve_batched(qp_ctx* c, const float* Q, const float* q, const float* 
   } else if (c->L.batched) {
     if ((e = run_batched(c, a, false)) != QP_OK) return e;
   } else {
+    if (c->fb && (e = cuda_ok(cudaMemsetAsync(a.fb_count, 0, 2 * sizeof(int), c->stream))) != QP_OK) return e;
     c->ks.solve<<<c->grid, c->ks.threads, c->L.smem, c->stream>>>(a);
     if ((e = cuda_ok(cudaGetLastError())) != QP_OK) return e;
+    if ((e = launch_fallback(c, a, false, 0, 1, c->stream)) != QP_OK) return e;
   }
   if (pipe) {
     // outputs already copied chunk by chunk
@@ -848,6 +937,7 @@ qp_err qp_backward_batched(qp_ctx* c, const float* dl_dx, float* dQ, float* dq, 
   a.flops = c->flops_bwd;
   a.kglob = c->kglob;
   const bool implicit = c->c.formulation != QP_EXPLICIT;
+  if (implicit) set_fb(c, a, true, 0);
   if (implicit) {
     if (c->bwd_dirty &&
         (e = cuda_ok(cudaMemsetAsync(c->sched + 16, 0, sizeof(int) * 16, c->stream))) != QP_OK)
@@ -885,9 +975,14 @@ qp_err qp_backward_batched(qp_ctx* c, const float* dl_dx, float* dQ, float* dq, 
         // (the solve chunk, an earlier backward chunk), not after c->stream
         ac.sched = c->sched + 16 + ch;
         if ((e = cuda_ok(cudaMemsetAsync(ac.sched, 0, sizeof(int), st))) != QP_OK) return e;
+        if (c->fb) {
+          ac.fb_count = c->fb_ctl + 2 * (ch + qp_ctx::kPipe);
+          if ((e = cuda_ok(cudaMemsetAsync(ac.fb_count, 0, 2 * sizeof(int), st))) != QP_OK) return e;
+        }
       }
       c->ks.backward<<<std::min(c->grid, nb), c->ks.threads, c->L.smem, st>>>(ac);
       if ((e = cuda_ok(cudaGetLastError())) != QP_OK) return e;
+      if ((e = launch_fallback(c, ac, true, ch, KP, st)) != QP_OK) return e;
       for (int f = 0; f < 6; ++f)  // per-problem gradients (a.g* is null for shared / skipped fields)
         if (gdev[f] && ghost[f] && gper[f] > 0 &&
             (e = cuda_ok(cudaMemcpyAsync(ghost[f] + (size_t)b0 * gper[f], gdev[f] + (size_t)b0 * gper[f],
@@ -913,6 +1008,7 @@ qp_err qp_backward_batched(qp_ctx* c, const float* dl_dx, float* dQ, float* dq, 
     // instruction cache (two separate kernels made the overlap a net loss).
     // Not on the large-N path: its per-CTA global KKT workspaces are indexed
     // by blockIdx, which a solve CTA and a backward CTA would share.
+    if (c->fb && (e = cuda_ok(cudaMemsetAsync(a.fb_count, 0, 2 * sizeof(int), c->stream))) != QP_OK) return e;
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(c->grid);
     lc.blockDim = dim3(c->ks.threads);
@@ -924,9 +1020,13 @@ qp_err qp_backward_batched(qp_ctx* c, const float* dl_dx, float* dQ, float* dq, 
     lc.attrs = at;
     lc.numAttrs = 1;
     if ((e = cuda_ok(cudaLaunchKernelEx(&lc, c->ks.backward, a))) != QP_OK) return e;
+    if ((e = launch_fallback(c, a, true, 0, 1, c->stream)) != QP_OK) return e;
   } else {
+    if (c->fb && implicit && (e = cuda_ok(cudaMemsetAsync(a.fb_count, 0, 2 * sizeof(int), c->stream))) != QP_OK)
+      return e;
     c->ks.backward<<<c->grid, c->ks.threads, c->L.smem, c->stream>>>(a);
     if ((e = cuda_ok(cudaGetLastError())) != QP_OK) return e;
+    if (implicit && (e = launch_fallback(c, a, true, 0, 1, c->stream)) != QP_OK) return e;
   }
   if (shared) {
     auto osum = [&](float* out, const float* U, const float* V, const float* U2, const float* V2, int R, int Cc,

@@ -113,6 +113,40 @@ def g_rand(cfg: int, batch: int, n: int, m: int, p: int, start: int = 0) -> QPBa
                    meta={"recipe": "g_rand", "cfg": cfg, "start": start})
 
 
+def g_dup_active(cfg: int, batch: int, n: int, m: int, p: int, n_act: int, start: int = 0) -> QPBatch:
+    """Degenerate QPs that VIOLATE LICQ with many strongly active constraints
+    (the situation reading Q12c's kept-set cap must survive):
+    n_act distinct hyperplanes g_iᵀx = h_i, each appearing TWICE in G (2·n_act
+    active rows whose normals are linearly dependent), through a chosen point
+    x0; the other p − 2·n_act rows inactive with margins U(0.5, 1.5).  q is set
+    so that x0 is optimal with positive multipliers on the active rows:
+    q = −Q x0 − Σ_i λ_i g_i − Aᵀμ, λ_i ~ U(0.5, 1.5), b = A x0.  The solution
+    is therefore x* = x0 exactly (the multiplier split between the duplicates
+    is not unique).  Q, A as in g_rand; ∇ₓℓ ~ N(0, 1).  meta["x_star"] = x0."""
+    assert 2 * n_act <= p
+    Qs = np.empty((batch, n, n), F32); qs = np.empty((batch, n), F32)
+    As = np.empty((batch, m, n), F32); bs = np.empty((batch, m), F32)
+    Gs = np.empty((batch, p, n), F32); hs = np.empty((batch, p), F32)
+    dls = np.empty((batch, n), F32); xs = np.empty((batch, n))
+    for j in range(batch):
+        rng = _rng(cfg, start + j)
+        M = rng.standard_normal((n, n))
+        Q = _sym(M @ M.T / n + 0.1 * np.eye(n)).astype(F32).astype(np.float64)
+        A = (rng.standard_normal((m, n)) / np.sqrt(n)).astype(F32).astype(np.float64)
+        Gd = (rng.standard_normal((n_act, n)) / np.sqrt(n)).astype(F32).astype(np.float64)
+        Gi = (rng.standard_normal((p - 2 * n_act, n)) / np.sqrt(n)).astype(F32).astype(np.float64)
+        x0 = rng.standard_normal(n).astype(F32).astype(np.float64)
+        lam = rng.uniform(0.5, 1.5, n_act)
+        mu = rng.standard_normal(m)
+        G = np.concatenate([Gd, Gd, Gi])
+        h = np.concatenate([Gd @ x0, Gd @ x0, Gi @ x0 + rng.uniform(0.5, 1.5, p - 2 * n_act)])
+        q = -(Q @ x0) - Gd.T @ lam - A.T @ mu
+        Qs[j], qs[j], As[j], bs[j] = Q, q, A, A @ x0
+        Gs[j], hs[j], dls[j], xs[j] = G, h, rng.standard_normal(n), x0
+    return QPBatch(n, m, p, Qs, qs, As, bs, Gs, hs, dls, batch,
+                   meta={"recipe": "g_dup_active", "cfg": cfg, "start": start, "x_star": xs})
+
+
 def g_rand_shared(cfg: int, batch: int, n: int, m: int, p: int, start: int = 0) -> QPBatch:
     """Config 4 ("end-to-end/bilevel"): Q, A, b, G, h shared across the batch
     (drawn once from stream [cfg, 0]); per-instance q_b~N(0,1) and ∇ₓℓ_b~N(0,1)

@@ -178,6 +178,12 @@ qp_err qp_destroy(qp_ctx* ctx);
  * All pointers device memory; asynchronous on `stream`. */
 qp_err qp_debug_tc_syrk(const float* G, const float* om, const float* Q, int32_t n, int32_t p, float* H,
                         void* stream);
+/* Diagnostic (tests only): with the environment variable QPB200_GUARD set at
+ * qp_create, every ctx workspace is allocated with 64 KB guard bands of 0xFF
+ * on both sides; this synchronises the ctx stream and counts the guard words
+ * that no longer hold 0xFFFFFFFF (out-of-bounds writes by a kernel).
+ * QP_ERR_UNSUPPORTED without guard mode. */
+qp_err qp_debug_check_guards(qp_ctx* ctx, int64_t* bad_words);
 const char* qp_error_string(qp_err err);
 
 #ifdef __cplusplus

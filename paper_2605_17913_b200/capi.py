@@ -41,7 +41,7 @@ class QpInfo(C.Structure):
 
 EXPORTS = ("qp_config_default", "qp_create", "qp_set_stream", "qp_get_info", "qp_max_kkt_dim",
            "qp_solve_batched", "qp_backward_batched", "qp_last_flops", "qp_destroy", "qp_error_string",
-           "qp_debug_tc_syrk")
+           "qp_debug_tc_syrk", "qp_debug_check_guards")
 
 _lib = None
 
@@ -72,6 +72,8 @@ def load(path: str | None = None):
     L.qp_last_flops.argtypes = [V, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.qp_debug_tc_syrk.argtypes = [V, V, V, C.c_int32, C.c_int32, V, V]
     L.qp_debug_tc_syrk.restype = C.c_int
+    L.qp_debug_check_guards.argtypes = [V, C.POINTER(C.c_int64)]
+    L.qp_debug_check_guards.restype = C.c_int
     L.qp_error_string.argtypes = [C.c_int]
     L.qp_error_string.restype = C.c_char_p
     for f in ("qp_config_default", "qp_create", "qp_set_stream", "qp_get_info", "qp_solve_batched",
@@ -132,3 +134,10 @@ def qp_debug_tc_syrk(G, om, Q, n, p, H, stream=None):
 
 def qp_destroy(h):
     load().qp_destroy(h)
+
+
+def qp_debug_check_guards(h) -> int:
+    """Guard words overwritten in the ctx workspaces (QPB200_GUARD mode)."""
+    n = C.c_int64()
+    check(load().qp_debug_check_guards(h, C.byref(n)), "qp_debug_check_guards")
+    return n.value

@@ -251,6 +251,8 @@ struct qp_ctx {
   int* fb_flag = nullptr;   // [B]
   int* fb_list = nullptr;   // [2B]: solve list, backward list (chunk segments at b0)
   int* fb_ctl = nullptr;    // [2][kPipe][2]: count, launch counter per call and chunk
+  bool guard = false;                               // QPB200_GUARD: guard bands around workspaces
+  std::vector<std::pair<char*, size_t>> guards;     // (allocation base, payload bytes)
   static constexpr int kPipe = 8;
   bool pipe = false;
   cudaStream_t pst[kPipe] = {};
@@ -261,11 +263,27 @@ namespace {
 
 qp_err cuda_ok(cudaError_t e) { return e == cudaSuccess ? QP_OK : QP_ERR_CUDA; }
 
+// Guard mode (QPB200_GUARD=1, tests: the memcheck substitute of
+// tests/test_gpu_memcheck.py — compute-sanitizer is not available on the GPU
+// pool): every workspace gets kGuard bytes of 0xFF before and after it;
+// qp_debug_check_guards counts guard words a kernel overwrote.
+constexpr size_t kGuard = 64 * 1024;
+
 template <typename T>
 qp_err dalloc(qp_ctx* c, T** p, size_t count) {
   *p = nullptr;
   if (count == 0) return QP_OK;
-  if (cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T)) != cudaSuccess) return QP_ERR_OOM;
+  if (c->guard) {
+    char* base = nullptr;
+    const size_t bytes = count * sizeof(T);
+    if (cudaMalloc(reinterpret_cast<void**>(&base), bytes + 2 * kGuard) != cudaSuccess) return QP_ERR_OOM;
+    if (cudaMemset(base, 0xFF, kGuard) != cudaSuccess || cudaMemset(base + kGuard + bytes, 0xFF, kGuard) != cudaSuccess)
+      return QP_ERR_CUDA;
+    c->guards.push_back({base, bytes});
+    *p = reinterpret_cast<T*>(base + kGuard);
+  } else if (cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T)) != cudaSuccess) {
+    return QP_ERR_OOM;
+  }
   c->workspace += (int64_t)(count * sizeof(T));
   return QP_OK;
 }
@@ -277,6 +295,11 @@ void free_all(qp_ctx* c) {
   void* ptrs[] = {c->kglobf, c->fb_flag, c->fb_list, c->fb_ctl, c->ug, c->dtg, c->whi, c->wlo, c->gghi, c->gglo, c->slotmap, c->bst, c->bctl, c->tl, c->sched, c->done, c->kglob, c->flops_solve, c->flops_bwd, c->prof, c->own_status, c->wx, c->wy, c->wz, c->wdx, c->wdy, c->wdz, c->dQ_, c->dq_, c->dA_, c->db_,
                   c->dG_, c->dh_, c->dx_, c->ds_, c->dz_, c->dy_, c->ddl_, c->dit_, c->dst_, c->gQ_, c->gq_,
                   c->gA_, c->gb_, c->gG_, c->gh_};
+  if (c->guard) {  // guard mode: the allocations start kGuard bytes before each pointer
+    for (auto& g : c->guards) cudaFree(g.first);
+    c->guards.clear();
+    return;
+  }
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -562,6 +585,7 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
   qp_ctx* ctx = new (std::nothrow) qp_ctx();
   if (!ctx) return QP_ERR_OOM;
   ctx->d = *d; ctx->c = c; ctx->device = device; ctx->stream = static_cast<cudaStream_t>(stream); ctx->L = L;
+  ctx->guard = getenv("QPB200_GUARD") != nullptr;
   qp_err e = QP_OK;
   ctx->ks = pick_kernels(L, c.formulation);
   if (!ctx->ks.solve) { delete ctx; return QP_ERR_UNSUPPORTED; }  // standard arm: path 1 sizes only
@@ -1104,6 +1128,22 @@ qp_err qp_debug_tc_syrk(const float* G, const float* om, const float* Q, int32_t
     return QP_ERR_CUDA;
   k<<<1, 128, qpb::tc::SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(G, om, Q, n, p, H);
   return cuda_ok(cudaGetLastError());
+}
+
+qp_err qp_debug_check_guards(qp_ctx* c, int64_t* bad_words) {
+  if (!c || !bad_words) return QP_ERR_INVALID_ARG;
+  *bad_words = 0;
+  if (!c->guard) return QP_ERR_UNSUPPORTED;
+  if (cudaSetDevice(c->device) != cudaSuccess || cudaStreamSynchronize(c->stream) != cudaSuccess) return QP_ERR_CUDA;
+  std::vector<uint32_t> h(kGuard / 4);
+  for (auto& g : c->guards) {
+    for (int side = 0; side < 2; ++side) {
+      const char* src = side == 0 ? g.first : g.first + kGuard + g.second;
+      if (cudaMemcpy(h.data(), src, kGuard, cudaMemcpyDeviceToHost) != cudaSuccess) return QP_ERR_CUDA;
+      for (uint32_t w : h) *bad_words += (w != 0xFFFFFFFFu);
+    }
+  }
+  return QP_OK;
 }
 
 qp_err qp_destroy(qp_ctx* c) {

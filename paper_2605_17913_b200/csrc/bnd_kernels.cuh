@@ -90,9 +90,17 @@ __host__ inline long long bnd_state_floats(int n4, int m, int p, int N4max) {
 // float4 copy of a state block (global ↔ shared), whole CTA, then a barrier
 template <int NT>
 __device__ __forceinline__ void copy_block(float* __restrict__ dst, const float* __restrict__ src, long long nf) {
+  // 8 loads in flight per thread before the stores (the copy is latency-bound)
   const float4* s4 = reinterpret_cast<const float4*>(src);
   float4* d4 = reinterpret_cast<float4*>(dst);
-  for (long long i = threadIdx.x; i < (nf >> 2); i += NT) d4[i] = s4[i];
+  const int n4 = (int)(nf >> 2);
+  for (int i0 = threadIdx.x; i0 < n4; i0 += 8 * NT) {
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) if (i0 + u * NT < n4) v[u] = s4[i0 + u * NT];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) if (i0 + u * NT < n4) d4[i0 + u * NT] = v[u];
+  }
   __syncthreads();
 }
 
@@ -545,17 +553,29 @@ __global__ void __launch_bounds__(NT) bnd_pdiag(const BArgs ba) {
   const int c1 = min(c0 + W, N4), w = c1 - c0;
   float* K = ba.kw + (long long)bid * ba.kstride;
   float* rinv = carve_state(gst, a).rinv;
-  for (int e = tid; e < w * (W / 4); e += NT) {
-    const int r = e / (W / 4), q = e - r * (W / 4), i = c0 + r, j = c0 + 4 * q;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (4 * q < w && j <= i) {
-      v = *reinterpret_cast<const float4*>(K + L.off(i) + j);
-      if (c0 > 0) {  // the panel's Schur update from bnd_tc_update
-        const float4 u = *reinterpret_cast<const float4*>(ba.ug + (long long)bid * ba.ustride + r * W + 4 * q);
-        v.x -= u.x; v.y -= u.y; v.z -= u.z; v.w -= u.w;
+  {
+    // lane: quad q = lane % 16 of rows r0 + 2·u (u < 32): all loads of a batch in flight first
+    const float* Ub = ba.ug + (long long)bid * ba.ustride;
+    const int q = tid & 15, rr = tid >> 4;
+    const bool qok = 4 * q < w;
+#pragma unroll 1
+    for (int r0 = rr; r0 < w; r0 += 16 * (NT / 16)) {
+      float4 v[16], u[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        const int r = r0 + t * (NT / 16), i = c0 + r, j = c0 + 4 * q;
+        const bool ok = r < w && qok && j <= i;
+        v[t] = ok ? *reinterpret_cast<const float4*>(K + L.off(i) + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        u[t] = (ok && c0 > 0) ? *reinterpret_cast<const float4*>(Ub + r * W + 4 * q) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        const int r = r0 + t * (NT / 16);
+        if (r < w)  // the panel's Schur update from bnd_tc_update subtracted
+          *reinterpret_cast<float4*>(D + r * DS + 4 * q) =
+              make_float4(v[t].x - u[t].x, v[t].y - u[t].y, v[t].z - u[t].z, v[t].w - u[t].w);
       }
     }
-    *reinterpret_cast<float4*>(D + r * DS + 4 * q) = v;
   }
   __syncthreads();
   PanelLayout P;
@@ -596,9 +616,20 @@ __global__ void __launch_bounds__(NT, 4) bnd_prows(const BArgs ba) {
   float* K = ba.kw + (long long)bid * ba.kstride;
   const float* rinv = carve_state(gst, a).rinv;
   const float4* dt = reinterpret_cast<const float4*>(ba.dtg + (long long)bid * (W * W));
-  for (int e = tid; e < W * W / 4; e += NT) {
-    const int k = e / (W / 4), q = e - k * (W / 4);
-    *reinterpret_cast<float4*>(DT + k * DS + 4 * q) = dt[e];
+  {
+    static_assert(W * W / 4 % NT == 0 || NT > W * W / 4, "bnd_prows: DT staging");
+    constexpr int U = (W * W / 4 + NT - 1) / NT;
+    float4 v[U];
+#pragma unroll
+    for (int t = 0; t < U; ++t) if (tid + t * NT < W * W / 4) v[t] = dt[tid + t * NT];
+#pragma unroll
+    for (int t = 0; t < U; ++t) {
+      const int e = tid + t * NT;
+      if (e < W * W / 4) {
+        const int k = e / (W / 4), q = e - k * (W / 4);
+        *reinterpret_cast<float4*>(DT + k * DS + 4 * q) = v[t];
+      }
+    }
   }
   for (int k = tid; k < W; k += NT) rl[k] = rinv[c0 + k];
   __syncthreads();

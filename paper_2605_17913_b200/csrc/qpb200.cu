@@ -232,7 +232,10 @@ struct qp_ctx {
   long long bst_stride = 0;
   int bchunk = 0;
   int* bctl = nullptr;       // device: [0] problems iterating, [1] largest N4
-  int* hctl = nullptr;       // pinned host copy
+  int* hctl = nullptr;       // pinned host copy ([4 per lane])
+  int nlanes = 1, lane_cap = 0;         // concurrent sub-batches of a chunk, problems per lane
+  cudaStream_t bstr[4] = {};            // lane streams (bstr[0] = the ctx stream at call time)
+  cudaEvent_t bev[5] = {};              // ordering / read-back events
   int blaunch[2] = {0, 0};   // kernel launches of the last solve / backward
   // shared G: the assembly as one batched GEMM (kr_gemm.cuh)
   bool kr = false;
@@ -437,75 +440,129 @@ qp_err run_batched(qp_ctx* c, const qpb::Args& a0, bool bwd) {
   const int T = (n4 + qpb::tc::TM - 1) / qpb::tc::TM;
   const int sst = (int)(c->bst_stride * 4), ssv = (int)(c->L.N4max * 4);
   const int stc = qpb::tc::SMEM_BYTES;
+  const int krN = (qpb::kr::npairs(n4) + qpb::kr::BN - 1) / qpb::kr::BN;
+  const size_t kpad = (size_t)qpb::kr::nkc(c->d.p) * qpb::kr::BK;
   int launches = 0;
-  cudaStream_t st = c->stream;
-  for (int b0 = 0; b0 < B; b0 += c->bchunk) {
-    const int nb = std::min(c->bchunk, B - b0);
-    qpb::BArgs ba;
-    std::memset(&ba, 0, sizeof(ba));
-    ba.a = chunk_args(a0, b0, nb);
-    ba.a.bwd = bwd ? 1 : 0;
-    ba.st = c->bst; ba.st_stride = c->bst_stride;
-    ba.kw = c->kglob; ba.kstride = c->L.kglob;
-    ba.ctl = c->bctl;
-    ba.ntiles = c->kr ? 0 : T * (T + 1) / 2;
-    ba.w = kBW;
-    ba.kr = c->kr ? 1 : 0;
-    ba.whi = c->whi; ba.wlo = c->wlo; ba.slotmap = c->slotmap; ba.dtg = c->dtg;
-    ba.ug = c->ug; ba.ustride = (long long)c->L.N4max * 64;
-    qpb::kr::GemmArgs ga;
-    const int krN = (qpb::kr::npairs(n4) + qpb::kr::BN - 1) / qpb::kr::BN;
-    if (c->kr) {
-      ga.whi = c->whi; ga.wlo = c->wlo; ga.gghi = c->gghi; ga.gglo = c->gglo;
-      ga.count = c->bctl; ga.slotmap = c->slotmap;
-      ga.kw = c->kglob; ga.kstride = c->L.kglob; ga.st = c->bst; ga.st_stride = c->bst_stride;
-      ga.Q = ba.a.Q; ga.sQ = ba.a.sQ;
-      ga.n = c->d.n; ga.n4 = n4; ga.m = m; ga.p = c->d.p;
-      if (b0 == 0) {  // GG = the Khatri-Rao square of the shared G, once per call
-        qpb::kr::kr_prep<<<4 * 148, 256, 0, st>>>(a0.G, c->d.n, n4, c->d.p, c->gghi, c->gglo);
-        ++launches;
-      }
-    }
-    if (cudaMemsetAsync(c->bctl, 0, 2 * sizeof(int), st) != cudaSuccess) return QP_ERR_CUDA;
-    qpb::bnd_begin<kBS><<<nb, kBS, sst, st>>>(ba);
+  // lanes: the chunk is split into c->nlanes sub-batches whose iteration
+  // loops run interleaved on their own streams, so that one sub-batch's
+  // phase kernels fill the tail waves of the other's
+  c->bstr[0] = c->stream;
+  cudaEvent_t ev0 = c->bev[0];
+  if (cudaEventRecord(ev0, c->stream) != cudaSuccess) return QP_ERR_CUDA;
+  for (int l = 1; l < c->nlanes; ++l)
+    if (cudaStreamWaitEvent(c->bstr[l], ev0, 0) != cudaSuccess) return QP_ERR_CUDA;
+  if (c->kr) {  // GG = the Khatri-Rao square of the shared G, once per call (lane 0; the others wait below)
+    qpb::kr::kr_prep<<<4 * 148, 256, 0, c->stream>>>(a0.G, c->d.n, n4, c->d.p, c->gghi, c->gglo);
     ++launches;
-    int N4cur = bwd ? 0 : qpb::r4(n4 + m);  // the initial system (solve)
-    const int kmax = bwd ? c->c.relax_max_iter : c->c.max_iter;
-    for (int k = bwd ? 0 : -1; k <= kmax + 1; ++k) {
-      if (k >= 0) {
-        if (cudaMemsetAsync(c->bctl, 0, 2 * sizeof(int), st) != cudaSuccess) return QP_ERR_CUDA;
-        ba.k = k;
-        qpb::bnd_resid<kBS><<<nb, kBS, sst, st>>>(ba);
-        ++launches;
-        if (cudaMemcpyAsync(c->hctl, c->bctl, 2 * sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-            cudaStreamSynchronize(st) != cudaSuccess)
-          return QP_ERR_CUDA;
-        if (c->hctl[0] == 0) break;
-        N4cur = c->hctl[1];
-      }
-      if (c->kr) qpb::bnd_scatter<kBS><<<nb, kBS, 0, st>>>(ba);
-      else qpb::bnd_assemble<kBT><<<dim3(ba.ntiles + 1, nb), kBT, stc, st>>>(ba);
-      ++launches;
+    if (cudaEventRecord(ev0, c->stream) != cudaSuccess) return QP_ERR_CUDA;
+    for (int l = 1; l < c->nlanes; ++l)
+      if (cudaStreamWaitEvent(c->bstr[l], ev0, 0) != cudaSuccess) return QP_ERR_CUDA;
+  }
+  struct Lane {
+    cudaStream_t st;
+    qpb::BArgs ba;
+    qpb::kr::GemmArgs ga;
+    int nb, N4cur, k;
+    bool live;
+  };
+  const int NL = c->nlanes, lcap = c->lane_cap;
+  for (int b0 = 0; b0 < B; b0 += NL * lcap) {
+    Lane ln[4];
+    int nlive = 0;
+    for (int l = 0; l < NL; ++l) {
+      Lane& L = ln[l];
+      const int lb0 = b0 + l * lcap;
+      L.nb = std::max(0, std::min(lcap, B - lb0));
+      L.live = L.nb > 0;
+      if (!L.live) continue;
+      ++nlive;
+      L.st = c->bstr[l];
+      qpb::BArgs& ba = L.ba;
+      std::memset(&ba, 0, sizeof(ba));
+      ba.a = chunk_args(a0, lb0, L.nb);
+      ba.a.bwd = bwd ? 1 : 0;
+      ba.st = c->bst + (size_t)l * lcap * c->bst_stride; ba.st_stride = c->bst_stride;
+      ba.kw = c->kglob + (size_t)l * lcap * c->L.kglob; ba.kstride = c->L.kglob;
+      ba.ctl = c->bctl + 4 * l;
+      ba.ntiles = c->kr ? 0 : T * (T + 1) / 2;
+      ba.w = kBW;
+      ba.kr = c->kr ? 1 : 0;
+      const size_t wrows = (size_t)((lcap + qpb::kr::BM - 1) / qpb::kr::BM) * qpb::kr::BM;
+      ba.whi = c->whi ? c->whi + l * wrows * kpad : nullptr;
+      ba.wlo = c->wlo ? c->wlo + l * wrows * kpad : nullptr;
+      ba.slotmap = c->slotmap ? c->slotmap + (size_t)l * lcap : nullptr;
+      ba.dtg = c->dtg + (size_t)l * lcap * 64 * 64;
+      ba.ug = c->ug + (size_t)l * lcap * c->L.N4max * 64; ba.ustride = (long long)c->L.N4max * 64;
+      qpb::kr::GemmArgs& ga = L.ga;
       if (c->kr) {
-        qpb::kr::kr_gemm<<<dim3(krN, (nb + qpb::kr::BM - 1) / qpb::kr::BM), 128, qpb::kr::SMEM_BYTES, st>>>(ga);
-        ++launches;
+        ga.whi = ba.whi; ga.wlo = ba.wlo; ga.gghi = c->gghi; ga.gglo = c->gglo;
+        ga.count = ba.ctl; ga.slotmap = ba.slotmap;
+        ga.kw = ba.kw; ga.kstride = c->L.kglob; ga.st = ba.st; ga.st_stride = c->bst_stride;
+        ga.Q = ba.a.Q; ga.sQ = ba.a.sQ;
+        ga.n = c->d.n; ga.n4 = n4; ga.m = m; ga.p = c->d.p;
       }
-      for (int c0 = 0; c0 < N4cur; c0 += kBW) {
-        ba.c0 = c0;
-        if (c0 > 0) {
-          qpb::bnd_tc_update<kBT><<<dim3((N4cur - c0 + qpb::tc::TM - 1) / qpb::tc::TM, nb), kBT, stc, st>>>(ba);
+      if (cudaMemsetAsync(ba.ctl, 0, 2 * sizeof(int), L.st) != cudaSuccess) return QP_ERR_CUDA;
+      qpb::bnd_begin<kBS><<<L.nb, kBS, sst, L.st>>>(ba);
+      ++launches;
+      L.N4cur = bwd ? 0 : qpb::r4(n4 + m);  // the initial system (solve)
+      L.k = bwd ? 0 : -1;
+    }
+    const int kmax = bwd ? c->c.relax_max_iter : c->c.max_iter;
+    while (nlive > 0) {
+      // residuals + stopping test of every live lane, then the read-backs
+      for (int l = 0; l < NL; ++l) {
+        Lane& L = ln[l];
+        if (!L.live || L.k < 0) continue;
+        if (cudaMemsetAsync(L.ba.ctl, 0, 2 * sizeof(int), L.st) != cudaSuccess) return QP_ERR_CUDA;
+        L.ba.k = L.k;
+        qpb::bnd_resid<kBS><<<L.nb, kBS, sst, L.st>>>(L.ba);
+        ++launches;
+        if (cudaMemcpyAsync(c->hctl + 4 * l, L.ba.ctl, 2 * sizeof(int), cudaMemcpyDeviceToHost, L.st) != cudaSuccess ||
+            cudaEventRecord(c->bev[1 + l], L.st) != cudaSuccess)
+          return QP_ERR_CUDA;
+      }
+      for (int l = 0; l < NL; ++l) {
+        Lane& L = ln[l];
+        if (!L.live) continue;
+        if (L.k >= 0) {
+          if (cudaEventSynchronize(c->bev[1 + l]) != cudaSuccess) return QP_ERR_CUDA;
+          if (c->hctl[4 * l] == 0 || L.k > kmax + 1) { L.live = false; --nlive; continue; }
+          L.N4cur = c->hctl[4 * l + 1];
+        }
+        qpb::BArgs& ba = L.ba;
+        cudaStream_t st = L.st;
+        const int nb = L.nb;
+        if (c->kr) qpb::bnd_scatter<kBS><<<nb, kBS, 0, st>>>(ba);
+        else qpb::bnd_assemble<kBT><<<dim3(ba.ntiles + 1, nb), kBT, stc, st>>>(ba);
+        ++launches;
+        if (c->kr) {
+          qpb::kr::kr_gemm<<<dim3(krN, (nb + qpb::kr::BM - 1) / qpb::kr::BM), 128, qpb::kr::SMEM_BYTES, st>>>(L.ga);
           ++launches;
         }
-        qpb::bnd_pdiag<32><<<nb, 32, 0, st>>>(ba);
-        if (c0 + kBW < N4cur)
-          qpb::bnd_prows<kBT><<<dim3((N4cur - c0 - kBW + kBT - 1) / kBT, nb), kBT, 0, st>>>(ba);
+        for (int c0 = 0; c0 < L.N4cur; c0 += kBW) {
+          ba.c0 = c0;
+          if (c0 > 0) {
+            qpb::bnd_tc_update<kBT><<<dim3((L.N4cur - c0 + qpb::tc::TM - 1) / qpb::tc::TM, nb), kBT, stc, st>>>(ba);
+            ++launches;
+          }
+          qpb::bnd_pdiag<32><<<nb, 32, 0, st>>>(ba);
+          if (c0 + kBW < L.N4cur)
+            qpb::bnd_prows<kBT><<<dim3((L.N4cur - c0 - kBW + kBT - 1) / kBT, nb), kBT, 0, st>>>(ba);
+          launches += 2;
+        }
+        qpb::bnd_solve<kBT><<<nb, kBT, ssv, st>>>(ba);
+        qpb::bnd_update<kBS><<<nb, kBS, sst, st>>>(ba);
         launches += 2;
+        ++L.k;
       }
-      qpb::bnd_solve<kBT><<<nb, kBT, ssv, st>>>(ba);
-      qpb::bnd_update<kBS><<<nb, kBS, sst, st>>>(ba);
-      launches += 2;
     }
     if (cudaGetLastError() != cudaSuccess) return QP_ERR_CUDA;
+  }
+  // the ctx stream continues after every lane
+  for (int l = 1; l < NL; ++l) {
+    if (cudaEventRecord(c->bev[1 + l], c->bstr[l]) != cudaSuccess ||
+        cudaStreamWaitEvent(c->stream, c->bev[1 + l], 0) != cudaSuccess)
+      return QP_ERR_CUDA;
   }
   c->blaunch[bwd ? 1 : 0] = launches;
   return QP_OK;
@@ -643,21 +700,33 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
     long long cap = (long long)(fr / 2 / per);
     if (const char* e2 = getenv("QPB200_BCHUNK")) cap = atoll(e2);  // tests: force several chunks
     ctx->bchunk = (int)std::max(1LL, std::min<long long>(d->batch, cap));
+    // two lanes when the chunk holds enough problems to fill the GPU twice
+    ctx->nlanes = ctx->bchunk >= 2 * 4 * 148 ? 2 : 1;
+    if (const char* e2 = getenv("QPB200_BLANES")) ctx->nlanes = std::max(1, std::min(4, atoi(e2)));
+    ctx->nlanes = std::min(ctx->nlanes, ctx->bchunk);
+    ctx->lane_cap = (ctx->bchunk + ctx->nlanes - 1) / ctx->nlanes;
+    ctx->bchunk = ctx->lane_cap * ctx->nlanes;
+    for (int l = 0; l < ctx->nlanes; ++l)
+      if (l > 0 && cudaStreamCreateWithFlags(&ctx->bstr[l], cudaStreamNonBlocking) != cudaSuccess) {
+        free_all(ctx); delete ctx; return QP_ERR_CUDA;
+      }
+    for (auto& ev : ctx->bev)
+      if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) { free_all(ctx); delete ctx; return QP_ERR_CUDA; }
     if ((e = dalloc(ctx, &ctx->bst, (size_t)ctx->bchunk * ctx->bst_stride)) != QP_OK ||
         (e = dalloc(ctx, &ctx->kglob, (size_t)ctx->bchunk * (size_t)L.kglob)) != QP_OK ||
-        (e = dalloc(ctx, &ctx->bctl, 4)) != QP_OK ||
+        (e = dalloc(ctx, &ctx->bctl, 16)) != QP_OK ||
         (e = dalloc(ctx, &ctx->dtg, (size_t)ctx->bchunk * 64 * 64)) != QP_OK ||
         (e = dalloc(ctx, &ctx->ug, (size_t)ctx->bchunk * L.N4max * 64)) != QP_OK) {
       free_all(ctx); delete ctx; return e;
     }
-    if (cudaMallocHost(&ctx->hctl, 4 * sizeof(int)) != cudaSuccess || bnd_setup(ctx) != QP_OK) {
+    if (cudaMallocHost(&ctx->hctl, 16 * sizeof(int)) != cudaSuccess || bnd_setup(ctx) != QP_OK) {
       free_all(ctx); delete ctx; return QP_ERR_CUDA;
     }
     // shared G: the assembly runs as one GEMM over the batch (kr_gemm.cuh)
     ctx->kr = d->bstride_G == 0 && d->p > 0 && !getenv("QPB200_NO_KR");
     if (ctx->kr) {
       const size_t kpad = (size_t)qpb::kr::nkc(d->p) * qpb::kr::BK;
-      const size_t mrows = (size_t)((ctx->bchunk + qpb::kr::BM - 1) / qpb::kr::BM) * qpb::kr::BM;
+      const size_t mrows = (size_t)ctx->nlanes * ((ctx->lane_cap + qpb::kr::BM - 1) / qpb::kr::BM) * qpb::kr::BM;
       const size_t nrows = (size_t)((qpb::kr::npairs(L.n4) + qpb::kr::BN - 1) / qpb::kr::BN) * qpb::kr::BN;
       if ((e = dalloc(ctx, &ctx->whi, mrows * kpad)) || (e = dalloc(ctx, &ctx->wlo, mrows * kpad)) ||
           (e = dalloc(ctx, &ctx->gghi, nrows * kpad)) || (e = dalloc(ctx, &ctx->gglo, nrows * kpad)) ||
@@ -1152,6 +1221,10 @@ qp_err qp_destroy(qp_ctx* c) {
   free_all(c);
   for (auto& st : c->pst)
     if (st) cudaStreamDestroy(st);
+  for (int l = 1; l < 4; ++l)
+    if (c->bstr[l]) cudaStreamDestroy(c->bstr[l]);
+  for (auto& ev : c->bev)
+    if (ev) cudaEventDestroy(ev);
   for (auto& ev : c->pev)
     if (ev) cudaEventDestroy(ev);
   delete c;

@@ -131,7 +131,8 @@ __global__ void __launch_bounds__(128, 1) kr_gemm(const GemmArgs g) {
   extern __shared__ __align__(1024) float krsm[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int count = *g.count;
-  const int mt = blockIdx.y, nt = blockIdx.x;
+  // problem tiles vary fastest: the CTAs that share a GG tile run together (one DRAM read of GG per call)
+  const int mt = blockIdx.x, nt = blockIdx.y;
   if (mt * BM >= count) return;
   const int nk = nkc(g.p), np = npairs(g.n4);
   float* stage = krsm;

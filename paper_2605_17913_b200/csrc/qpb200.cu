@@ -536,7 +536,7 @@ qp_err run_batched(qp_ctx* c, const qpb::Args& a0, bool bwd) {
         else qpb::bnd_assemble<kBT><<<dim3(ba.ntiles + 1, nb), kBT, stc, st>>>(ba);
         ++launches;
         if (c->kr) {
-          qpb::kr::kr_gemm<<<dim3(krN, (nb + qpb::kr::BM - 1) / qpb::kr::BM), 128, qpb::kr::SMEM_BYTES, st>>>(L.ga);
+          qpb::kr::kr_gemm<<<dim3((nb + qpb::kr::BM - 1) / qpb::kr::BM, krN), 128, qpb::kr::SMEM_BYTES, st>>>(L.ga);
           ++launches;
         }
         for (int c0 = 0; c0 < L.N4cur; c0 += kBW) {

@@ -24,14 +24,16 @@
 // slot in this iteration's list of iterating problems; GG by kr_prep once per
 // call.
 //
-// Kernel: one CTA per (128 problems, 256 pairs) output tile, 128 threads,
-// 2-stage ring of 96 KB: thread 0 produces (bulk copies), thread 32 issues
-// the MMAs (tcgen05.mma.cta_group::1.kind::tf32, M = 128, N = 256, K = 8;
-// accumulator 256 fp32 columns of TMEM) and commits each stage back to the
-// producer, then all four warps drain TMEM (tcgen05.ld.32x32b.x32), transpose
-// through shared memory and write each problem's pairs into its packed KKT
-// workspace (ipm_cta.cuh layout), adding Q and the padding identity, and
-// record max|diag| (the pivot floor's scale) per problem.
+// Kernel: persistent, one CTA per SM, 192 threads, (128 problems × 256
+// pairs) output tiles, 2-stage ring of 96 KB: a producer warp issues the bulk
+// copies, an MMA warp issues tcgen05.mma.cta_group::1.kind::tf32 (M = 128,
+// N = 256, K = 8) into one of two TMEM accumulators (2 × 256 fp32 columns)
+// and commits each stage back to the producer, and four epilogue warps drain
+// the other accumulator (tcgen05.ld.32x32b.x32), transpose through shared
+// memory and write each problem's pairs into its packed KKT workspace
+// (ipm_cta.cuh layout), adding Q and the padding identity, and record
+// max|diag| (the pivot floor's scale) per problem — the epilogue of one tile
+// overlapping the copies and MMAs of the next.
 #pragma once
 #include "ipm_cta.cuh"
 #include "tc_syrk.cuh"
@@ -127,135 +129,170 @@ __device__ __forceinline__ uint32_t idesc_256() {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
 
-__global__ void __launch_bounds__(128, 1) kr_gemm(const GemmArgs g) {
+// Persistent, warp-specialised: grid = min(tiles, SMs), tiles (problem tile
+// fastest) strided over the CTAs.  Warp 4 produces (bulk copies into the
+// 2-stage ring), warp 5 issues the MMAs into one of TWO TMEM accumulators
+// (2 × 256 columns), warps 0-3 drain the other accumulator (epilogue) at the
+// same time — so the epilogue of tile t overlaps the loads and MMAs of tile
+// t + 1.  mbarriers: full/empty per ring stage, tfull/tempty per accumulator.
+constexpr int WS_THREADS = 192;
+constexpr int WS_SMEM_BYTES = STAGES * STAGE_FL * 4 + 4 * 32 * 33 * 4 + 256;
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(mbar)) : "memory");
+}
+
+__global__ void __launch_bounds__(WS_THREADS, 1) kr_gemm(const GemmArgs g) {
   extern __shared__ __align__(1024) float krsm[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int count = *g.count;
-  // problem tiles vary fastest: the CTAs that share a GG tile run together (one DRAM read of GG per call)
-  const int mt = blockIdx.x, nt = blockIdx.y;
-  if (mt * BM >= count) return;
   const int nk = nkc(g.p), np = npairs(g.n4);
+  const int mtiles = (count + BM - 1) / BM, ntiles = (np + BN - 1) / BN, tiles = mtiles * ntiles;
+  if ((int)blockIdx.x >= tiles) return;
   float* stage = krsm;
-  uint64_t* full = reinterpret_cast<uint64_t*>(krsm + STAGES * STAGE_FL);
+  float* scr = krsm + STAGES * STAGE_FL;  // epilogue transpose scratch, [4 warps][32][33]
+  uint64_t* full = reinterpret_cast<uint64_t*>(scr + 4 * 32 * 33);
   uint64_t* empty = full + STAGES;
-  uint64_t* done = empty + STAGES;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(tslot)),
-                 "n"(BN));
+                 "n"(2 * BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) { tc::mbar_init(full + s, 1); tc::mbar_init(empty + s, 1); }
-    tc::mbar_init(done, 1);
+    for (int a = 0; a < 2; ++a) { tc::mbar_init(tfull + a, 1); tc::mbar_init(tempty + a, 4); }
   }
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tslot;
-  if (tid == 0) {
-    // producer: four bulk copies per K chunk into the ring
-    for (int kc = 0; kc < nk; ++kc) {
-      const int s = kc % STAGES;
-      if (kc >= STAGES) tc::mbar_wait(empty + s, ((kc / STAGES) - 1) & 1);
-      float* st = stage + s * STAGE_FL;
-      mbar_expect_tx(full + s, STAGE_FL * 4);
-      const long long ao = ((long long)mt * nk + kc) * A_FL, bo = ((long long)nt * nk + kc) * B_FL;
-      bulk_g2s(st, g.whi + ao, A_FL * 4, full + s);
-      bulk_g2s(st + A_FL, g.wlo + ao, A_FL * 4, full + s);
-      bulk_g2s(st + 2 * A_FL, g.gghi + bo, B_FL * 4, full + s);
-      bulk_g2s(st + 2 * A_FL + B_FL, g.gglo + bo, B_FL * 4, full + s);
+  if (warp == 4) {
+    if (lane == 0) {  // producer: four bulk copies per K chunk into the ring
+      int it = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int mt = t % mtiles, nt = t / mtiles;
+        for (int kc = 0; kc < nk; ++kc, ++it) {
+          const int s = it % STAGES;
+          if (it >= STAGES) tc::mbar_wait(empty + s, ((it / STAGES) - 1) & 1);
+          float* st = stage + s * STAGE_FL;
+          mbar_expect_tx(full + s, STAGE_FL * 4);
+          const long long ao = ((long long)mt * nk + kc) * A_FL, bo = ((long long)nt * nk + kc) * B_FL;
+          bulk_g2s(st, g.whi + ao, A_FL * 4, full + s);
+          bulk_g2s(st + A_FL, g.wlo + ao, A_FL * 4, full + s);
+          bulk_g2s(st + 2 * A_FL, g.gghi + bo, B_FL * 4, full + s);
+          bulk_g2s(st + 2 * A_FL + B_FL, g.gglo + bo, B_FL * 4, full + s);
+        }
+      }
     }
-  } else if (tid == 32) {
-    // MMA issuer: 4 k-steps of 8 per chunk, three products each (3×TF32)
-    const uint32_t idesc = idesc_256();
-    for (int kc = 0; kc < nk; ++kc) {
-      const int s = kc % STAGES;
-      tc::mbar_wait(full + s, (kc / STAGES) & 1);
+  } else if (warp == 5) {
+    if (lane == 0) {  // MMA issuer: 4 k-steps of 8 per chunk, three products each (3×TF32)
+      const uint32_t idesc = idesc_256();
+      int it = 0, li = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++li) {
+        const int acc = li & 1;
+        if (li >= 2) tc::mbar_wait(tempty + acc, ((li >> 1) - 1) & 1);  // the epilogue drained it
+        tc::tc_fence_after();
+        const uint32_t tacc = tmem + (uint32_t)(acc * BN);
+        for (int kc = 0; kc < nk; ++kc, ++it) {
+          const int s = it % STAGES;
+          tc::mbar_wait(full + s, (it / STAGES) & 1);
+          tc::tc_fence_after();
+          const float* st = stage + s * STAGE_FL;
+          const uint32_t ahi = tc::smem_u32(st), alo = tc::smem_u32(st + A_FL);
+          const uint32_t bhi = tc::smem_u32(st + 2 * A_FL), blo = tc::smem_u32(st + 2 * A_FL + B_FL);
+#pragma unroll
+          for (int ks = 0; ks < BK / 8; ++ks) {
+            const uint32_t off = ks * 2 * 128;
+            const uint32_t acc0 = (kc > 0 || ks > 0) ? 1u : 0u;
+            tc::mma_tf32(tacc, tc::make_desc(ahi + off), tc::make_desc(bhi + off), idesc, acc0);
+            tc::mma_tf32(tacc, tc::make_desc(ahi + off), tc::make_desc(blo + off), idesc, 1u);
+            tc::mma_tf32(tacc, tc::make_desc(alo + off), tc::make_desc(bhi + off), idesc, 1u);
+          }
+          tc::commit(empty + s);
+        }
+        tc::commit(tfull + acc);
+      }
+    }
+  } else {
+    // ---- epilogue warps 0-3: warp w holds problems (slots) mt*128 + 32w + [0, 32) ----
+    float* T = scr + warp * (32 * 33);
+    const int n = g.n, n4 = g.n4, m = g.m;
+    int li = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++li) {
+      const int mt = t % mtiles, nt = t / mtiles, acc = li & 1;
+      tc::mbar_wait(tfull + acc, (li >> 1) & 1);
       tc::tc_fence_after();
-      const float* st = stage + s * STAGE_FL;
-      const uint32_t ahi = tc::smem_u32(st), alo = tc::smem_u32(st + A_FL);
-      const uint32_t bhi = tc::smem_u32(st + 2 * A_FL), blo = tc::smem_u32(st + 2 * A_FL + B_FL);
+      __syncwarp();
+      // lane r: problem of slot mt*128 + 32w + r and the parameters of its packed
+      // layout (KLayout: only the last 16-row block differs between sizes)
+      const int slot_l = mt * BM + 32 * warp + lane;
+      const int nrow = min(32, count - (mt * BM + 32 * warp));  // warp-uniform (may be ≤ 0)
+      int b_l = 0, nbm1_l = 0, baseL_l = 0, Ll_l = 0;
+      float* stb_l = nullptr;
+      if (lane < nrow) {
+        b_l = g.slotmap[slot_l];
+        stb_l = g.st + (long long)b_l * g.st_stride;
+        const int pa = reinterpret_cast<const int*>(stb_l)[6];  // BScal::pa
+        const KLayout L = KLayout::make(n4 + pa + m, n4);
+        nbm1_l = L.NB - 1; baseL_l = L.baseL; Ll_l = L.Ll;
+      }
+      float dmx = 0.f;  // lane r: max |diag| of problem r over this tile's pairs
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        float v[32];
+        tc::tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(acc * BN + c0), v);
 #pragma unroll
-      for (int ks = 0; ks < BK / 8; ++ks) {
-        const uint32_t off = ks * 2 * 128;
-        const uint32_t acc0 = (kc > 0 || ks > 0) ? 1u : 0u;
-        tc::mma_tf32(tmem, tc::make_desc(ahi + off), tc::make_desc(bhi + off), idesc, acc0);
-        tc::mma_tf32(tmem, tc::make_desc(ahi + off), tc::make_desc(blo + off), idesc, 1u);
-        tc::mma_tf32(tmem, tc::make_desc(alo + off), tc::make_desc(bhi + off), idesc, 1u);
-      }
-      tc::commit(empty + s);
-    }
-    tc::commit(done);
-  }
-  tc::mbar_wait(done, 0);
-  tc::tc_fence_after();
-  __syncwarp();
-  // ---- epilogue: warp w holds problems (slots) mt*128 + 32w + [0, 32) ----
-  float* T = stage + warp * (32 * 33);  // per-warp transpose scratch (the ring is idle now)
-  const int n = g.n, n4 = g.n4, m = g.m;
-  // lane r: problem of slot mt*128 + 32w + r and the parameters of its packed
-  // layout (KLayout: only the last 16-row block differs between sizes)
-  const int slot_l = mt * BM + 32 * warp + lane;
-  const int nrow = min(32, count - (mt * BM + 32 * warp));  // warp-uniform
-  int b_l = 0, nbm1_l = 0, baseL_l = 0, Ll_l = 0;
-  float* stb_l = nullptr;
-  if (lane < nrow) {
-    b_l = g.slotmap[slot_l];
-    stb_l = g.st + (long long)b_l * g.st_stride;
-    const int pa = reinterpret_cast<const int*>(stb_l)[6];  // BScal::pa
-    const KLayout L = KLayout::make(n4 + pa + m, n4);
-    nbm1_l = L.NB - 1; baseL_l = L.baseL; Ll_l = L.Ll;
-  }
-  float dmx = 0.f;  // lane r: max |diag| of problem r over this tile's pairs
-  for (int c0 = 0; c0 < BN; c0 += 32) {
-    float v[32];
-    tc::tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)c0, v);
-#pragma unroll
-    for (int c = 0; c < 32; ++c) T[lane * 33 + c] = v[c];
-    __syncwarp();
-    if (nrow > 0) {
-      // lane = pair column
-      const int t = nt * BN + c0 + lane;
-      const bool tok = t < np;
-      int i = 0, j = 0;
-      if (tok) {
-        i = (int)((sqrtf(8.f * t + 1.f) - 1.f) * 0.5f);
-        while ((i + 1) * (i + 2) / 2 <= t) ++i;
-        while (i * (i + 1) / 2 > t) --i;
-        j = t - i * (i + 1) / 2;
-      }
-      const int bi = i >> 4, ti = i & 15;
-      const int offr = 128 * bi * (bi + 1) + 64 * bi + ti * (16 * bi + 20) + j;  // row i in a full block
-      const bool inner = tok && i < n && j < n, isdiag = tok && i == j && i < n;
-      const bool anyd = __any_sync(0xffffffffu, isdiag);
-      float q = 0.f;
-      if (g.sQ == 0 && inner) q = __ldg(g.Q + (size_t)i * n + j);
-      for (int r = 0; r < nrow; ++r) {
-        const int b = __shfl_sync(0xffffffffu, b_l, r);
-        const int nbm1 = __shfl_sync(0xffffffffu, nbm1_l, r);
-        const int baseL = __shfl_sync(0xffffffffu, baseL_l, r);
-        const int Ll = __shfl_sync(0xffffffffu, Ll_l, r);
-        float val = 0.f;
-        if (tok) {
-          const float qq = g.sQ == 0 ? q : (inner ? __ldg(g.Q + g.sQ * b + (size_t)i * n + j) : 0.f);
-          val = inner ? qq + T[r * 33 + lane] : (i == j ? 1.f : 0.f);
-          const int off = bi < nbm1 ? offr : baseL + ti * Ll + j;
-          g.kw[(long long)b * g.kstride + off] = val;
+        for (int c = 0; c < 32; ++c) T[lane * 33 + c] = v[c];
+        __syncwarp();
+        if (nrow > 0) {
+          const int tp = nt * BN + c0 + lane;  // lane = pair column
+          const bool tok = tp < np;
+          int i = 0, j = 0;
+          if (tok) {
+            i = (int)((sqrtf(8.f * tp + 1.f) - 1.f) * 0.5f);
+            while ((i + 1) * (i + 2) / 2 <= tp) ++i;
+            while (i * (i + 1) / 2 > tp) --i;
+            j = tp - i * (i + 1) / 2;
+          }
+          const int bi = i >> 4, ti = i & 15;
+          const int offr = 128 * bi * (bi + 1) + 64 * bi + ti * (16 * bi + 20) + j;  // row i in a full block
+          const bool inner = tok && i < n && j < n, isdiag = tok && i == j && i < n;
+          const bool anyd = __any_sync(0xffffffffu, isdiag);
+          float q = 0.f;
+          if (g.sQ == 0 && inner) q = __ldg(g.Q + (size_t)i * n + j);
+          for (int r = 0; r < nrow; ++r) {
+            const int b = __shfl_sync(0xffffffffu, b_l, r);
+            const int nbm1 = __shfl_sync(0xffffffffu, nbm1_l, r);
+            const int baseL = __shfl_sync(0xffffffffu, baseL_l, r);
+            const int Ll = __shfl_sync(0xffffffffu, Ll_l, r);
+            float val = 0.f;
+            if (tok) {
+              const float qq = g.sQ == 0 ? q : (inner ? __ldg(g.Q + g.sQ * b + (size_t)i * n + j) : 0.f);
+              val = inner ? qq + T[r * 33 + lane] : (i == j ? 1.f : 0.f);
+              const int off = bi < nbm1 ? offr : baseL + ti * Ll + j;
+              g.kw[(long long)b * g.kstride + off] = val;
+            }
+            if (anyd) {
+              const float mx =
+                  __uint_as_float(__reduce_max_sync(0xffffffffu, isdiag ? __float_as_uint(fabsf(val)) : 0u));
+              if (lane == r) dmx = fmaxf(dmx, mx);
+            }
+          }
         }
-        if (anyd) {
-          const float mx = __uint_as_float(__reduce_max_sync(0xffffffffu, isdiag ? __float_as_uint(fabsf(val)) : 0u));
-          if (lane == r) dmx = fmaxf(dmx, mx);
-        }
+        __syncwarp();
       }
+      if (lane < nrow && dmx > 0.f) atomicMax(reinterpret_cast<int*>(stb_l) + 4, __float_as_int(dmx));  // BScal::dmax
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty + acc);
     }
-    __syncwarp();
   }
-  if (lane < nrow && dmx > 0.f) atomicMax(reinterpret_cast<int*>(stb_l) + 4, __float_as_int(dmx));  // BScal::dmax
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(BN));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * BN));
 }
 
 }  // namespace kr

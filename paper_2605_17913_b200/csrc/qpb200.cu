@@ -234,6 +234,7 @@ struct qp_ctx {
   int* bctl = nullptr;       // device: [0] problems iterating, [1] largest N4
   int* hctl = nullptr;       // pinned host copy ([4 per lane])
   int nlanes = 1, lane_cap = 0;         // concurrent sub-batches of a chunk, problems per lane
+  int sms = 148;                        // multiprocessors (persistent kr_gemm grid)
   cudaStream_t bstr[4] = {};            // lane streams (bstr[0] = the ctx stream at call time)
   cudaEvent_t bev[5] = {};              // ordering / read-back events
   int blaunch[2] = {0, 0};   // kernel launches of the last solve / backward
@@ -423,7 +424,7 @@ qp_err bnd_setup(const qp_ctx* c) {
       cudaFuncSetAttribute(qpb::bnd_solve<kBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, ssv) ||
       cudaFuncSetAttribute(qpb::bnd_assemble<kBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, stc) ||
       cudaFuncSetAttribute(qpb::bnd_tc_update<kBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, stc) ||
-      cudaFuncSetAttribute(qpb::kr::kr_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, qpb::kr::SMEM_BYTES))
+      cudaFuncSetAttribute(qpb::kr::kr_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, qpb::kr::WS_SMEM_BYTES))
     return QP_ERR_CUDA;
   return QP_OK;
 }
@@ -536,7 +537,8 @@ qp_err run_batched(qp_ctx* c, const qpb::Args& a0, bool bwd) {
         else qpb::bnd_assemble<kBT><<<dim3(ba.ntiles + 1, nb), kBT, stc, st>>>(ba);
         ++launches;
         if (c->kr) {
-          qpb::kr::kr_gemm<<<dim3((nb + qpb::kr::BM - 1) / qpb::kr::BM, krN), 128, qpb::kr::SMEM_BYTES, st>>>(L.ga);
+          qpb::kr::kr_gemm<<<std::min(c->sms / NL, ((nb + qpb::kr::BM - 1) / qpb::kr::BM) * krN), qpb::kr::WS_THREADS,
+                             qpb::kr::WS_SMEM_BYTES, st>>>(L.ga);
           ++launches;
         }
         for (int c0 = 0; c0 < L.N4cur; c0 += kBW) {
@@ -704,6 +706,7 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
     ctx->nlanes = ctx->bchunk >= 2 * 4 * 148 ? 2 : 1;
     if (const char* e2 = getenv("QPB200_BLANES")) ctx->nlanes = std::max(1, std::min(4, atoi(e2)));
     ctx->nlanes = std::min(ctx->nlanes, ctx->bchunk);
+    cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);
     ctx->lane_cap = (ctx->bchunk + ctx->nlanes - 1) / ctx->nlanes;
     ctx->bchunk = ctx->lane_cap * ctx->nlanes;
     for (int l = 0; l < ctx->nlanes; ++l)

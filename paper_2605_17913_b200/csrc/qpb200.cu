@@ -235,6 +235,7 @@ struct qp_ctx {
   int* hctl = nullptr;       // pinned host copy ([4 per lane])
   int nlanes = 1, lane_cap = 0;         // concurrent sub-batches of a chunk, problems per lane
   int sms = 148;                        // multiprocessors (persistent kr_gemm grid)
+  int kr_div = 2;                       // kr_gemm grid = sms / kr_div (room for the other lane's kernels)
   cudaStream_t bstr[4] = {};            // lane streams (bstr[0] = the ctx stream at call time)
   cudaEvent_t bev[5] = {};              // ordering / read-back events
   int blaunch[2] = {0, 0};   // kernel launches of the last solve / backward
@@ -537,7 +538,7 @@ qp_err run_batched(qp_ctx* c, const qpb::Args& a0, bool bwd) {
         else qpb::bnd_assemble<kBT><<<dim3(ba.ntiles + 1, nb), kBT, stc, st>>>(ba);
         ++launches;
         if (c->kr) {
-          qpb::kr::kr_gemm<<<std::min(c->sms / NL, ((nb + qpb::kr::BM - 1) / qpb::kr::BM) * krN), qpb::kr::WS_THREADS,
+          qpb::kr::kr_gemm<<<std::min(c->sms / c->kr_div, ((nb + qpb::kr::BM - 1) / qpb::kr::BM) * krN), qpb::kr::WS_THREADS,
                              qpb::kr::WS_SMEM_BYTES, st>>>(L.ga);
           ++launches;
         }
@@ -707,6 +708,8 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
     if (const char* e2 = getenv("QPB200_BLANES")) ctx->nlanes = std::max(1, std::min(4, atoi(e2)));
     ctx->nlanes = std::min(ctx->nlanes, ctx->bchunk);
     cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);
+    ctx->kr_div = ctx->nlanes;
+    if (const char* e2 = getenv("QPB200_KR_DIV")) ctx->kr_div = std::max(1, atoi(e2));  // A/B
     ctx->lane_cap = (ctx->bchunk + ctx->nlanes - 1) / ctx->nlanes;
     ctx->bchunk = ctx->lane_cap * ctx->nlanes;
     for (int l = 0; l < ctx->nlanes; ++l)

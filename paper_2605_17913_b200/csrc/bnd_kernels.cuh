@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(NT) bnd_begin(const BArgs ba) {
 // of this iteration's Newton system — exactly the head of the persistent
 // kernel's loop body.
 // ---------------------------------------------------------------------------
-template <int NT>
+template <int NT, bool LARGE = false>
 __global__ void __launch_bounds__(NT) bnd_resid(const BArgs ba) {
   extern __shared__ __align__(16) float sm[];
   const Args& a = ba.a;
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(NT) bnd_resid(const BArgs ba) {
   const int k = ba.k;
   const float kappa = manifold_coords<NT>(S, a);
   const float kt = bwd ? a.kappa_relax : a.sigma * kappa;
-  const Norms R = residuals<NT>(S, a, P, kappa, kappa - kt);
+  const Norms R = residuals<NT, LARGE>(S, a, P, kappa, kappa - kt);
   bool fin = false, adj = false;
   int status = ST_CONVERGED;
   float fl = h.fl, phi_prev = h.phi_prev;

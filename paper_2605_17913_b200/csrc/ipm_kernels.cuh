@@ -532,7 +532,7 @@ struct Norms {
   bool spill;  // reading Q12c guard: the capped elimination would exceed fb_bound
 };
 
-template <int NT>
+template <int NT, bool LARGE = false>
 __device__ Norms residuals(const Smem& S, const Args& a, const Prob& P, float kappa, float r_kappa) {
   const int tid = threadIdx.x;
   const int n = a.n, n4 = a.n4, p = a.p, m = a.m;
@@ -643,7 +643,61 @@ __device__ Norms residuals(const Smem& S, const Args& a, const Prob& P, float ka
     __syncthreads();
   }
   float mrt = 0.f, mqx = 0.f, mq = 0.f, mgz = 0.f, may = 0.f, obj = 0.f;
-  for (int j = tid; j < n; j += NT) {
+  auto col_epi = [&](int j, float qx, float gz, float gt, float ay) {
+    const float qj = __ldg(P.q + j);
+    const float rt = qx + qj + gz + ay;
+    S.rhs[j] = -(rt - gt);
+    mrt = fmaxf(mrt, fabsf(rt)); mqx = fmaxf(mqx, fabsf(qx)); mq = fmaxf(mq, fabsf(qj));
+    mgz = fmaxf(mgz, fabsf(gz)); may = fmaxf(may, fabsf(ay));
+    obj = fmaf(S.x[j], fmaf(0.5f, qx, qj), obj);
+    if (!isfinite(rt)) nonfin += 1.f;
+  };
+  bool quads = false;
+  if constexpr (LARGE) {
+    // large n (batched engine): a thread owns a column QUAD (float4 loads of
+    // Q, G, A rows) and keeps 8 rows in flight — the per-problem GEMVs of
+    // config 5 (G: 8 MB per problem, from DRAM) are bound by bytes in flight
+    quads = n >= 2 * NT && !(n & 3) &&
+            !((reinterpret_cast<uintptr_t>(P.Q) | reinterpret_cast<uintptr_t>(P.G) |
+               (m > 0 ? reinterpret_cast<uintptr_t>(P.A) : 0)) & 15);
+    if (quads) {
+      for (int j4 = tid; j4 < (n >> 2); j4 += NT) {
+        const int j = 4 * j4;
+        float4 qx = make_float4(0.f, 0.f, 0.f, 0.f), gz = qx, gt = qx, ay = qx;
+        auto mat = [&](const float* M, int rows, const float* vec, const float* vec2, float4& acc, float4& acc2) {
+          for (int i0 = 0; i0 < rows; i0 += 8) {
+            float4 g[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              g[u] = i0 + u < rows ? __ldg(reinterpret_cast<const float4*>(M + (size_t)(i0 + u) * n + j))
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              if (i0 + u < rows) {
+                const float xv = vec[i0 + u];
+                acc.x = fmaf(g[u].x, xv, acc.x); acc.y = fmaf(g[u].y, xv, acc.y);
+                acc.z = fmaf(g[u].z, xv, acc.z); acc.w = fmaf(g[u].w, xv, acc.w);
+                if (vec2) {
+                  const float tv = vec2[i0 + u];
+                  acc2.x = fmaf(g[u].x, tv, acc2.x); acc2.y = fmaf(g[u].y, tv, acc2.y);
+                  acc2.z = fmaf(g[u].z, tv, acc2.z); acc2.w = fmaf(g[u].w, tv, acc2.w);
+                }
+              }
+            }
+          }
+        };
+        float4 dummy;
+        mat(P.Q, n, S.x, nullptr, qx, dummy);
+        mat(P.G, p, S.z, S.t, gz, gt);
+        mat(P.A, m, S.y, nullptr, ay, dummy);
+        col_epi(j, qx.x, gz.x, gt.x, ay.x);
+        col_epi(j + 1, qx.y, gz.y, gt.y, ay.y);
+        col_epi(j + 2, qx.z, gz.z, gt.z, ay.z);
+        col_epi(j + 3, qx.w, gz.w, gt.w, ay.w);
+      }
+    }
+  }
+  for (int j = tid; !quads && j < n; j += NT) {
     float qx = 0.f, gz = 0.f, gt = 0.f, ay = 0.f;
     if (ng > 1) {
       for (int g = 0; g < ng; ++g) {
@@ -661,13 +715,7 @@ __device__ Norms residuals(const Smem& S, const Args& a, const Prob& P, float ka
       }
       for (int l = 0; l < m; ++l) ay = fmaf(__ldg(P.A + l * n + j), S.y[l], ay);
     }
-    const float qj = __ldg(P.q + j);
-    const float rt = qx + qj + gz + ay;
-    S.rhs[j] = -(rt - gt);
-    mrt = fmaxf(mrt, fabsf(rt)); mqx = fmaxf(mqx, fabsf(qx)); mq = fmaxf(mq, fabsf(qj));
-    mgz = fmaxf(mgz, fabsf(gz)); may = fmaxf(may, fabsf(ay));
-    obj = fmaf(S.x[j], fmaf(0.5f, qx, qj), obj);
-    if (!isfinite(rt)) nonfin += 1.f;
+    col_epi(j, qx, gz, gt, ay);
   }
   for (int j = n + tid; j < n4; j += NT) S.rhs[j] = 0.f;
   const int N = n4 + pa + m;

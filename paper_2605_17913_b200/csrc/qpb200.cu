@@ -421,6 +421,7 @@ qp_err bnd_setup(const qp_ctx* c) {
   const int stc = qpb::tc::SMEM_BYTES;
   if (cudaFuncSetAttribute(qpb::bnd_begin<kBS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sst) ||
       cudaFuncSetAttribute(qpb::bnd_resid<kBS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sst) ||
+      cudaFuncSetAttribute(qpb::bnd_resid<kBS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sst) ||
       cudaFuncSetAttribute(qpb::bnd_update<kBS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sst) ||
       cudaFuncSetAttribute(qpb::bnd_solve<kBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, ssv) ||
       cudaFuncSetAttribute(qpb::bnd_assemble<kBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, stc) ||
@@ -517,7 +518,10 @@ qp_err run_batched(qp_ctx* c, const qpb::Args& a0, bool bwd) {
         if (!L.live || L.k < 0) continue;
         if (cudaMemsetAsync(L.ba.ctl, 0, 2 * sizeof(int), L.st) != cudaSuccess) return QP_ERR_CUDA;
         L.ba.k = L.k;
-        qpb::bnd_resid<kBS><<<L.nb, kBS, sst, L.st>>>(L.ba);
+        if (c->d.n >= 2 * kBS)  // column-quad GEMVs with 8 rows in flight (config 5)
+          qpb::bnd_resid<kBS, true><<<L.nb, kBS, sst, L.st>>>(L.ba);
+        else
+          qpb::bnd_resid<kBS><<<L.nb, kBS, sst, L.st>>>(L.ba);
         ++launches;
         if (cudaMemcpyAsync(c->hctl + 4 * l, L.ba.ctl, 2 * sizeof(int), cudaMemcpyDeviceToHost, L.st) != cudaSuccess ||
             cudaEventRecord(c->bev[1 + l], L.st) != cudaSuccess)

@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--relax-mode", type=int, default=None, choices=(0, 2),
+                    help="Alg. 2 linear solves: 0 exact Newton, 2 guarded chord (reading Q26); default: the library's")
     ap.add_argument("--dump", default=None,
                     help="write this rank's outputs of the last timed step to DIR/rank<r>.npz (tests)")
     return ap.parse_args()
@@ -119,6 +121,13 @@ class ClockSampler:
 def workload_of(a) -> dict:
     """The workload bench.py runs: BASELINE.json config `--config`, or an N4
     application shape `--workload` (generators.WORKLOADS)."""
+    w = _workload_of(a)
+    if getattr(a, "relax_mode", None) is not None:
+        w["solver"]["relax_mode"] = a.relax_mode
+    return w
+
+
+def _workload_of(a) -> dict:
     if getattr(a, "workload", None):
         w = gen.WORKLOADS[a.workload]
         b1 = gen.make_workload(a.workload, batch=1)

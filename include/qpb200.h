@@ -78,6 +78,19 @@ enum {
 
 enum { QP_IMPLICIT = 0, QP_EXPLICIT = 1 };   /* formulation: Eq. 14 or Eq. 8 */
 enum { QP_MEM_DEVICE = 0, QP_MEM_HOST = 1, QP_MEM_HOST_ASYNC = 2 };
+/* Alg. 2's linear solves (qp_config.relax_mode): exact Newton, a fresh
+ * factorisation per step (reading Q6); or the guarded chord of SURVEY §8(f)
+ * N2(i) (reading Q26): the solve caches the factorisation of its first
+ * iterate with κ < √10·κ_relax ("the matrix factorizations K̃ computed during
+ * the forward solve ... can be heavily reused"; "if K̃ not cached",
+ * P:513) and Alg. 2 takes chord steps on it — the current residuals, the
+ * cached Jacobian — while each shrinks ψ = max(φ, |κ/κ_relax − 1|) by
+ * chord_rho (at most chord_max of them); from the first that does not it
+ * takes exact Newton steps.  A chord phase ends only at φ ≤ relax_tol.
+ * Either way the final factorisation is at the relaxed point, so Alg. 3's
+ * gradients are the exact IFT gradients there.  Path 4 only (elsewhere the
+ * relax is exact Newton; qp_info.relax_mode reports the mode in effect). */
+enum { QP_RELAX_NEWTON = 0, QP_RELAX_CHORD = 2 };
 
 typedef struct {
   int32_t batch;   /* B ≥ 1                                                     */
@@ -104,6 +117,10 @@ typedef struct {
   int32_t mem_kind;       /* QP_MEM_DEVICE (default) | QP_MEM_HOST | QP_MEM_HOST_ASYNC     */
   float relax_tol;        /* Alg. 2 residual tolerance (Q5b); default 1e-6; the relax loop */
                           /* also stops at the f32 floor (φ ≤ tol and no 10% progress)     */
+  int32_t relax_mode;     /* QP_RELAX_NEWTON (default) | QP_RELAX_CHORD (reading Q26)      */
+  int32_t chord_max;      /* QP_RELAX_CHORD: most chord steps per problem; default 8       */
+  float chord_rho;        /* QP_RELAX_CHORD: contraction a chord step must reach, (0, 1];  */
+                          /* default 0.5                                                    */
 } qp_config;
 
 typedef struct qp_ctx qp_ctx;
@@ -129,6 +146,9 @@ typedef struct {
                            /* reduced system (reading Q12c); p = no cap                    */
   int32_t handed_solve;    /* problems the last solve / backward handed to the uncapped    */
   int32_t handed_backward; /* large-N kernel (reading Q12c guard); synchronises the stream */
+  int32_t relax_mode;      /* the Alg. 2 mode in effect (QP_RELAX_*)                       */
+  int32_t chord_steps;     /* chord steps of the last backward, summed over the batch      */
+                           /* (0 unless QP_RELAX_CHORD is in effect)                        */
 } qp_info;
 
 /* Fill *cfg with the defaults listed above. */

@@ -45,7 +45,8 @@ class OracleCfg(C.Structure):
                 ("tau", C.c_double), ("kappa_relax", C.c_double), ("relax_ktol", C.c_double),
                 ("relax_max_iter", C.c_int32), ("kkt_solver", C.c_int32),
                 ("formulation", C.c_int32), ("pivot_floor_rel", C.c_double), ("relax_tol", C.c_double),
-                ("partition_cap", C.c_int32), ("relax_mode", C.c_int32)]
+                ("partition_cap", C.c_int32), ("relax_mode", C.c_int32),
+                ("chord_max", C.c_int32), ("chord_rho", C.c_double)]
 
 
 @dataclass
@@ -63,7 +64,9 @@ class Cfg:
     pivot_floor_rel: float = float(np.sqrt(np.finfo(np.float32).eps))
     relax_tol: float = 1e-6
     partition_cap: int = -1  # SOLVER_M_PART: reading Q12c (-1 = keep every v_i > 0)
-    relax_mode: int = 0      # 0: Alg. 2 by exact Newton (Q6); 1: chord steps with Alg. 1's factor (N2(i))
+    relax_mode: int = 0      # 0: Alg. 2 by exact Newton (Q6); 1: chord steps with Alg. 1's factor (N2(i)); 2: guarded chord (Q26)
+    chord_max: int = 8       # relax_mode 2: most chord steps
+    chord_rho: float = 0.5   # relax_mode 2: contraction a chord step must reach
 
     @staticmethod
     def f64(**kw) -> "Cfg":
@@ -79,7 +82,8 @@ class Cfg:
     def c(self) -> OracleCfg:
         return OracleCfg(self.tol, self.max_iter, self.sigma, self.tau, self.kappa_relax,
                          self.relax_ktol, self.relax_max_iter, self.kkt_solver, self.formulation,
-                         self.pivot_floor_rel, self.relax_tol, self.partition_cap, self.relax_mode)
+                         self.pivot_floor_rel, self.relax_tol, self.partition_cap, self.relax_mode,
+                         self.chord_max, self.chord_rho)
 
 
 def lib():

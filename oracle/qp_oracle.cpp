@@ -26,6 +26,8 @@
 #include <atomic>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <thread>
@@ -56,7 +58,10 @@ typedef struct {
   double pivot_floor_rel; // LDL pivot floor theta = rel*max|diag| (Q12)
   double relax_tol;       // Alg. 2 residual tolerance (reading Q5b)
   int32_t partition_cap;  // SOLVER_M_PART: most constraints kept in augmented form (reading Q12c); -1 = no cap
-  int32_t relax_mode;     // 0: Alg. 2 by exact Newton (Q6); 1: chord steps with Alg. 1's factor nearest kappa_relax (N2(i))
+  int32_t relax_mode;     // 0: Alg. 2 by exact Newton (Q6); 1: chord steps with Alg. 1's factor nearest kappa_relax (N2(i));
+                          // 2: guarded chord (N2(i), reading Q26): chord steps while they contract, then exact Newton
+  int32_t chord_max;      // relax_mode 2: most chord steps
+  double chord_rho;       // relax_mode 2: a chord step must shrink psi = max(phi, |kappa/kappa_relax - 1|) by this factor
 } oracle_cfg;
 }
 
@@ -563,25 +568,46 @@ static int relax_qp_implicit(const Prob<T>& P, const oracle_cfg& cfg, T* x, T* y
   std::vector<T> v(p), dx(n), dy(m), dz(p), ds(p), dv(p);
   Res<T> R;
   T phi_prev = std::numeric_limits<T>::infinity();
+  // relax_mode 2 (guarded chord, reading Q26): chord steps on the cached Alg. 1
+  // factorisation while each shrinks psi = max(phi, |kappa/kappa_relax - 1|) by
+  // chord_rho, at most chord_max of them; from the first that does not, exact
+  // Newton (Q6) to the end.  relax_mode 1: chord steps throughout.
+  const bool guarded = cfg.relax_mode == 2;
+  bool use_chord = chord != nullptr;
+  int nchord = 0;
+  T psi_prev = std::numeric_limits<T>::infinity();
   for (int k = 0;; ++k) {
     for (int i = 0; i < p; ++i) v[i] = z[i] - s[i];
     T kappa = mean_sz(s, z, p);
     residuals(P, x, y, z, s, kappa, true, R);
     *iters = k;
     bool kok = p == 0 || std::fabs(kappa / kr - T(1)) <= ktol;
-    const bool done = kok && relax_done(R, tol, rtol, phi_prev);
-    if (!chord || done) {
+    if (use_chord && guarded) {
+      const T psi = std::max(rel_phi(R), p == 0 ? T(0) : std::fabs(kappa / kr - T(1)));
+      if (nchord >= cfg.chord_max || (nchord > 0 && !(psi <= T(cfg.chord_rho) * psi_prev))) {
+        use_chord = false;
+        phi_prev = std::numeric_limits<T>::infinity();  // the stall test (Q5b) measures Newton steps only
+      }
+      psi_prev = psi;
+    }
+    // a guarded chord stops only at phi <= relax_tol: a slow chord is not the working-precision floor
+    const bool done = kok && (use_chord && guarded ? rel_phi(R) <= rtol : relax_done(R, tol, rtol, phi_prev));
+    if (!use_chord || done) {
       // exact Newton (or the final factorisation at the relaxed point, for Alg. 3)
       F = factor_kkt(P, v.data(), kappa, cfg.kkt_solver, fr, cfg.partition_cap);
       if (!finite_all(F.dp) || !finite_all(F.dm) || !F.ok) return ST_NUMERICAL_FAILURE | (STG_RELAX << 8);
     }
-    if (done) return ST_CONVERGED;
+    if (done) {
+      if (chord && std::getenv("ORACLE_CHORD_STATS")) std::fprintf(stderr, "chord_stats %d %d\n", k, nchord);
+      return ST_CONVERGED;
+    }
     phi_prev = kok ? rel_phi(R) : std::numeric_limits<T>::infinity();
     if (k == cfg.relax_max_iter) return ST_MAX_ITER | (STG_RELAX << 8);
     T rk = kappa - kr;  // kappa_target = kappa_relax
     T dk;
     // chord step (N2(i)): the Newton system of Alg. 1's cached factorisation, current residuals
-    newton_direction(P, chord ? *chord : F, R, rk, dx.data(), dy.data(), dz.data(), ds.data(), dv.data(), dk);
+    newton_direction(P, use_chord ? *chord : F, R, rk, dx.data(), dy.data(), dz.data(), ds.data(), dv.data(), dk);
+    if (use_chord) ++nchord;
     if (!finite_all(dx) || !finite_all(dv) || !finite_all(dz) || !finite_all(ds))
       return ST_NUMERICAL_FAILURE | (STG_RELAX << 8);
     T alpha = linesearch(s, z, ds.data(), dz.data(), p, tau);
@@ -872,7 +898,7 @@ static void backward_batch(const oracle_cfg& cfg, const BatchData<T>& D, int B, 
     } else {
       Factor<T> F, C;
       const Factor<T>* chord = nullptr;
-      if (cfg.relax_mode == 1) {
+      if (cfg.relax_mode == 1 || cfg.relax_mode == 2) {
         // N2(i): the factorisation Alg. 1 computed nearest kappa_relax, recomputed
         // here by re-running the (deterministic) forward solve
         std::vector<T> xs(n), ys(m), zs(p), ss(p);

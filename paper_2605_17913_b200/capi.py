@@ -17,6 +17,7 @@ ERRORS = {0: "ok", -1: "invalid argument", -2: "unsupported shape", -3: "pointer
 QP_CONVERGED, QP_MAX_ITER, QP_NUMERICAL_FAILURE = 0, 2, 3
 QP_IMPLICIT, QP_EXPLICIT = 0, 1
 QP_MEM_DEVICE, QP_MEM_HOST, QP_MEM_HOST_ASYNC = 0, 1, 2
+QP_RELAX_NEWTON, QP_RELAX_CHORD = 0, 2
 
 
 class QpDims(C.Structure):
@@ -29,14 +30,16 @@ class QpConfig(C.Structure):
     _fields_ = [("tol", C.c_float), ("max_iter", C.c_int32), ("sigma", C.c_float), ("tau", C.c_float),
                 ("kappa_relax", C.c_float), ("relax_ktol", C.c_float), ("relax_max_iter", C.c_int32),
                 ("formulation", C.c_int32), ("pivot_floor_rel", C.c_float), ("mem_kind", C.c_int32),
-                ("relax_tol", C.c_float)]
+                ("relax_tol", C.c_float), ("relax_mode", C.c_int32), ("chord_max", C.c_int32),
+                ("chord_rho", C.c_float)]
 
 
 class QpInfo(C.Structure):
     _fields_ = [("path", C.c_int32), ("threads", C.c_int32), ("smem_bytes", C.c_int32),
                 ("ctas_per_sm", C.c_int32), ("kkt_dim", C.c_int32), ("launches_solve", C.c_int32),
                 ("launches_backward", C.c_int32), ("workspace_bytes", C.c_int64),
-                ("partition_cap", C.c_int32), ("handed_solve", C.c_int32), ("handed_backward", C.c_int32)]
+                ("partition_cap", C.c_int32), ("handed_solve", C.c_int32), ("handed_backward", C.c_int32),
+                ("relax_mode", C.c_int32), ("chord_steps", C.c_int32)]
 
 
 EXPORTS = ("qp_config_default", "qp_create", "qp_set_stream", "qp_get_info", "qp_max_kkt_dim",

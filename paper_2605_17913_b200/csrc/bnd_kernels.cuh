@@ -47,14 +47,20 @@
 
 namespace qpb {
 
-enum { BM_DONE = 0, BM_INIT = 1, BM_NEWTON = 2, BM_ADJ = 3 };
+enum { BM_DONE = 0, BM_INIT = 1, BM_NEWTON = 2, BM_ADJ = 3, BM_CHORD = 4 };
 
 // Per-problem scalars: the first 16 words of every state block.
 struct BScal {
   float kappa, kt, fl, phi_prev;
   float dmax;  // max |diag| of this iteration's KKT matrix (pivot floor θ = floor_rel·dmax)
   int mode, pa, it, status, ok;
-  int pad[6];
+  // guarded chord relax (reading Q26).  Solve: chord = 1 once this problem
+  // cached a factorisation, cache_now = 1 on the iteration that does.
+  // Backward: chord = 1 while chord steps are taken, nchord of them so far,
+  // psi_prev = the previous ψ = max(φ, |κ/κ_relax − 1|).
+  int chord, cache_now, nchord;
+  float psi_prev;
+  int pad[2];
 };
 static_assert(sizeof(BScal) == 64, "BScal: 16 words");
 
@@ -164,6 +170,10 @@ __global__ void __launch_bounds__(NT) bnd_begin(const BArgs ba) {
   if (tid == 0) {
     h.kappa = 0.f; h.kt = 0.f; h.fl = 0.f; h.phi_prev = INFINITY; h.dmax = 0.f;
     h.pa = 0; h.it = 0; h.status = ST_CONVERGED; h.ok = 0;
+    h.cache_now = 0; h.nchord = 0; h.psi_prev = INFINITY;
+    // solve: nothing cached yet; backward: chord steps iff the solve cached a factor
+    h.chord = (a.bwd && a.kc && a.relax_mode == 2) ? a.chord_ok[bid] : 0;
+    if (!a.bwd && a.chord_ok) a.chord_ok[bid] = 0;
   }
   if (!a.bwd) {
     for (int i = tid; i < p; i += NT) { S.om[i] = 1.f; S.v[i] = -1.f; }
@@ -230,40 +240,86 @@ __global__ void __launch_bounds__(NT) bnd_resid(const BArgs ba) {
   const int k = ba.k;
   const float kappa = manifold_coords<NT>(S, a);
   const float kt = bwd ? a.kappa_relax : a.sigma * kappa;
-  const Norms R = residuals<NT, LARGE>(S, a, P, kappa, kappa - kt);
-  bool fin = false, adj = false;
-  int status = ST_CONVERGED;
-  float fl = h.fl, phi_prev = h.phi_prev;
-  if (R.nonfin > 0.f) {
-    status = ST_FAIL | ((bwd ? STG_RELAX : STG_SCALING) << 8);
-    fin = true;
-  } else if (!bwd) {
-    if (converged_solve(R, a.tol)) {
-      fl += iter_flops(n, m, p, 0, true, false, false);
-      fin = true;
-    } else if (k == a.max_iter) {
-      fl += iter_flops(n, m, p, 0, true, false, false);
-      status = ST_MAX_ITER;
-      fin = true;
+  // guarded chord relax (reading Q26): a problem in chord mode computes its
+  // residuals with the cached Jacobian (the right-hand side of the chord step)
+  const bool was_chord = bwd && h.chord;
+  const float* cj = was_chord ? a.chd + (long long)bid * a.chd_stride : nullptr;
+  if (was_chord) {
+    const int p4 = (p + 3) & ~3;
+    for (int i = tid; i < p; i += NT) {
+      S.dp[i] = cj[4 + i]; S.dm[i] = cj[4 + p4 + i]; S.c[i] = cj[4 + 2 * p4 + i];
+      S.widx[i] = __float_as_int(cj[4 + 3 * p4 + i]);
     }
-  } else {
-    const bool kok = p == 0 || fabsf(kappa / a.kappa_relax - 1.f) <= a.relax_ktol;
-    adj = kok && relax_done(R, a.tol, a.relax_tol, phi_prev);
-    phi_prev = kok ? rel_phi(R) : INFINITY;
-    if (!adj && k == a.relax_max_iter) {
-      status = ST_MAX_ITER | (STG_RELAX << 8);
-      fin = true;
-    }
+    __syncthreads();
   }
+  // One call site for both passes (a second pass recomputes the current
+  // Jacobian when a chord phase ends): a single inlined copy of residuals(),
+  // so a problem that leaves chord mode computes exactly what exact Newton does.
+  Norms R;
+  bool fin = false, adj = false, chord = was_chord, cache = false, keep = was_chord;
+  int status = ST_CONVERGED, nchord = h.nchord;
+  float fl = h.fl, phi_prev = h.phi_prev, psi_prev = h.psi_prev;
+#pragma unroll 1
+  for (int pass = 0;; ++pass) {
+    R = residuals<NT, LARGE>(S, a, P, kappa, kappa - kt, keep, keep ? __float_as_int(cj[0]) : 0);
+    if (pass == 1) break;
+    if (R.nonfin > 0.f) {
+      status = ST_FAIL | ((bwd ? STG_RELAX : STG_SCALING) << 8);
+      fin = true;
+    } else if (!bwd) {
+      if (converged_solve(R, a.tol)) {
+        fl += iter_flops(n, m, p, 0, true, false, false);
+        fin = true;
+      } else if (k == a.max_iter) {
+        fl += iter_flops(n, m, p, 0, true, false, false);
+        status = ST_MAX_ITER;
+        fin = true;
+      } else if (a.kc && a.relax_mode == 2 && !h.chord && kappa < sqrtf(10.f) * a.kappa_relax) {
+        cache = true;  // this iteration's factorisation is the one Alg. 2 will reuse
+      }
+    } else {
+      const bool kok = p == 0 || fabsf(kappa / a.kappa_relax - 1.f) <= a.relax_ktol;
+      if (chord) {  // the guard: chord steps while each shrinks ψ by chord_rho, at most chord_max
+        const float psi = fmaxf(rel_phi(R), p == 0 ? 0.f : fabsf(kappa / a.kappa_relax - 1.f));
+        if (nchord >= a.chord_max || (nchord > 0 && !(psi <= a.chord_rho * psi_prev))) {
+          chord = false;
+          phi_prev = INFINITY;  // the stall test (Q5b) measures Newton steps only
+        }
+        psi_prev = psi;
+      }
+      // a chord stops only at φ ≤ relax_tol (a slow chord is not the f32 floor)
+      adj = kok && (chord ? rel_phi(R) <= a.relax_tol : relax_done(R, a.tol, a.relax_tol, phi_prev));
+      phi_prev = kok ? rel_phi(R) : INFINITY;
+      if (!adj && k == a.relax_max_iter) {
+        status = ST_MAX_ITER | (STG_RELAX << 8);
+        fin = true;
+      }
+    }
+    // leaving chord mode: this iteration factors, with the Jacobian of the current point
+    if (!(was_chord && !fin && (adj || !chord))) break;
+    keep = false;
+    __syncthreads();
+  }
+  if (adj || fin) chord = false;
   __syncthreads();
   if (tid == 0) {
     h.it = k; h.status = status; h.fl = fl; h.phi_prev = phi_prev;
     h.kappa = kappa; h.kt = kt; h.pa = R.pa; h.dmax = 0.f; h.ok = 0;
+    h.psi_prev = psi_prev; h.cache_now = cache ? 1 : 0;
+    if (bwd) h.chord = chord ? 1 : 0;
+    else if (cache) h.chord = 1;
   }
   if (fin) {
     __syncthreads();
     if (!bwd) bnd_finish_solve<NT>(a, S, h, bid);
     else bnd_finish_backward<NT>(a, S, h, bid);
+  } else if (chord) {  // a chord step: no assembly, no factorisation (reading Q26)
+    if (tid == 0) {
+      h.mode = BM_CHORD;
+      h.nchord = nchord + 1;
+      h.fl = fl + iter_flops(n, m, p, R.pa, true, false, true);
+      atomicAdd(ba.ctl + 2, 1);
+    }
   } else {
     if (adj)  // Algorithm 3: the relaxed system with right-hand side (−∇ₓℓ, 0, 0)
       for (int j = tid; j < a.N4max; j += NT) S.rhs[j] = j < n ? -__ldg(a.dl + (long long)bid * n + j) : 0.f;
@@ -273,6 +329,7 @@ __global__ void __launch_bounds__(NT) bnd_resid(const BArgs ba) {
       h.fl = fl + iter_flops(n, m, p, R.pa, true, true, true);
       slot = atomicAdd(ba.ctl, 1);
       atomicMax(ba.ctl + 1, r4(n4 + R.pa + m));
+      if (cache) atomicAdd(ba.ctl + 3, 1);
       if (ba.kr) ba.slotmap[slot] = bid;
     }
     if (ba.kr) {  // this problem's Ω row for the batched assembly GEMM
@@ -332,7 +389,7 @@ __global__ void __launch_bounds__(NT) bnd_scatter(const BArgs ba) {
   const int bid = blockIdx.x;
   float* gst = st_of(ba, bid);
   BScal& h = scal_of(gst);
-  if (h.mode == BM_DONE) return;
+  if (h.mode == BM_DONE || h.mode == BM_CHORD) return;
   const int pa = h.pa;
   const KLayout L = bnd_layout(a, pa);
   float dmax = 0.f;
@@ -359,7 +416,7 @@ __global__ void __launch_bounds__(NT) bnd_assemble(const BArgs ba) {
   const int n = a.n, n4 = a.n4, p = a.p;
   float* gst = st_of(ba, bid);
   BScal& h = scal_of(gst);
-  if (h.mode == BM_DONE) return;
+  if (h.mode == BM_DONE || h.mode == BM_CHORD) return;
   const Smem S = carve_state(gst, a);  // global state (read only here)
   const int pa = h.pa;
   const KLayout L = bnd_layout(a, pa);
@@ -420,7 +477,7 @@ __global__ void __launch_bounds__(NT, 3) bnd_tc_update(const BArgs ba) {
   const Args& a = ba.a;
   const int bid = blockIdx.y, tid = threadIdx.x;
   const BScal& h = scal_of(st_of(ba, bid));
-  if (h.mode == BM_DONE) return;
+  if (h.mode == BM_DONE || h.mode == BM_CHORD) return;
   const KLayout L = bnd_layout(a, h.pa);
   const int c0 = ba.c0, i0 = c0 + TM * (int)blockIdx.x, N4 = L.N4, npos = L.npos;
   if (c0 >= N4 || i0 >= N4) return;
@@ -546,7 +603,7 @@ __global__ void __launch_bounds__(NT) bnd_pdiag(const BArgs ba) {
   const int bid = blockIdx.x, tid = threadIdx.x;
   float* gst = st_of(ba, bid);
   const BScal& h = scal_of(gst);
-  if (h.mode == BM_DONE) return;
+  if (h.mode == BM_DONE || h.mode == BM_CHORD) return;
   const KLayout L = bnd_layout(a, h.pa);
   const int c0 = ba.c0, N4 = L.N4;
   if (c0 >= N4) return;
@@ -608,7 +665,7 @@ __global__ void __launch_bounds__(NT, 4) bnd_prows(const BArgs ba) {
   const int bid = blockIdx.y, tid = threadIdx.x;
   float* gst = st_of(ba, bid);
   const BScal& h = scal_of(gst);
-  if (h.mode == BM_DONE) return;
+  if (h.mode == BM_DONE || h.mode == BM_CHORD) return;
   const KLayout L = bnd_layout(a, h.pa);
   const int c0 = ba.c0, N4 = L.N4, c1 = c0 + W;
   const int r0 = c1 + NT * (int)blockIdx.x;
@@ -669,6 +726,40 @@ __global__ void __launch_bounds__(NT, 4) bnd_prows(const BArgs ba) {
 }
 
 // ---------------------------------------------------------------------------
+// bnd_cache: grid (chunks, B), after the panel loop of a solve iteration in
+// which some problems reached κ < √10·κ_relax for the first time (reading
+// Q26): their factor (packed L), pivot reciprocals, partition and Jacobian
+// vectors go to the chord cache that the backward's chord steps solve with.
+// ---------------------------------------------------------------------------
+template <int NT>
+__global__ void __launch_bounds__(NT) bnd_cache(const BArgs ba) {
+  const Args& a = ba.a;
+  const int bid = blockIdx.y, tid = threadIdx.x;
+  float* gst = st_of(ba, bid);
+  const BScal& h = scal_of(gst);
+  if (h.mode != BM_NEWTON || !h.cache_now) return;
+  const KLayout L = bnd_layout(a, h.pa);
+  const float4* src = reinterpret_cast<const float4*>(ba.kw + (long long)bid * ba.kstride);
+  float4* dst = reinterpret_cast<float4*>(a.kc + (long long)bid * a.kc_stride);
+  const int n4v = (L.size() + 3) >> 2;
+  for (int i = blockIdx.x * NT + tid; i < n4v; i += gridDim.x * NT) dst[i] = src[i];
+  if (blockIdx.x == 0) {
+    const Smem S = carve_state(gst, a);
+    float* cj = a.chd + (long long)bid * a.chd_stride;
+    const int p = a.p, p4 = (p + 3) & ~3;
+    for (int i = tid; i < p; i += NT) {
+      cj[4 + i] = S.dp[i]; cj[4 + p4 + i] = S.dm[i]; cj[4 + 2 * p4 + i] = S.c[i];
+      cj[4 + 3 * p4 + i] = __int_as_float(S.widx[i]);
+    }
+    for (int i = tid; i < L.N4; i += NT) cj[4 + 4 * p4 + i] = S.rinv[i];
+    if (tid == 0) {
+      cj[0] = __int_as_float(h.pa); cj[1] = h.kappa;
+      a.chord_ok[bid] = 1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // bnd_solve: grid B — forward and backward substitution with the factor
 // (solve_qd), right-hand side staged in shared memory.
 // ---------------------------------------------------------------------------
@@ -682,9 +773,11 @@ __global__ void __launch_bounds__(NT) bnd_solve(const BArgs ba) {
   if (h.mode == BM_DONE) return;
   const KLayout L = bnd_layout(a, h.pa);
   const Smem G = carve_state(gst, a);
-  const float* K = ba.kw + (long long)bid * ba.kstride;
+  const bool chord = h.mode == BM_CHORD;  // the cached factorisation of the solve (reading Q26)
+  const float* K = chord ? a.kc + (long long)bid * a.kc_stride : ba.kw + (long long)bid * ba.kstride;
+  const float* rinv = chord ? a.chd + (long long)bid * a.chd_stride + 4 + 4 * ((a.p + 3) & ~3) : G.rinv;
   copy_block<NT>(sm, G.rhs, L.N4);
-  solve_qd<NT, false, true>(K, L, G.rinv, sm);
+  solve_qd<NT, false, true>(K, L, rinv, sm);
   __syncthreads();
   copy_block<NT>(G.rhs, sm, L.N4);
 }
@@ -737,7 +830,7 @@ __global__ void __launch_bounds__(NT) bnd_update(const BArgs ba) {
     } else if (tid == 0) {
       h.mode = BM_NEWTON;
     }
-  } else if (mode == BM_NEWTON) {
+  } else if (mode == BM_NEWTON || mode == BM_CHORD) {
     float kappa = h.kappa;
     int stage = 0;
     const bool okstep = newton_update<NT>(S, a, P, pa, kappa, kappa - h.kt, &stage);

@@ -65,7 +65,25 @@ struct Args {
   int* fb_count;             // its length
   const int* plist;          // list-driven launch (the fallback): problems plist[i], i < *pcount
   const int* pcount;
+  // Guarded chord relax (reading Q26): the
+  // solve caches the factorisation of its first iterate with κ < √10·κ_relax
+  // (the factor, its pivot reciprocals and the Jacobian vectors it was built
+  // from); the backward takes chord steps on it while they contract
+  int relax_mode;            // 0: exact Newton (Q6); 2: guarded chord
+  int chord_max;             // most chord steps per problem
+  float chord_rho;           // contraction a chord step must reach
+  float* kc;                 // [B][kc_stride] cached factors (nullptr = no chord)
+  long long kc_stride;
+  float* chd;                // [B][chd_stride] cached Jacobian: {pa, κ, ·, ·}, d₊[p4], d₋[p4], c[p4], widx[p4], rinv[N4max]
+  long long chd_stride;
+  int* chord_ok;             // [B] 1 = this problem's solve cached a factor
 };
+
+// chord cache block of one problem (floats): 4 scalars, then d₊, d₋, c, widx, rinv
+__host__ __device__ inline long long chd_floats(int p, int N4max) {
+  const int p4 = (p + 3) & ~3;
+  return 4 + 4LL * p4 + ((N4max + 3) & ~3);
+}
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -532,22 +550,31 @@ struct Norms {
   bool spill;  // reading Q12c guard: the capped elimination would exceed fb_bound
 };
 
+// keep_jac (a chord step of the guarded chord relax, reading Q26): the
+// Jacobian vectors d₊, d₋, c and the partition (widx, pa_keep) already in S
+// are those of the cached factorisation and are kept; only the residuals are
+// of the current point.  The norms do not depend on the Jacobian.
 template <int NT, bool LARGE = false>
-__device__ Norms residuals(const Smem& S, const Args& a, const Prob& P, float kappa, float r_kappa) {
+__device__ Norms residuals(const Smem& S, const Args& a, const Prob& P, float kappa, float r_kappa,
+                           bool keep_jac = false, int pa_keep = 0) {
   const int tid = threadIdx.x;
   const int n = a.n, n4 = a.n4, p = a.p, m = a.m;
   float mz = 0.f, ms = 0.f, mh = 0.f, mrzs = 0.f, nonfin = 0.f;
   for (int k = tid; k < p; k += NT) {
     const float zk = S.z[k], sk = S.s[k], vk = S.v[k];
     const float rz = zk - ret_b(vk, kappa), rs = sk - ret_b(-vk, kappa);
-    const float dp = ret_db(vk, kappa), dm = ret_db(-vk, kappa);
-    S.rz[k] = rz; S.rs[k] = rs; S.c[k] = ret_dk(vk, kappa);
-    S.dp[k] = dp; S.dm[k] = dm;
+    S.rz[k] = rz; S.rs[k] = rs;
+    if (!keep_jac) {
+      S.c[k] = ret_dk(vk, kappa);
+      S.dp[k] = ret_db(vk, kappa); S.dm[k] = ret_db(-vk, kappa);
+    }
     mz = fmaxf(mz, fabsf(zk)); ms = fmaxf(ms, fabsf(sk)); mh = fmaxf(mh, fabsf(__ldg(P.h + k)));
     mrzs = fmaxf(mrzs, fmaxf(fabsf(rz), fabsf(rs)));
   }
-  bool capped;
-  const int pa = compact_active<NT>(S, p, false, a.pcap, &capped);
+  bool capped = false;
+  int pa = pa_keep;
+  if (!keep_jac) pa = compact_active<NT>(S, p, false, a.pcap, &capped);
+  else __syncthreads();
   // Reading Q12c guard: when the cap bound, no eliminated constraint with
   // v_k > 0 may carry a weight ω_k = d₊/d₋ above fb_bound (every factored
   // entry stays bounded); otherwise the problem goes to the

@@ -222,6 +222,14 @@ struct qp_ctx {
   unsigned long long* tl = nullptr;  // QPB200_TIMELINE diagnostics: [2][B][3]
   int epoch = 0;
   bool bwd_dirty = true;  // backward counters used since the last solve zeroed them
+  // guarded chord relax (reading Q26): per problem the solve's cached factor,
+  // its Jacobian block and a flag (allocated for the whole batch when enabled)
+  float* kc = nullptr;
+  long long kc_stride = 0;
+  float* chd = nullptr;
+  long long chd_stride = 0;
+  int* chord_ok = nullptr;
+  int chord_steps = 0;     // chord steps of the last backward (summed over the batch)
   float* flops_solve = nullptr;        // per-problem algorithmic flops of the last calls
   float* flops_bwd = nullptr;
   // host-memory mode, path 1: the batch runs in kPipe chunks on their own
@@ -231,7 +239,7 @@ struct qp_ctx {
   float* bst = nullptr;
   long long bst_stride = 0;
   int bchunk = 0;
-  int* bctl = nullptr;       // device: [0] problems iterating, [1] largest N4
+  int* bctl = nullptr;       // device: [0] problems factoring, [1] largest N4 among them, [2] chord steps, [3] caching
   int* hctl = nullptr;       // pinned host copy ([4 per lane])
   int nlanes = 1, lane_cap = 0;         // concurrent sub-batches of a chunk, problems per lane
   int sms = 148;                        // multiprocessors (persistent kr_gemm grid)
@@ -297,7 +305,7 @@ size_t field_elems(int64_t stride, int32_t B, size_t per) { return stride == 0 ?
 
 void free_all(qp_ctx* c) {
   if (c->hctl) cudaFreeHost(c->hctl);
-  void* ptrs[] = {c->kglobf, c->fb_flag, c->fb_list, c->fb_ctl, c->ug, c->dtg, c->whi, c->wlo, c->gghi, c->gglo, c->slotmap, c->bst, c->bctl, c->tl, c->sched, c->done, c->kglob, c->flops_solve, c->flops_bwd, c->prof, c->own_status, c->wx, c->wy, c->wz, c->wdx, c->wdy, c->wdz, c->dQ_, c->dq_, c->dA_, c->db_,
+  void* ptrs[] = {c->kc, c->chd, c->chord_ok, c->kglobf, c->fb_flag, c->fb_list, c->fb_ctl, c->ug, c->dtg, c->whi, c->wlo, c->gghi, c->gglo, c->slotmap, c->bst, c->bctl, c->tl, c->sched, c->done, c->kglob, c->flops_solve, c->flops_bwd, c->prof, c->own_status, c->wx, c->wy, c->wz, c->wdx, c->wdy, c->wdz, c->dQ_, c->dq_, c->dA_, c->db_,
                   c->dG_, c->dh_, c->dx_, c->ds_, c->dz_, c->dy_, c->ddl_, c->dit_, c->dst_, c->gQ_, c->gq_,
                   c->gA_, c->gb_, c->gG_, c->gh_};
   if (c->guard) {  // guard mode: the allocations start kGuard bytes before each pointer
@@ -328,6 +336,9 @@ qpb::Args base_args(const qp_ctx* c) {
   a.tol = c->c.tol; a.sigma = c->c.sigma; a.tau = c->c.tau; a.kappa_relax = c->c.kappa_relax;
   a.relax_ktol = c->c.relax_ktol; a.floor_rel = c->c.pivot_floor_rel; a.relax_tol = c->c.relax_tol;
   a.max_iter = c->c.max_iter; a.relax_max_iter = c->c.relax_max_iter;
+  a.relax_mode = c->kc ? c->c.relax_mode : 0;
+  a.chord_max = c->c.chord_max; a.chord_rho = c->c.chord_rho;
+  a.kc = c->kc; a.kc_stride = c->kc_stride; a.chd = c->chd; a.chd_stride = c->chd_stride; a.chord_ok = c->chord_ok;
   return a;
 }
 
@@ -356,6 +367,7 @@ qpb::Args chunk_args(qpb::Args a, int b0, int nb) {
   if (a.fb_flag) a.fb_flag += o;
   if (a.fb_list) a.fb_list += o;
   if (a.prof) a.prof += 8 * o;
+  if (a.kc) { a.kc += o * a.kc_stride; a.chd += o * a.chd_stride; a.chord_ok += o; }
   return a;
 }
 
@@ -446,6 +458,7 @@ qp_err run_batched(qp_ctx* c, const qpb::Args& a0, bool bwd) {
   const int krN = (qpb::kr::npairs(n4) + qpb::kr::BN - 1) / qpb::kr::BN;
   const size_t kpad = (size_t)qpb::kr::nkc(c->d.p) * qpb::kr::BK;
   int launches = 0;
+  if (bwd) c->chord_steps = 0;
   // lanes: the chunk is split into c->nlanes sub-batches whose iteration
   // loops run interleaved on their own streams, so that one sub-batch's
   // phase kernels fill the tail waves of the other's
@@ -504,7 +517,7 @@ qp_err run_batched(qp_ctx* c, const qpb::Args& a0, bool bwd) {
         ga.Q = ba.a.Q; ga.sQ = ba.a.sQ;
         ga.n = c->d.n; ga.n4 = n4; ga.m = m; ga.p = c->d.p;
       }
-      if (cudaMemsetAsync(ba.ctl, 0, 2 * sizeof(int), L.st) != cudaSuccess) return QP_ERR_CUDA;
+      if (cudaMemsetAsync(ba.ctl, 0, 4 * sizeof(int), L.st) != cudaSuccess) return QP_ERR_CUDA;
       qpb::bnd_begin<kBS><<<L.nb, kBS, sst, L.st>>>(ba);
       ++launches;
       L.N4cur = bwd ? 0 : qpb::r4(n4 + m);  // the initial system (solve)
@@ -516,32 +529,41 @@ qp_err run_batched(qp_ctx* c, const qpb::Args& a0, bool bwd) {
       for (int l = 0; l < NL; ++l) {
         Lane& L = ln[l];
         if (!L.live || L.k < 0) continue;
-        if (cudaMemsetAsync(L.ba.ctl, 0, 2 * sizeof(int), L.st) != cudaSuccess) return QP_ERR_CUDA;
+        if (cudaMemsetAsync(L.ba.ctl, 0, 4 * sizeof(int), L.st) != cudaSuccess) return QP_ERR_CUDA;
         L.ba.k = L.k;
         if (c->d.n >= 2 * kBS)  // column-quad GEMVs with 8 rows in flight (config 5)
           qpb::bnd_resid<kBS, true><<<L.nb, kBS, sst, L.st>>>(L.ba);
         else
           qpb::bnd_resid<kBS><<<L.nb, kBS, sst, L.st>>>(L.ba);
         ++launches;
-        if (cudaMemcpyAsync(c->hctl + 4 * l, L.ba.ctl, 2 * sizeof(int), cudaMemcpyDeviceToHost, L.st) != cudaSuccess ||
+        if (cudaMemcpyAsync(c->hctl + 4 * l, L.ba.ctl, 4 * sizeof(int), cudaMemcpyDeviceToHost, L.st) != cudaSuccess ||
             cudaEventRecord(c->bev[1 + l], L.st) != cudaSuccess)
           return QP_ERR_CUDA;
       }
       for (int l = 0; l < NL; ++l) {
         Lane& L = ln[l];
         if (!L.live) continue;
+        // [0] problems that factor this iteration, [2] chord steps (reading
+        // Q26: solve + update only), [3] problems caching their factor
+        bool factor = true, cache = false;
         if (L.k >= 0) {
           if (cudaEventSynchronize(c->bev[1 + l]) != cudaSuccess) return QP_ERR_CUDA;
-          if (c->hctl[4 * l] == 0 || L.k > kmax + 1) { L.live = false; --nlive; continue; }
+          if (c->hctl[4 * l] + c->hctl[4 * l + 2] == 0 || L.k > kmax + 1) { L.live = false; --nlive; continue; }
           L.N4cur = c->hctl[4 * l + 1];
+          factor = c->hctl[4 * l] > 0;
+          cache = c->hctl[4 * l + 3] > 0;
+          if (bwd) c->chord_steps += c->hctl[4 * l + 2];
         }
         qpb::BArgs& ba = L.ba;
         cudaStream_t st = L.st;
         const int nb = L.nb;
+        if (!factor) L.N4cur = 0;
+        if (factor) {
         if (c->kr) qpb::bnd_scatter<kBS><<<nb, kBS, 0, st>>>(ba);
         else qpb::bnd_assemble<kBT><<<dim3(ba.ntiles + 1, nb), kBT, stc, st>>>(ba);
         ++launches;
-        if (c->kr) {
+        }
+        if (factor && c->kr) {
           qpb::kr::kr_gemm<<<std::min(c->sms / c->kr_div, ((nb + qpb::kr::BM - 1) / qpb::kr::BM) * krN), qpb::kr::WS_THREADS,
                              qpb::kr::WS_SMEM_BYTES, st>>>(L.ga);
           ++launches;
@@ -556,6 +578,10 @@ qp_err run_batched(qp_ctx* c, const qpb::Args& a0, bool bwd) {
           if (c0 + kBW < L.N4cur)
             qpb::bnd_prows<kBT><<<dim3((L.N4cur - c0 - kBW + kBT - 1) / kBT, nb), kBT, 0, st>>>(ba);
           launches += 2;
+        }
+        if (cache) {
+          qpb::bnd_cache<kBT><<<dim3(8, nb), kBT, 0, st>>>(ba);
+          ++launches;
         }
         qpb::bnd_solve<kBT><<<nb, kBT, ssv, st>>>(ba);
         qpb::bnd_update<kBS><<<nb, kBS, sst, st>>>(ba);
@@ -592,6 +618,9 @@ qp_err qp_config_default(qp_config* cfg) {
   cfg->pivot_floor_rel = 3.4526698e-4f;  // sqrt(FLT_EPSILON)
   cfg->mem_kind = QP_MEM_DEVICE;
   cfg->relax_tol = 1e-6f;
+  cfg->relax_mode = QP_RELAX_NEWTON;
+  cfg->chord_max = 8;
+  cfg->chord_rho = 0.5f;
   return QP_OK;
 }
 
@@ -625,7 +654,9 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
   if (!(c.tol > 0.f) || c.max_iter < 0 || !(c.sigma > 0.f && c.sigma < 1.f) || !(c.tau > 0.f && c.tau <= 1.f) ||
       !(c.kappa_relax > 0.f) || !(c.relax_ktol > 0.f) || !(c.relax_tol > 0.f) || c.relax_max_iter < 0 || !(c.pivot_floor_rel >= 0.f) ||
       (c.formulation != QP_IMPLICIT && c.formulation != QP_EXPLICIT) ||
-      (c.mem_kind != QP_MEM_DEVICE && c.mem_kind != QP_MEM_HOST && c.mem_kind != QP_MEM_HOST_ASYNC))
+      (c.mem_kind != QP_MEM_DEVICE && c.mem_kind != QP_MEM_HOST && c.mem_kind != QP_MEM_HOST_ASYNC) ||
+      (c.relax_mode != QP_RELAX_NEWTON && c.relax_mode != QP_RELAX_CHORD) || c.chord_max < 0 ||
+      !(c.chord_rho > 0.f && c.chord_rho <= 1.f))
     return QP_ERR_INVALID_ARG;
   const int64_t strides[6] = {d->bstride_Q, d->bstride_q, d->bstride_A, d->bstride_b, d->bstride_G, d->bstride_h};
   const int64_t need[6] = {(int64_t)d->n * d->n, d->n, (int64_t)d->m_eq * d->n, d->m_eq, (int64_t)d->p * d->n,
@@ -732,6 +763,23 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
     if (cudaMallocHost(&ctx->hctl, 16 * sizeof(int)) != cudaSuccess || bnd_setup(ctx) != QP_OK) {
       free_all(ctx); delete ctx; return QP_ERR_CUDA;
     }
+    // guarded chord relax (reading Q26): a cached factor per problem of the
+    // whole batch, when it fits in a quarter of the free device memory
+    // (otherwise the relax stays exact Newton: qp_info.relax_mode says which)
+    if (c.relax_mode == QP_RELAX_CHORD && c.formulation == QP_IMPLICIT && d->p > 0) {
+      size_t fr2 = 0, tot2 = 0;
+      cudaMemGetInfo(&fr2, &tot2);
+      const long long cs = qpb::chd_floats(d->p, L.N4max);
+      const size_t need = (size_t)d->batch * 4 * ((size_t)L.kglob + (size_t)cs + 1);
+      if (need <= fr2 / 4) {
+        ctx->kc_stride = L.kglob; ctx->chd_stride = cs;
+        if ((e = dalloc(ctx, &ctx->kc, (size_t)d->batch * (size_t)L.kglob)) ||
+            (e = dalloc(ctx, &ctx->chd, (size_t)d->batch * (size_t)cs)) || (e = dalloc(ctx, &ctx->chord_ok, (size_t)d->batch))) {
+          free_all(ctx); delete ctx; return e;
+        }
+        if (cudaMemset(ctx->chord_ok, 0, sizeof(int) * d->batch) != cudaSuccess) { free_all(ctx); delete ctx; return QP_ERR_CUDA; }
+      }
+    }
     // shared G: the assembly runs as one GEMM over the batch (kr_gemm.cuh)
     ctx->kr = d->bstride_G == 0 && d->p > 0 && !getenv("QPB200_NO_KR");
     if (ctx->kr) {
@@ -825,6 +873,8 @@ qp_err qp_get_info(const qp_ctx* c, qp_info* info) {
     info->ctas_per_sm = 0;                            // varies by phase kernel
   }
   info->workspace_bytes = c->workspace;
+  info->relax_mode = c->kc ? c->c.relax_mode : QP_RELAX_NEWTON;
+  info->chord_steps = c->chord_steps;
   info->handed_solve = info->handed_backward = 0;
   if (c->fb) {  // reading Q12c guard: hand-over counts of the last calls (all chunks)
     int h[4 * qp_ctx::kPipe];

@@ -88,8 +88,10 @@ enum { QP_MEM_DEVICE = 0, QP_MEM_HOST = 1, QP_MEM_HOST_ASYNC = 2 };
  * chord_rho (at most chord_max of them); from the first that does not it
  * takes exact Newton steps.  A chord phase ends only at φ ≤ relax_tol.
  * Either way the final factorisation is at the relaxed point, so Alg. 3's
- * gradients are the exact IFT gradients there.  Path 4 only (elsewhere the
- * relax is exact Newton; qp_info.relax_mode reports the mode in effect). */
+ * gradients are the exact IFT gradients there.  Paths 1 and 4 (paths 2/3
+ * and the standard arm relax by exact Newton; so does a batch whose cache —
+ * one factor per problem — would not fit in a quarter of the free device
+ * memory); qp_info.relax_mode reports the mode in effect. */
 enum { QP_RELAX_NEWTON = 0, QP_RELAX_CHORD = 2 };
 
 typedef struct {
@@ -117,7 +119,7 @@ typedef struct {
   int32_t mem_kind;       /* QP_MEM_DEVICE (default) | QP_MEM_HOST | QP_MEM_HOST_ASYNC     */
   float relax_tol;        /* Alg. 2 residual tolerance (Q5b); default 1e-6; the relax loop */
                           /* also stops at the f32 floor (φ ≤ tol and no 10% progress)     */
-  int32_t relax_mode;     /* QP_RELAX_NEWTON (default) | QP_RELAX_CHORD (reading Q26)      */
+  int32_t relax_mode;     /* QP_RELAX_CHORD (default) | QP_RELAX_NEWTON (reading Q26, Q6) */
   int32_t chord_max;      /* QP_RELAX_CHORD: most chord steps per problem; default 8       */
   float chord_rho;        /* QP_RELAX_CHORD: contraction a chord step must reach, (0, 1];  */
                           /* default 0.5                                                    */

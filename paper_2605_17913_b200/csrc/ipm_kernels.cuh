@@ -77,6 +77,7 @@ struct Args {
   float* chd;                // [B][chd_stride] cached Jacobian: {pa, κ, ·, ·}, d₊[p4], d₋[p4], c[p4], widx[p4], rinv[N4max]
   long long chd_stride;
   int* chord_ok;             // [B] 1 = this problem's solve cached a factor
+  int* chord_cnt;            // backward: chord steps taken, summed over the batch (path 1)
 };
 
 // chord cache block of one problem (floats): 4 scalars, then d₊, d₋, c, widx, rinv
@@ -927,6 +928,14 @@ __device__ __forceinline__ void ipm_problem(const Args& a, const Smem& S, const 
   unsigned long long tph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long t0 = clock64();
   bool handed = false;  // reading Q12c guard: this problem goes to the fallback launch
+  // guarded chord relax (reading Q26; path 1 only).  Solve: cached = this
+  // problem stored the factorisation of its first iterate with κ < √10·κ_relax
+  // (chord cache of Args).  Backward: chord = chord steps on it are being taken.
+  const bool chord_on = !BIG && a.kc && a.relax_mode == 2;
+  bool cached = false, chord = false;
+  int nchord = 0;
+  float psi_prev = INFINITY;
+  if (chord_on && !bwd && tid == 0) a.chord_ok[bid] = 0;
   if (a.fb_bound > 0.f) {
     if (!bwd) {
       if (tid == 0) a.fb_flag[bid] = 0;
@@ -947,12 +956,15 @@ __device__ __forceinline__ void ipm_problem(const Args& a, const Smem& S, const 
     __syncthreads();
     if (lost) status = ST_FAIL | (STG_BACKWARD << 8);
     else if ((__ldcg(a.status + bid) & 0xff) != ST_CONVERGED) status = ST_FAIL | (STG_RELAX << 8);
+    chord = chord_on && __ldcg(a.chord_ok + bid) != 0;
   }
   for (int k = bwd ? 0 : -1; status == ST_CONVERGED; ++k) {
     const bool init = k < 0;
     float kappa = 0.f, kt = 0.f;
     int pa = 0;
     bool adj = false;  // backward: relaxed — this iteration's solve is Alg. 3's
+    bool chord_step = false;  // backward: a chord step on the solve's cached factorisation (Q26)
+    bool cache = false;       // solve: this iteration's factorisation goes to the chord cache
     const float *cw = S.om, *ev = S.om;
     if (init) {
       // [[Q, Gᵀ, Aᵀ], [G, −I, 0], [A, 0, 0]] (x, ẑ, y) = (−q, h, b); the congruence
@@ -974,7 +986,38 @@ __device__ __forceinline__ void ipm_problem(const Args& a, const Smem& S, const 
     } else {
       kappa = manifold_coords<NT>(S, a);
       kt = bwd ? a.kappa_relax : a.sigma * kappa;  // κ_target: κ_relax (Alg. 2) or σκ (Alg. 1)
-      const Norms R = residuals<NT>(S, a, P, kappa, kappa - kt);
+      const float* cj = a.chd + (long long)bid * a.chd_stride;
+      const bool was_chord = chord;
+      if (was_chord) {  // the cached Jacobian: the right-hand side of a chord step
+        const int p4 = (p + 3) & ~3;
+        for (int i = tid; i < p; i += NT) {
+          S.dp[i] = __ldcg(cj + 4 + i); S.dm[i] = __ldcg(cj + 4 + p4 + i); S.c[i] = __ldcg(cj + 4 + 2 * p4 + i);
+          S.widx[i] = __float_as_int(__ldcg(cj + 4 + 3 * p4 + i));
+        }
+        __syncthreads();
+      }
+      // one call site; a second pass (current Jacobian) when a chord phase ends
+      bool keep = was_chord, fin = false;
+      Norms R;
+#pragma unroll 1
+      for (int pass = 0;; ++pass) {
+        R = residuals<NT>(S, a, P, kappa, kappa - kt, keep, keep ? __float_as_int(__ldcg(cj)) : 0);
+        if (pass == 1 || !was_chord || R.spill || R.nonfin > 0.f) break;
+        const bool kok = p == 0 || fabsf(kappa / a.kappa_relax - 1.f) <= a.relax_ktol;
+        const float psi = fmaxf(rel_phi(R), p == 0 ? 0.f : fabsf(kappa / a.kappa_relax - 1.f));
+        if (nchord >= a.chord_max || (nchord > 0 && !(psi <= a.chord_rho * psi_prev))) {
+          chord = false;
+          phi_prev = INFINITY;  // the stall test (Q5b) measures Newton steps only
+        }
+        psi_prev = psi;
+        // a chord stops only at φ ≤ relax_tol (a slow chord is not the f32 floor)
+        adj = kok && (chord ? rel_phi(R) <= a.relax_tol : relax_done(R, a.tol, a.relax_tol, phi_prev));
+        fin = !adj && k == a.relax_max_iter;
+        if (fin || !(adj || !chord)) break;
+        chord = false;
+        keep = false;
+        __syncthreads();
+      }
       long long t1 = clock64(); tph[0] += t1 - t0; t0 = t1;
       it = k;
       if (R.spill) {
@@ -992,11 +1035,14 @@ __device__ __forceinline__ void ipm_problem(const Args& a, const Smem& S, const 
         if (converged_solve(R, a.tol)) break;
         if (k == a.max_iter) { status = ST_MAX_ITER; break; }
         fl -= iter_flops(n, m, p, 0, true, false, false);  // counted again below with the step
+        if (chord_on && !cached && kappa < sqrtf(10.f) * a.kappa_relax) cache = cached = true;
       } else {
         const bool kok = p == 0 || fabsf(kappa / a.kappa_relax - 1.f) <= a.relax_ktol;
-        adj = kok && relax_done(R, a.tol, a.relax_tol, phi_prev);
+        if (!was_chord) adj = kok && relax_done(R, a.tol, a.relax_tol, phi_prev);
         phi_prev = kok ? rel_phi(R) : INFINITY;
         if (!adj && k == a.relax_max_iter) { status = ST_MAX_ITER | (STG_RELAX << 8); break; }
+        chord_step = chord;
+        if (chord_step) ++nchord;
       }
       pa = R.pa;
       cw = S.dp; ev = S.dm;
@@ -1004,11 +1050,41 @@ __device__ __forceinline__ void ipm_problem(const Args& a, const Smem& S, const 
     const KLayout L = KLayout::make(n4 + pa + m, n4);
     float* const K = kkt_ptr<BIG>(S, a, L);
     tph[5] += pa; tph[6] += L.N; tph[7] = tph[7] > (unsigned long long)L.N ? tph[7] : (unsigned long long)L.N;
-    fl += iter_flops(n, m, p, pa, !init, true, true);
-    const float dmax = assemble<NT, BIG>(K, S, a, P, L, pa, S.om, cw, ev);
-    long long t1 = clock64(); tph[1] += t1 - t0; t0 = t1;
-    factor_any<NT, BIG, MAXN4>(K, S, L, a.floor_rel * dmax);
-    t1 = clock64(); tph[2] += t1 - t0; t0 = t1;
+    long long t1;
+    if (chord_step) {
+      // the solve's cached factorisation (reading Q26) into the KKT buffer
+      fl += iter_flops(n, m, p, pa, true, false, true);
+      const float4* src = reinterpret_cast<const float4*>(a.kc + (long long)bid * a.kc_stride);
+      float4* dst = reinterpret_cast<float4*>(K);
+      for (int i = tid; i < (L.size() + 3) >> 2; i += NT) dst[i] = __ldcg(src + i);
+      const float* cr = a.chd + (long long)bid * a.chd_stride + 4 + 4 * ((p + 3) & ~3);
+      for (int i = tid; i < L.N4; i += NT) S.rinv[i] = __ldcg(cr + i);
+      if constexpr (!BIG) for (int i = tid; i < L.N4; i += NT) S.ro[i] = L.off(i);
+      __syncthreads();
+      t1 = clock64(); tph[2] += t1 - t0; t0 = t1;
+    } else {
+      fl += iter_flops(n, m, p, pa, !init, true, true);
+      const float dmax = assemble<NT, BIG>(K, S, a, P, L, pa, S.om, cw, ev);
+      t1 = clock64(); tph[1] += t1 - t0; t0 = t1;
+      factor_any<NT, BIG, MAXN4>(K, S, L, a.floor_rel * dmax);
+      t1 = clock64(); tph[2] += t1 - t0; t0 = t1;
+      if (cache) {  // Alg. 1's factorisation nearest κ_relax: to the chord cache (reading Q26)
+        float4* dst = reinterpret_cast<float4*>(a.kc + (long long)bid * a.kc_stride);
+        const float4* src = reinterpret_cast<const float4*>(K);
+        for (int i = tid; i < (L.size() + 3) >> 2; i += NT) dst[i] = src[i];
+        float* cj = a.chd + (long long)bid * a.chd_stride;
+        const int p4 = (p + 3) & ~3;
+        for (int i = tid; i < p; i += NT) {
+          cj[4 + i] = S.dp[i]; cj[4 + p4 + i] = S.dm[i]; cj[4 + 2 * p4 + i] = S.c[i];
+          cj[4 + 3 * p4 + i] = __int_as_float(S.widx[i]);
+        }
+        for (int i = tid; i < L.N4; i += NT) cj[4 + 4 * p4 + i] = S.rinv[i];
+        if (tid == 0) {
+          cj[0] = __int_as_float(pa); cj[1] = kappa;
+          a.chord_ok[bid] = 1;
+        }
+      }
+    }
     if (adj) {
       // Algorithm 3: reduced system with right-hand side (−∇ₓℓ, 0, 0).  The
       // cotangent may be the output of the kernel launched just before this
@@ -1101,6 +1177,7 @@ __device__ __forceinline__ void ipm_problem(const Args& a, const Smem& S, const 
     }
     write_gradients<NT>(S, a, bid);
     if (tid == 0) {
+      if (nchord > 0 && a.chord_cnt) atomicAdd(a.chord_cnt, nchord);
       if (a.riters) a.riters[bid] = it;
       if (a.rstatus) a.rstatus[bid] = status;
       if (a.flops) a.flops[bid] = fl + 2.f * (n * n + m * n + p * n);  // + gradient outer products

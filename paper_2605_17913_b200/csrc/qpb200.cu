@@ -229,7 +229,8 @@ struct qp_ctx {
   float* chd = nullptr;
   long long chd_stride = 0;
   int* chord_ok = nullptr;
-  int chord_steps = 0;     // chord steps of the last backward (summed over the batch)
+  int chord_steps = 0;     // chord steps of the last backward (summed over the batch; path 4)
+  int* chord_cnt = nullptr;  // device counter of the same (path 1)
   float* flops_solve = nullptr;        // per-problem algorithmic flops of the last calls
   float* flops_bwd = nullptr;
   // host-memory mode, path 1: the batch runs in kPipe chunks on their own
@@ -305,7 +306,7 @@ size_t field_elems(int64_t stride, int32_t B, size_t per) { return stride == 0 ?
 
 void free_all(qp_ctx* c) {
   if (c->hctl) cudaFreeHost(c->hctl);
-  void* ptrs[] = {c->kc, c->chd, c->chord_ok, c->kglobf, c->fb_flag, c->fb_list, c->fb_ctl, c->ug, c->dtg, c->whi, c->wlo, c->gghi, c->gglo, c->slotmap, c->bst, c->bctl, c->tl, c->sched, c->done, c->kglob, c->flops_solve, c->flops_bwd, c->prof, c->own_status, c->wx, c->wy, c->wz, c->wdx, c->wdy, c->wdz, c->dQ_, c->dq_, c->dA_, c->db_,
+  void* ptrs[] = {c->kc, c->chd, c->chord_ok, c->chord_cnt, c->kglobf, c->fb_flag, c->fb_list, c->fb_ctl, c->ug, c->dtg, c->whi, c->wlo, c->gghi, c->gglo, c->slotmap, c->bst, c->bctl, c->tl, c->sched, c->done, c->kglob, c->flops_solve, c->flops_bwd, c->prof, c->own_status, c->wx, c->wy, c->wz, c->wdx, c->wdy, c->wdz, c->dQ_, c->dq_, c->dA_, c->db_,
                   c->dG_, c->dh_, c->dx_, c->ds_, c->dz_, c->dy_, c->ddl_, c->dit_, c->dst_, c->gQ_, c->gq_,
                   c->gA_, c->gb_, c->gG_, c->gh_};
   if (c->guard) {  // guard mode: the allocations start kGuard bytes before each pointer
@@ -339,6 +340,7 @@ qpb::Args base_args(const qp_ctx* c) {
   a.relax_mode = c->kc ? c->c.relax_mode : 0;
   a.chord_max = c->c.chord_max; a.chord_rho = c->c.chord_rho;
   a.kc = c->kc; a.kc_stride = c->kc_stride; a.chd = c->chd; a.chd_stride = c->chd_stride; a.chord_ok = c->chord_ok;
+  a.chord_cnt = c->chord_cnt;
   return a;
 }
 
@@ -618,7 +620,7 @@ qp_err qp_config_default(qp_config* cfg) {
   cfg->pivot_floor_rel = 3.4526698e-4f;  // sqrt(FLT_EPSILON)
   cfg->mem_kind = QP_MEM_DEVICE;
   cfg->relax_tol = 1e-6f;
-  cfg->relax_mode = QP_RELAX_NEWTON;
+  cfg->relax_mode = QP_RELAX_CHORD;
   cfg->chord_max = 8;
   cfg->chord_rho = 0.5f;
   return QP_OK;
@@ -763,23 +765,6 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
     if (cudaMallocHost(&ctx->hctl, 16 * sizeof(int)) != cudaSuccess || bnd_setup(ctx) != QP_OK) {
       free_all(ctx); delete ctx; return QP_ERR_CUDA;
     }
-    // guarded chord relax (reading Q26): a cached factor per problem of the
-    // whole batch, when it fits in a quarter of the free device memory
-    // (otherwise the relax stays exact Newton: qp_info.relax_mode says which)
-    if (c.relax_mode == QP_RELAX_CHORD && c.formulation == QP_IMPLICIT && d->p > 0) {
-      size_t fr2 = 0, tot2 = 0;
-      cudaMemGetInfo(&fr2, &tot2);
-      const long long cs = qpb::chd_floats(d->p, L.N4max);
-      const size_t need = (size_t)d->batch * 4 * ((size_t)L.kglob + (size_t)cs + 1);
-      if (need <= fr2 / 4) {
-        ctx->kc_stride = L.kglob; ctx->chd_stride = cs;
-        if ((e = dalloc(ctx, &ctx->kc, (size_t)d->batch * (size_t)L.kglob)) ||
-            (e = dalloc(ctx, &ctx->chd, (size_t)d->batch * (size_t)cs)) || (e = dalloc(ctx, &ctx->chord_ok, (size_t)d->batch))) {
-          free_all(ctx); delete ctx; return e;
-        }
-        if (cudaMemset(ctx->chord_ok, 0, sizeof(int) * d->batch) != cudaSuccess) { free_all(ctx); delete ctx; return QP_ERR_CUDA; }
-      }
-    }
     // shared G: the assembly runs as one GEMM over the batch (kr_gemm.cuh)
     ctx->kr = d->bstride_G == 0 && d->p > 0 && !getenv("QPB200_NO_KR");
     if (ctx->kr) {
@@ -791,6 +776,26 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
           (e = dalloc(ctx, &ctx->slotmap, ctx->bchunk))) {
         free_all(ctx); delete ctx; return e;
       }
+    }
+  }
+  // guarded chord relax (reading Q26): a cached factor per problem of the
+  // whole batch (path 4: the packed workspace; path 1: the shared-memory KKT
+  // buffer's contents), when it fits in a quarter of the free device memory
+  // (otherwise the relax stays exact Newton: qp_info.relax_mode says which)
+  if (c.relax_mode == QP_RELAX_CHORD && c.formulation == QP_IMPLICIT && d->p > 0 && (L.batched || !L.big)) {
+    size_t fr2 = 0, tot2 = 0;
+    cudaMemGetInfo(&fr2, &tot2);
+    const long long ks = L.batched ? (long long)L.kglob : (long long)((L.ksmem + 3) & ~3);
+    const long long cs = qpb::chd_floats(d->p, L.N4max);
+    const size_t need = (size_t)d->batch * 4 * ((size_t)ks + (size_t)cs + 1);
+    if (need <= fr2 / 4) {
+      ctx->kc_stride = ks; ctx->chd_stride = cs;
+      if ((e = dalloc(ctx, &ctx->kc, (size_t)d->batch * (size_t)ks)) ||
+          (e = dalloc(ctx, &ctx->chd, (size_t)d->batch * (size_t)cs)) || (e = dalloc(ctx, &ctx->chord_ok, (size_t)d->batch)) ||
+          (e = dalloc(ctx, &ctx->chord_cnt, 1))) {
+        free_all(ctx); delete ctx; return e;
+      }
+      if (cudaMemset(ctx->chord_ok, 0, sizeof(int) * d->batch) != cudaSuccess) { free_all(ctx); delete ctx; return QP_ERR_CUDA; }
     }
   }
   const int B = d->batch, n = d->n, m = d->m_eq, p = d->p;
@@ -875,6 +880,11 @@ qp_err qp_get_info(const qp_ctx* c, qp_info* info) {
   info->workspace_bytes = c->workspace;
   info->relax_mode = c->kc ? c->c.relax_mode : QP_RELAX_NEWTON;
   info->chord_steps = c->chord_steps;
+  if (c->chord_cnt && !c->L.batched) {  // path 1: the device counter of the last backward
+    if (cudaStreamSynchronize(c->stream) != cudaSuccess ||
+        cudaMemcpy(&info->chord_steps, c->chord_cnt, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess)
+      return QP_ERR_CUDA;
+  }
   info->handed_solve = info->handed_backward = 0;
   if (c->fb) {  // reading Q12c guard: hand-over counts of the last calls (all chunks)
     int h[4 * qp_ctx::kPipe];
@@ -1101,6 +1111,9 @@ qp_err qp_backward_batched(qp_ctx* c, const float* dl_dx, float* dQ, float* dq, 
     a.epoch = c->epoch;
     a.tl = c->tl ? c->tl + 3 * (size_t)B : nullptr;
   }
+  // chord-step counter (diagnostic; with QP_MEM_HOST_ASYNC the chunks are not
+  // ordered after this reset, so the count is approximate there)
+  if (c->chord_cnt && (e = cuda_ok(cudaMemsetAsync(c->chord_cnt, 0, sizeof(int), c->stream))) != QP_OK) return e;
   if (pipe) {
     // chunk ch on stream pst[ch]: H2D of its cotangents, its kernel, D2H of its
     // per-problem gradients; shared-field sums follow on c->stream

@@ -38,7 +38,7 @@ def test_chord_cfg4_subset(monkeypatch, chunk):
     assert g["info"]["chord_steps"] > 0
     c32 = O.Cfg.f32(relax_mode=2)
     check_against_oracle(b, g, cfg32=c32)
-    gn = run_gpu(b)  # exact-Newton relax: the solve is bitwise the same, the gradients agree
+    gn = run_gpu(b, relax_mode=0)  # exact-Newton relax: the solve is bitwise the same, the gradients agree
     for k in ("x", "s", "z", "y", "iters", "status"):
         assert np.array_equal(g[k], gn[k]), k
     for k in GRADS:
@@ -64,7 +64,7 @@ def test_chord_max_zero_is_newton():
     """chord_max = 0: the guard leaves chord mode before the first step, so
     the backward is exact Newton — bitwise the relax_mode = 0 result."""
     b = gen.make_config(4, batch=8)
-    g0 = run_gpu(b)
+    g0 = run_gpu(b, relax_mode=0)
     g1 = run_gpu(b, relax_mode=2, chord_max=0)
     assert g1["info"]["chord_steps"] == 0
     for k in GRADS + ("relax_iters", "grad_status"):
@@ -79,3 +79,41 @@ def test_chord_strict_guard_falls_back():
     g = run_gpu(b, relax_mode=2, chord_rho=1e-6)
     assert 0 < g["info"]["chord_steps"] <= 2 * 8
     check_against_oracle(b, g, cfg32=O.Cfg.f32(relax_mode=2, chord_rho=1e-6))
+
+
+# ---------------------------------------------------------------------------
+# path 1 (one persistent CTA per QP, KKT in shared memory): the solve copies
+# its factor to the cache, a chord step copies it back into the KKT buffer
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("cfg,batch", [(1, 16), (2, 96), (3, 48)])
+def test_chord_path1(cfg, batch):
+    b = gen.make_config(cfg, batch=batch)
+    g = run_gpu(b, **CHORD)
+    assert g["info"]["path"] == 1 and g["info"]["relax_mode"] == 2
+    assert g["info"]["chord_steps"] > 0
+    check_against_oracle(b, g, cfg32=O.Cfg.f32(relax_mode=2))
+    gn = run_gpu(b, relax_mode=0)
+    for k in ("x", "s", "z", "y", "iters", "status"):
+        assert np.array_equal(g[k], gn[k]), k
+    assert gn["info"]["relax_mode"] == 0 and gn["info"]["chord_steps"] == 0
+
+
+def test_chord_path1_max_zero_is_newton():
+    b = gen.make_config(2, batch=64)
+    g0 = run_gpu(b, relax_mode=0)
+    g1 = run_gpu(b, relax_mode=2, chord_max=0)
+    assert g1["info"]["chord_steps"] == 0
+    for k in GRADS + ("relax_iters", "grad_status"):
+        assert np.array_equal(g0[k], g1[k]), k
+
+
+@pytest.mark.parametrize("mem", ["host", "host_async"])
+def test_chord_path1_host_modes(mem):
+    """Host-buffer modes (8 chunk streams; host_async: each backward chunk
+    follows its solve chunk on its stream, with the programmatic backward
+    launch): the same results as device mode."""
+    b = gen.make_config(2, batch=301)
+    gd = run_gpu(b, **CHORD)
+    gh = run_gpu(b, mem=mem, **CHORD)
+    for k in ("x", "iters") + GRADS + ("relax_iters",):
+        assert np.array_equal(gd[k], gh[k]), k

@@ -18,7 +18,8 @@ def check_against_oracle(batch, g, iters_slack=1, grad_tol=TOL_GRAD, cfg32=None)
     x <= 1e-4, every gradient field <= 1e-3 per problem, iterations within
     +-1 of the f32 oracle; a miss passes only where the f32 oracle misses the
     same bar on the same problem (precision limit, reported)."""
-    c32 = cfg32 or O.Cfg.f32()
+    # the f32 oracle runs the GPU's Alg. 2 mode (guarded chord, reading Q26, or exact Newton)
+    c32 = cfg32 or O.Cfg.f32(relax_mode=int(g.get("info", {}).get("relax_mode", 0)))
     r64 = O.solve(batch, O.Cfg.f64(), "f64")
     r32 = O.solve(batch, c32, "f32")
     assert np.all(r64["status"] == 0)
@@ -574,7 +575,7 @@ def test_q12c_guard_licq_violating_many_active(monkeypatch, mem):
     for j in range(4):
         within_bar(res[:, j], res32[:, j], TOL_RES, f"residual {j}", report)
     assert np.abs(g["iters"].astype(int) - r32["iters"].astype(int)).max() <= 1
-    g64, g32 = O.backward(b, r64, c64, "f64"), O.backward(b, r32, O.Cfg.f32(), "f32")
+    g64, g32 = O.backward(b, r64, c64, "f64"), O.backward(b, r32, O.Cfg.f32(relax_mode=int(g["info"]["relax_mode"])), "f32")
     for k in GRADS:
         within_bar(rel_err_rows(g[k], g64[k]), rel_err_rows(g32[k], g64[k]), TOL_GRAD, k, report)
     print("precision-limited:", report)

@@ -740,8 +740,11 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
     long long cap = (long long)(fr / 2 / per);
     if (const char* e2 = getenv("QPB200_BCHUNK")) cap = atoll(e2);  // tests: force several chunks
     ctx->bchunk = (int)std::max(1LL, std::min<long long>(d->batch, cap));
-    // two lanes when the chunk holds enough problems to fill the GPU twice
-    ctx->nlanes = ctx->bchunk >= 2 * 4 * 148 ? 2 : 1;
+    // lanes: two for large chunks (config 4, 8192 problems: 42.4 K QP/s vs
+    // 41.8 K with three, 40.9 K with four); four for chunks of 256 to 1183
+    // problems, whose phase kernels alone fill few waves (config 5, 256
+    // problems: 532 / 564 / 577 / 583 QP/s with one / two / three / four)
+    ctx->nlanes = ctx->bchunk >= 2 * 4 * 148 ? 2 : ctx->bchunk >= 256 ? 4 : 1;
     if (const char* e2 = getenv("QPB200_BLANES")) ctx->nlanes = std::max(1, std::min(4, atoi(e2)));
     ctx->nlanes = std::min(ctx->nlanes, ctx->bchunk);
     cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);

@@ -82,6 +82,12 @@ struct BArgs {
   float* dtg;           // [B][64·64]: the current panel's factored diagonal block, transposed (bnd_pdiag → bnd_prows)
   float* ug;            // [B][ustride]: the panel's Schur update U[i − c0][0:64] (bnd_tc_update → bnd_pdiag / bnd_prows)
   long long ustride;
+  // TMA tensor maps of the KKT workspaces (bnd_tc_update_tma): one 128-byte
+  // CUtensorMap per 16-row block b of the uniform packed layout, 3-D
+  // {16b + 20 columns, 16 rows, problems}; this lane's first problem in them
+  const char* tmaps;
+  int lane_b0;
+  int ntiles_tu;        // bnd_tc_update_tma: 128-row tiles of the panel in the lane's largest system
 };
 
 __device__ __forceinline__ float* st_of(const BArgs& b, int bid) { return b.st + (long long)bid * b.st_stride; }
@@ -111,7 +117,7 @@ __device__ __forceinline__ void copy_block(float* __restrict__ dst, const float*
 }
 
 // The problem's KKT layout of this iteration: N = n4 + |kept| + m.
-__device__ __forceinline__ KLayout bnd_layout(const Args& a, int pa) { return KLayout::make(a.n4 + pa + a.m, a.n4); }
+__device__ __forceinline__ KLayout bnd_layout(const Args& a, int pa) { return KLayout::make(a.n4 + pa + a.m, a.n4, true); }
 
 // Solve finished (converged / failed / max_iter): outputs to the caller.
 template <int NT>
@@ -572,6 +578,258 @@ __global__ void __launch_bounds__(NT, 3) bnd_tc_update(const BArgs ba) {
     __syncwarp();
   }
   tc::tmem_free(tmem);
+}
+
+// ---------------------------------------------------------------------------
+// bnd_tc_update_tma: the same Schur update of a panel as bnd_tc_update, its
+// operands staged by the Tensor Memory Accelerator.  Per 32-deep K chunk one
+// thread issues 3-D tensor copies (cp.async.bulk.tensor, one per 16-row
+// block: A = rows [i0, i0 + 128), B = rows [c0, c0 + 64), columns [k0, k0 +
+// 32)) into an S-stage ring of fp32 tiles in the 128-byte-swizzled K-major
+// layout (a row's 128 bytes, 16-byte chunks XOR-permuted by row mod 8),
+// completing on the stage's mbarrier.  The CTA splits a landed chunk IN
+// PLACE for 3×TF32 — hi = tf32(x) over x, lo = tf32(x − hi) into the stage's
+// lo tiles, the sign S_k applied to B — and one thread issues the 12 MMAs
+// reading the swizzled tiles directly (SWIZZLE_128B descriptors).  Because
+// every stage carries its own operands, the split of chunk k + 1 overlaps
+// the MMAs of chunk k, and a stage is refilled (chunk k − 1 + S) once its
+// MMAs have completed (tcgen05.commit on the stage's second mbarrier).  The
+// ring hides the HBM latency that bounds the register-staged kernel
+// (profiles/r2: 36 % of its stall samples wait on those loads).
+// ---------------------------------------------------------------------------
+namespace tu {
+constexpr int TM = 128, BW = 64, TK = 32;
+constexpr int TA = TM * TK * 4, TB = BW * TK * 4;  // 16 KB, 8 KB
+constexpr int RAW = TA + TB;                        // a TMA stage: raw A, raw B
+constexpr int OPS = 2 * (TA + TB);                  // an operand buffer: hi A, hi B, lo A, lo B
+__host__ __device__ constexpr int smem_bytes(int S, int NOB = 2) { return 1024 + S * RAW + NOB * OPS + 256; }
+
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const void* map, int c0, int c1, int c2, uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(mbar)
+      : "memory");
+}
+__device__ __forceinline__ void expect_tx(uint32_t mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+}
+// K-major SWIZZLE_128B operand: 8-row groups 1024 B apart (SBO); the K step
+// inside the 128-byte swizzle atom advances the start address (32 B per 8 tf32)
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;              // LBO (unused by swizzled K-major layouts)
+  d |= (uint64_t)(1024 >> 4) << 32;    // SBO
+  d |= (uint64_t)1 << 46;              // version (sm_100)
+  d |= (uint64_t)2 << 61;              // layout: SWIZZLE_128B
+  return d;
+}
+}  // namespace tu
+
+// Persistent and warp-specialised (448 threads, one CTA per SM): work items
+// are (problem, 128-row tile) pairs of the panel, strided over the grid
+// (tile fastest); every role walks the same item sequence.
+//   warp 8      producer: TMA copies of item j's K chunk into raw stage j % S
+//   warps 0-7   split: raw stage → 3×TF32 hi/lo operand buffer j % 2 (SW128);
+//               warp w takes rows 8·(w % 4) + 32·t + [0, 8) at K quads
+//               4·(w / 4) + [0, 4)
+//   warp 9      MMA issuer: 12 tcgen05.mma per chunk into one of TWO TMEM
+//               accumulators (one per tile, alternating)
+//   warps 10-13 epilogue: the other accumulator → U (TMEM lane quarter w % 4)
+// mbarriers: full / rawfree per raw stage, opfull / opfree per operand
+// buffer, accfull / accfree per accumulator.
+constexpr int TU_THREADS = 448;
+constexpr int TU_SPLIT = 8;  // split warps
+
+template <int S, int NOB>
+__global__ void __launch_bounds__(TU_THREADS, 1) bnd_tc_update_tma(const BArgs ba) {
+  using namespace tu;
+  constexpr int SA = TM / 32, SB = BW / 32;  // 32-row groups of A and B per split thread
+  extern __shared__ unsigned char smdyn[];
+  const Args& a = ba.a;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int c0 = ba.c0, nk = c0 / TK;  // c0 is a multiple of 64
+  const int T = ba.ntiles_tu;          // row tiles of the largest problem of the lane
+  const long long nq = (long long)ba.a.B * T;
+  // the work-item walk shared by every role: q = blockIdx.x + g·gridDim.x,
+  // problem q / T, tile q % T, skipped unless the problem factors and has that tile
+  struct Item { int y, i0, N4, npos; };
+  auto valid = [&](long long q, Item& it) {
+    const int y = (int)(q / T), t = (int)(q % T);
+    const BScal& h = scal_of(st_of(ba, y));
+    if (h.mode == BM_DONE || h.mode == BM_CHORD) return false;
+    const KLayout L = bnd_layout(a, h.pa);
+    const int i0 = c0 + TM * t;
+    if (c0 >= L.N4 || i0 >= L.N4) return false;
+    it.y = y; it.i0 = i0; it.N4 = L.N4; it.npos = L.npos;
+    return true;
+  };
+  auto next = [&](long long& q, Item& it) {  // advance to the next valid item (q < 0: start)
+    q = q < 0 ? (long long)blockIdx.x : q + gridDim.x;
+    while (q < nq && !valid(q, it)) q += gridDim.x;
+    return q < nq;
+  };
+  const uint32_t base_s = (tc::smem_u32(smdyn) + 1023u) & ~1023u;
+  unsigned char* base = smdyn + (base_s - tc::smem_u32(smdyn));
+  unsigned char* opb = base + S * RAW;
+  uint64_t* full = reinterpret_cast<uint64_t*>(opb + NOB * OPS);
+  uint64_t* rawfree = full + S;
+  uint64_t* opfull = rawfree + S;
+  uint64_t* opfree = opfull + NOB;
+  uint64_t* accfull = opfree + NOB;
+  uint64_t* accfree = accfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(accfree + 2);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(tc::smem_u32(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int st = 0; st < S; ++st) { tc::mbar_init(full + st, 1); tc::mbar_init(rawfree + st, TU_SPLIT); }
+    for (int b = 0; b < NOB; ++b) { tc::mbar_init(opfull + b, TU_SPLIT); tc::mbar_init(opfree + b, 1); }
+    for (int b = 0; b < 2; ++b) { tc::mbar_init(accfull + b, 1); tc::mbar_init(accfree + b, 4); }
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tslot;
+  if (warp == TU_SPLIT) {
+    if (lane == 0) {  // producer
+      long long q = -1;
+      Item it;
+      int j = 0;
+      while (next(q, it)) {
+        const int bA = it.i0 >> 4, bB = c0 >> 4, c1 = min(c0 + BW, it.N4);
+        int nA = 0, nB = 0;
+        for (int t = 0; t < SA * 2; ++t) nA += (16 * (bA + t) < it.N4) ? 1 : 0;
+        for (int t = 0; t < SB * 2; ++t) nB += (16 * (bB + t) < c1) ? 1 : 0;
+        const int prob = ba.lane_b0 + it.y;
+        for (int kc = 0; kc < nk; ++kc, ++j) {
+          const int st = j % S;
+          if (j >= S) tc::mbar_wait(rawfree + st, (uint32_t)(((j / S) - 1) & 1));
+          const uint32_t mb = tc::smem_u32(full + st);
+          expect_tx(mb, (uint32_t)(nA + nB) * 2048u);
+          const uint32_t dA = base_s + st * RAW, dB = dA + TA;
+          for (int t = 0; t < nA; ++t) tma_load_3d(dA + t * 2048, ba.tmaps + (size_t)(bA + t) * 128, TK * kc, 0, prob, mb);
+          for (int t = 0; t < nB; ++t) tma_load_3d(dB + t * 2048, ba.tmaps + (size_t)(bB + t) * 128, TK * kc, 0, prob, mb);
+        }
+      }
+    }
+  } else if (warp == TU_SPLIT + 1) {
+    if (lane == 0) {  // MMA issuer
+      long long q = -1;
+      Item it;
+      int j = 0, u = 0;
+      while (next(q, it)) {
+        const int acc = u & 1;
+        const int c1 = min(c0 + BW, it.N4), wn = (c1 - c0 + 15) & ~15;
+        const uint32_t idesc = tc_idesc_n(wn), tacc = tmem + (uint32_t)(acc * BW);
+        if (u >= 2) tc::mbar_wait(accfree + acc, (uint32_t)(((u >> 1) - 1) & 1));  // drained by the epilogue
+        tc::tc_fence_after();
+        for (int kc = 0; kc < nk; ++kc, ++j) {
+          const int b = j % NOB;
+          tc::mbar_wait(opfull + b, (uint32_t)((j / NOB) & 1));
+          tc::tc_fence_after();
+          const uint32_t uhA = base_s + S * RAW + b * OPS, uhB = uhA + TA, ulA = uhB + TB, ulB = ulA + TA;
+#pragma unroll
+          for (int ks = 0; ks < TK / 8; ++ks) {
+            const uint32_t off = ks * 32;  // 8 tf32 of K in the 128-byte swizzle atom
+            const uint32_t acc0 = (kc > 0 || ks > 0) ? 1u : 0u;
+            tc::mma_tf32(tacc, desc_sw128(uhA + off), desc_sw128(uhB + off), idesc, acc0);
+            tc::mma_tf32(tacc, desc_sw128(uhA + off), desc_sw128(ulB + off), idesc, 1u);
+            tc::mma_tf32(tacc, desc_sw128(ulA + off), desc_sw128(uhB + off), idesc, 1u);
+          }
+          tc::commit(opfree + b);
+        }
+        tc::commit(accfull + acc);
+        ++u;
+      }
+    }
+  } else if (warp < TU_SPLIT) {
+    // split: a quarter-warp takes rows 8·w4 + [0, 8) at one K quad (8 distinct
+    // swizzled 16-byte chunks: conflict-free); rows past N4 / c1 become zeros
+    const int rl8 = lane & 7, qq = (lane >> 3) + 4 * (warp >> 2), w4 = warp & 3;
+    long long q = -1;
+    Item it;
+    int j = 0;
+    while (next(q, it)) {
+      const int c1 = min(c0 + BW, it.N4);
+      for (int kc = 0; kc < nk; ++kc, ++j) {
+        const int st = j % S, b = j % NOB, k0 = TK * kc;
+        const float* rA = reinterpret_cast<const float*>(base + st * RAW);
+        const float* rB = rA + TA / 4;
+        float* hA = reinterpret_cast<float*>(opb + b * OPS);
+        float* hB = hA + TA / 4;
+        float* lA = hB + TB / 4;
+        float* lB = lA + TA / 4;
+        tc::mbar_wait(full + st, (uint32_t)((j / S) & 1));
+        if (j >= NOB) tc::mbar_wait(opfree + b, (uint32_t)(((j / NOB) - 1) & 1));  // the MMAs of item j − NOB read it
+        float4 v[1][SA + SB];
+        {
+          const int sw = (qq ^ rl8) << 2;
+#pragma unroll
+          for (int s2 = 0; s2 < SA + SB; ++s2) {
+            const bool isb = s2 >= SA;
+            const int r = 8 * w4 + rl8 + 32 * (isb ? s2 - SA : s2);
+            v[0][s2] = *reinterpret_cast<const float4*>((isb ? rB : rA) + r * TK + sw);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) kr::mbar_arrive(rawfree + st);  // this warp has read the raw stage
+        {
+          const int h2 = 0, qd = qq;
+          const bool neg = k0 + 4 * qd >= it.npos;  // S_k on the B operand (npos is a multiple of 4)
+          const int sw = (qd ^ rl8) << 2;
+#pragma unroll
+          for (int s2 = 0; s2 < SA + SB; ++s2) {
+            const bool isb = s2 >= SA;
+            const int r = 8 * w4 + rl8 + 32 * (isb ? s2 - SA : s2);
+            const bool ok = isb ? c0 + r < c1 : it.i0 + r < it.N4;
+            float4 x = ok ? v[h2][s2] : make_float4(0.f, 0.f, 0.f, 0.f), hi, lo;
+            if (isb && neg) { x.x = -x.x; x.y = -x.y; x.z = -x.z; x.w = -x.w; }
+            hi.x = tc::to_tf32(x.x); lo.x = tc::to_tf32(x.x - hi.x);
+            hi.y = tc::to_tf32(x.y); lo.y = tc::to_tf32(x.y - hi.y);
+            hi.z = tc::to_tf32(x.z); lo.z = tc::to_tf32(x.z - hi.z);
+            hi.w = tc::to_tf32(x.w); lo.w = tc::to_tf32(x.w - hi.w);
+            *reinterpret_cast<float4*>((isb ? hB : hA) + r * TK + sw) = hi;
+            *reinterpret_cast<float4*>((isb ? lB : lA) + r * TK + sw) = lo;
+          }
+        }
+        tc::fence_async_smem();
+        __syncwarp();
+        if (lane == 0) kr::mbar_arrive(opfull + b);
+      }
+    }
+  } else {
+    // epilogue warps 10-13: TMEM lane quarter g = warp % 4 → rows i0 + 32g + lane of U
+    const int g = warp & 3;
+    long long q = -1;
+    Item it;
+    int u = 0;
+    while (next(q, it)) {
+      const int acc = u & 1;
+      const int c1 = min(c0 + BW, it.N4), wn = (c1 - c0 + 15) & ~15;
+      tc::mbar_wait(accfull + acc, (uint32_t)((u >> 1) & 1));
+      tc::tc_fence_after();
+      const int i = it.i0 + 32 * g + lane;
+      float* U = ba.ug + (long long)it.y * ba.ustride;
+      for (int cc = 0; cc < wn; cc += 32) {
+        float v[32];
+        tc::tmem_ld32(tmem + ((uint32_t)(32 * g) << 16) + (uint32_t)(acc * BW + cc), v);
+        if (i < it.N4) {
+          float4* dst = reinterpret_cast<float4*>(U + (long long)(i - c0) * BW + cc);
+#pragma unroll
+          for (int q4 = 0; q4 < 8; ++q4) dst[q4] = make_float4(v[4 * q4], v[4 * q4 + 1], v[4 * q4 + 2], v[4 * q4 + 3]);
+        }
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) kr::mbar_arrive(accfree + acc);
+      ++u;
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
 }
 
 // ---------------------------------------------------------------------------

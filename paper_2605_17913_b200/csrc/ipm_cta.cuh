@@ -60,14 +60,17 @@ __host__ __device__ __forceinline__ int r4(int x) { return (x + 3) & ~3; }
 struct KLayout {
   int N, N4, NB, npos;  // real dim, padded dim (×4), #16-blocks, #positive pivots
   int wl, Ll, baseL;    // last block: width, row length, offset
-  __host__ __device__ static KLayout make(int N, int npos) {
+  // uniform: the last block keeps the row length 16b + 20 of every other
+  // block, so row offsets do not depend on N (the batched engine: one TMA
+  // tensor map per 16-row block serves every problem and iteration)
+  __host__ __device__ static KLayout make(int N, int npos, bool uniform = false) {
     KLayout L;
     L.N = N;
     L.N4 = r4(N);
     L.NB = (L.N4 + KB - 1) / KB;
     L.npos = npos;
     L.wl = L.N4 - KB * (L.NB - 1);
-    L.Ll = ((L.N4 >> 2) & 1) ? L.N4 : L.N4 + 4;
+    L.Ll = uniform ? 16 * (L.NB - 1) + 20 : ((L.N4 >> 2) & 1) ? L.N4 : L.N4 + 4;
     const int b = L.NB - 1;
     L.baseL = 128 * b * (b + 1) + 64 * b;
     return L;

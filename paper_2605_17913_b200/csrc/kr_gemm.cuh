@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) kr_gemm(const GemmArgs g) {
         b_l = g.slotmap[slot_l];
         stb_l = g.st + (long long)b_l * g.st_stride;
         const int pa = reinterpret_cast<const int*>(stb_l)[6];  // BScal::pa
-        const KLayout L = KLayout::make(n4 + pa + m, n4);
+        const KLayout L = KLayout::make(n4 + pa + m, n4, true);  // bnd_layout
         nbm1_l = L.NB - 1; baseL_l = L.baseL; Ll_l = L.Ll;
       }
       float dmx = 0.f;  // lane r: max |diag| of problem r over this tile's pairs

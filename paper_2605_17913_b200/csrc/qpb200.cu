@@ -3,6 +3,7 @@
 // Every step of the hot path runs in the kernels of ipm_kernels.cuh; this file
 // only marshals.  There is no CPU fallback: without a CUDA device every entry
 // point returns QP_ERR_CUDA.
+#include <cuda.h>  // CUtensorMap (types only: the encoder comes from cudaGetDriverEntryPoint)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -157,6 +158,12 @@ Layout make_layout(int n, int m, int p, int formulation, int batch = 0, int sms 
     // is asked for (A/B experiments, parity tests of that kernel)
     L.batched = formulation != QP_EXPLICIT && !getenv("QPB200_PERSISTENT_BIG") && !force_big;
   }
+  if (L.batched) {
+    // path 4: uniform packed layout (bnd_layout), the last 16-row block
+    // allocated in full (the TMA boxes of bnd_tc_update read 16 rows)
+    const qpb::KLayout K = qpb::KLayout::make(L.Nmax, L.n4, true);
+    L.kglob = K.baseL + 16LL * K.Ll;
+  }
   L.ksmem = L.ncap > 0 ? qpb::KLayout::make(L.ncap, L.n4).size() : 0;
   L.smem = qpb::ipm_smem_bytes(L.n4, m, p, L.N4max, L.ksmem, tc_floats(L.big), ro_ints(L, L.big));
   return L;
@@ -254,6 +261,8 @@ struct qp_ctx {
   int* slotmap = nullptr;
   float* dtg = nullptr;  // [bchunk][64·64] panel diagonal blocks (bnd_pdiag → bnd_prows)
   float* ug = nullptr;   // [bchunk][N4max·64] panel Schur updates (bnd_tc_update → bnd_pdiag / bnd_prows)
+  char* tmaps = nullptr;  // device: one CUtensorMap per 16-row block of the KKT workspaces (bnd_tc_update_tma)
+  int tma_stages = 0;     // 0: register-staged bnd_tc_update; else bnd_tc_update_tma<raw stages, operand buffers> as 10·S + NOB
   // reading Q12c guard (path 1 with a kept-set cap): problems whose capped
   // elimination would exceed fb_bound go to the uncapped large-N kernel,
   // launched (list-driven) right after each path-1 launch
@@ -306,7 +315,7 @@ size_t field_elems(int64_t stride, int32_t B, size_t per) { return stride == 0 ?
 
 void free_all(qp_ctx* c) {
   if (c->hctl) cudaFreeHost(c->hctl);
-  void* ptrs[] = {c->kc, c->chd, c->chord_ok, c->chord_cnt, c->kglobf, c->fb_flag, c->fb_list, c->fb_ctl, c->ug, c->dtg, c->whi, c->wlo, c->gghi, c->gglo, c->slotmap, c->bst, c->bctl, c->tl, c->sched, c->done, c->kglob, c->flops_solve, c->flops_bwd, c->prof, c->own_status, c->wx, c->wy, c->wz, c->wdx, c->wdy, c->wdz, c->dQ_, c->dq_, c->dA_, c->db_,
+  void* ptrs[] = {c->tmaps, c->kc, c->chd, c->chord_ok, c->chord_cnt, c->kglobf, c->fb_flag, c->fb_list, c->fb_ctl, c->ug, c->dtg, c->whi, c->wlo, c->gghi, c->gglo, c->slotmap, c->bst, c->bctl, c->tl, c->sched, c->done, c->kglob, c->flops_solve, c->flops_bwd, c->prof, c->own_status, c->wx, c->wy, c->wz, c->wdx, c->wdy, c->wdz, c->dQ_, c->dq_, c->dA_, c->db_,
                   c->dG_, c->dh_, c->dx_, c->ds_, c->dz_, c->dy_, c->ddl_, c->dit_, c->dst_, c->gQ_, c->gq_,
                   c->gA_, c->gb_, c->gG_, c->gh_};
   if (c->guard) {  // guard mode: the allocations start kGuard bytes before each pointer
@@ -440,8 +449,50 @@ qp_err bnd_setup(const qp_ctx* c) {
       cudaFuncSetAttribute(qpb::bnd_solve<kBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, ssv) ||
       cudaFuncSetAttribute(qpb::bnd_assemble<kBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, stc) ||
       cudaFuncSetAttribute(qpb::bnd_tc_update<kBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, stc) ||
+      cudaFuncSetAttribute(qpb::bnd_tc_update_tma<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, qpb::tu::smem_bytes(2, 2)) ||
+      cudaFuncSetAttribute(qpb::bnd_tc_update_tma<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, qpb::tu::smem_bytes(4, 2)) ||
       cudaFuncSetAttribute(qpb::kr::kr_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, qpb::kr::WS_SMEM_BYTES))
     return QP_ERR_CUDA;
+  return QP_OK;
+}
+
+// TMA tensor maps of the batched engine's KKT workspaces (bnd_tc_update_tma):
+// for every 16-row block b of the uniform packed layout (bnd_layout) a 3-D
+// map {columns 16b + 20, rows 16, problems bchunk} with row stride (16b + 20)
+// floats and problem stride kglob floats, 32 × 16 boxes, 128-byte swizzle.
+qp_err make_tmaps(qp_ctx* c) {
+  typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !fn)
+    return QP_ERR_CUDA;
+  const EncodeTiled encode = reinterpret_cast<EncodeTiled>(fn);
+  const int NB = (c->L.N4max + 15) / 16;
+  std::vector<CUtensorMap> maps(NB);
+  for (int b = 0; b < NB; ++b) {
+    const long long rl = 16LL * b + 20;
+    void* gaddr = c->kglob + (128LL * b * (b + 1) + 64LL * b);
+    const cuuint64_t dims[3] = {(cuuint64_t)rl, 16, (cuuint64_t)c->bchunk};
+    const cuuint64_t strides[2] = {(cuuint64_t)(rl * 4), (cuuint64_t)(c->L.kglob * 4)};
+    const cuuint32_t box[3] = {32, 16, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    if (encode(&maps[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, gaddr, dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return QP_ERR_CUDA;
+  }
+  qp_err e;
+  if ((e = dalloc(c, &c->tmaps, (size_t)NB * sizeof(CUtensorMap))) != QP_OK) return e;
+  if (cudaMemcpy(c->tmaps, maps.data(), (size_t)NB * sizeof(CUtensorMap), cudaMemcpyHostToDevice) != cudaSuccess)
+    return QP_ERR_CUDA;
+  // opt-in (QPB200_TC_TMA = 42: four raw stages, two operand buffers; 22:
+  // two and two): measured 2-3 % slower than the register-staged kernel on
+  // config 4 and 8 % on config 5, so the default stays that
+  c->tma_stages = 0;
+  if (const char* e2 = getenv("QPB200_TC_TMA")) c->tma_stages = atoi(e2) == 22 ? 22 : 42;  // A/B
   return QP_OK;
 }
 
@@ -511,6 +562,7 @@ qp_err run_batched(qp_ctx* c, const qpb::Args& a0, bool bwd) {
       ba.slotmap = c->slotmap ? c->slotmap + (size_t)l * lcap : nullptr;
       ba.dtg = c->dtg + (size_t)l * lcap * 64 * 64;
       ba.ug = c->ug + (size_t)l * lcap * c->L.N4max * 64; ba.ustride = (long long)c->L.N4max * 64;
+      ba.tmaps = c->tmaps; ba.lane_b0 = l * lcap;
       qpb::kr::GemmArgs& ga = L.ga;
       if (c->kr) {
         ga.whi = ba.whi; ga.wlo = ba.wlo; ga.gghi = c->gghi; ga.gglo = c->gglo;
@@ -573,7 +625,19 @@ qp_err run_batched(qp_ctx* c, const qpb::Args& a0, bool bwd) {
         for (int c0 = 0; c0 < L.N4cur; c0 += kBW) {
           ba.c0 = c0;
           if (c0 > 0) {
-            qpb::bnd_tc_update<kBT><<<dim3((L.N4cur - c0 + qpb::tc::TM - 1) / qpb::tc::TM, nb), kBT, stc, st>>>(ba);
+            const int tl = (L.N4cur - c0 + qpb::tc::TM - 1) / qpb::tc::TM;
+            if (c->tma_stages) {
+              // persistent, warp-specialised: one CTA per SM of this lane's share
+              ba.ntiles_tu = tl;
+              const long long items = (long long)tl * nb;
+              const int grid = (int)std::min<long long>(items, std::max(1, c->sms / c->nlanes));
+              const int v = c->tma_stages;  // raw stages × 10 + operand buffers
+              const int S = v / 10, NOB = v % 10, sb = qpb::tu::smem_bytes(S, NOB);
+              if (v == 22) qpb::bnd_tc_update_tma<2, 2><<<grid, qpb::TU_THREADS, sb, st>>>(ba);
+              else qpb::bnd_tc_update_tma<4, 2><<<grid, qpb::TU_THREADS, sb, st>>>(ba);
+            } else {
+              qpb::bnd_tc_update<kBT><<<dim3(tl, nb), kBT, stc, st>>>(ba);
+            }
             ++launches;
           }
           qpb::bnd_pdiag<32><<<nb, 32, 0, st>>>(ba);
@@ -768,6 +832,7 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
     if (cudaMallocHost(&ctx->hctl, 16 * sizeof(int)) != cudaSuccess || bnd_setup(ctx) != QP_OK) {
       free_all(ctx); delete ctx; return QP_ERR_CUDA;
     }
+    if (getenv("QPB200_TC_TMA") && (e = make_tmaps(ctx)) != QP_OK) { free_all(ctx); delete ctx; return e; }
     // shared G: the assembly runs as one GEMM over the batch (kr_gemm.cuh)
     ctx->kr = d->bstride_G == 0 && d->p > 0 && !getenv("QPB200_NO_KR");
     if (ctx->kr) {

@@ -87,6 +87,11 @@ struct BArgs {
   // {16b + 20 columns, 16 rows, problems}; this lane's first problem in them
   const char* tmaps;
   int lane_b0;
+  // Q and G shared by the batch: the residual GEMVs as batched GEMMs
+  // (bnd_sgemm): per problem Q x, Gᵀ z, Gᵀ t ([3][n4]); G x lands in the
+  // state's gx segment.  nullptr = per-problem GEMVs inside bnd_resid
+  float* pre;
+  long long pre_stride;
   int ntiles_tu;        // bnd_tc_update_tma: 128-row tiles of the panel in the lane's largest system
 };
 
@@ -267,7 +272,8 @@ __global__ void __launch_bounds__(NT) bnd_resid(const BArgs ba) {
   float fl = h.fl, phi_prev = h.phi_prev, psi_prev = h.psi_prev;
 #pragma unroll 1
   for (int pass = 0;; ++pass) {
-    R = residuals<NT, LARGE>(S, a, P, kappa, kappa - kt, keep, keep ? __float_as_int(cj[0]) : 0);
+    R = residuals<NT, LARGE>(S, a, P, kappa, kappa - kt, keep, keep ? __float_as_int(cj[0]) : 0,
+                             ba.pre ? ba.pre + (long long)bid * ba.pre_stride : nullptr);
     if (pass == 1) break;
     if (R.nonfin > 0.f) {
       status = ST_FAIL | ((bwd ? STG_RELAX : STG_SCALING) << 8);
@@ -984,6 +990,96 @@ __global__ void __launch_bounds__(NT, 4) bnd_prows(const BArgs ba) {
 }
 
 // ---------------------------------------------------------------------------
+// bnd_sgemm: C[M×N] = A[M×K] · op(B) in FP32 (FMA, the arithmetic of the
+// per-problem GEMVs it replaces), op(B) = Bᵀ for B [N×K] (BT) or B [K×N].
+// With Q and G shared by the batch (config 4) the residual products of all
+// problems are GEMMs: G X, Q X (NT) and Gᵀ Z, Gᵀ T (NN) with the problems'
+// x, z, t rows read in place from their state blocks (lda = state stride):
+// the shared matrix is read once per 64-problem tile instead of once per
+// problem.  64×64 tiles, K in steps of 16, 256 threads with 4×4 outputs each.
+// ---------------------------------------------------------------------------
+template <bool BT>
+__global__ void __launch_bounds__(256) bnd_sgemm(const float* __restrict__ A, long long lda,
+                                                 const float* __restrict__ B, long long ldb, float* __restrict__ C,
+                                                 long long ldc, int M, int N, int K) {
+  constexpr int BM = 64, BN = 64, BK = 16;
+  __shared__ __align__(16) float As[BK][BM + 4], Bs[BK][BN + 4];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const bool va = !(lda & 3) && !(reinterpret_cast<uintptr_t>(A) & 15);
+  const bool vb = !(ldb & 3) && !(reinterpret_cast<uintptr_t>(B) & 15);
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += BK) {
+    {  // A tile: row r = tid / 4, k quad (tid % 4)·4, stored k-major
+      const int r = tid >> 2, kq = (tid & 3) * 4, gm = m0 + r, gk = k0 + kq;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (gm < M) {
+        const float* src = A + (long long)gm * lda + gk;
+        if (va && gk + 3 < K) v = *reinterpret_cast<const float4*>(src);
+        else {
+          if (gk < K) v.x = src[0];
+          if (gk + 1 < K) v.y = src[1];
+          if (gk + 2 < K) v.z = src[2];
+          if (gk + 3 < K) v.w = src[3];
+        }
+      }
+      As[kq][r] = v.x; As[kq + 1][r] = v.y; As[kq + 2][r] = v.z; As[kq + 3][r] = v.w;
+    }
+    if constexpr (BT) {  // B [N×K]: like A
+      const int r = tid >> 2, kq = (tid & 3) * 4, gn = n0 + r, gk = k0 + kq;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (gn < N) {
+        const float* src = B + (long long)gn * ldb + gk;
+        if (vb && gk + 3 < K) v = __ldg(reinterpret_cast<const float4*>(src));
+        else {
+          if (gk < K) v.x = __ldg(src);
+          if (gk + 1 < K) v.y = __ldg(src + 1);
+          if (gk + 2 < K) v.z = __ldg(src + 2);
+          if (gk + 3 < K) v.w = __ldg(src + 3);
+        }
+      }
+      Bs[kq][r] = v.x; Bs[kq + 1][r] = v.y; Bs[kq + 2][r] = v.z; Bs[kq + 3][r] = v.w;
+    } else {  // B [K×N]: k row tid / 16, column quad (tid % 16)·4
+      const int kr = tid >> 4, nq = (tid & 15) * 4, gk = k0 + kr, gn = n0 + nq;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (gk < K) {
+        const float* src = B + (long long)gk * ldb + gn;
+        if (vb && gn + 3 < N) v = __ldg(reinterpret_cast<const float4*>(src));
+        else {
+          if (gn < N) v.x = __ldg(src);
+          if (gn + 1 < N) v.y = __ldg(src + 1);
+          if (gn + 2 < N) v.z = __ldg(src + 2);
+          if (gn + 3 < N) v.w = __ldg(src + 3);
+        }
+      }
+      *reinterpret_cast<float4*>(&Bs[kr][nq]) = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { av[i] = As[kk][ty + 16 * i]; bv[i] = Bs[kk][tx + 16 * i]; }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gm = m0 + ty + 16 * i;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gn = n0 + tx + 16 * j;
+      if (gn < N) C[(long long)gm * ldc + gn] = acc[i][j];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // bnd_cache: grid (chunks, B), after the panel loop of a solve iteration in
 // which some problems reached κ < √10·κ_relax for the first time (reading
 // Q26): their factor (packed L), pivot reciprocals, partition and Jacobian
@@ -1035,6 +1131,11 @@ __global__ void __launch_bounds__(NT) bnd_solve(const BArgs ba) {
   const float* K = chord ? a.kc + (long long)bid * a.kc_stride : ba.kw + (long long)bid * ba.kstride;
   const float* rinv = chord ? a.chd + (long long)bid * a.chd_stride + 4 + 4 * ((a.p + 3) & ~3) : G.rinv;
   copy_block<NT>(sm, G.rhs, L.N4);
+  if (ba.pre && (h.mode == BM_NEWTON || h.mode == BM_CHORD)) {  // + Gᵀ t of the batched GEMM (residuals, pre)
+    const float* gt = ba.pre + (long long)bid * ba.pre_stride + 2 * a.n4;
+    for (int j = threadIdx.x; j < a.n; j += NT) sm[j] += gt[j];
+    __syncthreads();
+  }
   solve_qd<NT, false, true>(K, L, rinv, sm);
   __syncthreads();
   copy_block<NT>(G.rhs, sm, L.N4);
@@ -1063,7 +1164,12 @@ __global__ void __launch_bounds__(NT) bnd_update(const BArgs ba) {
     for (int j = tid; j < n; j += NT) S.x[j] = S.rhs[j];
     for (int l = tid; l < m; l += NT) S.y[l] = S.rhs[n4 + l];
     __syncthreads();
-    rowdots<NT>(P.G, p, n, S.x, S.dz);
+    if (ba.pre) {  // G x from the batched GEMM after bnd_solve (x = the solve's rhs)
+      for (int i = tid; i < p; i += NT) S.dz[i] = S.gx[i];
+      __syncthreads();
+    } else {
+      rowdots<NT>(P.G, p, n, S.x, S.dz);
+    }
     for (int i = tid; i < p; i += NT) S.dz[i] -= __ldg(P.h + i);  // ẑ = Gx − h
     __syncthreads();
     float ap = -INFINITY, ad = -INFINITY, bad = 0.f;
@@ -1091,7 +1197,7 @@ __global__ void __launch_bounds__(NT) bnd_update(const BArgs ba) {
   } else if (mode == BM_NEWTON || mode == BM_CHORD) {
     float kappa = h.kappa;
     int stage = 0;
-    const bool okstep = newton_update<NT>(S, a, P, pa, kappa, kappa - h.kt, &stage);
+    const bool okstep = newton_update<NT>(S, a, P, pa, kappa, kappa - h.kt, &stage, ba.pre != nullptr);
     if (!okstep) {
       if (tid == 0) h.status = ST_FAIL | ((bwd ? STG_RELAX : stage) << 8);
       __syncthreads();
@@ -1101,7 +1207,7 @@ __global__ void __launch_bounds__(NT) bnd_update(const BArgs ba) {
       h.kappa = kappa;
     }
   } else {  // BM_ADJ: dv = G dx + w (f2 = 0), dz = d₊ ⊙ dv (reading Q8), Alg. 3 outer products
-    recover_dv<NT>(S, a, P, true);
+    recover_dv<NT>(S, a, P, true, ba.pre != nullptr);
     for (int i = tid; i < p; i += NT) S.dz[i] = S.dp[i] * S.gx[i];
     for (int j = tid; j < n; j += NT) S.dx[j] = S.rhs[j];
     for (int l = tid; l < m; l += NT) S.dy[l] = S.rhs[n4 + pa + l];

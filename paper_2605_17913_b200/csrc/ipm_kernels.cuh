@@ -555,9 +555,14 @@ struct Norms {
 // Jacobian vectors d₊, d₋, c and the partition (widx, pa_keep) already in S
 // are those of the cached factorisation and are kept; only the residuals are
 // of the current point.  The norms do not depend on the Jacobian.
+//
+// pre (batched engine with Q and G shared by the batch): the GEMV products
+// came from batched GEMMs over the whole batch (bnd_gemm): S.gx[0:p) = G x
+// already in place, pre[0:n) = Q x, pre[n4:n4+n) = Gᵀ z; Gᵀ t is added to
+// the right-hand side later (pre[2n4:], by bnd_solve), so rhs[0:n) = −r_t here.
 template <int NT, bool LARGE = false>
 __device__ Norms residuals(const Smem& S, const Args& a, const Prob& P, float kappa, float r_kappa,
-                           bool keep_jac = false, int pa_keep = 0) {
+                           bool keep_jac = false, int pa_keep = 0, const float* pre = nullptr) {
   const int tid = threadIdx.x;
   const int n = a.n, n4 = a.n4, p = a.p, m = a.m;
   float mz = 0.f, ms = 0.f, mh = 0.f, mrzs = 0.f, nonfin = 0.f;
@@ -590,7 +595,7 @@ __device__ Norms residuals(const Smem& S, const Args& a, const Prob& P, float ka
     spill = vv[0] > a.fb_bound;
   }
   // rows: r_i = Gx + s − h, r_e = Ax − b (warp per row); f2, t, rhs_w, rhs_y
-  rowdots<NT>(P.G, p, n, S.x, S.gx);
+  if (!pre) rowdots<NT>(P.G, p, n, S.x, S.gx);
   rowdots<NT>(P.A, m, n, S.x, S.gx + p);
   for (int k = tid; k < p; k += NT) {
     const float ri = S.gx[k] + S.s[k] - __ldg(P.h + k);
@@ -615,7 +620,7 @@ __device__ Norms residuals(const Smem& S, const Args& a, const Prob& P, float ka
   // used only where that gives more groups than one column per thread
   const int gw2 = ((n >> 1) + 31) & ~31;
   const int ng2 = min(min(NT, 128) / gw2, 4);
-  const bool pairs = ng2 > ng && !(n & 1) &&
+  const bool pairs = !pre && ng2 > ng && !(n & 1) &&
                      !((reinterpret_cast<uintptr_t>(P.Q) | reinterpret_cast<uintptr_t>(P.G) |
                         (m > 0 ? reinterpret_cast<uintptr_t>(P.A) : 0)) & 7);
   if (pairs) {
@@ -649,7 +654,7 @@ __device__ Norms residuals(const Smem& S, const Args& a, const Prob& P, float ka
       *reinterpret_cast<float2*>(cs + 2 * cw + j) = gt; *reinterpret_cast<float2*>(cs + 3 * cw + j) = ay;
     }
     __syncthreads();
-  } else if (ng > 1) {
+  } else if (ng > 1 && !pre) {
     const int grp = tid / gw, j = tid - grp * gw;
     if (grp < ng && j < n) {
       float qx = 0.f, gz = 0.f, gt = 0.f, ay = 0.f;
@@ -685,7 +690,7 @@ __device__ Norms residuals(const Smem& S, const Args& a, const Prob& P, float ka
     // large n (batched engine): a thread owns a column QUAD (float4 loads of
     // Q, G, A rows) and keeps 8 rows in flight — the per-problem GEMVs of
     // config 5 (G: 8 MB per problem, from DRAM) are bound by bytes in flight
-    quads = n >= 2 * NT && !(n & 3) &&
+    quads = !pre && n >= 2 * NT && !(n & 3) &&
             !((reinterpret_cast<uintptr_t>(P.Q) | reinterpret_cast<uintptr_t>(P.G) |
                (m > 0 ? reinterpret_cast<uintptr_t>(P.A) : 0)) & 15);
     if (quads) {
@@ -727,7 +732,11 @@ __device__ Norms residuals(const Smem& S, const Args& a, const Prob& P, float ka
   }
   for (int j = tid; !quads && j < n; j += NT) {
     float qx = 0.f, gz = 0.f, gt = 0.f, ay = 0.f;
-    if (ng > 1) {
+    if (pre) {  // Q x and Gᵀ z from the batched GEMMs; Gᵀ t added by bnd_solve
+      qx = pre[j];
+      gz = pre[a.n4 + j];
+      for (int l = 0; l < m; ++l) ay = fmaf(__ldg(P.A + l * n + j), S.y[l], ay);
+    } else if (ng > 1) {
       for (int g = 0; g < ng; ++g) {
         const float* cs = S.colscr + g * 4 * cw;
         qx += cs[j]; gz += cs[cw + j]; gt += cs[2 * cw + j]; ay += cs[3 * cw + j];
@@ -813,9 +822,9 @@ __device__ float manifold_coords(const Smem& S, const Args& a) {
 // (i ∈ A) or eliminated: w_i = (d₊_i g_iᵀΔx − f2_i)/d₋_i (v_i ≤ 0).  Writes
 // S.gx[k] = Δv_k.  (f2 = 0 for the adjoint.)
 template <int NT>
-__device__ void recover_dv(const Smem& S, const Args& a, const Prob& P, bool zero_f2) {
+__device__ void recover_dv(const Smem& S, const Args& a, const Prob& P, bool zero_f2, bool gx_ready = false) {
   const int n4 = a.n4;
-  rowdots<NT>(P.G, a.p, a.n, S.rhs, S.gx);
+  if (!gx_ready) rowdots<NT>(P.G, a.p, a.n, S.rhs, S.gx);  // (gx_ready: G Δx from a batched GEMM)
   for (int k = threadIdx.x; k < a.p; k += NT) {
     const float gdx = S.gx[k];
     const int wi = S.widx[k];
@@ -831,11 +840,11 @@ __device__ void recover_dv(const Smem& S, const Args& a, const Prob& P, bool zer
 // finite.
 template <int NT>
 __device__ bool newton_update(const Smem& S, const Args& a, const Prob& P, int pa, float& kappa, float r_kappa,
-                              int* stage) {
+                              int* stage, bool gx_ready = false) {
   const int tid = threadIdx.x;
   const int n = a.n, n4 = a.n4, p = a.p, m = a.m;
   const float dk = -r_kappa;
-  recover_dv<NT>(S, a, P, false);
+  recover_dv<NT>(S, a, P, false, gx_ready);
   float amax = INFINITY, bad = 0.f;
   for (int k = tid; k < p; k += NT) {
     const float dv = S.gx[k];

@@ -262,6 +262,9 @@ struct qp_ctx {
   float* dtg = nullptr;  // [bchunk][64·64] panel diagonal blocks (bnd_pdiag → bnd_prows)
   float* ug = nullptr;   // [bchunk][N4max·64] panel Schur updates (bnd_tc_update → bnd_pdiag / bnd_prows)
   char* tmaps = nullptr;  // device: one CUtensorMap per 16-row block of the KKT workspaces (bnd_tc_update_tma)
+  // Q and G shared: residual GEMVs as batched GEMMs (bnd_sgemm), per problem [3][n4]
+  float* pre = nullptr;
+  long long off_x = 0, off_z = 0, off_t = 0, off_gx = 0, off_rhs = 0;  // state-block offsets (floats)
   int tma_stages = 0;     // 0: register-staged bnd_tc_update; else bnd_tc_update_tma<raw stages, operand buffers> as 10·S + NOB
   // reading Q12c guard (path 1 with a kept-set cap): problems whose capped
   // elimination would exceed fb_bound go to the uncapped large-N kernel,
@@ -315,7 +318,7 @@ size_t field_elems(int64_t stride, int32_t B, size_t per) { return stride == 0 ?
 
 void free_all(qp_ctx* c) {
   if (c->hctl) cudaFreeHost(c->hctl);
-  void* ptrs[] = {c->tmaps, c->kc, c->chd, c->chord_ok, c->chord_cnt, c->kglobf, c->fb_flag, c->fb_list, c->fb_ctl, c->ug, c->dtg, c->whi, c->wlo, c->gghi, c->gglo, c->slotmap, c->bst, c->bctl, c->tl, c->sched, c->done, c->kglob, c->flops_solve, c->flops_bwd, c->prof, c->own_status, c->wx, c->wy, c->wz, c->wdx, c->wdy, c->wdz, c->dQ_, c->dq_, c->dA_, c->db_,
+  void* ptrs[] = {c->pre, c->tmaps, c->kc, c->chd, c->chord_ok, c->chord_cnt, c->kglobf, c->fb_flag, c->fb_list, c->fb_ctl, c->ug, c->dtg, c->whi, c->wlo, c->gghi, c->gglo, c->slotmap, c->bst, c->bctl, c->tl, c->sched, c->done, c->kglob, c->flops_solve, c->flops_bwd, c->prof, c->own_status, c->wx, c->wy, c->wz, c->wdx, c->wdy, c->wdz, c->dQ_, c->dq_, c->dA_, c->db_,
                   c->dG_, c->dh_, c->dx_, c->ds_, c->dz_, c->dy_, c->ddl_, c->dit_, c->dst_, c->gQ_, c->gq_,
                   c->gA_, c->gb_, c->gG_, c->gh_};
   if (c->guard) {  // guard mode: the allocations start kGuard bytes before each pointer
@@ -563,6 +566,8 @@ qp_err run_batched(qp_ctx* c, const qpb::Args& a0, bool bwd) {
       ba.dtg = c->dtg + (size_t)l * lcap * 64 * 64;
       ba.ug = c->ug + (size_t)l * lcap * c->L.N4max * 64; ba.ustride = (long long)c->L.N4max * 64;
       ba.tmaps = c->tmaps; ba.lane_b0 = l * lcap;
+      ba.pre = c->pre ? c->pre + (size_t)l * lcap * 3 * n4 : nullptr;
+      ba.pre_stride = 3LL * n4;
       qpb::kr::GemmArgs& ga = L.ga;
       if (c->kr) {
         ga.whi = ba.whi; ga.wlo = ba.wlo; ga.gghi = c->gghi; ga.gglo = c->gglo;
@@ -585,11 +590,29 @@ qp_err run_batched(qp_ctx* c, const qpb::Args& a0, bool bwd) {
         if (!L.live || L.k < 0) continue;
         if (cudaMemsetAsync(L.ba.ctl, 0, 4 * sizeof(int), L.st) != cudaSuccess) return QP_ERR_CUDA;
         L.ba.k = L.k;
+        if (c->pre) {  // G x, Q x, Gᵀ z of every problem of the lane as three GEMMs
+          const int n = c->d.n, p = c->d.p, mb = (L.nb + 63) / 64;
+          const long long ss = c->bst_stride;
+          float* st0 = L.ba.st;
+          qpb::bnd_sgemm<true><<<dim3((p + 63) / 64, mb), 256, 0, L.st>>>(st0 + c->off_x, ss, a0.G, n,
+                                                                            st0 + c->off_gx, ss, L.nb, p, n);
+          qpb::bnd_sgemm<true><<<dim3((n + 63) / 64, mb), 256, 0, L.st>>>(st0 + c->off_x, ss, a0.Q, n, L.ba.pre,
+                                                                            L.ba.pre_stride, L.nb, n, n);
+          qpb::bnd_sgemm<false><<<dim3((n + 63) / 64, mb), 256, 0, L.st>>>(st0 + c->off_z, ss, a0.G, n,
+                                                                             L.ba.pre + n4, L.ba.pre_stride, L.nb, n, p);
+          launches += 3;
+        }
         if (c->d.n >= 2 * kBS)  // column-quad GEMVs with 8 rows in flight (config 5)
           qpb::bnd_resid<kBS, true><<<L.nb, kBS, sst, L.st>>>(L.ba);
         else
           qpb::bnd_resid<kBS><<<L.nb, kBS, sst, L.st>>>(L.ba);
         ++launches;
+        if (c->pre) {  // Gᵀ t (t: this iteration's right-hand-side vector of bnd_resid), added by bnd_solve
+          const int n = c->d.n, p = c->d.p;
+          qpb::bnd_sgemm<false><<<dim3((n + 63) / 64, (L.nb + 63) / 64), 256, 0, L.st>>>(
+              L.ba.st + c->off_t, c->bst_stride, a0.G, n, L.ba.pre + 2 * n4, L.ba.pre_stride, L.nb, n, p);
+          ++launches;
+        }
         if (cudaMemcpyAsync(c->hctl + 4 * l, L.ba.ctl, 4 * sizeof(int), cudaMemcpyDeviceToHost, L.st) != cudaSuccess ||
             cudaEventRecord(c->bev[1 + l], L.st) != cudaSuccess)
           return QP_ERR_CUDA;
@@ -650,6 +673,12 @@ qp_err run_batched(qp_ctx* c, const qpb::Args& a0, bool bwd) {
           ++launches;
         }
         qpb::bnd_solve<kBT><<<nb, kBT, ssv, st>>>(ba);
+        if (c->pre) {  // G Δx (the solve's x part) of every problem: Δv recovery / the initial ẑ in bnd_update
+          const int n = c->d.n, p = c->d.p;
+          qpb::bnd_sgemm<true><<<dim3((p + 63) / 64, (nb + 63) / 64), 256, 0, st>>>(
+              ba.st + c->off_rhs, c->bst_stride, a0.G, n, ba.st + c->off_gx, c->bst_stride, nb, p, n);
+          ++launches;
+        }
         qpb::bnd_update<kBS><<<nb, kBS, sst, st>>>(ba);
         launches += 2;
         ++L.k;
@@ -835,6 +864,14 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
     if (getenv("QPB200_TC_TMA") && (e = make_tmaps(ctx)) != QP_OK) { free_all(ctx); delete ctx; return e; }
     // shared G: the assembly runs as one GEMM over the batch (kr_gemm.cuh)
     ctx->kr = d->bstride_G == 0 && d->p > 0 && !getenv("QPB200_NO_KR");
+    // shared Q and G: the residual GEMVs as batched GEMMs too (bnd_sgemm)
+    if (ctx->kr && d->bstride_Q == 0 && !getenv("QPB200_NO_PRE")) {
+      if ((e = dalloc(ctx, &ctx->pre, (size_t)ctx->bchunk * 3 * L.n4)) != QP_OK) { free_all(ctx); delete ctx; return e; }
+      const qpb::Smem S0 = qpb::layout(nullptr, L.n4, d->m_eq, d->p, L.N4max, 0, 0, 0);
+      ctx->off_x = 16 + (S0.x - (float*)nullptr); ctx->off_z = 16 + (S0.z - (float*)nullptr);
+      ctx->off_t = 16 + (S0.t - (float*)nullptr); ctx->off_gx = 16 + (S0.gx - (float*)nullptr);
+      ctx->off_rhs = 16 + (S0.rhs - (float*)nullptr);
+    }
     if (ctx->kr) {
       const size_t kpad = (size_t)qpb::kr::nkc(d->p) * qpb::kr::BK;
       const size_t mrows = (size_t)ctx->nlanes * ((ctx->lane_cap + qpb::kr::BM - 1) / qpb::kr::BM) * qpb::kr::BM;

@@ -265,6 +265,7 @@ struct qp_ctx {
   // Q and G shared: residual GEMVs as batched GEMMs (bnd_sgemm), per problem [3][n4]
   float* pre = nullptr;
   long long off_x = 0, off_z = 0, off_t = 0, off_gx = 0, off_rhs = 0;  // state-block offsets (floats)
+  int solve_nt = 128;    // threads of bnd_solve per problem
   int tma_stages = 0;     // 0: register-staged bnd_tc_update; else bnd_tc_update_tma<raw stages, operand buffers> as 10·S + NOB
   // reading Q12c guard (path 1 with a kept-set cap): problems whose capped
   // elimination would exceed fb_bound go to the uncapped large-N kernel,
@@ -450,6 +451,9 @@ qp_err bnd_setup(const qp_ctx* c) {
       cudaFuncSetAttribute(qpb::bnd_resid<kBS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sst) ||
       cudaFuncSetAttribute(qpb::bnd_update<kBS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sst) ||
       cudaFuncSetAttribute(qpb::bnd_solve<kBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, ssv) ||
+      cudaFuncSetAttribute(qpb::bnd_solve<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, ssv) ||
+      cudaFuncSetAttribute(qpb::bnd_solve<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, ssv) ||
+      cudaFuncSetAttribute(qpb::bnd_solve<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, ssv) ||
       cudaFuncSetAttribute(qpb::bnd_assemble<kBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, stc) ||
       cudaFuncSetAttribute(qpb::bnd_tc_update<kBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, stc) ||
       cudaFuncSetAttribute(qpb::bnd_tc_update_tma<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, qpb::tu::smem_bytes(2, 2)) ||
@@ -672,7 +676,10 @@ qp_err run_batched(qp_ctx* c, const qpb::Args& a0, bool bwd) {
           qpb::bnd_cache<kBT><<<dim3(8, nb), kBT, 0, st>>>(ba);
           ++launches;
         }
-        qpb::bnd_solve<kBT><<<nb, kBT, ssv, st>>>(ba);
+        if (c->solve_nt == 1024) qpb::bnd_solve<1024><<<nb, 1024, ssv, st>>>(ba);
+        else if (c->solve_nt == 512) qpb::bnd_solve<512><<<nb, 512, ssv, st>>>(ba);
+        else if (c->solve_nt == 256) qpb::bnd_solve<256><<<nb, 256, ssv, st>>>(ba);
+        else qpb::bnd_solve<kBT><<<nb, kBT, ssv, st>>>(ba);
         if (c->pre) {  // G Δx (the solve's x part) of every problem: Δv recovery / the initial ẑ in bnd_update
           const int n = c->d.n, p = c->d.p;
           qpb::bnd_sgemm<true><<<dim3((p + 63) / 64, (nb + 63) / 64), 256, 0, st>>>(
@@ -862,6 +869,11 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
       free_all(ctx); delete ctx; return QP_ERR_CUDA;
     }
     if (getenv("QPB200_TC_TMA") && (e = make_tmaps(ctx)) != QP_OK) { free_all(ctx); delete ctx; return e; }
+    // triangular solves of large systems: more threads per problem keep more
+    // factor rows in flight (config 5, N ≈ 1.7-3 K: 560 → 609 QP/s at 512;
+    // config 4, N ≈ 340: 128 stays, 256 is 5 % slower)
+    ctx->solve_nt = L.N4max >= 1024 ? 512 : 128;
+    if (const char* e2 = getenv("QPB200_SOLVE_NT")) ctx->solve_nt = atoi(e2);
     // shared G: the assembly runs as one GEMM over the batch (kr_gemm.cuh)
     ctx->kr = d->bstride_G == 0 && d->p > 0 && !getenv("QPB200_NO_KR");
     // shared Q and G: the residual GEMVs as batched GEMMs too (bnd_sgemm)

@@ -149,7 +149,8 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def oracle_rate(W: dict, target_s: float, batch_cap: int, start: int = 0, prec: str = "f64"):
+def oracle_rate(W: dict, target_s: float, batch_cap: int, start: int = 0, prec: str = "f64",
+                single_pass: bool = False):
     """Time the oracle on a bounded sample of the workload, all host cores:
     prec "f64" = the parity reference (paper-literal Eq. 14 + GEPP), "f32" =
     the iteration-count reference (M_PART, the CUDA path's algorithm class).
@@ -163,6 +164,8 @@ def oracle_rate(W: dict, target_s: float, batch_cap: int, start: int = 0, prec: 
     oracle.backward(pilot, r, cfg, prec, nthreads=nt)
     dt = time.perf_counter() - t0
     rate = pilot.batch / max(dt, 1e-6)
+    if single_pass:  # (very large problems: the pilot is the sample)
+        return rate, nt, pilot.batch, dt
     ns = int(min(batch_cap, max(pilot.batch, round(rate * target_s))))
     ns = max(nt, (ns // nt) * nt) if ns >= nt else ns
     samp = W["make"](ns, start)
@@ -331,7 +334,9 @@ def main():
     # SURVEY §8(d) algorithmic flops (K14-literal) of this rank's launches,
     # from the measured per-problem iteration counts
     k14_s = float(sum(FL.k14_solve(n, m, p, int(i)) for i in iters))
-    k14_b = float(sum(FL.k14_backward(n, m, p, int(r)) for r in riters))
+    # chord steps (reading Q26) factor nothing: the batch total from qp_info
+    k14_b = float(sum(FL.k14_backward(n, m, p, int(r)) for r in riters)) - \
+        float(info.get("chord_steps", 0)) * (n + p + m) ** 3 / 3
     # executed flops of the reduced systems, counted inside the kernels
     x_s, x_b = S.last_flops()
     f_dom, x_dom, ms_dom = (k14_s, x_s, ms_solve) if dom_solve else (k14_b, x_b, ms_bwd)
@@ -398,7 +403,17 @@ def main():
         Sh.close()
 
     cpu = None
-    if rank == 0 and world == 1 and not a.no_cpu:
+    if rank == 0 and world == 1 and not a.no_cpu and n + m + p > 2048:
+        # config-5 size: the f64 paper-literal solve (Eq. 14 + GEPP, N = 3072)
+        # takes ~10 min per problem on one core (reading Q25); one problem per
+        # host core of the f32 oracle (M_PART) is the bounded sample
+        r32, cores, ns32, dt32 = oracle_rate(c, a.cpu_seconds, B, prec="f32", single_pass=True)
+        cpu = {"value": r32, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
+               "sample": f"first {ns32} problems of {c['name']} ({dt32:.1f} s), one per host thread: f32 oracle "
+                         f"(M_PART, reading Q12b), init + Alg. 1 + Alg. 2 + Alg. 3; the f64 Eq. 14 + GEPP oracle "
+                         f"is not timed at this size (~10 min per problem, DESIGN.md reading Q25)",
+               "f32_value": r32}
+    elif rank == 0 and world == 1 and not a.no_cpu:
         rate, cores, ns, dt = oracle_rate(c, a.cpu_seconds, B)
         r32, _, ns32, dt32 = oracle_rate(c, a.cpu_seconds / 3, B, prec="f32")
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),

@@ -73,15 +73,16 @@ def k14_solve(n: int, m: int, p: int, iters) -> float:
         (2 * n * n + 6 * p * n + 4 * m * n)
 
 
-def k14_backward(n: int, m: int, p: int, relax_iters) -> float:
-    """qp_backward_batched, one problem: Alg. 2 with `relax_iters` Newton steps
-    (relax_iters + 1 residual evaluations and factorisations: factor-then-check,
-    reading Q6), the Alg. 3 adjoint solve 2N², and the outer products of the
-    gradients 2(n² + mn + pn)."""
+def k14_backward(n: int, m: int, p: int, relax_iters, chord: float = 0) -> float:
+    """qp_backward_batched, one problem: Alg. 2 with `relax_iters` steps
+    (relax_iters + 1 residual evaluations; factor-then-check, reading Q6: one
+    factorisation per evaluation except for the `chord` steps of the guarded
+    chord relax, reading Q26, which reuse the solve's), the Alg. 3 adjoint
+    solve 2N², and the outer products of the gradients 2(n² + mn + pn)."""
     N = n + p + m
     resid = 2 * n * n + 6 * p * n + 4 * m * n
-    return (relax_iters + 1) * (N ** 3 / 3 + resid) + relax_iters * 2 * N ** 2 + 2 * N ** 2 + \
-        2 * (n * n + m * n + p * n)
+    return (relax_iters + 1) * resid + (relax_iters + 1 - chord) * N ** 3 / 3 + relax_iters * 2 * N ** 2 + \
+        2 * N ** 2 + 2 * (n * n + m * n + p * n)
 
 
 def data_bytes(n, m, p, shared=()) -> tuple[int, int]:

@@ -840,11 +840,13 @@ qp_err qp_create(qp_ctx** out, const qp_dims* d, const qp_config* cfg, int devic
     long long cap = (long long)(fr / 2 / per);
     if (const char* e2 = getenv("QPB200_BCHUNK")) cap = atoll(e2);  // tests: force several chunks
     ctx->bchunk = (int)std::max(1LL, std::min<long long>(d->batch, cap));
-    // lanes: two for large chunks (config 4, 8192 problems: 42.4 K QP/s vs
-    // 41.8 K with three, 40.9 K with four); four for chunks of 256 to 1183
-    // problems, whose phase kernels alone fill few waves (config 5, 256
-    // problems: 532 / 564 / 577 / 583 QP/s with one / two / three / four)
-    ctx->nlanes = ctx->bchunk >= 2 * 4 * 148 ? 2 : ctx->bchunk >= 256 ? 4 : 1;
+    // lanes: four for large systems (N ≥ 1024) in chunks of 256+ problems,
+    // whose phase kernels alone fill few waves (config 5, 256 problems: 532 /
+    // 564 / 577 / 583 QP/s with one / two / three / four); otherwise two for
+    // chunks of 1184+ problems (config 4, 8192 problems: 42.4 K vs 41.8 K with
+    // three, 40.9 K with four; 2048 problems: 39.1 K vs 37.9 K with one) and
+    // one below (1024 problems: 30.9 K vs 30.7 K with two, 30.4 K with four)
+    ctx->nlanes = (L.N4max >= 1024 && ctx->bchunk >= 256) ? 4 : ctx->bchunk >= 2 * 4 * 148 ? 2 : 1;
     if (const char* e2 = getenv("QPB200_BLANES")) ctx->nlanes = std::max(1, std::min(4, atoi(e2)));
     ctx->nlanes = std::min(ctx->nlanes, ctx->bchunk);
     cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);

@@ -55,3 +55,15 @@ def test_bezier_shapes_structure_feasibility(K):
     res = linprog(c, A_ub=np.hstack([G, np.ones((b.p, 1))]), b_ub=h, A_eq=np.hstack([A, np.zeros((b.m, 1))]),
                   b_eq=bb, bounds=[(None, None)] * b.n + [(None, 1.0)], method="highs")
     assert res.status == 0 and -res.fun > 1e-3, res.message
+
+
+def test_k14_backward_counts_no_factorisation_for_chord_steps():
+    """flops.k14_backward (SURVEY §8(d) work model): a chord step of the
+    guarded chord relax (reading Q26) reuses the solve's factorisation, so
+    each removes exactly N³/3 from the K14-literal count."""
+    from paper_2605_17913_b200 import flops as FL
+    n, m, p = 50, 10, 100
+    N = n + m + p
+    base = FL.k14_backward(n, m, p, 4)
+    assert abs(FL.k14_backward(n, m, p, 4, chord=3) - (base - 3 * N ** 3 / 3)) <= 1e-6 * base
+    assert FL.k14_backward(n, m, p, 4, chord=0) == base

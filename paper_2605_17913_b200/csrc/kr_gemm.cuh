@@ -227,18 +227,16 @@ __global__ void __launch_bounds__(WS_THREADS, 1) kr_gemm(const GemmArgs g) {
       tc::mbar_wait(tfull + acc, (li >> 1) & 1);
       tc::tc_fence_after();
       __syncwarp();
-      // lane r: problem of slot mt*128 + 32w + r and the parameters of its packed
-      // layout (KLayout: only the last 16-row block differs between sizes)
+      // lane r: problem of slot mt*128 + 32w + r (the batched engine's packed
+      // layout is uniform, bnd_layout: a row's offset does not depend on the
+      // problem's system size, so one offset per pair serves every problem)
       const int slot_l = mt * BM + 32 * warp + lane;
       const int nrow = min(32, count - (mt * BM + 32 * warp));  // warp-uniform (may be ≤ 0)
-      int b_l = 0, nbm1_l = 0, baseL_l = 0, Ll_l = 0;
+      int b_l = 0;
       float* stb_l = nullptr;
       if (lane < nrow) {
         b_l = g.slotmap[slot_l];
         stb_l = g.st + (long long)b_l * g.st_stride;
-        const int pa = reinterpret_cast<const int*>(stb_l)[6];  // BScal::pa
-        const KLayout L = KLayout::make(n4 + pa + m, n4, true);  // bnd_layout
-        nbm1_l = L.NB - 1; baseL_l = L.baseL; Ll_l = L.Ll;
       }
       float dmx = 0.f;  // lane r: max |diag| of problem r over this tile's pairs
       for (int c0 = 0; c0 < BN; c0 += 32) {
@@ -258,21 +256,17 @@ __global__ void __launch_bounds__(WS_THREADS, 1) kr_gemm(const GemmArgs g) {
             j = tp - i * (i + 1) / 2;
           }
           const int bi = i >> 4, ti = i & 15;
-          const int offr = 128 * bi * (bi + 1) + 64 * bi + ti * (16 * bi + 20) + j;  // row i in a full block
+          const int off = 128 * bi * (bi + 1) + 64 * bi + ti * (16 * bi + 20) + j;  // KLayout::make(.., true).off(i) + j
           const bool inner = tok && i < n && j < n, isdiag = tok && i == j && i < n;
           const bool anyd = __any_sync(0xffffffffu, isdiag);
           float q = 0.f;
           if (g.sQ == 0 && inner) q = __ldg(g.Q + (size_t)i * n + j);
           for (int r = 0; r < nrow; ++r) {
             const int b = __shfl_sync(0xffffffffu, b_l, r);
-            const int nbm1 = __shfl_sync(0xffffffffu, nbm1_l, r);
-            const int baseL = __shfl_sync(0xffffffffu, baseL_l, r);
-            const int Ll = __shfl_sync(0xffffffffu, Ll_l, r);
             float val = 0.f;
             if (tok) {
               const float qq = g.sQ == 0 ? q : (inner ? __ldg(g.Q + g.sQ * b + (size_t)i * n + j) : 0.f);
               val = inner ? qq + T[r * 33 + lane] : (i == j ? 1.f : 0.f);
-              const int off = bi < nbm1 ? offr : baseL + ti * Ll + j;
               g.kw[(long long)b * g.kstride + off] = val;
             }
             if (anyd) {

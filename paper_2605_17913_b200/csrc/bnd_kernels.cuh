@@ -92,6 +92,11 @@ struct BArgs {
   // state's gx segment.  nullptr = per-problem GEMVs inside bnd_resid
   float* pre;
   long long pre_stride;
+  // forward substitution fused into the factorisation: bnd_pdiag solves the
+  // panel's diagonal block for its rows of the right-hand side, bnd_prows
+  // subtracts the panel's contribution from every row below, bnd_solve runs
+  // only the backward substitution (chord steps: both)
+  int fuse;
   int ntiles_tu;        // bnd_tc_update_tma: 128-row tiles of the panel in the lane's largest system
 };
 
@@ -405,6 +410,11 @@ __global__ void __launch_bounds__(NT) bnd_scatter(const BArgs ba) {
   const int pa = h.pa;
   const KLayout L = bnd_layout(a, pa);
   float dmax = 0.f;
+  if (ba.pre && h.mode == BM_NEWTON) {  // + Gᵀ t of the batched GEMM, before the fused forward substitution
+    float* rhs = carve_state(gst, a).rhs;
+    const float* gt = ba.pre + (long long)bid * ba.pre_stride + 2 * a.n4;
+    for (int j = threadIdx.x; j < a.n; j += NT) rhs[j] += gt[j];
+  }
   scatter_rows<NT>(a, carve_state(gst, a), L, ba.kw + (long long)bid * ba.kstride, prob_of(a, bid), pa, dmax);
 #pragma unroll
   for (int o = 16; o; o >>= 1) dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
@@ -905,6 +915,33 @@ __global__ void __launch_bounds__(NT) bnd_pdiag(const BArgs ba) {
   __syncthreads();
   for (int b = c0 / KB + (tid >> 5); KB * b < c1; b += NT / 32) invert_diag_block(D - c0, P, b, rinv);
   __syncthreads();
+  if (ba.fuse) {
+    // the forward substitution of the panel's rows (solve_qd's forward loop
+    // on the panel, rows below it in bnd_prows): per 16-block u_b = W_b r_b,
+    // then r_i −= L_ib u_b for the panel's rows below the block
+    __shared__ float ur[W];
+    float* rhs = carve_state(gst, a).rhs;
+    for (int e = tid; e < w; e += NT) ur[e] = rhs[c0 + e];
+    __syncthreads();
+    for (int k0l = 0; k0l < w; k0l += KB) {
+      const int kb = min(KB, w - k0l);
+      float u = 0.f;
+      if (tid < kb) {
+        u = rinv[c0 + k0l + tid] * ur[k0l + tid];
+        for (int c = 0; c < tid; ++c) u = fmaf(D[(k0l + c) * DS + k0l + tid], ur[k0l + c], u);  // W[t][c], row c col t
+      }
+      __syncthreads();
+      if (tid < kb) ur[k0l + tid] = u;
+      __syncthreads();
+      for (int il = k0l + KB + tid; il < w; il += NT) {
+        float acc = ur[il];
+        for (int c = 0; c < kb; ++c) acc = fmaf(-D[il * DS + k0l + c], ur[k0l + c], acc);
+        ur[il] = acc;
+      }
+      __syncthreads();
+    }
+    for (int e = tid; e < w; e += NT) rhs[c0 + e] = ur[e];
+  }
   for (int e = tid; e < w * (W / 4); e += NT) {  // row i keeps columns up to the end of its 16-block
     const int r = e / (W / 4), q = e - r * (W / 4), i = c0 + r, j = c0 + 4 * q;
     if (4 * q < w && j < ((i >> 4) + 1) * KB)
@@ -953,6 +990,10 @@ __global__ void __launch_bounds__(NT, 4) bnd_prows(const BArgs ba) {
     }
   }
   for (int k = tid; k < W; k += NT) rl[k] = rinv[c0 + k];
+  __shared__ float ur[W];  // the panel's forward-substituted right-hand side (bnd_pdiag, fused)
+  float* rhs = carve_state(gst, a).rhs;
+  if (ba.fuse)
+    for (int k = tid; k < W; k += NT) ur[k] = rhs[c0 + k];
   __syncthreads();
   const int i = r0 + tid;
   if (i >= N4) return;
@@ -981,12 +1022,18 @@ __global__ void __launch_bounds__(NT, 4) bnd_prows(const BArgs ba) {
       x[4 * j4 + 3] = fmaf(xk, d.w, x[4 * j4 + 3]);
     }
   }
+  float ri = ba.fuse ? rhs[i] : 0.f;
 #pragma unroll
   for (int q = 0; q < W / 4; ++q) {
     const float s0 = sgn_of(c0 + 4 * q, L.npos);  // S_k (npos is a multiple of 4)
-    reinterpret_cast<float4*>(row)[q] =
-        make_float4(s0 * x[4 * q], s0 * x[4 * q + 1], s0 * x[4 * q + 2], s0 * x[4 * q + 3]);
+    const float4 l = make_float4(s0 * x[4 * q], s0 * x[4 * q + 1], s0 * x[4 * q + 2], s0 * x[4 * q + 3]);
+    reinterpret_cast<float4*>(row)[q] = l;
+    if (ba.fuse) {  // r_i −= L_i,panel u_panel (fused forward substitution)
+      ri = fmaf(-l.x, ur[4 * q], ri); ri = fmaf(-l.y, ur[4 * q + 1], ri);
+      ri = fmaf(-l.z, ur[4 * q + 2], ri); ri = fmaf(-l.w, ur[4 * q + 3], ri);
+    }
   }
+  if (ba.fuse) rhs[i] = ri;
 }
 
 // ---------------------------------------------------------------------------
@@ -1131,12 +1178,12 @@ __global__ void __launch_bounds__(NT) bnd_solve(const BArgs ba) {
   const float* K = chord ? a.kc + (long long)bid * a.kc_stride : ba.kw + (long long)bid * ba.kstride;
   const float* rinv = chord ? a.chd + (long long)bid * a.chd_stride + 4 + 4 * ((a.p + 3) & ~3) : G.rinv;
   copy_block<NT>(sm, G.rhs, L.N4);
-  if (ba.pre && (h.mode == BM_NEWTON || h.mode == BM_CHORD)) {  // + Gᵀ t of the batched GEMM (residuals, pre)
+  if (ba.pre && chord) {  // + Gᵀ t of the batched GEMM (residuals, pre; bnd_scatter adds it for a Newton step)
     const float* gt = ba.pre + (long long)bid * ba.pre_stride + 2 * a.n4;
     for (int j = threadIdx.x; j < a.n; j += NT) sm[j] += gt[j];
     __syncthreads();
   }
-  solve_qd<NT, false, true>(K, L, rinv, sm);
+  solve_qd<NT, false, true>(K, L, rinv, sm, nullptr, !(ba.fuse && !chord));
   __syncthreads();
   copy_block<NT>(G.rhs, sm, L.N4);
 }

@@ -615,11 +615,11 @@ __device__ int factor_big(float* __restrict__ K, const KLayout& L, const float t
 // ------------------------------------------------------------------------
 template <int NT, bool TAB = false, bool UNR = false>
 __device__ void solve_qd(const float* __restrict__ K, const KLayout& L, const float* __restrict__ rinv,
-                         float* __restrict__ rhs, const int* __restrict__ tab = nullptr) {
+                         float* __restrict__ rhs, const int* __restrict__ tab = nullptr, bool fwd = true) {
   const int tid = threadIdx.x;
   const int N4 = L.N4;
-  // forward: L u = b
-  for (int b = 0; b < L.NB; ++b) {
+  // forward: L u = b (fwd = false: already done during the factorisation, rhs holds u)
+  for (int b = 0; fwd && b < L.NB; ++b) {
     const int k0 = KB * b, kb = L.bw(b);
     const float* D = K + row_off<TAB>(L, tab, k0) + k0;
     const int Lb = L.len(b);

@@ -572,6 +572,7 @@ qp_err run_batched(qp_ctx* c, const qpb::Args& a0, bool bwd) {
       ba.tmaps = c->tmaps; ba.lane_b0 = l * lcap;
       ba.pre = c->pre ? c->pre + (size_t)l * lcap * 3 * n4 : nullptr;
       ba.pre_stride = 3LL * n4;
+      ba.fuse = getenv("QPB200_NO_FUSE") ? 0 : 1;
       qpb::kr::GemmArgs& ga = L.ga;
       if (c->kr) {
         ga.whi = ba.whi; ga.wlo = ba.wlo; ga.gghi = c->gghi; ga.gglo = c->gglo;

@@ -864,6 +864,9 @@ __global__ void __launch_bounds__(TU_THREADS, 1) bnd_tc_update_tma(const BArgs b
 //     (j > k), stored L_ik = S_k x_k: the TRSM and the in-panel Schur updates
 //     of all four 16-column blocks in one pass over the row.
 // ---------------------------------------------------------------------------
+#ifndef QPB200_PDIAG_QS
+#define QPB200_PDIAG_QS 4  // bnd_pdiag trailing-update rows per pass (ipm_cta.cuh factor_big_range)
+#endif
 namespace pnl {
 constexpr int W = 64, DS = 68;  // panel width, dense row stride (odd multiple of 16 B)
 }
@@ -911,7 +914,7 @@ __global__ void __launch_bounds__(NT) bnd_pdiag(const BArgs ba) {
   __syncthreads();
   PanelLayout P;
   P.N4 = c1; P.NB = L.NB; P.npos = L.npos; P.c0 = c0; P.S = DS; P.base = L;
-  factor_big_range<NT>(D - c0, P, a.floor_rel * h.dmax, rinv, scr, c0, c1);
+  factor_big_range<NT, PanelLayout, QPB200_PDIAG_QS>(D - c0, P, a.floor_rel * h.dmax, rinv, scr, c0, c1);
   __syncthreads();
   for (int b = c0 / KB + (tid >> 5); KB * b < c1; b += NT / 32) invert_diag_block(D - c0, P, b, rinv);
   __syncthreads();

@@ -445,7 +445,9 @@ struct PanelLayout {
   __device__ __forceinline__ int bw(int b) const { return base.bw(b); }
 };
 
-template <int NT, class LT = KLayout>
+// QS: rows of a 32×32 super-tile a lane accumulates per pass (8: one pass;
+// 4: two passes with half the accumulator registers)
+template <int NT, class LT = KLayout, int QS = 8>
 __device__ int factor_big_range(float* __restrict__ K, const LT& L, const float theta, float* __restrict__ rinv,
                                 float* __restrict__ scr, const int c0, const int c1) {
   constexpr int NW = NT / 32;
@@ -533,24 +535,29 @@ __device__ int factor_big_range(float* __restrict__ K, const LT& L, const float 
         int J = 0, rem = st;
         while (rem >= T - J) { rem -= T - J; ++J; }
         const int I = J + rem;
-        const int rb = k1 + 32 * I + ty, cb = k1 + 32 * J + tx;
-        int roff[8], coff[4];
-        bool rok[8], cok[4];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int rr = rb + 4 * q;
-          rok[q] = rr < N4;
-          roff[q] = rok[q] ? L.off(rr) : 0;
-        }
+        const int cb = k1 + 32 * J + tx;
+        int coff[4];
+        bool cok[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const int cc = cb + 8 * c;
           cok[c] = cc < ncol;
           coff[c] = cok[c] ? L.off(cc) : 0;
         }
-        float acc[8][4];
+#pragma unroll 1
+        for (int hh = 0; hh < 8 / QS; ++hh) {
+        const int rb = k1 + 32 * I + ty + 4 * QS * hh;
+        int roff[QS];
+        bool rok[QS];
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
+        for (int q = 0; q < QS; ++q) {
+          const int rr = rb + 4 * q;
+          rok[q] = rr < N4;
+          roff[q] = rok[q] ? L.off(rr) : 0;
+        }
+        float acc[QS][4];
+#pragma unroll
+        for (int q = 0; q < QS; ++q)
 #pragma unroll
           for (int c = 0; c < 4; ++c)
             acc[q][c] = (rok[q] && cok[c] && cb + 8 * c <= rb + 4 * q) ? K[roff[q] + cb + 8 * c] : 0.f;
@@ -566,7 +573,7 @@ __device__ int factor_big_range(float* __restrict__ K, const LT& L, const float 
             lc[c] = t;
           }
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
+          for (int q = 0; q < QS; ++q) {
             const float4 lr = rok[q] ? *reinterpret_cast<const float4*>(K + roff[q] + k0 + 4 * q4)
                                      : make_float4(0, 0, 0, 0);
 #pragma unroll
@@ -581,12 +588,13 @@ __device__ int factor_big_range(float* __restrict__ K, const LT& L, const float 
           }
         }
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
+        for (int q = 0; q < QS; ++q)
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             const int cc = cb + 8 * c;
             if (rok[q] && cok[c] && cc <= rb + 4 * q) K[roff[q] + cc] = acc[q][c];
           }
+        }
       }
     }
     __syncthreads();

@@ -28,10 +28,13 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// tf32(x) rounded to nearest, ties away from zero — cvt.rna.tf32.f32 for
+// every finite x (and ±inf on overflow), as two integer operations: adding
+// half a tf32 ulp to the magnitude bits and clearing the 13 low mantissa
+// bits (ptxas expands cvt.rna.tf32 into a compare, add, mask and select;
+// this halves the split work of the 3×TF32 staging loops)
 __device__ __forceinline__ float to_tf32(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 
 // Canonical K-major, no swizzle: element (mn, k) of a TM×TK tile.  Core

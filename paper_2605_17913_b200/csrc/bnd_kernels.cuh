@@ -1196,7 +1196,7 @@ __global__ void __launch_bounds__(NT) bnd_solve(const BArgs ba) {
 // the Newton step with its fraction-to-boundary step length and retraction
 // (NEWTON), or Alg. 3's gradients from the relaxed factorisation (ADJ).
 // ---------------------------------------------------------------------------
-template <int NT>
+template <int NT, bool LARGE = false>
 __global__ void __launch_bounds__(NT) bnd_update(const BArgs ba) {
   extern __shared__ __align__(16) float sm[];
   const Args& a = ba.a;
@@ -1218,7 +1218,8 @@ __global__ void __launch_bounds__(NT) bnd_update(const BArgs ba) {
       for (int i = tid; i < p; i += NT) S.dz[i] = S.gx[i];
       __syncthreads();
     } else {
-      rowdots<NT>(P.G, p, n, S.x, S.dz);
+      if constexpr (LARGE) rowdots_large<NT>(P.G, p, n, S.x, S.dz);
+      else rowdots<NT>(P.G, p, n, S.x, S.dz);
     }
     for (int i = tid; i < p; i += NT) S.dz[i] -= __ldg(P.h + i);  // ẑ = Gx − h
     __syncthreads();
@@ -1247,7 +1248,7 @@ __global__ void __launch_bounds__(NT) bnd_update(const BArgs ba) {
   } else if (mode == BM_NEWTON || mode == BM_CHORD) {
     float kappa = h.kappa;
     int stage = 0;
-    const bool okstep = newton_update<NT>(S, a, P, pa, kappa, kappa - h.kt, &stage, ba.pre != nullptr);
+    const bool okstep = newton_update<NT, LARGE>(S, a, P, pa, kappa, kappa - h.kt, &stage, ba.pre != nullptr);
     if (!okstep) {
       if (tid == 0) h.status = ST_FAIL | ((bwd ? STG_RELAX : stage) << 8);
       __syncthreads();
@@ -1257,7 +1258,7 @@ __global__ void __launch_bounds__(NT) bnd_update(const BArgs ba) {
       h.kappa = kappa;
     }
   } else {  // BM_ADJ: dv = G dx + w (f2 = 0), dz = d₊ ⊙ dv (reading Q8), Alg. 3 outer products
-    recover_dv<NT>(S, a, P, true, ba.pre != nullptr);
+    recover_dv<NT, LARGE>(S, a, P, true, ba.pre != nullptr);
     for (int i = tid; i < p; i += NT) S.dz[i] = S.dp[i] * S.gx[i];
     for (int j = tid; j < n; j += NT) S.dx[j] = S.rhs[j];
     for (int l = tid; l < m; l += NT) S.dy[l] = S.rhs[n4 + pa + l];

@@ -535,6 +535,49 @@ __device__ __noinline__ void rowdots(const float* __restrict__ Mat, int rows, in
   __syncthreads();
 }
 
+// Large n (the batched engine at config-5 size: G is 8 MB per problem and
+// streams from HBM): eight rows in flight per warp, float4 loads of the
+// matrix and the vector; falls back to rowdots for n not a multiple of 4 or
+// unaligned rows.  Ends with a barrier.
+template <int NT>
+__device__ __noinline__ void rowdots_large(const float* __restrict__ Mat, int rows, int n, const float* vec,
+                                           float* out) {
+  if ((n & 3) || ((reinterpret_cast<uintptr_t>(Mat) | reinterpret_cast<uintptr_t>(vec)) & 15)) {
+    rowdots<NT>(Mat, rows, n, vec, out);
+    return;
+  }
+  constexpr int NW = NT / 32, R = 8;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, n4 = n >> 2;
+  const float4* v4 = reinterpret_cast<const float4*>(vec);
+  for (int r0 = warp * R; r0 < rows; r0 += NW * R) {
+    float acc[R];
+#pragma unroll
+    for (int u = 0; u < R; ++u) acc[u] = 0.f;
+    for (int j = lane; j < n4; j += 32) {
+      const float4 xv = v4[j];
+      float4 g[R];
+#pragma unroll
+      for (int u = 0; u < R; ++u)
+        g[u] = r0 + u < rows ? __ldg(reinterpret_cast<const float4*>(Mat + (size_t)(r0 + u) * n) + j)
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < R; ++u)
+        acc[u] = fmaf(g[u].w, xv.w, fmaf(g[u].z, xv.z, fmaf(g[u].y, xv.y, fmaf(g[u].x, xv.x, acc[u]))));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1)
+#pragma unroll
+      for (int u = 0; u < R; ++u) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
+    if (lane < R && r0 + lane < rows) {
+      float v = acc[0];
+#pragma unroll
+      for (int u = 1; u < R; ++u) v = lane == u ? acc[u] : v;
+      out[r0 + lane] = v;
+    }
+  }
+  __syncthreads();
+}
+
 // ------------------------------------------------------------------------
 // Residuals (Eq. 4; Eq. 10), the norms of the relative
 // stopping test (reading Q4), d₊, d₋, c, ω and the active set at (v, κ), and
@@ -595,7 +638,10 @@ __device__ Norms residuals(const Smem& S, const Args& a, const Prob& P, float ka
     spill = vv[0] > a.fb_bound;
   }
   // rows: r_i = Gx + s − h, r_e = Ax − b (warp per row); f2, t, rhs_w, rhs_y
-  if (!pre) rowdots<NT>(P.G, p, n, S.x, S.gx);
+  if (!pre) {
+    if constexpr (LARGE) rowdots_large<NT>(P.G, p, n, S.x, S.gx);
+    else rowdots<NT>(P.G, p, n, S.x, S.gx);
+  }
   rowdots<NT>(P.A, m, n, S.x, S.gx + p);
   for (int k = tid; k < p; k += NT) {
     const float ri = S.gx[k] + S.s[k] - __ldg(P.h + k);
@@ -821,10 +867,13 @@ __device__ float manifold_coords(const Smem& S, const Args& a) {
 // Recover Δv from the reduced solution: Δv_i = g_iᵀΔx + w_i with w_i solved
 // (i ∈ A) or eliminated: w_i = (d₊_i g_iᵀΔx − f2_i)/d₋_i (v_i ≤ 0).  Writes
 // S.gx[k] = Δv_k.  (f2 = 0 for the adjoint.)
-template <int NT>
+template <int NT, bool LARGE = false>
 __device__ void recover_dv(const Smem& S, const Args& a, const Prob& P, bool zero_f2, bool gx_ready = false) {
   const int n4 = a.n4;
-  if (!gx_ready) rowdots<NT>(P.G, a.p, a.n, S.rhs, S.gx);  // (gx_ready: G Δx from a batched GEMM)
+  if (!gx_ready) {  // (gx_ready: G Δx from a batched GEMM)
+    if constexpr (LARGE) rowdots_large<NT>(P.G, a.p, a.n, S.rhs, S.gx);
+    else rowdots<NT>(P.G, a.p, a.n, S.rhs, S.gx);
+  }
   for (int k = threadIdx.x; k < a.p; k += NT) {
     const float gdx = S.gx[k];
     const int wi = S.widx[k];
@@ -838,13 +887,13 @@ __device__ void recover_dv(const Smem& S, const Args& a, const Prob& P, bool zer
 // 4-6); α = min(1, τ α_max) (Eq. 6 + Q3); step on (x, y, v, κ) and retract
 // (P:425-429).  Returns false (iterate untouched) if the direction is not
 // finite.
-template <int NT>
+template <int NT, bool LARGE = false>
 __device__ bool newton_update(const Smem& S, const Args& a, const Prob& P, int pa, float& kappa, float r_kappa,
                               int* stage, bool gx_ready = false) {
   const int tid = threadIdx.x;
   const int n = a.n, n4 = a.n4, p = a.p, m = a.m;
   const float dk = -r_kappa;
-  recover_dv<NT>(S, a, P, false, gx_ready);
+  recover_dv<NT, LARGE>(S, a, P, false, gx_ready);
   float amax = INFINITY, bad = 0.f;
   for (int k = tid; k < p; k += NT) {
     const float dv = S.gx[k];

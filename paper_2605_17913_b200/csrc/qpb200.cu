@@ -450,6 +450,7 @@ qp_err bnd_setup(const qp_ctx* c) {
       cudaFuncSetAttribute(qpb::bnd_resid<kBS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sst) ||
       cudaFuncSetAttribute(qpb::bnd_resid<kBS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sst) ||
       cudaFuncSetAttribute(qpb::bnd_update<kBS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sst) ||
+      cudaFuncSetAttribute(qpb::bnd_update<kBS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sst) ||
       cudaFuncSetAttribute(qpb::bnd_solve<kBT>, cudaFuncAttributeMaxDynamicSharedMemorySize, ssv) ||
       cudaFuncSetAttribute(qpb::bnd_solve<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, ssv) ||
       cudaFuncSetAttribute(qpb::bnd_solve<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, ssv) ||
@@ -687,7 +688,10 @@ qp_err run_batched(qp_ctx* c, const qpb::Args& a0, bool bwd) {
               ba.st + c->off_rhs, c->bst_stride, a0.G, n, ba.st + c->off_gx, c->bst_stride, nb, p, n);
           ++launches;
         }
-        qpb::bnd_update<kBS><<<nb, kBS, sst, st>>>(ba);
+        if (c->d.n >= 2 * kBS)  // eight G rows in flight per warp (config 5)
+          qpb::bnd_update<kBS, true><<<nb, kBS, sst, st>>>(ba);
+        else
+          qpb::bnd_update<kBS><<<nb, kBS, sst, st>>>(ba);
         launches += 2;
         ++L.k;
       }

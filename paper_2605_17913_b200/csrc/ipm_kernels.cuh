@@ -1044,7 +1044,7 @@ __device__ __forceinline__ void ipm_problem(const Args& a, const Smem& S, const 
     } else {
       kappa = manifold_coords<NT>(S, a);
       kt = bwd ? a.kappa_relax : a.sigma * kappa;  // κ_target: κ_relax (Alg. 2) or σκ (Alg. 1)
-      const float* cj = a.chd + (long long)bid * a.chd_stride;
+      const float* cj = chord_on ? a.chd + (long long)bid * a.chd_stride : nullptr;
       const bool was_chord = chord;
       if (was_chord) {  // the cached Jacobian: the right-hand side of a chord step
         const int p4 = (p + 3) & ~3;

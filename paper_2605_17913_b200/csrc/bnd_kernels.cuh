@@ -1046,7 +1046,8 @@ __global__ void __launch_bounds__(NT, 4) bnd_prows(const BArgs ba) {
 // problems are GEMMs: G X, Q X (NT) and Gᵀ Z, Gᵀ T (NN) with the problems'
 // x, z, t rows read in place from their state blocks (lda = state stride):
 // the shared matrix is read once per 64-problem tile instead of once per
-// problem.  64×64 tiles, K in steps of 16, 256 threads with 4×4 outputs each.
+// problem.  64×64 tiles, K in steps of 16, 256 threads with 4×4 outputs each
+// (float4 operand reads from shared memory, float4 stores).
 // ---------------------------------------------------------------------------
 template <bool BT>
 __global__ void __launch_bounds__(256) bnd_sgemm(const float* __restrict__ A, long long lda,
@@ -1106,10 +1107,10 @@ __global__ void __launch_bounds__(256) bnd_sgemm(const float* __restrict__ A, lo
     }
     __syncthreads();
 #pragma unroll
-    for (int kk = 0; kk < BK; ++kk) {
-      float av[4], bv[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) { av[i] = As[kk][ty + 16 * i]; bv[i] = Bs[kk][tx + 16 * i]; }
+    for (int kk = 0; kk < BK; ++kk) {  // thread (ty, tx): rows 4·ty + [0, 4), columns 4·tx + [0, 4)
+      const float4 a4 = *reinterpret_cast<const float4*>(&As[kk][4 * ty]);
+      const float4 b4 = *reinterpret_cast<const float4*>(&Bs[kk][4 * tx]);
+      const float av[4] = {a4.x, a4.y, a4.z, a4.w}, bv[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -1117,14 +1118,18 @@ __global__ void __launch_bounds__(256) bnd_sgemm(const float* __restrict__ A, lo
     }
     __syncthreads();
   }
+  const bool vc = !(ldc & 3) && !(reinterpret_cast<uintptr_t>(C) & 15);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const int gm = m0 + ty + 16 * i;
+    const int gm = m0 + 4 * ty + i, gn = n0 + 4 * tx;
     if (gm >= M) continue;
+    float* dst = C + (long long)gm * ldc + gn;
+    if (vc && gn + 3 < N) {
+      *reinterpret_cast<float4*>(dst) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+    } else {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int gn = n0 + tx + 16 * j;
-      if (gn < N) C[(long long)gm * ldc + gn] = acc[i][j];
+      for (int j = 0; j < 4; ++j)
+        if (gn + j < N) dst[j] = acc[i][j];
     }
   }
 }

@@ -400,6 +400,46 @@ __device__ __forceinline__ void scatter_rows(const Args& a, const Smem& S, const
   }
 }
 
+// bnd_scatter's version: one warp per row r ≥ n4, each element written once
+// (columns < n: the C / A row or zeros on padding rows; columns n .. len:
+// zeros, float4 from n4; then the diagonal), instead of zeroing the whole
+// tail of the workspace and writing the C / A rows over it
+template <int NT>
+__device__ __forceinline__ void scatter_rows_once(const Args& a, const Smem& S, const KLayout& L, float* K,
+                                                  const Prob& P, int pa, float& dmax) {
+  const int tid = threadIdx.x, lane = tid & 31, n = a.n, n4 = a.n4, N = L.N, N4 = L.N4;
+  for (int r = n4 + (tid >> 5); r < N4; r += NT / 32) {
+    const int rr = r - n4;
+    const float* src = nullptr;
+    float w = 1.f, d;
+    if (rr < pa) {
+      const int kk = S.act[rr];
+      src = P.G + (size_t)kk * n;
+      w = S.dp[kk];
+      const float e = S.dm[kk];
+      d = -e;
+      dmax = fmaxf(dmax, fabsf(e));
+    } else if (r < N) {
+      src = P.A + (size_t)(rr - pa) * n;
+      d = 0.f;
+    } else {
+      d = -1.f;
+    }
+    float* dst = K + L.off(r);
+    const int len = L.len(r >> 4);
+    float4* d4 = reinterpret_cast<float4*>(dst);
+    for (int q = (n4 >> 2) + lane; q < (len >> 2); q += 32) d4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (src) {
+      for (int j = lane; j < n; j += 32) dst[j] = w * __ldg(src + j);
+    } else {
+      for (int j = lane; j < n; j += 32) dst[j] = 0.f;
+    }
+    for (int j = n + lane; j < n4; j += 32) dst[j] = 0.f;
+    __syncwarp();
+    if (lane == 0) dst[r] = d;
+  }
+}
+
 template <int NT>
 __global__ void __launch_bounds__(NT) bnd_scatter(const BArgs ba) {
   const Args& a = ba.a;
@@ -415,7 +455,7 @@ __global__ void __launch_bounds__(NT) bnd_scatter(const BArgs ba) {
     const float* gt = ba.pre + (long long)bid * ba.pre_stride + 2 * a.n4;
     for (int j = threadIdx.x; j < a.n; j += NT) rhs[j] += gt[j];
   }
-  scatter_rows<NT>(a, carve_state(gst, a), L, ba.kw + (long long)bid * ba.kstride, prob_of(a, bid), pa, dmax);
+  scatter_rows_once<NT>(a, carve_state(gst, a), L, ba.kw + (long long)bid * ba.kstride, prob_of(a, bid), pa, dmax);
 #pragma unroll
   for (int o = 16; o; o >>= 1) dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
   if ((threadIdx.x & 31) == 0 && dmax > 0.f) atomicMax(reinterpret_cast<int*>(&h.dmax), __float_as_int(dmax));

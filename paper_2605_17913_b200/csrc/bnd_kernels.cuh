@@ -363,44 +363,8 @@ __global__ void __launch_bounds__(NT) bnd_resid(const BArgs ba) {
 // kept C rows d₊ₖ gₖ, the A rows, the diagonal −d₋ / 0 / −1) when H comes
 // from kr_gemm (shared G); bnd_assemble's last CTA does the same otherwise.
 // ---------------------------------------------------------------------------
-template <int NT>
-__device__ __forceinline__ void scatter_rows(const Args& a, const Smem& S, const KLayout& L, float* K, const Prob& P,
-                                             int pa, float& dmax) {
-  const int tid = threadIdx.x, n = a.n, n4 = a.n4, N = L.N, N4 = L.N4;
-  if (n4 < N4) {
-    float4* K4 = reinterpret_cast<float4*>(K);
-    for (int i = (L.off(n4) >> 2) + tid; i < (L.size() >> 2); i += NT) K4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  __syncthreads();
-  // one warp per row: coalesced row segments of G / A into row n4 + rr
-  const int nrow = N - n4;
-  for (int rr = tid >> 5; rr < nrow; rr += NT / 32) {
-    const float* src;
-    float w = 1.f;
-    if (rr < pa) {
-      const int kk = S.act[rr];
-      src = P.G + (size_t)kk * n;
-      w = S.dp[kk];
-    } else {
-      src = P.A + (size_t)(rr - pa) * n;
-    }
-    float* dst = K + L.off(n4 + rr);
-    for (int j = tid & 31; j < n; j += 32) dst[j] = w * __ldg(src + j);
-  }
-  for (int r = n4 + tid; r < N4; r += NT) {
-    float d;
-    if (r < n4 + pa) {
-      const float e = S.dm[S.act[r - n4]];
-      d = -e;
-      dmax = fmaxf(dmax, fabsf(e));
-    } else {
-      d = r < N ? 0.f : -1.f;
-    }
-    K[L.off(r) + r] = d;
-  }
-}
 
-// bnd_scatter's version: one warp per row r ≥ n4, each element written once
+// One warp per row r ≥ n4 (bnd_scatter, and bnd_assemble's last CTA), each element written once
 // (columns < n: the C / A row or zeros on padding rows; columns n .. len:
 // zeros, float4 from n4; then the diagonal), instead of zeroing the whole
 // tail of the workspace and writing the C / A rows over it
@@ -429,7 +393,13 @@ __device__ __forceinline__ void scatter_rows_once(const Args& a, const Smem& S, 
     const int len = L.len(r >> 4);
     float4* d4 = reinterpret_cast<float4*>(dst);
     for (int q = (n4 >> 2) + lane; q < (len >> 2); q += 32) d4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (src) {
+    if (src && !(n & 3) && !(reinterpret_cast<uintptr_t>(src) & 15)) {  // float4 row copy
+      const float4* s4 = reinterpret_cast<const float4*>(src);
+      for (int q = lane; q < (n >> 2); q += 32) {
+        const float4 v = __ldg(s4 + q);
+        d4[q] = make_float4(w * v.x, w * v.y, w * v.z, w * v.w);
+      }
+    } else if (src) {
       for (int j = lane; j < n; j += 32) dst[j] = w * __ldg(src + j);
     } else {
       for (int j = lane; j < n; j += 32) dst[j] = 0.f;
@@ -487,7 +457,7 @@ __global__ void __launch_bounds__(NT) bnd_assemble(const BArgs ba) {
   const int N = L.N, N4 = L.N4;
   float dmax = 0.f;
   if ((int)blockIdx.x == ba.ntiles) {
-    scatter_rows<NT>(a, S, L, K, P, pa, dmax);
+    scatter_rows_once<NT>(a, S, L, K, P, pa, dmax);
   } else {
     int I = 0, t = blockIdx.x;
     while (t > I) { t -= I + 1; ++I; }

@@ -692,6 +692,15 @@ __device__ void solve_qd(const float* __restrict__ K, const KLayout& L, const fl
     __syncthreads();
     if (b > 0) {
       const float* Bk = K + row_off<TAB>(L, tab, k0);
+      if constexpr (UNR) {  // (K in global memory) L2 prefetch of the next block row, one per 128-byte line
+        const int kp = k0 - KB, nl = (kp + 31) >> 5;
+        const float* Bp = K + row_off<TAB>(L, tab, kp);
+        const int Lp = L.len(b - 1);
+        for (int q = tid; q < KB * nl; q += NT) {
+          const int i = q / nl, c = (q - i * nl) << 5;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(Bp + i * Lp + c));
+        }
+      }
       for (int j = tid; j < k0; j += NT) {
         float acc = rhs[j];
         if constexpr (UNR) {

@@ -745,6 +745,11 @@ __device__ Norms residuals(const Smem& S, const Args& a, const Prob& P, float ka
         float4 qx = make_float4(0.f, 0.f, 0.f, 0.f), gz = qx, gt = qx, ay = qx;
         auto mat = [&](const float* M, int rows, const float* vec, const float* vec2, float4& acc, float4& acc2) {
           for (int i0 = 0; i0 < rows; i0 += 8) {
+            // L2 prefetch of the rows four steps ahead, one per 128-byte line (every 8th quad)
+            if (!(j4 & 7))
+#pragma unroll
+              for (int u = 0; u < 8; ++u)
+                if (i0 + 32 + u < rows) asm volatile("prefetch.global.L2 [%0];" ::"l"(M + (size_t)(i0 + 32 + u) * n + j));
             float4 g[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u)
